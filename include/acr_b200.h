@@ -1,0 +1,103 @@
+/* acr_b200 -- C ABI of the B200-native ACR factor/solve hot path.
+ *
+ * Replaces the reference's only solve entry point,
+ *   acrsolve.reduction.acr_solve(sys, tol, cutoff_blocks=1, leaf_size=32,
+ *                                inversion_order="forward")
+ *   (/root/reference/pkg/src/acrsolve/reduction.py:273-326, re-exported at
+ *   __init__.py:20-22),
+ * split into plan / factor / solve so that several right-hand sides reuse one
+ * factorisation.  The reference has no FFI; its "plugin API" is that Python
+ * function, which paper_1604_00617_b200.acr_solve mirrors on top of this ABI.
+ *
+ * All array arguments are fp64 DEVICE pointers owned by the caller (torch
+ * tensors in the Python shim); the library borrows them for the call.  The
+ * library owns its HODLR storage (stream-ordered cudaMallocAsync).  `stream`
+ * is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Status codes: 0 ok, 1 bad argument (Python: ValueError), 2 singular pivot
+ * (SingularBlockError / LinAlgError), 3 CUDA error, 4 internal limit.
+ */
+#ifndef ACR_B200_H
+#define ACR_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct acr_plan acr_plan_t;
+
+enum { ACR_OK = 0, ACR_EARG = 1, ACR_ESINGULAR = 2, ACR_ECUDA = 3,
+       ACR_EINTERNAL = 4 };
+
+/* m block rows of dimension n; H parameters as reference Tolerance
+ * (hodlr.py:29-44: eps > 0, max_rank_cap >= 1 or 0 for none), leaf_size
+ * (cluster.py:54-71), cutoff_blocks >= 1 (reduction.py:284-285). */
+int acr_plan_create(int m, int n, int leaf_size, double eps, int max_rank_cap,
+                    int cutoff_blocks, acr_plan_t** out);
+void acr_plan_destroy(acr_plan_t* p);
+
+/* option 1: keep every level's D blocks for export (tests); value 0/1 */
+int acr_plan_set_option(acr_plan_t* p, int option, long long value);
+
+/* Factor phase (reference lift_system reduction.py:156-166 + reduce_level
+ * loop :294-302 + the cutoff LU oracles.py:20-31), no right-hand side.
+ * Bands: D_sub (m,n-1), D_diag (m,n), D_sup (m,n-1), E (m-1,n), F (m-1,n),
+ * row-major (problems.py:97-104).  inversion_order 0 forward, 1 reversed
+ * (only changes which singular block is reported first). */
+int acr_factor(acr_plan_t* p, const double* D_sub, const double* D_diag,
+               const double* D_sup, const double* E, const double* F,
+               int inversion_order, void* stream);
+
+/* Solve phase: forward RHS sweep (reduction.py:204-216), cutoff solve
+ * (:305-310), back-substitution (:235-256).  rhs and u are (m*n, nrhs)
+ * row-major; u may alias rhs. */
+int acr_solve(acr_plan_t* p, const double* rhs, int nrhs, double* u,
+              void* stream);
+
+/* Report (SolveReport fields, reduction.py:124-153). */
+int acr_levels(const acr_plan_t* p);
+int acr_cutoff_blocks(const acr_plan_t* p);
+int acr_tree_depths(const acr_plan_t* p);
+/* per-level rank profile, level in [0, levels]; arrays of tree_depths */
+int acr_rank_profile(const acr_plan_t* p, int level, int* max_by_depth,
+                     double* mean_by_depth);
+/* reference-accounted storage bytes (hodlr.py:157-163, reduction.py:80-110)
+ * for an nrhs-column right-hand side */
+long long acr_storage_bytes(const acr_plan_t* p, int nrhs);
+long long acr_device_bytes(const acr_plan_t* p);
+double acr_factor_ms(const acr_plan_t* p);
+double acr_solve_ms(const acr_plan_t* p);
+long long acr_kernel_launches(const acr_plan_t* p);
+int acr_last_error(const acr_plan_t* p, char* buf, int len);
+/* error of the last plan-less call (acr_plan_create failures) */
+int acr_global_error(char* buf, int len);
+
+/* Dense export of one block for tests: which 0 = D, 1 = E, 2 = F of the
+ * level-`level` system (requires option 1 for level < levels), 3 = Dinv of
+ * even block `block` from the level's elimination record.  out: n x n
+ * row-major device buffer. */
+int acr_block_to_dense(acr_plan_t* p, int level, int which, int block,
+                       double* out, void* stream);
+
+/* ||A u - f||_2 per column and ||f||_2 per column straight from the bands
+ * (oracles.py:34-49); u, f (m*n, k) row-major; out_r, out_f host arrays[k]. */
+int acr_residual(int m, int n, int k, const double* D_sub, const double* D_diag,
+                 const double* D_sup, const double* E, const double* F,
+                 const double* u, const double* f, double* out_r,
+                 double* out_f, void* stream);
+
+/* Kernel-level entry points (parity tests against hodlr.py:176-200 and
+ * algebra.py:199-207 on captured operands).  U (m x R) and V (k x R) are
+ * column-major; Uo (m x R), Vo (k x R) receive the truncated factor. */
+int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
+                        double eps, int max_rank_cap, double* Uo, double* Vo,
+                        int* rank_out, void* stream);
+/* A: s x s row-major; X: inverse; *singular set to 1 on a zero pivot or a
+ * non-finite result. */
+int acr_leaf_inverse(int s, const double* A, double* X, int* singular,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,67 @@
+// Host-side launchers of the ACR kernels (internal; the public C ABI is
+// include/acr_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include "acr_types.cuh"
+
+namespace acr {
+
+long long trunc_need_doubles(int um, int vm, int R);
+cudaError_t launch_trunc(const TruncArgs& a, int nelem, size_t smem_bytes,
+                         cudaStream_t st);
+
+// leaf kernels (k_leaf.cu)
+cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
+                           int* sing, cudaStream_t st);
+cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
+                            const HB* C, int nelem, Src PX, RankRef xr,
+                            cudaStream_t st);
+cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
+                            int nleaf, Src U, Src V, RankRef rr, int node,
+                            int fside, cudaStream_t st);
+cudaError_t launch_leafadd(const TreeDev& T, const HB* A, const HB* B,
+                           const HB* C, double sb, int nelem, cudaStream_t st);
+cudaError_t launch_negate(const TreeDev& T, const HB* H, int nelem,
+                          cudaStream_t st);
+cudaError_t launch_copyhb(const TreeDev& T, const HB* S, const HB* D, int nelem,
+                          int* overflow, cudaStream_t st);
+cudaError_t launch_zerohb(const TreeDev& T, const HB* D, int nelem,
+                          cudaStream_t st);
+cudaError_t launch_lift(const TreeDev& T, const double* sub, const double* diag,
+                        const double* sup, const HB* D, int nelem,
+                        cudaStream_t st);
+cudaError_t launch_liftdiag(const TreeDev& T, const double* d, const HB* D,
+                            int nelem, cudaStream_t st);
+cudaError_t launch_build_tab(HB* tab, HB base, long long sl, long long sf,
+                             long long sr, int first, int step, int count,
+                             cudaStream_t st);
+
+// HODLR x panel (k_hmat.cu)
+cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
+                        int nelem, cudaStream_t st);
+cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
+                      const int* nodes, int nnodes, int nelem, int kcap,
+                      cudaStream_t st);
+cudaError_t launch_rhs_combine(const double* f, long long fs, const double* a,
+                               long long as, const double* b, long long bs,
+                               double* out, long long os, int count, int len,
+                               cudaStream_t st);
+
+// dense kernels (k_dense.cu)
+cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
+                           const int* rowblk, const int* colblk, double* A,
+                           int ld, cudaStream_t st);
+cudaError_t lu_factor(double* A, int N, int* piv, int* info, cudaStream_t st);
+cudaError_t lu_solve(const double* A, int N, const int* piv, double* B,
+                     int nrhs, cudaStream_t st);
+cudaError_t launch_rhs_in(const double* rhs, int N, int k, int n, double* P,
+                          cudaStream_t st);
+cudaError_t launch_u_out(const double* P, int N, int k, int n, double* u,
+                         cudaStream_t st);
+cudaError_t launch_residual(int m, int n, int k, const double* sub,
+                            const double* diag, const double* sup,
+                            const double* E, const double* F, const double* u,
+                            const double* f, double* partial, int nparts,
+                            cudaStream_t st);
+
+}  // namespace acr

@@ -1,0 +1,1460 @@
+// ACR engine: plan, level loop, batched invert / multiply / add schedules,
+// solve sweep, report, and the C ABI of include/acr_b200.h.
+//
+// Every HODLR operation of the reference (algebra.py) is executed for ALL
+// blocks of a level at once: the host walks the reference's recursion
+// structure once (it is identical for every block because one cluster tree
+// serves all blocks, reduction.py:159) and launches one batched kernel per
+// step; data-dependent branches (zero ranks, passthroughs, rank-1 shortcuts)
+// are decided per block on the device from device-resident ranks.  The
+// truncation schedule is the reference's.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "acr_launch.h"
+#include "acr_types.cuh"
+#include "../../include/acr_b200.h"
+
+namespace acr {
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+struct ArgError : std::runtime_error {
+  explicit ArgError(const std::string& s) : std::runtime_error(s) {}
+};
+struct SingularError : std::runtime_error {
+  explicit SingularError(const std::string& s) : std::runtime_error(s) {}
+};
+struct InternalError : std::runtime_error {
+  explicit InternalError(const std::string& s) : std::runtime_error(s) {}
+};
+
+#define CK(x)                                                              \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess)                                                 \
+      throw acr::CudaError(std::string(cudaGetErrorString(e_)) + " at " +       \
+                      __FILE__ + ":" + std::to_string(__LINE__));          \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// stream-ordered device memory
+// ---------------------------------------------------------------------------
+struct Dev {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaStream_t st = 0;
+  Dev() {}
+  Dev(size_t bytes, cudaStream_t s) { alloc(bytes, s); }
+  void alloc(size_t bytes, cudaStream_t s) {
+    release();
+    st = s;
+    n = bytes;
+    if (bytes) CK(cudaMallocAsync(&p, bytes, s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    n = 0;
+  }
+  ~Dev() { release(); }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+  Dev(Dev&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
+  Dev& operator=(Dev&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      st = o.st;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// ---------------------------------------------------------------------------
+// node table (mirrors paper_1604_00617_b200/tree.py, reference cluster.py)
+// ---------------------------------------------------------------------------
+struct HostTree {
+  int n = 0, leaf = 0, bw = 0, nd = 0, nnodes = 0, maxdepth = 0, nleaves = 0;
+  std::vector<int> lo, hi, mid, depth, parent, c0, c1, isleaf, anc, posA,
+      startA, listA, startB, listB, branches, iota;
+
+  bool in_subtree(int b, int mu) const {
+    int k = depth[b] - depth[mu];
+    return k >= 0 && anc[b * (maxdepth + 1) + k] == mu;
+  }
+
+  void build(int n_, int leaf_) {
+    n = n_;
+    leaf = leaf_;
+    lo = {0};
+    hi = {n};
+    depth = {0};
+    parent = {-1};
+    for (size_t i = 0; i < lo.size(); ++i) {
+      int a = lo[i], b = hi[i];
+      if (b - a <= leaf) {
+        c0.push_back(-1);
+        c1.push_back(-1);
+      } else {
+        int m = (a + b) / 2;
+        int c = (int)lo.size();
+        lo.push_back(a); hi.push_back(m);
+        lo.push_back(m); hi.push_back(b);
+        depth.push_back(depth[i] + 1); depth.push_back(depth[i] + 1);
+        parent.push_back((int)i); parent.push_back((int)i);
+        c0.push_back(c);
+        c1.push_back(c + 1);
+      }
+    }
+    nnodes = (int)lo.size();
+    mid.resize(nnodes);
+    isleaf.resize(nnodes);
+    bw = 0;
+    nd = 0;
+    maxdepth = 0;
+    nleaves = 0;
+    for (int v = 0; v < nnodes; ++v) {
+      mid[v] = (lo[v] + hi[v]) / 2;
+      isleaf[v] = c0[v] < 0;
+      maxdepth = std::max(maxdepth, depth[v]);
+      if (isleaf[v]) {
+        bw = std::max(bw, hi[v] - lo[v]);
+        ++nleaves;
+      } else {
+        nd = std::max(nd, depth[v] + 1);
+        branches.push_back(v);
+      }
+      iota.push_back(v);
+    }
+    const int D1 = maxdepth + 1;
+    anc.assign((size_t)nnodes * D1, -1);
+    for (int v = 0; v < nnodes; ++v) {
+      int a = v;
+      for (int t = 0; t <= depth[v]; ++t) {
+        anc[(size_t)v * D1 + t] = a;
+        a = parent[a];
+      }
+    }
+    posA.assign((size_t)nnodes * nnodes, -1);
+    startA.assign(nnodes + 1, 0);
+    startB.assign(nnodes + 1, 0);
+    listA.clear();
+    listB.clear();
+    for (int mu = 0; mu < nnodes; ++mu) {
+      startA[mu] = (int)listA.size() / 3;
+      int cnt = 0;
+      for (int b = 0; b < nnodes; ++b) {
+        if (isleaf[b] || !in_subtree(b, mu)) continue;
+        posA[(size_t)mu * nnodes + b] = cnt++;
+        for (int s = 0; s < 2; ++s) {
+          listA.push_back(mu);
+          listA.push_back(b);
+          listA.push_back(s);
+        }
+      }
+      startB[mu] = (int)listB.size() / 2;
+      std::vector<int> lv;
+      for (int b = 0; b < nnodes; ++b)
+        if (isleaf[b] && in_subtree(b, mu)) lv.push_back(b);
+      std::sort(lv.begin(), lv.end(), [&](int x, int y) { return lo[x] < lo[y]; });
+      for (int b : lv) {
+        listB.push_back(mu);
+        listB.push_back(b);
+      }
+    }
+    startA[nnodes] = (int)listA.size() / 3;
+    startB[nnodes] = (int)listB.size() / 2;
+  }
+
+  int nleaves_under(int mu) const { return startB[mu + 1] - startB[mu]; }
+  int nA(int mu0, int mu1) const { return startA[mu1] - startA[mu0]; }
+};
+
+struct DeviceTree {
+  Dev buf;
+  TreeDev T;
+  const int* d_listA = nullptr;
+  const int* d_branches = nullptr;
+  const int* d_iota = nullptr;
+
+  void upload(const HostTree& h, cudaStream_t st) {
+    std::vector<const std::vector<int>*> parts = {
+        &h.lo, &h.hi, &h.mid, &h.depth, &h.parent, &h.c0, &h.c1, &h.isleaf,
+        &h.anc, &h.posA, &h.startA, &h.listA, &h.startB, &h.listB,
+        &h.branches, &h.iota};
+    size_t tot = 0;
+    for (auto* p : parts) tot += p->size() + 1;
+    std::vector<int> host(tot, 0);
+    std::vector<size_t> off;
+    size_t o = 0;
+    for (auto* p : parts) {
+      off.push_back(o);
+      std::copy(p->begin(), p->end(), host.begin() + o);
+      o += p->size() + 1;
+    }
+    buf.alloc(tot * sizeof(int), st);
+    CK(cudaMemcpyAsync(buf.p, host.data(), tot * sizeof(int),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    const int* b = buf.as<int>();
+    T.n = h.n;
+    T.bw = h.bw;
+    T.nd = h.nd;
+    T.nnodes = h.nnodes;
+    T.maxdepth = h.maxdepth;
+    T.nleaves = h.nleaves;
+    T.lo = b + off[0];
+    T.hi = b + off[1];
+    T.mid = b + off[2];
+    T.depth = b + off[3];
+    T.parent = b + off[4];
+    T.c0 = b + off[5];
+    T.c1 = b + off[6];
+    T.isleaf = b + off[7];
+    T.anc = b + off[8];
+    T.posA = b + off[9];
+    T.startA = b + off[10];
+    T.listA = b + off[11];
+    T.startB = b + off[12];
+    T.listB = b + off[13];
+    d_listA = T.listA;
+    d_branches = b + off[14];
+    d_iota = b + off[15];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// a contiguous set of HODLR blocks with one column capacity
+// ---------------------------------------------------------------------------
+struct Batch {
+  int cnt = 0, R = 0;
+  Dev leaf, U, V, rk;
+  long long sl = 0, sf = 0, sr = 0;
+  void alloc(const HostTree& t, int cnt_, int R_, cudaStream_t st) {
+    cnt = cnt_;
+    R = std::max(R_, 1);
+    sl = (long long)t.n * t.bw;
+    sf = (long long)std::max(t.nd, 1) * R * t.n;
+    sr = 2LL * t.nnodes;
+    leaf.alloc(sizeof(double) * sl * std::max(cnt, 1), st);
+    U.alloc(sizeof(double) * sf * std::max(cnt, 1), st);
+    V.alloc(sizeof(double) * sf * std::max(cnt, 1), st);
+    rk.alloc(sizeof(int) * sr * std::max(cnt, 1), st);
+  }
+  HB base() const {
+    HB h;
+    h.leaf = leaf.as<double>();
+    h.U = U.as<double>();
+    h.V = V.as<double>();
+    h.rk = rk.as<int>();
+    h.R = R;
+    h.pad_ = 0;
+    return h;
+  }
+  long long bytes() const {
+    return (long long)(leaf.n + U.n + V.n + rk.n);
+  }
+};
+
+struct Seg {
+  const Batch* b;
+  int first, step, count;
+};
+
+struct Level {
+  int m = 0;
+  int R = 1;
+  Batch D, E, F;   // E element 0 and F element m-1 unused (rank 0)
+};
+
+struct Record {
+  int m = 0;
+  Batch Dinv, E, F;
+  std::vector<int> hDinv, hE, hF;   // host ranks (storage accounting)
+};
+
+struct Profile {
+  std::vector<int> mx;
+  std::vector<double> mean;
+};
+
+static Src s_pan(double* p, long long s, int C) {
+  Src x;
+  memset(&x, 0, sizeof(x));
+  x.kind = 0;
+  x.p = p;
+  x.s = s;
+  x.C = C;
+  return x;
+}
+static Src s_hbU(const HB* t) {
+  Src x;
+  memset(&x, 0, sizeof(x));
+  x.kind = 2;
+  x.hb = t;
+  return x;
+}
+static Src s_hbV(const HB* t) {
+  Src x = s_hbU(t);
+  x.kind = 3;
+  return x;
+}
+static RankRef r_hb(const HB* t) {
+  RankRef r;
+  r.hb = t;
+  r.arr = nullptr;
+  r.s = 0;
+  return r;
+}
+static RankRef r_arr(const int* a, long long s) {
+  RankRef r;
+  r.hb = nullptr;
+  r.arr = a;
+  r.s = s;
+  return r;
+}
+static TOp op_own(Src U, Src V, RankRef r, double sc = 1.0) {
+  TOp o;
+  memset(&o, 0, sizeof(o));
+  o.U = U;
+  o.V = V;
+  o.rank = r;
+  o.sel = SEL_OWN;
+  o.scale = sc;
+  return o;
+}
+
+static const long long SMEM_MAX_BYTES = 196 * 1024;
+static const long long GSCR_BUDGET_BYTES = 2LL << 30;
+
+// ---------------------------------------------------------------------------
+// the plan
+// ---------------------------------------------------------------------------
+struct Plan {
+  int m, n, leaf, cutoff, cap;
+  double eps;
+  bool keep_levels = false;
+  HostTree ht;
+  DeviceTree dt;
+  cudaStream_t st = 0;
+  std::vector<Record> recs;
+  std::vector<Level> kept;
+  Level last;
+  Dev lu, piv, info;
+  int Nc = 0;
+  std::vector<Profile> prof;
+  std::vector<std::vector<int>> lastR;   // host ranks of the final level D, E, F
+  double fms = 0, sms = 0;
+  long long launches = 0;
+  bool factored = false;
+  std::string err;
+  // scratch pool
+  std::vector<Dev> scr;
+  Dev ovf, sing;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  Plan(int m_, int n_, int leaf_, double eps_, int cap_, int cutoff_)
+      : m(m_), n(n_), leaf(leaf_), cutoff(cutoff_), cap(cap_), eps(eps_) {
+    ht.build(n, leaf);
+    scr.resize(32);
+  }
+  ~Plan() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+
+  template <class T> T* scratch(int slot, size_t count) {
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (scr[slot].n < bytes) scr[slot].alloc(bytes + bytes / 4, st);
+    return scr[slot].as<T>();
+  }
+
+  Dev make_tab(std::initializer_list<Seg> segs) {
+    int tot = 0;
+    for (auto& s : segs) tot += std::max(s.count, 0);
+    Dev t(sizeof(HB) * std::max(tot, 1), st);
+    int o = 0;
+    for (auto& s : segs) {
+      if (s.count <= 0) continue;
+      CK(launch_build_tab(t.as<HB>() + o, s.b->base(), s.b->sl, s.b->sf, s.b->sr,
+                          s.first, s.step, s.count, st));
+      ++launches;
+      o += s.count;
+    }
+    return t;
+  }
+
+  // ---- truncation launcher: split by depth, size smem / global scratch ----
+  void run_trunc(TruncArgs a, int t0, int t1, const HB* out, int nelem, int Ra,
+                 int Rb) {
+    if (t1 <= t0 || nelem <= 0) return;
+    a.T = dt.T;
+    a.out = out;
+    a.eps = eps;
+    a.cap = cap;
+    a.overflow = ovf.as<int>();
+    const int Rw = (a.mode == TM_TRUNCATE) ? Ra : Ra + Rb;
+    int i = t0;
+    while (i < t1) {
+      int b = ht.listA[i * 3 + 1];
+      int d = ht.depth[b];
+      int j = i;
+      long long worst = 0;
+      while (j < t1 && ht.depth[ht.listA[j * 3 + 1]] == d) {
+        int bb = ht.listA[j * 3 + 1];
+        int um = ht.mid[bb] - ht.lo[bb], vm = ht.hi[bb] - ht.mid[bb];
+        worst = std::max(worst, trunc_need_doubles(std::max(um, vm), std::max(um, vm), Rw));
+        ++j;
+      }
+      TruncArgs A = a;
+      A.tasks = dt.d_listA + 3 * i;
+      A.ntasks = j - i;
+      long long wb = worst * 8 + 64;
+      if (wb <= SMEM_MAX_BYTES) {
+        A.smem_doubles = (int)worst;
+        A.gscr = nullptr;
+        A.gscr_ntasks = 0;
+        A.gscr_stride = 0;
+        CK(launch_trunc(A, nelem, (size_t)wb, st));
+        ++launches;
+      } else {
+        // global work areas; chunk elements to bound the scratch
+        long long per_elem = worst * (long long)A.ntasks * 8;
+        int chunk = (int)std::max<long long>(1, GSCR_BUDGET_BYTES / per_elem);
+        chunk = std::min(chunk, nelem);
+        double* g = scratch<double>(10, (size_t)worst * A.ntasks * chunk);
+        A.gscr = g;
+        A.gscr_stride = worst;
+        A.gscr_ntasks = A.ntasks;
+        A.smem_doubles = (int)(48 * 1024 / 8);
+        for (int e0 = 0; e0 < nelem; e0 += chunk) {
+          int ce = std::min(chunk, nelem - e0);
+          TruncArgs B = A;
+          B.out = out + e0;
+          offset_op(B.a, e0);
+          offset_op(B.b, e0);
+          CK(launch_trunc(B, ce, 48 * 1024, st));
+          ++launches;
+        }
+      }
+      i = j;
+    }
+  }
+
+  static void offset_src(Src& s, int e0) {
+    if (s.kind == 0) s.p = s.p ? s.p + e0 * s.s : nullptr;
+    else if (s.kind == 1) s.tab = s.tab ? s.tab + e0 : nullptr;
+    else s.hb = s.hb ? s.hb + e0 : nullptr;
+  }
+  static void offset_rank(RankRef& r, int e0) {
+    if (r.hb) r.hb += e0;
+    else if (r.arr) r.arr += e0 * r.s;
+  }
+  static void offset_op(TOp& o, int e0) {
+    offset_src(o.U, e0);
+    offset_src(o.V, e0);
+    offset_rank(o.rank, e0);
+  }
+
+  // ---- multiply: C = A B for G elements (reference algebra.py:159-185) ----
+  void multiply(const HB* A, const HB* B, const HB* C, int G, int RA, int RB,
+                int RC) {
+    if (G <= 0) return;
+    const int nd = std::max(ht.nd, 1), nn = ht.nnodes;
+    const int nA1 = ht.nA(1, nn);
+    long long per = (long long)nd * n * (2LL * RB + RA) * 8 + 2LL * nA1 * RA * RB * 8 +
+                    (long long)nn * 8;
+    int chunk = (int)std::max<long long>(1, (4LL << 30) / std::max<long long>(per, 1));
+    for (int g0 = 0; g0 < G; g0 += chunk) {
+      int cg = std::min(chunk, G - g0);
+      multiply_chunk(A + g0, B + g0, C + g0, cg, RA, RB, RC);
+    }
+  }
+
+  void multiply_chunk(const HB* A, const HB* B, const HB* C, int G, int RA,
+                      int RB, int RC) {
+    const int nd = std::max(ht.nd, 1), nn = ht.nnodes;
+    const long long ps = (long long)nd * n;
+    double* PX = scratch<double>(0, (size_t)G * ps * RB);
+    double* Yp = scratch<double>(1, (size_t)G * ps * RB);
+    double* Zp = scratch<double>(2, (size_t)G * ps * RA);
+    int* cr = scratch<int>(3, (size_t)G * nn * 2);
+    const int nA1 = ht.nA(1, nn);
+    double* tbY = scratch<double>(4, (size_t)G * std::max(nA1, 1) * RA * RB);
+    double* tbZ = scratch<double>(5, (size_t)G * std::max(nA1, 1) * RA * RB);
+    CK(cudaMemsetAsync(cr, 0, sizeof(int) * G * nn * 2, st));
+    // cross terms X11 = (U_A12 (V_A12^T U_B21), V_B21), X22 likewise
+    if (!ht.branches.empty()) {
+      GPJob j[2];
+      memset(j, 0, sizeof(j));
+      for (int s = 0; s < 2; ++s) {
+        j[s].X = s_hbV(A);
+        j[s].Y = s_hbU(B);
+        j[s].W = s_hbU(A);
+        j[s].Z = s_pan(PX, ps * RB, RB);
+        j[s].rx = r_hb(A);
+        j[s].ry = r_hb(B);
+        j[s].orank = cr;
+        j[s].ors = nn * 2;
+        j[s].oside = s;
+        j[s].alpha = 1.0;
+      }
+      j[0].hx = 1; j[0].hw = 0; j[0].sx = 0; j[0].sy = 1;
+      j[1].hx = 0; j[1].hw = 1; j[1].sx = 1; j[1].sy = 0;
+      CK(launch_gp(dt.T, j, 2, dt.d_branches, (int)ht.branches.size(), G,
+                   RA * RB, st));
+      ++launches;
+    }
+    CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), st));
+    ++launches;
+    if (ht.branches.empty()) return;
+    MMJob J[2];
+    memset(J, 0, sizeof(J));
+    J[0].H = A;
+    J[0].X = s_hbU(B);
+    J[0].Y = s_pan(Yp, ps * RB, RB);
+    J[0].trans = 0;
+    J[0].cols = r_hb(B);
+    J[0].cols_fixed = -1;
+    J[0].swap = 0;
+    J[0].tbuf = tbY;
+    J[0].RT = RA;
+    J[0].CT = RB;
+    J[1].H = B;
+    J[1].X = s_hbV(A);
+    J[1].Y = s_pan(Zp, ps * RA, RA);
+    J[1].trans = 1;
+    J[1].cols = r_hb(A);
+    J[1].cols_fixed = -1;
+    J[1].swap = 1;
+    J[1].tbuf = tbZ;
+    J[1].RT = RB;
+    J[1].CT = RA;
+    for (auto& j : J) {
+      j.alpha = 1.0;
+      j.mu0 = 1;
+      j.mu1 = nn;
+      j.nA = nA1;
+    }
+    CK(launch_hmat(dt.T, J, 2, G, st));
+    launches += 2;
+    // M2: off12 = combine(f1, f2), off21 = combine(g1, g2)
+    TruncArgs a;
+    memset(&a, 0, sizeof(a));
+    a.mode = TM_COMBINE_SWAP1;
+    a.a = op_own(s_pan(Yp, ps * RB, RB), s_hbV(B), r_hb(B));
+    a.b = op_own(s_hbU(A), s_pan(Zp, ps * RA, RA), r_hb(A));
+    run_trunc(a, ht.startA[0], ht.startA[1], C, G, RB, RA);
+    // M3: ancestors' cross terms, parent first, root last
+    for (int t = 1; t < ht.nd; ++t) {
+      int s0 = ht.startA[0];
+      while (s0 < ht.startA[1] && ht.depth[ht.listA[s0 * 3 + 1]] < t) ++s0;
+      if (s0 >= ht.startA[1]) break;
+      TruncArgs b;
+      memset(&b, 0, sizeof(b));
+      b.mode = TM_COMBINE;
+      b.a = op_own(s_hbU(C), s_hbV(C), r_hb(C));
+      b.b = op_own(s_pan(PX, ps * RB, RB), s_hbV(B), r_arr(cr, nn * 2));
+      b.b.sel = SEL_ANC;
+      b.b.t = t;
+      run_trunc(b, s0, ht.startA[1], C, G, RC, RB);
+    }
+  }
+
+  // ---- add: C = A + sb*B (reference algebra.py:100-112) ----
+  void add(const HB* A, const HB* B, const HB* C, int G, double sb, int RA,
+           int RB) {
+    if (G <= 0) return;
+    CK(launch_leafadd(dt.T, A, B, C, sb, G, st));
+    ++launches;
+    if (ht.branches.empty()) return;
+    TruncArgs a;
+    memset(&a, 0, sizeof(a));
+    a.mode = TM_COMBINE;
+    a.a = op_own(s_hbU(A), s_hbV(A), r_hb(A));
+    a.b = op_own(s_hbU(B), s_hbV(B), r_hb(B), sb);
+    run_trunc(a, ht.startA[0], ht.startA[1], C, G, RA, RB);
+  }
+
+  // ---- invert in place (reference algebra.py:192-240) ----
+  struct InvCtx {
+    const HB* H;
+    int G, R;
+    double *P1, *P2, *P3, *tb;
+    long long ps;
+    int* sing;
+  };
+
+  void invert(const HB* H, int G, int R, int* sing) {
+    if (G <= 0) return;
+    InvCtx c;
+    c.H = H;
+    c.G = G;
+    c.R = R;
+    c.ps = (long long)std::max(ht.nd, 1) * n;
+    c.P1 = scratch<double>(6, (size_t)G * c.ps * R);
+    c.P2 = scratch<double>(7, (size_t)G * c.ps * R);
+    c.P3 = scratch<double>(8, (size_t)G * c.ps * R);
+    int maxA = 1;
+    for (int v = 0; v < ht.nnodes; ++v) maxA = std::max(maxA, ht.nA(v, v + 1));
+    c.tb = scratch<double>(9, (size_t)G * maxA * R * R);
+    c.sing = sing;
+    inv_node(c, 0);
+  }
+
+  void inv_hmat(InvCtx& c, int mu, bool second) {
+    // first pass (mu = c0): T = x11 U12 -> P1, Hh = x11^T V21 -> P2
+    // second pass (mu = c1): Z = sinv U21 -> P1, S2 = sinv^T V12 -> P2
+    MMJob J[2];
+    memset(J, 0, sizeof(J));
+    for (int k = 0; k < 2; ++k) {
+      J[k].H = c.H;
+      J[k].cols = r_hb(c.H);
+      J[k].cols_fixed = -1;
+      J[k].alpha = 1.0;
+      J[k].mu0 = mu;
+      J[k].mu1 = mu + 1;
+      J[k].tbuf = c.tb + (size_t)k * 0;
+      J[k].RT = c.R;
+      J[k].CT = c.R;
+      J[k].nA = ht.nA(mu, mu + 1);
+    }
+    (void)second;
+    J[0].X = s_hbU(c.H);
+    J[0].Y = s_pan(c.P1, c.ps * c.R, c.R);
+    J[0].trans = 0;
+    J[0].swap = 0;
+    J[1].X = s_hbV(c.H);
+    J[1].Y = s_pan(c.P2, c.ps * c.R, c.R);
+    J[1].trans = 1;
+    J[1].swap = 1;
+    // the two jobs need distinct t-buffers
+    double* tb2 = scratch<double>(11, (size_t)c.G * std::max(J[0].nA, 1) * c.R * c.R);
+    J[1].tbuf = tb2;
+    CK(launch_hmat(dt.T, J, 2, c.G, st));
+    launches += 2;
+  }
+
+  void inv_lowrank(InvCtx& c, int nu, int mu, Src U, Src V, int fside) {
+    // add_lowrank(H_mu, (U, V)) with rank (nu, fside) if (nu, 1-fside) != 0
+    int t0 = ht.startA[mu], t1 = ht.startA[mu + 1];
+    if (t1 > t0) {
+      TruncArgs a;
+      memset(&a, 0, sizeof(a));
+      a.mode = TM_COMBINE;
+      a.a = op_own(s_hbU(c.H), s_hbV(c.H), r_hb(c.H));
+      a.b = op_own(U, V, r_hb(c.H));
+      a.b.sel = SEL_FIXED;
+      a.b.node = nu;
+      a.b.fside = fside;
+      run_trunc(a, t0, t1, c.H, c.G, c.R, c.R);
+    }
+    CK(launch_leaflr_n(dt.T, c.H, c.G, mu, ht.nleaves_under(mu), U, V, r_hb(c.H),
+                       nu, fside, st));
+    ++launches;
+  }
+
+  void inv_node(InvCtx& c, int nu) {
+    if (ht.isleaf[nu]) {
+      CK(launch_leafinv(dt.T, c.H, c.G, nu, c.sing, st));
+      ++launches;
+      return;
+    }
+    const int a0 = ht.c0[nu], a1 = ht.c1[nu];
+    const Src P1 = s_pan(c.P1, c.ps * c.R, c.R);
+    const Src P2 = s_pan(c.P2, c.ps * c.R, c.R);
+    const Src P3 = s_pan(c.P3, c.ps * c.R, c.R);
+    inv_node(c, a0);                                   // x11
+    inv_hmat(c, a0, false);                            // T, Hh
+    {
+      GPJob j;                                          // W = -U21 (V21^T T)
+      memset(&j, 0, sizeof(j));
+      j.X = s_hbV(c.H); j.hx = 0; j.rx = r_hb(c.H); j.sx = 1;
+      j.Y = P1; j.ry = r_hb(c.H); j.sy = 0;
+      j.W = s_hbU(c.H); j.hw = 1;
+      j.Z = P3;
+      j.alpha = -1.0;
+      CK(launch_gp(dt.T, &j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st));
+      ++launches;
+    }
+    inv_lowrank(c, nu, a1, P3, s_hbV(c.H), 0);         // S = H22 + W V12^T
+    inv_node(c, a1);                                   // sinv
+    inv_hmat(c, a1, true);                             // Z, S2
+    {
+      GPJob j;                                          // G = T (V12^T Z)
+      memset(&j, 0, sizeof(j));
+      j.X = s_hbV(c.H); j.hx = 1; j.rx = r_hb(c.H); j.sx = 0;
+      j.Y = P1; j.ry = r_hb(c.H); j.sy = 1;
+      j.W = P1; j.hw = 0;
+      j.Z = P3;
+      j.alpha = 1.0;
+      CK(launch_gp(dt.T, &j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st));
+      ++launches;
+    }
+    inv_lowrank(c, nu, a0, P3, P2, 1);                 // b11 = x11 + G Hh^T
+    TruncArgs a;                                       // b12, b21
+    memset(&a, 0, sizeof(a));
+    a.mode = TM_TRUNCATE;
+    a.a = op_own(P1, P2, r_hb(c.H), -1.0);
+    run_trunc(a, ht.startA[nu], ht.startA[nu] + 2, c.H, c.G, c.R, 0);
+  }
+
+  // ---- helpers for reports ----
+  void fetch_ranks(const Batch& b, std::vector<int>& out) {
+    out.resize((size_t)b.cnt * ht.nnodes * 2);
+    if (b.cnt)
+      CK(cudaMemcpyAsync(out.data(), b.rk.p, out.size() * sizeof(int),
+                         cudaMemcpyDeviceToHost, st));
+  }
+
+  long long hb_bytes(const int* rk) const {
+    long long s = 0;
+    for (int v = 0; v < ht.nnodes; ++v) {
+      int sz = ht.hi[v] - ht.lo[v];
+      if (ht.isleaf[v]) s += (long long)sz * sz;
+      else s += (long long)sz * (rk[v * 2] + rk[v * 2 + 1]);
+    }
+    return 8 * s;
+  }
+
+  int max_rank_of(const std::vector<int>& r) const {
+    int mx = 0;
+    for (int x : r) mx = std::max(mx, x);
+    return mx;
+  }
+
+  void profile_level(int mm, const std::vector<int>& dR, const std::vector<int>& eR,
+                     const std::vector<int>& fR) {
+    Profile p;
+    int nd = ht.nd;
+    p.mx.assign(nd, 0);
+    std::vector<long long> sum(nd, 0), cnt(nd, 0);
+    auto acc = [&](const std::vector<int>& r, int blk) {
+      const int* rk = r.data() + (size_t)blk * ht.nnodes * 2;
+      for (int v : ht.branches) {
+        int d = ht.depth[v];
+        for (int s = 0; s < 2; ++s) {
+          p.mx[d] = std::max(p.mx[d], rk[v * 2 + s]);
+          sum[d] += rk[v * 2 + s];
+          cnt[d] += 1;
+        }
+      }
+    };
+    for (int i = 0; i < mm; ++i) acc(dR, i);
+    for (int i = 1; i < mm; ++i) acc(eR, i);
+    for (int i = 0; i + 1 < mm; ++i) acc(fR, i);
+    p.mean.assign(nd, 0.0);
+    for (int d = 0; d < nd; ++d) p.mean[d] = cnt[d] ? (double)sum[d] / (double)cnt[d] : 0.0;
+    prof.push_back(p);
+  }
+
+  // ---- one reduction level (reference reduction.py:173-232) ----
+  bool reduce(Level& L, int Rout, int lvl, int order, Level& nx, Record& rec,
+              int& need) {
+    const int mm = L.m, ne = (mm + 1) / 2, no = mm / 2;
+    int nq = 0, nf = 0;
+    for (int j = 1; j < mm; j += 2) {
+      if (j + 1 <= mm - 1) ++nq;
+      if (j + 2 <= mm - 1) ++nf;
+    }
+    CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
+    int* sg = sing.as<int>();
+    {
+      std::vector<int> init(std::max(ne, 1), INT_MAX);
+      CK(cudaMemcpyAsync(sg, init.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    // 1. Dinv of the even blocks
+    rec.m = mm;
+    rec.Dinv.alloc(ht, ne, Rout, st);
+    {
+      Dev tDe = make_tab({{&L.D, 0, 2, ne}});
+      Dev tDi = make_tab({{&rec.Dinv, 0, 1, ne}});
+      CK(launch_copyhb(dt.T, tDe.as<HB>(), tDi.as<HB>(), ne, ovf.as<int>(), st));
+      ++launches;
+      invert(tDi.as<HB>(), ne, rec.Dinv.R, sg);
+    }
+    // 2. P_j = E_j Dinv_{j-1}, Q_j = F_j Dinv_{j+1}
+    Batch PQ;
+    PQ.alloc(ht, no + nq, Rout, st);
+    {
+      Dev tA = make_tab({{&L.E, 1, 2, no}, {&L.F, 1, 2, nq}});
+      Dev tB = make_tab({{&rec.Dinv, 0, 1, no}, {&rec.Dinv, 1, 1, nq}});
+      Dev tC = make_tab({{&PQ, 0, 1, no + nq}});
+      multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), no + nq, L.R, rec.Dinv.R, PQ.R);
+    }
+    // 3. X = P F_{j-1}, Y = Q E_{j+1}, E' = -P E_{j-1}, F' = -Q F_{j+1}
+    nx.m = no;
+    nx.R = Rout;
+    nx.D.alloc(ht, no, Rout, st);
+    nx.E.alloc(ht, no, Rout, st);
+    nx.F.alloc(ht, no, Rout, st);
+    Batch XY;
+    XY.alloc(ht, no + nq, Rout, st);
+    {
+      Dev tA = make_tab({{&PQ, 0, 1, no}, {&PQ, no, 1, nq}, {&PQ, 1, 1, no - 1},
+                         {&PQ, no, 1, nf}});
+      Dev tB = make_tab({{&L.F, 0, 2, no}, {&L.E, 2, 2, nq}, {&L.E, 2, 2, no - 1},
+                         {&L.F, 2, 2, nf}});
+      Dev tC = make_tab({{&XY, 0, 1, no + nq}, {&nx.E, 1, 1, no - 1}, {&nx.F, 0, 1, nf}});
+      int G = no + nq + std::max(no - 1, 0) + nf;
+      multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), G, PQ.R, L.R, Rout);
+      Dev tE = make_tab({{&nx.E, 1, 1, no - 1}, {&nx.F, 0, 1, nf}});
+      CK(launch_negate(dt.T, tE.as<HB>(), std::max(no - 1, 0) + nf, st));
+      ++launches;
+      Dev tZ = make_tab({{&nx.E, 0, 1, no > 0 ? 1 : 0}, {&nx.F, nf, 1, no - nf}});
+      CK(launch_zerohb(dt.T, tZ.as<HB>(), (no > 0 ? 1 : 0) + std::max(no - nf, 0), st));
+      ++launches;
+    }
+    // 4. D' = add(add(D_j, -X), -Y)
+    {
+      Dev tA = make_tab({{&L.D, 1, 2, no}});
+      Dev tB = make_tab({{&XY, 0, 1, no}});
+      Dev tC = make_tab({{&nx.D, 0, 1, no}});
+      add(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), no, -1.0, L.R, XY.R);
+      Dev tB2 = make_tab({{&XY, no, 1, nq}});
+      add(tC.as<HB>(), tB2.as<HB>(), tC.as<HB>(), nq, -1.0, nx.R, XY.R);
+    }
+    // overflow / singular checks (one sync per level)
+    int h_ovf = 0;
+    std::vector<int> hs(std::max(ne, 1));
+    CK(cudaMemcpyAsync(&h_ovf, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs.data(), sg, sizeof(int) * ne, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    // singular leaves: report the first block in inversion order
+    int bad = -1;
+    for (int k = 0; k < ne; ++k) {
+      int e = order ? ne - 1 - k : k;
+      if (hs[e] != INT_MAX) { bad = e; break; }
+    }
+    if (bad >= 0) {
+      int pos = hs[bad];
+      std::vector<int> lv;
+      for (int v = 0; v < ht.nnodes; ++v)
+        if (ht.isleaf[v]) lv.push_back(v);
+      std::sort(lv.begin(), lv.end(), [&](int x, int y) { return ht.lo[x] < ht.lo[y]; });
+      int v = lv[pos];
+      char buf[256];
+      snprintf(buf, sizeof(buf),
+               "singular dense leaf on index range [%d,%d): level %d, pivot block %d",
+               ht.lo[v], ht.hi[v], lvl, 2 * bad);
+      throw SingularError(buf);
+    }
+    if (h_ovf) {
+      if (h_ovf >= (1 << 29)) throw InternalError("truncation work area too small");
+      need = h_ovf;
+      return false;
+    }
+    // keep the level's couplings for the solve sweep
+    rec.E = std::move(L.E);
+    rec.F = std::move(L.F);
+    return true;
+  }
+
+  // ---- factor ----
+  void factor(const double* sub, const double* diag, const double* sup,
+              const double* E, const double* F, int order) {
+    recs.clear();
+    kept.clear();
+    prof.clear();
+    launches = 0;
+    factored = false;
+    if (!ovf.p) ovf.alloc(sizeof(int), st);
+    sing.alloc(sizeof(int) * std::max(m, 1), st);
+    if (!ev0) {
+      CK(cudaEventCreate(&ev0));
+      CK(cudaEventCreate(&ev1));
+    }
+    CK(cudaEventRecord(ev0, st));
+    Level L;
+    L.m = m;
+    L.R = 1;
+    L.D.alloc(ht, m, 1, st);
+    L.E.alloc(ht, m, 1, st);
+    L.F.alloc(ht, m, 1, st);
+    {
+      Dev tD = make_tab({{&L.D, 0, 1, m}});
+      CK(launch_lift(dt.T, sub, diag, sup, tD.as<HB>(), m, st));
+      Dev tE = make_tab({{&L.E, 1, 1, m - 1}});
+      CK(launch_liftdiag(dt.T, E, tE.as<HB>(), m - 1, st));
+      Dev tF = make_tab({{&L.F, 0, 1, m - 1}});
+      CK(launch_liftdiag(dt.T, F, tF.as<HB>(), m - 1, st));
+      Dev tZ = make_tab({{&L.E, 0, 1, 1}, {&L.F, m - 1, 1, 1}});
+      CK(launch_zerohb(dt.T, tZ.as<HB>(), 2, st));
+      launches += 4;
+    }
+    std::vector<int> dR, eR, fR;
+    fetch_ranks(L.D, dR);
+    fetch_ranks(L.E, eR);
+    fetch_ranks(L.F, fR);
+    CK(cudaStreamSynchronize(st));
+    profile_level(L.m, dR, eR, fR);
+    int maxr = std::max(max_rank_of(dR), 1);
+    int lvl = 0;
+    while (L.m > cutoff) {
+      int Rout = std::max(4, (3 * maxr + 1) / 2 + 4);
+      if (cap > 0) Rout = std::min(Rout, std::max(cap, 1) + 0);
+      Rout = std::max(Rout, L.R);
+      Record rec;
+      Level nx;
+      int need = 0;
+      int tries = 0;
+      while (!reduce(L, Rout, lvl, order, nx, rec, need)) {
+        Rout = std::max(need, 2 * Rout);
+        rec = Record();
+        nx = Level();
+        if (++tries > 8) throw InternalError("rank capacity retries exhausted");
+      }
+      fetch_ranks(rec.Dinv, rec.hDinv);
+      fetch_ranks(rec.E, rec.hE);
+      fetch_ranks(rec.F, rec.hF);
+      fetch_ranks(nx.D, dR);
+      fetch_ranks(nx.E, eR);
+      fetch_ranks(nx.F, fR);
+      CK(cudaStreamSynchronize(st));
+      profile_level(nx.m, dR, eR, fR);
+      maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
+      if (keep_levels) kept.push_back(std::move(L));
+      recs.push_back(std::move(rec));
+      L = std::move(nx);
+      ++lvl;
+    }
+    lastR = {dR, eR, fR};
+    // cutoff: dense LU of the remaining system
+    const int mc = L.m;
+    Nc = mc * n;
+    lu.alloc(sizeof(double) * (size_t)Nc * Nc, st);
+    piv.alloc(sizeof(int) * Nc, st);
+    if (!info.p) info.alloc(sizeof(int), st);
+    {
+      std::vector<int> rb, cb;
+      int cntb = 0;
+      for (int i = 0; i < mc; ++i) { rb.push_back(i); cb.push_back(i); ++cntb; }
+      for (int i = 1; i < mc; ++i) { rb.push_back(i); cb.push_back(i - 1); ++cntb; }
+      for (int i = 0; i + 1 < mc; ++i) { rb.push_back(i); cb.push_back(i + 1); ++cntb; }
+      Dev tab = make_tab({{&L.D, 0, 1, mc}, {&L.E, 1, 1, mc - 1}, {&L.F, 0, 1, mc - 1}});
+      Dev drc(sizeof(int) * 2 * cntb, st);
+      std::vector<int> h(rb);
+      h.insert(h.end(), cb.begin(), cb.end());
+      CK(cudaMemcpyAsync(drc.p, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(lu.p, 0, sizeof(double) * (size_t)Nc * Nc, st));
+      CK(launch_todense(dt.T, tab.as<HB>(), cntb, drc.as<int>(), drc.as<int>() + cntb,
+                        lu.as<double>(), Nc, st));
+      CK(lu_factor(lu.as<double>(), Nc, piv.as<int>(), info.as<int>(), st));
+      launches += 1 + 3 * ((Nc + 31) / 32);
+      int hinfo = 0;
+      CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(ev1, st));
+      CK(cudaStreamSynchronize(st));
+      if (hinfo) throw SingularError("matrix is singular to working precision");
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    fms = ms;
+    last = std::move(L);
+    factored = true;
+  }
+
+  // ---- solve (reference reduction.py:204-216, 305-311, 235-256) ----
+  void hmat_full(const HB* H, int G, int R, Src X, Src Y, int k) {
+    if (G <= 0) return;
+    MMJob J;
+    memset(&J, 0, sizeof(J));
+    J.H = H;
+    J.X = X;
+    J.Y = Y;
+    J.trans = 0;
+    J.cols_fixed = k;
+    J.alpha = 1.0;
+    J.mu0 = 0;
+    J.mu1 = 1;
+    J.nA = ht.nA(0, 1);
+    J.RT = R;
+    J.CT = k;
+    J.tbuf = scratch<double>(12, (size_t)G * std::max(J.nA, 1) * R * k);
+    CK(launch_hmat(dt.T, &J, 1, G, st));
+    launches += 2;
+  }
+
+  void solve(const double* rhs, int k, double* u) {
+    if (!factored) throw ArgError("acr_solve called before a successful acr_factor");
+    CK(cudaEventRecord(ev0, st));
+    const long long kn = (long long)k * n;
+    const int L = (int)recs.size();
+    std::vector<Dev> f(L + 1);
+    f[0].alloc(sizeof(double) * kn * m, st);
+    CK(launch_rhs_in(rhs, m * n, k, n, f[0].as<double>(), st));
+    ++launches;
+    for (int l = 0; l < L; ++l) {
+      Record& r = recs[l];
+      const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
+      int nq = 0;
+      for (int j = 1; j + 1 <= mm - 1; j += 2) ++nq;
+      double* fl = f[l].as<double>();
+      Dev z(sizeof(double) * kn * std::max(ne, 1), st);
+      Dev a(sizeof(double) * kn * std::max(no, 1), st);
+      Dev b(sizeof(double) * kn * std::max(nq, 1), st);
+      Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
+      hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl, 2 * kn, k), s_pan(z.as<double>(), kn, k), k);
+      Dev tE = make_tab({{&r.E, 1, 2, no}});
+      hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
+      Dev tF = make_tab({{&r.F, 1, 2, nq}});
+      hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k), s_pan(b.as<double>(), kn, k), k);
+      f[l + 1].alloc(sizeof(double) * kn * std::max(no, 1), st);
+      double* fn = f[l + 1].as<double>();
+      CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, b.as<double>(), kn, fn, kn, nq, (int)kn, st));
+      CK(launch_rhs_combine(fl + kn + 2 * kn * nq, 2 * kn, a.as<double>() + kn * nq, kn, nullptr, 0,
+                            fn + kn * nq, kn, no - nq, (int)kn, st));
+      launches += 2;
+    }
+    // cutoff solve
+    const int mc = last.m;
+    std::vector<Dev> uu(L + 1);
+    uu[L].alloc(sizeof(double) * kn * std::max(mc, 1), st);
+    {
+      Dev B(sizeof(double) * (size_t)Nc * k, st);
+      for (int i = 0; i < mc; ++i)
+        CK(cudaMemcpy2DAsync(B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
+                             f[L].as<double>() + i * kn, sizeof(double) * n,
+                             sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
+      CK(lu_solve(lu.as<double>(), Nc, piv.as<int>(), B.as<double>(), k, st));
+      ++launches;
+      for (int i = 0; i < mc; ++i)
+        CK(cudaMemcpy2DAsync(uu[L].as<double>() + i * kn, sizeof(double) * n,
+                             B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
+                             sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
+    }
+    // back-substitution
+    for (int l = L - 1; l >= 0; --l) {
+      Record& r = recs[l];
+      const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
+      uu[l].alloc(sizeof(double) * kn * mm, st);
+      double* ul = uu[l].as<double>();
+      if (no)
+        CK(cudaMemcpy2DAsync(ul + kn, sizeof(double) * 2 * kn, uu[l + 1].as<double>(),
+                             sizeof(double) * kn, sizeof(double) * kn, no,
+                             cudaMemcpyDeviceToDevice, st));
+      int nb = 0;
+      for (int i = 0; i <= mm - 2; i += 2) ++nb;
+      Dev a(sizeof(double) * kn * ne, st);
+      Dev b(sizeof(double) * kn * ne, st);
+      CK(cudaMemsetAsync(a.p, 0, sizeof(double) * kn * ne, st));
+      CK(cudaMemsetAsync(b.p, 0, sizeof(double) * kn * ne, st));
+      Dev tE = make_tab({{&r.E, 2, 2, ne - 1}});
+      hmat_full(tE.as<HB>(), ne - 1, r.E.R, s_pan(ul + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
+      Dev tF = make_tab({{&r.F, 0, 2, nb}});
+      hmat_full(tF.as<HB>(), nb, r.F.R, s_pan(ul + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
+      Dev rr(sizeof(double) * kn * ne, st);
+      CK(launch_rhs_combine(f[l].as<double>(), 2 * kn, a.as<double>(), kn, b.as<double>(), kn,
+                            rr.as<double>(), kn, ne, (int)kn, st));
+      ++launches;
+      Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
+      hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(rr.as<double>(), kn, k), s_pan(ul, 2 * kn, k), k);
+      uu[l + 1].release();
+    }
+    CK(launch_u_out(uu[0].as<double>(), m * n, k, n, u, st));
+    ++launches;
+    CK(cudaEventRecord(ev1, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    sms = ms;
+  }
+
+  long long storage_bytes(int k) const {
+    long long s = 0;
+    const long long seg = 8LL * n * k;
+    for (auto& r : recs) {
+      const int mm = r.m, ne = (mm + 1) / 2;
+      for (int e = 0; e < ne; ++e) {
+        int i = 2 * e;
+        s += hb_bytes(r.hDinv.data() + (size_t)e * ht.nnodes * 2);
+        if (i >= 1) s += hb_bytes(r.hE.data() + (size_t)i * ht.nnodes * 2);
+        if (i <= mm - 2) s += hb_bytes(r.hF.data() + (size_t)i * ht.nnodes * 2);
+        s += seg;
+      }
+    }
+    const int mc = last.m;
+    for (int i = 0; i < mc; ++i) {
+      s += hb_bytes(lastR[0].data() + (size_t)i * ht.nnodes * 2);
+      if (i >= 1) s += hb_bytes(lastR[1].data() + (size_t)i * ht.nnodes * 2);
+      if (i <= mc - 2) s += hb_bytes(lastR[2].data() + (size_t)i * ht.nnodes * 2);
+      s += seg;
+    }
+    return s;
+  }
+
+  long long device_bytes() const {
+    long long s = 0;
+    for (auto& r : recs) s += r.Dinv.bytes() + r.E.bytes() + r.F.bytes();
+    s += last.D.bytes() + last.E.bytes() + last.F.bytes();
+    s += (long long)lu.n;
+    return s;
+  }
+};
+
+}  // namespace acr
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using acr::Plan;
+
+struct acr_plan {
+  Plan* p;
+};
+
+static std::string g_err;
+
+static int set_err(acr_plan_t* h, int code, const std::string& msg) {
+  if (h && h->p) h->p->err = msg;
+  g_err = msg;
+  return code;
+}
+
+#define ACR_GUARD(h, ...)                                                   \
+  try {                                                                     \
+    __VA_ARGS__;                                                            \
+  } catch (const acr::ArgError& e) {                                        \
+    return set_err(h, ACR_EARG, e.what());                                  \
+  } catch (const acr::SingularError& e) {                                   \
+    return set_err(h, ACR_ESINGULAR, e.what());                             \
+  } catch (const acr::CudaError& e) {                                       \
+    return set_err(h, ACR_ECUDA, e.what());                                 \
+  } catch (const std::exception& e) {                                       \
+    return set_err(h, ACR_EINTERNAL, e.what());                             \
+  }
+
+extern "C" {
+
+int acr_plan_create(int m, int n, int leaf_size, double eps, int max_rank_cap,
+                    int cutoff_blocks, acr_plan_t** out) {
+  if (!out) return set_err(nullptr, ACR_EARG, "null output handle");
+  *out = nullptr;
+  if (m < 1 || n < 2) return set_err(nullptr, ACR_EARG, "need m >= 1 and n >= 2");
+  if (leaf_size < 1)
+    return set_err(nullptr, ACR_EARG, "leaf_size must be >= 1, got " + std::to_string(leaf_size));
+  if (!(eps > 0)) return set_err(nullptr, ACR_EARG, "eps must be > 0");
+  if (max_rank_cap < 0) return set_err(nullptr, ACR_EARG, "max_rank_cap must be positive");
+  if (cutoff_blocks < 1)
+    return set_err(nullptr, ACR_EARG,
+                   "cutoff_blocks must be >= 1, got " + std::to_string(cutoff_blocks));
+  acr_plan_t* h = new acr_plan_t;
+  h->p = nullptr;
+  try {
+    h->p = new Plan(m, n, leaf_size, eps, max_rank_cap, cutoff_blocks);
+    if (h->p->ht.bw > 128) throw acr::ArgError("leaf blocks larger than 128 are not supported");
+    cudaMemPool_t pool;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    h->p->dt.upload(h->p->ht, 0);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    delete h->p;
+    delete h;
+    return ACR_ECUDA;
+  }
+  *out = h;
+  return ACR_OK;
+}
+
+void acr_plan_destroy(acr_plan_t* h) {
+  if (!h) return;
+  if (h->p) {
+    cudaStreamSynchronize(h->p->st);
+    delete h->p;
+  }
+  delete h;
+}
+
+int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
+  if (!h || !h->p) return ACR_EARG;
+  if (option == 1) {
+    h->p->keep_levels = value != 0;
+    return ACR_OK;
+  }
+  return set_err(h, ACR_EARG, "unknown option");
+}
+
+int acr_factor(acr_plan_t* h, const double* D_sub, const double* D_diag,
+               const double* D_sup, const double* E, const double* F,
+               int inversion_order, void* stream) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  if (inversion_order != 0 && inversion_order != 1)
+    return set_err(h, ACR_EARG, "unknown inversion_order");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.st = (cudaStream_t)stream;
+    P.factor(D_sub, D_diag, D_sup, E, F, inversion_order);
+  });
+  return ACR_OK;
+}
+
+int acr_solve(acr_plan_t* h, const double* rhs, int nrhs, double* u,
+              void* stream) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  if (nrhs < 1) return set_err(h, ACR_EARG, "nrhs must be >= 1");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.st = (cudaStream_t)stream;
+    P.solve(rhs, nrhs, u);
+  });
+  return ACR_OK;
+}
+
+int acr_levels(const acr_plan_t* h) { return h && h->p ? (int)h->p->recs.size() : -1; }
+int acr_cutoff_blocks(const acr_plan_t* h) { return h && h->p ? h->p->last.m : -1; }
+int acr_tree_depths(const acr_plan_t* h) { return h && h->p ? h->p->ht.nd : -1; }
+
+int acr_rank_profile(const acr_plan_t* h, int level, int* mx, double* mean) {
+  if (!h || !h->p) return ACR_EARG;
+  const Plan& P = *h->p;
+  if (level < 0 || level >= (int)P.prof.size()) return ACR_EARG;
+  for (int d = 0; d < P.ht.nd; ++d) {
+    mx[d] = P.prof[level].mx[d];
+    mean[d] = P.prof[level].mean[d];
+  }
+  return ACR_OK;
+}
+
+long long acr_storage_bytes(const acr_plan_t* h, int nrhs) {
+  return h && h->p && h->p->factored ? h->p->storage_bytes(nrhs) : -1;
+}
+long long acr_device_bytes(const acr_plan_t* h) {
+  return h && h->p ? h->p->device_bytes() : -1;
+}
+double acr_factor_ms(const acr_plan_t* h) { return h && h->p ? h->p->fms : -1.0; }
+double acr_solve_ms(const acr_plan_t* h) { return h && h->p ? h->p->sms : -1.0; }
+long long acr_kernel_launches(const acr_plan_t* h) { return h && h->p ? h->p->launches : -1; }
+
+int acr_last_error(const acr_plan_t* h, char* buf, int len) {
+  const std::string& s = (h && h->p) ? h->p->err : g_err;
+  if (buf && len > 0) {
+    strncpy(buf, s.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)s.size();
+}
+
+int acr_global_error(char* buf, int len) {
+  if (buf && len > 0) {
+    strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)g_err.size();
+}
+
+int acr_block_to_dense(acr_plan_t* h, int level, int which, int block,
+                       double* out, void* stream) {
+  if (!h || !h->p) return ACR_EARG;
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.st = (cudaStream_t)stream;
+    const acr::Batch* b = nullptr;
+    int L = (int)P.recs.size();
+    if (which == 3) {
+      if (level < 0 || level >= L) throw acr::ArgError("level out of range");
+      b = &P.recs[level].Dinv;
+    } else {
+      if (level == L) {
+        b = which == 0 ? &P.last.D : which == 1 ? &P.last.E : &P.last.F;
+      } else if (level >= 0 && level < (int)P.kept.size()) {
+        b = which == 0 ? &P.kept[level].D
+                       : which == 1 ? &P.recs[level].E : &P.recs[level].F;
+      } else if (level >= 0 && level < L && which != 0) {
+        b = which == 1 ? &P.recs[level].E : &P.recs[level].F;
+      } else {
+        throw acr::ArgError("level not retained (set option 1 before acr_factor)");
+      }
+    }
+    if (block < 0 || block >= b->cnt) throw acr::ArgError("block out of range");
+    acr::Dev tab = P.make_tab({{b, block, 1, 1}});
+    acr::Dev rc(sizeof(int) * 2, P.st);
+    CK(cudaMemsetAsync(rc.p, 0, sizeof(int) * 2, P.st));
+    CK(acr::launch_todense(P.dt.T, tab.as<acr::HB>(), 1, rc.as<int>(), rc.as<int>() + 1,
+                           out, P.n, P.st));
+    CK(cudaStreamSynchronize(P.st));
+  });
+  return ACR_OK;
+}
+
+int acr_residual(int m, int n, int k, const double* D_sub, const double* D_diag,
+                 const double* D_sup, const double* E, const double* F,
+                 const double* u, const double* f, double* out_r, double* out_f,
+                 void* stream) {
+  ACR_GUARD(nullptr, {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int parts = 256;
+    acr::Dev part(sizeof(double) * parts * k * 2, st);
+    CK(acr::launch_residual(m, n, k, D_sub, D_diag, D_sup, E, F, u, f,
+                            part.as<double>(), parts, st));
+    std::vector<double> h((size_t)parts * k * 2);
+    CK(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * h.size(),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int c = 0; c < k; ++c) {
+      double a = 0, b = 0;
+      for (int p = 0; p < parts; ++p) {
+        a += h[((size_t)p * k + c) * 2];
+        b += h[((size_t)p * k + c) * 2 + 1];
+      }
+      out_r[c] = sqrt(a);
+      out_f[c] = sqrt(b);
+    }
+  });
+  return ACR_OK;
+}
+
+int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
+                        double eps, int max_rank_cap, double* Uo, double* Vo,
+                        int* rank_out, void* stream) {
+  if (m < 1 || k < 1 || R < 0) return set_err(nullptr, ACR_EARG, "bad shape");
+  ACR_GUARD(nullptr, {
+    cudaStream_t st = (cudaStream_t)stream;
+    // one branch node [0, m+k) split at m, two leaves
+    int nn = m + k;
+    std::vector<int> lo = {0, 0, m}, hi = {nn, m, nn}, mid = {m, m / 2, m + k / 2},
+                     depth = {0, 1, 1}, parent = {-1, 0, 0}, c0 = {1, -1, -1},
+                     c1 = {2, -1, -1}, isl = {0, 1, 1}, anc = {0, -1, 1, 0, 2, 0},
+                     listA = {0, 0, 0, 0, 0, 1};
+    std::vector<int> all;
+    std::vector<size_t> off;
+    for (auto* v : {&lo, &hi, &mid, &depth, &parent, &c0, &c1, &isl, &anc, &listA}) {
+      off.push_back(all.size());
+      all.insert(all.end(), v->begin(), v->end());
+    }
+    acr::Dev dtree(sizeof(int) * all.size(), st);
+    CK(cudaMemcpyAsync(dtree.p, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
+    const int* b = dtree.as<int>();
+    acr::TreeDev T;
+    memset(&T, 0, sizeof(T));
+    T.n = nn;
+    T.bw = std::max(m, k);
+    T.nd = 1;
+    T.nnodes = 3;
+    T.maxdepth = 1;
+    T.nleaves = 2;
+    T.lo = b + off[0]; T.hi = b + off[1]; T.mid = b + off[2]; T.depth = b + off[3];
+    T.parent = b + off[4]; T.c0 = b + off[5]; T.c1 = b + off[6]; T.isleaf = b + off[7];
+    T.anc = b + off[8];
+    int Rc = std::max(R, 1);
+    acr::Dev Ub(sizeof(double) * (size_t)Rc * nn, st), Vb(sizeof(double) * (size_t)Rc * nn, st);
+    acr::Dev rk(sizeof(int) * 6, st), ovf(sizeof(int), st);
+    for (int c = 0; c < R; ++c) {
+      CK(cudaMemcpyAsync(Ub.as<double>() + (size_t)c * nn, U + (size_t)c * m, sizeof(double) * m,
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(Vb.as<double>() + (size_t)c * nn + m, V + (size_t)c * k,
+                         sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+    }
+    int hr[6] = {R, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(rk.p, hr, sizeof(hr), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
+    acr::HB hb;
+    hb.leaf = nullptr;
+    hb.U = Ub.as<double>();
+    hb.V = Vb.as<double>();
+    hb.rk = rk.as<int>();
+    hb.R = Rc;
+    hb.pad_ = 0;
+    acr::Dev dhb(sizeof(acr::HB), st);
+    CK(cudaMemcpyAsync(dhb.p, &hb, sizeof(hb), cudaMemcpyHostToDevice, st));
+    acr::TruncArgs a;
+    memset(&a, 0, sizeof(a));
+    a.T = T;
+    a.mode = acr::TM_TRUNCATE;
+    a.a = acr::op_own(acr::s_hbU(dhb.as<acr::HB>()), acr::s_hbV(dhb.as<acr::HB>()),
+                      acr::r_hb(dhb.as<acr::HB>()));
+    a.out = dhb.as<acr::HB>();
+    a.tasks = dtree.as<int>() + off[9];
+    a.ntasks = 1;
+    a.eps = eps;
+    a.cap = max_rank_cap;
+    a.overflow = ovf.as<int>();
+    long long need = acr::trunc_need_doubles(m, k, Rc);
+    acr::Dev g;
+    if (need * 8 + 64 <= acr::SMEM_MAX_BYTES) {
+      a.smem_doubles = (int)need;
+      CK(acr::launch_trunc(a, 1, need * 8 + 64, st));
+    } else {
+      g.alloc(sizeof(double) * need, st);
+      a.gscr = g.as<double>();
+      a.gscr_stride = need;
+      a.gscr_ntasks = 1;
+      a.smem_doubles = 0;
+      CK(acr::launch_trunc(a, 1, 64, st));
+    }
+    int hr2[6];
+    CK(cudaMemcpyAsync(hr2, rk.p, sizeof(hr2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int r = hr2[0];
+    *rank_out = r;
+    for (int c = 0; c < r; ++c) {
+      CK(cudaMemcpyAsync(Uo + (size_t)c * m, Ub.as<double>() + (size_t)c * nn,
+                         sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(Vo + (size_t)c * k, Vb.as<double>() + (size_t)c * nn + m,
+                         sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+  return ACR_OK;
+}
+
+int acr_leaf_inverse(int s, const double* A, double* X, int* singular,
+                     void* stream) {
+  if (s < 1 || s > 128) return set_err(nullptr, ACR_EARG, "leaf size must be in [1,128]");
+  ACR_GUARD(nullptr, {
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<int> lo = {0}, hi = {s}, mid = {s / 2}, depth = {0}, parent = {-1},
+                     c0 = {-1}, c1 = {-1}, isl = {1};
+    std::vector<int> all;
+    std::vector<size_t> off;
+    for (auto* v : {&lo, &hi, &mid, &depth, &parent, &c0, &c1, &isl}) {
+      off.push_back(all.size());
+      all.insert(all.end(), v->begin(), v->end());
+    }
+    acr::Dev dtree(sizeof(int) * all.size(), st);
+    CK(cudaMemcpyAsync(dtree.p, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
+    const int* b = dtree.as<int>();
+    acr::TreeDev T;
+    memset(&T, 0, sizeof(T));
+    T.n = s;
+    T.bw = s;
+    T.nnodes = 1;
+    T.nleaves = 1;
+    T.lo = b + off[0]; T.hi = b + off[1]; T.mid = b + off[2]; T.depth = b + off[3];
+    T.parent = b + off[4]; T.c0 = b + off[5]; T.c1 = b + off[6]; T.isleaf = b + off[7];
+    CK(cudaMemcpyAsync(X, A, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
+    acr::HB hb;
+    memset(&hb, 0, sizeof(hb));
+    hb.leaf = X;
+    hb.R = 1;
+    acr::Dev dhb(sizeof(acr::HB), st), sg(sizeof(int), st);
+    CK(cudaMemcpyAsync(dhb.p, &hb, sizeof(hb), cudaMemcpyHostToDevice, st));
+    int big = INT_MAX;
+    CK(cudaMemcpyAsync(sg.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(acr::launch_leafinv(T, dhb.as<acr::HB>(), 1, 0, sg.as<int>(), st));
+    int hs = 0;
+    CK(cudaMemcpyAsync(&hs, sg.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *singular = hs != INT_MAX ? 1 : 0;
+  });
+  return ACR_OK;
+}
+
+}  // extern "C"

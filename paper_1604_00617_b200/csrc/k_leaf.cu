@@ -1,0 +1,440 @@
+// Dense-leaf kernels of the batched HODLR arithmetic.
+//   k_leafinv   leaf inverse, reference algebra.py:199-207 (np.linalg.solve(L, I)
+//               with partial pivoting; singular / non-finite flagged per block)
+//   k_leafgemm  leaf products of multiply (algebra.py:162-163) followed by the
+//               ancestors' cross terms, deepest first (algebra.py:165-168 via
+//               add_lowrank's exact dense update, algebra.py:134-135)
+//   k_leaflr    add_lowrank at the leaves of one subtree (algebra.py:134-135)
+//   k_leafadd   add() at the leaves (algebra.py:104-105)
+//   k_negate    scale(H, -1) (algebra.py:115-125)
+//   k_lift*     exact lift of the bands (hodlr.py:242-314)
+#include <climits>
+#include "acr_types.cuh"
+#include "acr_launch.h"
+
+namespace acr {
+
+static constexpr int LT = 128;
+
+// ---------------------------------------------------------------------------
+// leaf inverse: in-place Gauss-Jordan with row partial pivoting (the pivot
+// sequence equals getrf's), column swaps undone at the end.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(LT) k_leafinv(TreeDev T, const HB* H, int leaf,
+                                                int* sing) {
+  extern __shared__ double sm[];
+  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
+  const int ld = s + 1;
+  double* A = sm;
+  int* piv = reinterpret_cast<int*>(A + s * ld);
+  __shared__ double pv;
+  __shared__ int pidx, bad;
+  double* L = H[g].leaf + (long long)lo * bw;
+  for (int idx = tid; idx < s * s; idx += LT) {
+    int i = idx / s, j = idx - i * s;
+    A[i * ld + j] = L[(long long)i * bw + j];
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int k = 0; k < s; ++k) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + lane; i < s; i += 32) {
+        double v = fabs(A[i * ld + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) {
+        pidx = bi;
+        piv[k] = bi;
+        pv = A[bi * ld + k];
+        if (pv == 0.0) bad = 1;
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    const int p = pidx;
+    if (p != k)
+      for (int j = tid; j < s; j += LT) {
+        double t = A[k * ld + j];
+        A[k * ld + j] = A[p * ld + j];
+        A[p * ld + j] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / pv;
+    if (tid == 0) A[k * ld + k] = 1.0;
+    __syncthreads();
+    for (int j = tid; j < s; j += LT) A[k * ld + j] *= inv;
+    __syncthreads();
+    for (int idx = tid; idx < s * s; idx += LT) {
+      int i = idx / s, j = idx - i * s;
+      if (i == k || j == k) continue;
+      A[i * ld + j] -= A[i * ld + k] * A[k * ld + j];
+    }
+    __syncthreads();
+    for (int i = tid; i < s; i += LT)
+      if (i != k) A[i * ld + k] = -A[i * ld + k] * A[k * ld + k];
+    __syncthreads();
+  }
+  if (!bad) {
+    for (int k = s - 1; k >= 0; --k) {
+      int p = piv[k];
+      if (p != k)
+        for (int i = tid; i < s; i += LT) {
+          double t = A[i * ld + k];
+          A[i * ld + k] = A[i * ld + p];
+          A[i * ld + p] = t;
+        }
+      __syncthreads();
+    }
+    int nf = 0;
+    for (int idx = tid; idx < s * s; idx += LT) {
+      int i = idx / s, j = idx - i * s;
+      double v = A[i * ld + j];
+      if (!isfinite(v)) nf = 1;
+      L[(long long)i * bw + j] = v;
+    }
+    if (__syncthreads_or(nf) && tid == 0) bad = 1;
+  }
+  __syncthreads();
+  if (bad && tid == 0) {
+    // leaves are numbered by row order; the reference stops at the first
+    int pos = 0;
+    for (int v = 0; v < T.nnodes; ++v)
+      if (T.isleaf[v] && T.lo[v] < lo) ++pos;
+    atomicMin(sing + g, pos);
+  }
+}
+
+cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
+                           int* sing, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  int s = T.bw;
+  size_t smem = (size_t)s * (s + 1) * 8 + (size_t)s * 4 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_leafinv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  k_leafinv<<<nelem, LT, smem, st>>>(T, H, leaf, sing);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// leaf GEMM + ancestor cross terms
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(LT) k_leafgemm(TreeDev T, const HB* A,
+                                                 const HB* B, const HB* C,
+                                                 Src PX, RankRef xr) {
+  extern __shared__ double sm[];
+  const int g = blockIdx.y, tid = threadIdx.x;
+  const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
+  const int lo = T.lo[lam], s = T.hi[lam] - lo, bw = T.bw, n = T.n;
+  double* a = sm;
+  double* b = a + s * s;
+  const double* La = A[g].leaf + (long long)lo * bw;
+  const double* Lb = B[g].leaf + (long long)lo * bw;
+  for (int idx = tid; idx < s * s; idx += LT) {
+    int i = idx / s, j = idx - i * s;
+    a[idx] = La[(long long)i * bw + j];
+    b[idx] = Lb[(long long)i * bw + j];
+  }
+  __syncthreads();
+  const HB bb = B[g];
+  const int* cr = rank_base(xr, g);
+  double* Lc = C[g].leaf + (long long)lo * bw;
+  for (int idx = tid; idx < s * s; idx += LT) {
+    int i = idx / s, j = idx - i * s;
+    double acc = 0.0;
+    for (int l = 0; l < s; ++l) acc += a[i * s + l] * b[l * s + j];
+    int child = lam;
+    for (int al = T.parent[lam]; al >= 0; child = al, al = T.parent[al]) {
+      int r = cr[al * 2 + (child == T.c0[al] ? 0 : 1)];
+      if (!r) continue;
+      int slot = T.depth[al];
+      const double* P = src_col(PX, n, g, slot, 0) + lo;
+      const double* Q = bb.V + (long long)slot * bb.R * n + lo;
+      double z = 0.0;
+      for (int c = 0; c < r; ++c) z += P[(long long)c * n + i] * Q[(long long)c * n + j];
+      acc = acc + z;
+    }
+    Lc[(long long)i * bw + j] = acc;
+  }
+}
+
+cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
+                            const HB* C, int nelem, Src PX, RankRef xr,
+                            cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  size_t smem = 2ull * T.bw * T.bw * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_leafgemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  dim3 grid(T.nleaves, nelem);
+  k_leafgemm<<<grid, LT, smem, st>>>(T, A, B, C, PX, xr);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// add_lowrank at the leaves of subtree(mu): L += U V^T (exact dense update)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
+                                               Src Us, Src Vs, RankRef rr,
+                                               int node, int fside) {
+  const int g = blockIdx.y, tid = threadIdx.x, n = T.n, bw = T.bw;
+  const int* rb = rank_base(rr, g);
+  int r = rb[node * 2 + fside];
+  if (rb[node * 2 + 1 - fside] == 0) r = 0;
+  if (!r) return;
+  const int lam = T.listB[(T.startB[mu] + blockIdx.x) * 2 + 1];
+  const int lo = T.lo[lam], s = T.hi[lam] - lo;
+  const int slot = T.depth[node];
+  const double* U = src_col(Us, n, g, slot, 0) + lo;
+  const double* V = src_col(Vs, n, g, slot, 0) + lo;
+  double* L = H[g].leaf + (long long)lo * bw;
+  for (int idx = tid; idx < s * s; idx += LT) {
+    int i = idx / s, j = idx - i * s;
+    double z = 0.0;
+    for (int c = 0; c < r; ++c) z += U[(long long)c * n + i] * V[(long long)c * n + j];
+    L[(long long)i * bw + j] = L[(long long)i * bw + j] + z;
+  }
+}
+
+// variant with explicit leaf count (host knows the tree)
+cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
+                            int nleaf, Src U, Src V, RankRef rr, int node,
+                            int fside, cudaStream_t st) {
+  if (!nelem || !nleaf) return cudaSuccess;
+  dim3 grid(nleaf, nelem);
+  k_leaflr<<<grid, LT, 0, st>>>(T, H, mu, U, V, rr, node, fside);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// elementwise leaf ops
+// ---------------------------------------------------------------------------
+__global__ void k_leafadd(int len, const HB* A, const HB* B, const HB* C,
+                          double sb) {
+  const int g = blockIdx.y;
+  const double* a = A[g].leaf;
+  const double* b = B[g].leaf;
+  double* c = C[g].leaf;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += gridDim.x * blockDim.x)
+    c[i] = a[i] + sb * b[i];
+}
+
+cudaError_t launch_leafadd(const TreeDev& T, const HB* A, const HB* B,
+                           const HB* C, double sb, int nelem, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  int len = T.n * T.bw;
+  int bx = (len + 255) / 256;
+  if (bx > 64) bx = 64;
+  k_leafadd<<<dim3(bx, nelem), 256, 0, st>>>(len, A, B, C, sb);
+  return cudaGetLastError();
+}
+
+__global__ void k_negate(TreeDev T, const HB* H) {
+  const int g = blockIdx.y, n = T.n;
+  const HB h = H[g];
+  const int len = n * T.bw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += gridDim.x * blockDim.x)
+    h.leaf[i] = -1.0 * h.leaf[i];
+  // factors: U columns below the rank, per branch node and side
+  for (int v = blockIdx.x; v < T.nnodes; v += gridDim.x) {
+    if (T.isleaf[v]) continue;
+    int lo = T.lo[v], hi = T.hi[v], mid = T.mid[v];
+    long long slot = (long long)T.depth[v] * h.R * n;
+    for (int side = 0; side < 2; ++side) {
+      int r = h.rk[v * 2 + side];
+      int row = side ? mid : lo, len2 = side ? hi - mid : mid - lo;
+      for (int idx = threadIdx.x; idx < r * len2; idx += blockDim.x) {
+        int c = idx / len2, i = idx - c * len2;
+        double* p = h.U + slot + (long long)c * n + row + i;
+        *p = -1.0 * *p;
+      }
+    }
+  }
+}
+
+cudaError_t launch_negate(const TreeDev& T, const HB* H, int nelem,
+                          cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  k_negate<<<dim3(32, nelem), 256, 0, st>>>(T, H);
+  return cudaGetLastError();
+}
+
+__global__ void k_copyhb(TreeDev T, const HB* S, const HB* D, int* overflow) {
+  const int g = blockIdx.y, n = T.n;
+  const HB s = S[g], d = D[g];
+  const int len = n * T.bw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += gridDim.x * blockDim.x)
+    d.leaf[i] = s.leaf[i];
+  for (int v = blockIdx.x; v < T.nnodes; v += gridDim.x) {
+    if (T.isleaf[v]) {
+      if (threadIdx.x < 2) d.rk[v * 2 + threadIdx.x] = 0;
+      continue;
+    }
+    int lo = T.lo[v], hi = T.hi[v], mid = T.mid[v];
+    long long ss = (long long)T.depth[v] * s.R * n, ds = (long long)T.depth[v] * d.R * n;
+    for (int side = 0; side < 2; ++side) {
+      int r = s.rk[v * 2 + side];
+      if (r > d.R) {
+        if (threadIdx.x == 0) atomicMax(overflow, r);
+        r = d.R;
+      }
+      int ur = side ? mid : lo, ul = side ? hi - mid : mid - lo;
+      int vr = side ? lo : mid, vl = side ? mid - lo : hi - mid;
+      for (int idx = threadIdx.x; idx < r * ul; idx += blockDim.x) {
+        int c = idx / ul, i = idx - c * ul;
+        d.U[ds + (long long)c * n + ur + i] = s.U[ss + (long long)c * n + ur + i];
+      }
+      for (int idx = threadIdx.x; idx < r * vl; idx += blockDim.x) {
+        int c = idx / vl, i = idx - c * vl;
+        d.V[ds + (long long)c * n + vr + i] = s.V[ss + (long long)c * n + vr + i];
+      }
+      if (threadIdx.x == 0) d.rk[v * 2 + side] = r;
+    }
+  }
+}
+
+cudaError_t launch_copyhb(const TreeDev& T, const HB* S, const HB* D, int nelem,
+                          int* overflow, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  k_copyhb<<<dim3(32, nelem), 256, 0, st>>>(T, S, D, overflow);
+  return cudaGetLastError();
+}
+
+__global__ void k_zerohb(TreeDev T, const HB* D) {
+  const int g = blockIdx.y;
+  const HB d = D[g];
+  const int len = T.n * T.bw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += gridDim.x * blockDim.x)
+    d.leaf[i] = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * T.nnodes;
+       i += gridDim.x * blockDim.x)
+    d.rk[i] = 0;
+}
+
+cudaError_t launch_zerohb(const TreeDev& T, const HB* D, int nelem,
+                          cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  k_zerohb<<<dim3(16, nelem), 256, 0, st>>>(T, D);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// lift (hodlr.py:242-314): bands -> leaves + rank<=1 corner factors
+// ---------------------------------------------------------------------------
+__global__ void k_lift(TreeDev T, const double* sub, const double* diag,
+                       const double* sup, const HB* D) {
+  const int g = blockIdx.y, n = T.n, bw = T.bw;
+  const HB d = D[g];
+  const double* sb = sub + (long long)g * (n - 1);
+  const double* dg = diag + (long long)g * n;
+  const double* sp = sup + (long long)g * (n - 1);
+  // leaves
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * bw;
+       idx += gridDim.x * blockDim.x) {
+    int i = idx / bw, jj = idx - i * bw;
+    // leaf containing row i: walk the tree
+    int v = 0;
+    while (!T.isleaf[v]) v = (i < T.mid[v]) ? T.c0[v] : T.c1[v];
+    int lo = T.lo[v], s = T.hi[v] - lo;
+    double val = 0.0;
+    if (jj < s) {
+      int j = lo + jj;
+      if (j == i) val = dg[i];
+      else if (j == i + 1) val = sp[i];
+      else if (j == i - 1) val = sb[j];
+    }
+    d.leaf[idx] = val;
+  }
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < T.nnodes;
+       v += gridDim.x * blockDim.x) {
+    if (T.isleaf[v]) {
+      d.rk[v * 2] = d.rk[v * 2 + 1] = 0;
+      continue;
+    }
+    int lo = T.lo[v], hi = T.hi[v], mid = T.mid[v];
+    long long slot = (long long)T.depth[v] * d.R * n;
+    double a = sp[mid - 1];   // entry (mid-1, mid): U = a e_last, V = e_0
+    double b = sb[mid - 1];   // entry (mid, mid-1): U = b e_0, V = e_last
+    // zero the first column over the node rows, then place the corner
+    for (int i = lo; i < hi; ++i) { d.U[slot + i] = 0.0; d.V[slot + i] = 0.0; }
+    d.rk[v * 2] = a != 0.0 ? 1 : 0;
+    d.rk[v * 2 + 1] = b != 0.0 ? 1 : 0;
+    if (a != 0.0) { d.U[slot + mid - 1] = a; d.V[slot + mid] = 1.0; }
+    if (b != 0.0) { d.U[slot + mid] = b; d.V[slot + mid - 1] = 1.0; }
+  }
+}
+
+cudaError_t launch_lift(const TreeDev& T, const double* sub, const double* diag,
+                        const double* sup, const HB* D, int nelem,
+                        cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  k_lift<<<dim3(8, nelem), 256, 0, st>>>(T, sub, diag, sup, D);
+  return cudaGetLastError();
+}
+
+__global__ void k_liftdiag(TreeDev T, const double* dd, const HB* D) {
+  const int g = blockIdx.y, n = T.n, bw = T.bw;
+  const HB d = D[g];
+  const double* dg = dd + (long long)g * n;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * bw;
+       idx += gridDim.x * blockDim.x) {
+    int i = idx / bw, jj = idx - i * bw;
+    int v = 0;
+    while (!T.isleaf[v]) v = (i < T.mid[v]) ? T.c0[v] : T.c1[v];
+    d.leaf[idx] = (T.lo[v] + jj == i) ? dg[i] : 0.0;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * T.nnodes;
+       i += gridDim.x * blockDim.x)
+    d.rk[i] = 0;
+}
+
+cudaError_t launch_liftdiag(const TreeDev& T, const double* d, const HB* D,
+                            int nelem, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  k_liftdiag<<<dim3(8, nelem), 256, 0, st>>>(T, d, D);
+  return cudaGetLastError();
+}
+
+// HB table for a strided set of blocks: tab[i] = block (first + i*step)
+__global__ void k_build_tab(HB* tab, HB base, long long sl, long long sf,
+                            long long sr, int first, int step, int count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  long long e = first + (long long)i * step;
+  HB h = base;
+  h.leaf = base.leaf + e * sl;
+  h.U = base.U + e * sf;
+  h.V = base.V + e * sf;
+  h.rk = base.rk + e * sr;
+  tab[i] = h;
+}
+
+cudaError_t launch_build_tab(HB* tab, HB base, long long sl, long long sf,
+                             long long sr, int first, int step, int count,
+                             cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  k_build_tab<<<(count + 127) / 128, 128, 0, st>>>(tab, base, sl, sf, sr, first,
+                                                  step, count);
+  return cudaGetLastError();
+}
+
+}  // namespace acr

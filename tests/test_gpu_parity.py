@@ -1,0 +1,200 @@
+"""GPU parity: the sm_100a path through the C ABI against the reference's
+outputs (tests/golden, made by running the real reference) and the CPU
+oracle.  Tolerances follow BASELINE.json north_star: solution within
+10 x eps of the reference, residual no worse than 2x the reference's
+(plus 1e-15 absolute for residuals at the roundoff floor), and identical
+rank decisions (per-level max/mean rank profile, storage bytes)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_case, golden_profiles, load_npz
+from oracle import acr_oracle as O
+from paper_1604_00617_b200 import problems as P
+from paper_1604_00617_b200.system import SingularBlockError, Tolerance
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def solver_mod():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1604_00617_b200 import solver
+    return solver
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _check_against_golden(rep, u, z, prefix, eps, u_ref=None, stride=1):
+    if u_ref is None:
+        u_ref = z[prefix + "u"]
+    rel = _rel(u[::stride], u_ref)
+    assert rel <= 10 * eps, f"solution differs by {rel:.2e} (eps {eps})"
+    res_ref = float(z[prefix + "residual"])
+    assert rep.residual <= 2 * res_ref + 1e-15, (rep.residual, res_ref)
+    assert rep.levels == int(z[prefix + "levels"])
+    prof = golden_profiles(z, prefix)
+    assert [p.max_by_depth for p in rep.per_level_ranks] == [p[0] for p in prof]
+    np.testing.assert_allclose(
+        [x for p in rep.per_level_ranks for x in p.mean_by_depth],
+        [x for p in prof for x in p[1]], rtol=0, atol=1e-9)
+    assert rep.storage_bytes == int(z[prefix + "storage_bytes"])
+
+
+def test_truncate_kernel_vectors(solver_mod):
+    from paper_1604_00617_b200 import _capi
+    import ctypes as C
+    lib = _capi.load()
+    z = load_npz("kernels_cfg1.npz")
+    for i in range(int(z["n_trunc"])):
+        U, V = z[f"t{i}/U"], z[f"t{i}/V"]
+        m, R = U.shape
+        k = V.shape[0]
+        dU = torch.tensor(U.T.copy(), device="cuda")   # column-major
+        dV = torch.tensor(V.T.copy(), device="cuda")
+        oU = torch.zeros((max(R, 1), m), dtype=torch.float64, device="cuda")
+        oV = torch.zeros((max(R, 1), k), dtype=torch.float64, device="cuda")
+        r = C.c_int()
+        rc = lib.acr_truncate_factor(m, k, R, C.c_void_p(dU.data_ptr()),
+                                     C.c_void_p(dV.data_ptr()), float(z[f"t{i}/eps"]), 0,
+                                     C.c_void_p(oU.data_ptr()), C.c_void_p(oV.data_ptr()),
+                                     C.byref(r), None)
+        assert rc == 0, _capi.last_error()
+        assert r.value == int(z[f"t{i}/rank"]), i
+        Uo = oU[:r.value].cpu().numpy().T
+        Vo = oV[:r.value].cpu().numpy().T
+        ref = z[f"t{i}/dense"]
+        scale = np.linalg.norm(U) * np.linalg.norm(V)
+        assert np.linalg.norm(Uo @ Vo.T - ref) <= 1e-13 * max(scale, 1e-300), i
+
+
+def test_leaf_inverse_kernel_vectors(solver_mod):
+    from paper_1604_00617_b200 import _capi
+    import ctypes as C
+    lib = _capi.load()
+    z = load_npz("kernels_cfg1.npz")
+    for i in range(int(z["n_inv"])):
+        A, X = z[f"i{i}/A"], z[f"i{i}/X"]
+        s = A.shape[0]
+        dA = torch.tensor(A, device="cuda")
+        dX = torch.empty_like(dA)
+        sg = C.c_int()
+        assert lib.acr_leaf_inverse(s, C.c_void_p(dA.data_ptr()), C.c_void_p(dX.data_ptr()),
+                                    C.byref(sg), None) == 0
+        assert sg.value == 0
+        assert _rel(dX.cpu().numpy(), X) <= 1e-13
+    Z = torch.zeros((8, 8), dtype=torch.float64, device="cuda")
+    dX = torch.empty_like(Z)
+    sg = C.c_int()
+    lib.acr_leaf_inverse(8, C.c_void_p(Z.data_ptr()), C.c_void_p(dX.data_ptr()), C.byref(sg), None)
+    assert sg.value == 1
+
+
+SMALL = ["rand_m4", "rand_m5", "rand_m6", "rand_m7", "rand_13x13", "rand_16x6_c4",
+         "rand_20x4_c4", "rand_7x4_c2", "poisson16", "checker16", "helm16_k1",
+         "conv16_a100", "helm16_k2", "poisson32_e8", "conv32_a100_e8", "poisson32_e2",
+         "poisson32_e6", "helm63_k6pi", "conv63_a1e4", "poisson128_e6", "rand_cap2"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_small_systems_against_reference(solver_mod, small_golden, name):
+    sys_, tol, leaf, cut = golden_case(small_golden, name)
+    u, rep = solver_mod.acr_solve(sys_, tol, cutoff_blocks=cut, leaf_size=leaf)
+    _check_against_golden(rep, u, small_golden, f"{name}/", max(tol.eps, 1e-13))
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
+def test_config_against_reference(solver_mod, cfg):
+    path = os.path.join(GOLDEN, f"{cfg}.npz")
+    if not os.path.exists(path):
+        pytest.skip("golden missing")
+    z = load_npz(f"{cfg}.npz")
+    c = P.CONFIGS[cfg]
+    u, rep = solver_mod.acr_solve(P.make_config(cfg), Tolerance(c["eps"]),
+                                  leaf_size=c["leaf"])
+    stride = int(z["u_stride"])
+    _check_against_golden(rep, u, z, "", c["eps"], stride=stride)
+
+
+def test_forward_reversed_bitwise(solver_mod):
+    s = P.random_system(16, 16, seed=11)
+    a, _ = solver_mod.acr_solve(s, Tolerance(1e-8), leaf_size=8, inversion_order="forward")
+    b, _ = solver_mod.acr_solve(s, Tolerance(1e-8), leaf_size=8, inversion_order="reversed")
+    np.testing.assert_array_equal(a, b)
+
+
+def test_run_to_run_bitwise(solver_mod):
+    s = P.make_config("cfg1")
+    a, _ = solver_mod.acr_solve(s, Tolerance(1e-8), leaf_size=16)
+    b, _ = solver_mod.acr_solve(s, Tolerance(1e-8), leaf_size=16)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_singular_pivot(solver_mod):
+    s = P.random_system(4, 4, seed=6)
+    s.D_diag[2] = 0.0
+    s.D_sub[2] = 0.0
+    s.D_sup[2] = 0.0
+    with pytest.raises(SingularBlockError, match=r"\[0,2\): level 0, pivot block 2"):
+        solver_mod.acr_solve(s, Tolerance(1e-12), leaf_size=2)
+
+
+def test_invalid_arguments(solver_mod):
+    s = P.random_system(4, 4, seed=1)
+    with pytest.raises(ValueError):
+        solver_mod.acr_solve(s, Tolerance(1e-12), cutoff_blocks=0)
+    with pytest.raises(ValueError):
+        solver_mod.acr_solve(s, Tolerance(1e-12), inversion_order="random")
+
+
+def test_level_blocks_against_oracle(solver_mod):
+    s = P.random_system(8, 16, seed=21)
+    tol = Tolerance(1e-10)
+    t = O.build_node_table(16, 4)
+    lv0 = O.lift(s, t)
+    lv1, rec0 = O.reduce_level(lv0, t, tol)
+    sol = solver_mod.AcrSolver(8, 16, tol, 1, 4, keep_levels=True)
+    sol.factor(s)
+    for i in range(4):
+        ref = rec0["Dinv"][i].to_dense(t)
+        got = sol.block_dense(0, "Dinv", i).cpu().numpy()
+        assert _rel(got, ref) <= 1e-12
+    # level-1 system lives in the record of level 1 (E/F) and in kept D of level 1
+    lv2, rec1 = O.reduce_level(lv1, t, tol)
+    for i in range(2):
+        ref = rec1["Dinv"][i].to_dense(t)
+        got = sol.block_dense(1, "Dinv", i).cpu().numpy()
+        assert _rel(got, ref) <= 1e-11
+    for i in range(4):
+        ref = lv1.D[i].to_dense(t)
+        got = sol.block_dense(1, "D", i).cpu().numpy()
+        assert _rel(got, ref) <= 1e-11
+
+
+def test_multi_rhs_against_oracle(solver_mod):
+    s = P.random_system(12, 16, seed=5, k=4)
+    tol = Tolerance(1e-10)
+    u, rep = solver_mod.acr_solve(s, tol, leaf_size=4)
+    uo, _ = O.acr_solve(s, tol, leaf_size=4)
+    assert u.shape == (12 * 16, 4)
+    assert _rel(u, uo) <= 1e-9
+    assert rep.residual <= 1e-8
+
+
+def test_single_block_and_cutoff(solver_mod):
+    s = P.random_system(1, 16, seed=3)
+    u, rep = solver_mod.acr_solve(s, Tolerance(1e-12), leaf_size=4)
+    uo, _ = O.acr_solve(s, Tolerance(1e-12), leaf_size=4)
+    assert rep.levels == 0 and _rel(u, uo) <= 1e-13
+    s = P.random_system(9, 8, seed=4)
+    u, rep = solver_mod.acr_solve(s, Tolerance(1e-12), cutoff_blocks=3, leaf_size=4)
+    uo, ro = O.acr_solve(s, Tolerance(1e-12), cutoff_blocks=3, leaf_size=4)
+    assert rep.levels == ro.levels and rep.cutoff_blocks == ro.cutoff_blocks
+    assert _rel(u, uo) <= 1e-11
