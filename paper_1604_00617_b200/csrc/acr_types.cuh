@@ -129,6 +129,7 @@ struct MMJob {
   double* tbuf;             // [g][entryA - startA[mu0]][RT][CT]
   int RT, CT;
   int nA;                   // startA[mu1] - startA[mu0]
+  int nB;                   // startB[mu1] - startB[mu0]
 };
 
 // Z[rows hw of nu] = alpha * W[rows hw] (X[rows hx]^T Y[rows hx])

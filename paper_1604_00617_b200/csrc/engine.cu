@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -251,6 +252,7 @@ struct Batch {
     U.alloc(sizeof(double) * sf * std::max(cnt, 1), st);
     V.alloc(sizeof(double) * sf * std::max(cnt, 1), st);
     rk.alloc(sizeof(int) * sr * std::max(cnt, 1), st);
+    CK(cudaMemsetAsync(rk.p, 0, rk.n, st));
   }
   HB base() const {
     HB h;
@@ -333,6 +335,12 @@ static TOp op_own(Src U, Src V, RankRef r, double sc = 1.0) {
   o.sel = SEL_OWN;
   o.scale = sc;
   return o;
+}
+
+static bool dbg() {
+  static int v = -1;
+  if (v < 0) v = getenv("ACR_DEBUG") ? 1 : 0;
+  return v == 1;
 }
 
 static const long long SMEM_MAX_BYTES = 196 * 1024;
@@ -546,6 +554,7 @@ struct Plan {
       j.mu0 = 1;
       j.mu1 = nn;
       j.nA = nA1;
+      j.nB = ht.startB[nn] - ht.startB[1];
     }
     CK(launch_hmat(dt.T, J, 2, G, st));
     launches += 2;
@@ -629,6 +638,7 @@ struct Plan {
       J[k].RT = c.R;
       J[k].CT = c.R;
       J[k].nA = ht.nA(mu, mu + 1);
+      J[k].nB = ht.nleaves_under(mu);
     }
     (void)second;
     J[0].X = s_hbU(c.H);
@@ -730,7 +740,9 @@ struct Plan {
 
   int max_rank_of(const std::vector<int>& r) const {
     int mx = 0;
-    for (int x : r) mx = std::max(mx, x);
+    const size_t per = (size_t)ht.nnodes * 2;
+    for (size_t b = 0; b + per <= r.size(); b += per)
+      for (int v : ht.branches) mx = std::max({mx, r[b + v * 2], r[b + v * 2 + 1]});
     return mx;
   }
 
@@ -852,8 +864,11 @@ struct Plan {
                ht.lo[v], ht.hi[v], lvl, 2 * bad);
       throw SingularError(buf);
     }
+    if (dbg())
+      fprintf(stderr, "[acr] level %d m=%d Rout=%d overflow=%d\n", lvl, mm, Rout, h_ovf);
     if (h_ovf) {
       if (h_ovf >= (1 << 29)) throw InternalError("truncation work area too small");
+      if (h_ovf > 4 * n + 64) throw InternalError("implausible rank " + std::to_string(h_ovf));
       need = h_ovf;
       return false;
     }
@@ -981,6 +996,7 @@ struct Plan {
     J.mu0 = 0;
     J.mu1 = 1;
     J.nA = ht.nA(0, 1);
+    J.nB = ht.nleaves_under(0);
     J.RT = R;
     J.CT = k;
     J.tbuf = scratch<double>(12, (size_t)G * std::max(J.nA, 1) * R * k);

@@ -135,11 +135,9 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
   int nA = 0, nB = 0, cmax = 0;
   for (int k = 0; k < njobs; ++k) {
     nA = jobs[k].nA > nA ? jobs[k].nA : nA;
+    nB = jobs[k].nB > nB ? jobs[k].nB : nB;
     cmax = jobs[k].CT > cmax ? jobs[k].CT : cmax;
   }
-  // leaf counts per job come from host-side copies held by the caller via nA
-  // field semantics; B-range size is computed on device, grid sized by T.
-  nB = T.nleaves;
   if (nA > 0) {
     dim3 g(nA, nelem, njobs);
     k_hmatA<<<g, HT, 0, st>>>(T, JJ);
