@@ -36,7 +36,9 @@ int acr_plan_create(int m, int n, int leaf_size, double eps, int max_rank_cap,
                     int cutoff_blocks, acr_plan_t** out);
 void acr_plan_destroy(acr_plan_t* p);
 
-/* option 1: keep every level's D blocks for export (tests); value 0/1 */
+/* option 1: keep every level's D blocks for export (tests); value 0/1
+ * option 2: per-kernel-class instrumentation (CUDA events around every
+ *           launch of a class + algorithmic FLOP/byte counters); 0/1 */
 int acr_plan_set_option(acr_plan_t* p, int option, long long value);
 
 /* Factor phase (reference lift_system reduction.py:156-166 + reduce_level
@@ -68,6 +70,11 @@ long long acr_device_bytes(const acr_plan_t* p);
 double acr_factor_ms(const acr_plan_t* p);
 double acr_solve_ms(const acr_plan_t* p);
 long long acr_kernel_launches(const acr_plan_t* p);
+/* Instrumented factor only (option 2): class 0 recompression (k_trunc),
+ * 1 leaf inverse, 2 leaf GEMM, 3 HODLR x panel.  counters (class 0):
+ * [0] algorithmic FLOPs, [1] algorithmic bytes. */
+int acr_kernel_stats(const acr_plan_t* p, int cls, long long* launches,
+                     double* ms, unsigned long long* counters);
 int acr_last_error(const acr_plan_t* p, char* buf, int len);
 /* error of the last plan-less call (acr_plan_create failures) */
 int acr_global_error(char* buf, int len);

@@ -31,6 +31,8 @@ _SIGS = [
     ("acr_factor_ms", C.c_double, [C.c_void_p]),
     ("acr_solve_ms", C.c_double, [C.c_void_p]),
     ("acr_kernel_launches", C.c_longlong, [C.c_void_p]),
+    ("acr_kernel_stats", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_longlong),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_ulonglong)]),
     ("acr_last_error", C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
     ("acr_global_error", C.c_int, [C.c_char_p, C.c_int]),
     ("acr_block_to_dense", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int,

@@ -111,6 +111,7 @@ struct TruncArgs {
   long long gscr_stride;    // doubles per (g, task)
   int gscr_ntasks;          // tasks [0, gscr_ntasks) of the slice own a global area
   int smem_doubles;         // dynamic smem capacity in doubles
+  unsigned long long* ctr;  // optional [flops, bytes] algorithmic counters
 };
 
 // HODLR x panel product over subtrees (reference algebra.py:52-83):

@@ -367,6 +367,16 @@ struct Plan {
   long long launches = 0;
   bool factored = false;
   std::string err;
+  // per-kernel-class instrumentation (option 2)
+  bool prof_on = false;
+  enum { NCLS = 8 };
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  std::vector<std::pair<int, size_t>> evmarks;   // (class, index of start event)
+  double kms[NCLS] = {0};
+  long long kcnt[NCLS] = {0};
+  unsigned long long kctr[2] = {0, 0};
+  Dev dctr;
   // scratch pool
   std::vector<Dev> scr;
   Dev ovf, sing;
@@ -380,6 +390,46 @@ struct Plan {
   ~Plan() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (auto e : evpool) cudaEventDestroy(e);
+  }
+
+  cudaEvent_t next_event() {
+    if (evused == evpool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      evpool.push_back(e);
+    }
+    return evpool[evused++];
+  }
+  // bracket a launch of class `cls` with events when profiling
+  void kbegin(int cls) {
+    if (!prof_on) return;
+    evmarks.push_back({cls, evused});
+    CK(cudaEventRecord(next_event(), st));
+  }
+  void kend() {
+    if (!prof_on) return;
+    CK(cudaEventRecord(next_event(), st));
+  }
+  void prof_reset() {
+    evused = 0;
+    evmarks.clear();
+    for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; }
+    kctr[0] = kctr[1] = 0;
+    if (prof_on) {
+      if (!dctr.p) dctr.alloc(2 * sizeof(unsigned long long), st);
+      CK(cudaMemsetAsync(dctr.p, 0, 2 * sizeof(unsigned long long), st));
+    }
+  }
+  void prof_collect() {   // after a stream sync
+    if (!prof_on) return;
+    for (auto& mk : evmarks) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, evpool[mk.second], evpool[mk.second + 1]));
+      kms[mk.first] += ms;
+      kcnt[mk.first] += 1;
+    }
+    CK(cudaMemcpy(kctr, dctr.p, sizeof(kctr), cudaMemcpyDeviceToHost));
   }
 
   template <class T> T* scratch(int slot, size_t count) {
@@ -434,7 +484,10 @@ struct Plan {
         A.gscr = nullptr;
         A.gscr_ntasks = 0;
         A.gscr_stride = 0;
+        A.ctr = prof_on ? dctr.as<unsigned long long>() : nullptr;
+        kbegin(0);
         CK(launch_trunc(A, nelem, (size_t)wb, st));
+        kend();
         ++launches;
       } else {
         // global work areas; chunk elements to bound the scratch
@@ -452,7 +505,10 @@ struct Plan {
           B.out = out + e0;
           offset_op(B.a, e0);
           offset_op(B.b, e0);
+          B.ctr = prof_on ? dctr.as<unsigned long long>() : nullptr;
+          kbegin(0);
           CK(launch_trunc(B, ce, 48 * 1024, st));
+          kend();
           ++launches;
         }
       }
@@ -524,7 +580,9 @@ struct Plan {
                    RA * RB, st));
       ++launches;
     }
+    kbegin(2);
     CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), st));
+    kend();
     ++launches;
     if (ht.branches.empty()) return;
     MMJob J[2];
@@ -556,7 +614,9 @@ struct Plan {
       j.nA = nA1;
       j.nB = ht.startB[nn] - ht.startB[1];
     }
+    kbegin(3);
     CK(launch_hmat(dt.T, J, 2, G, st));
+    kend();
     launches += 2;
     // M2: off12 = combine(f1, f2), off21 = combine(g1, g2)
     TruncArgs a;
@@ -652,7 +712,9 @@ struct Plan {
     // the two jobs need distinct t-buffers
     double* tb2 = scratch<double>(11, (size_t)c.G * std::max(J[0].nA, 1) * c.R * c.R);
     J[1].tbuf = tb2;
+    kbegin(3);
     CK(launch_hmat(dt.T, J, 2, c.G, st));
+    kend();
     launches += 2;
   }
 
@@ -677,7 +739,9 @@ struct Plan {
 
   void inv_node(InvCtx& c, int nu) {
     if (ht.isleaf[nu]) {
+      kbegin(1);
       CK(launch_leafinv(dt.T, c.H, c.G, nu, c.sing, st));
+      kend();
       ++launches;
       return;
     }
@@ -885,6 +949,7 @@ struct Plan {
     kept.clear();
     prof.clear();
     launches = 0;
+    prof_reset();
     factored = false;
     if (!ovf.p) ovf.alloc(sizeof(int), st);
     sing.alloc(sizeof(int) * std::max(m, 1), st);
@@ -978,6 +1043,7 @@ struct Plan {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
     fms = ms;
+    prof_collect();
     last = std::move(L);
     factored = true;
   }
@@ -1205,6 +1271,10 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
     h->p->keep_levels = value != 0;
     return ACR_OK;
   }
+  if (option == 2) {
+    h->p->prof_on = value != 0;
+    return ACR_OK;
+  }
   return set_err(h, ACR_EARG, "unknown option");
 }
 
@@ -1258,6 +1328,19 @@ long long acr_device_bytes(const acr_plan_t* h) {
 double acr_factor_ms(const acr_plan_t* h) { return h && h->p ? h->p->fms : -1.0; }
 double acr_solve_ms(const acr_plan_t* h) { return h && h->p ? h->p->sms : -1.0; }
 long long acr_kernel_launches(const acr_plan_t* h) { return h && h->p ? h->p->launches : -1; }
+
+int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
+                     double* ms, unsigned long long* counters) {
+  if (!h || !h->p || cls < 0 || cls >= Plan::NCLS) return ACR_EARG;
+  const Plan& P = *h->p;
+  *launches = P.kcnt[cls];
+  *ms = P.kms[cls];
+  if (counters) {
+    counters[0] = cls == 0 ? P.kctr[0] : 0;
+    counters[1] = cls == 0 ? P.kctr[1] : 0;
+  }
+  return ACR_OK;
+}
 
 int acr_last_error(const acr_plan_t* h, char* buf, int len) {
   const std::string& s = (h && h->p) ? h->p->err : g_err;

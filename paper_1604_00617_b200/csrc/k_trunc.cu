@@ -246,7 +246,11 @@ __global__ void __launch_bounds__(TT) k_trunc(TruncArgs A) {
         r = out.R;
       }
       if (r) copy_factor(s, Uo, Vo, um, vm, n, r);
-      if (tid == 0) *ro = r;
+      if (tid == 0) {
+        *ro = r;
+        if (A.ctr && r && !(s.U == Uo && s.V == Vo && s.sc == 1.0))
+          atomicAdd(A.ctr + 1, 16ull * (um + vm) * r);
+      }
       return;
     }
   } else {
@@ -362,6 +366,12 @@ __global__ void __launch_bounds__(TT) k_trunc(TruncArgs A) {
   if (keep > out.R) {
     if (tid == 0) atomicMax(A.overflow, keep);
     keep = 0;
+  }
+  if (A.ctr && tid == 0) {   // census formulas of SURVEY.md Appendix C
+    unsigned long long fl = 4ull * um * R * R + 4ull * vm * R * R + 24ull * R * R * R +
+                            2ull * (um + vm) * R * keep;
+    atomicAdd(A.ctr, fl);
+    atomicAdd(A.ctr + 1, 8ull * ((unsigned long long)um * R + vm * R + um * keep + vm * keep));
   }
   if (keep == 0) {
     if (tid == 0) *ro = 0;

@@ -1,0 +1,29 @@
+"""Quick timing of factor/solve per config on the GPU (development aid)."""
+import sys, time, json
+import numpy as np, torch
+sys.path.insert(0, ".")
+from paper_1604_00617_b200 import problems as P
+from paper_1604_00617_b200.solver import AcrSolver, relative_residual_gpu
+from paper_1604_00617_b200.system import Tolerance
+
+cfgs = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
+for name in cfgs:
+    c = P.CONFIGS[name]
+    t0 = time.time()
+    s = P.make_config(name)
+    tg = time.time() - t0
+    sol = AcrSolver(s.n_blocks, s.block_dim, Tolerance(c["eps"]), 1, c["leaf"])
+    bands = sol.device_bands(s)
+    f = torch.as_tensor(s.rhs, device="cuda")
+    times = []
+    for it in range(3):
+        sol.factor(bands)
+        times.append(sol.factor_ms)
+    u = sol.solve(f)
+    res = relative_residual_gpu(bands, u, f, s.n_blocks, s.block_dim)
+    prof = sol.rank_profiles()
+    print(json.dumps(dict(cfg=name, gen_s=round(tg, 2), factor_ms=[round(x, 2) for x in times],
+                          solve_ms=round(sol.solve_ms, 2), residual=res,
+                          max_rank=max(p.max_rank for p in prof), launches=sol.kernel_launches,
+                          storage=sol.storage_bytes(s.n_rhs),
+                          unknowns_per_s=s.n_unknowns / (min(times) / 1e3))), flush=True)
