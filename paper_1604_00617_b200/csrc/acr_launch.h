@@ -7,8 +7,15 @@
 namespace acr {
 
 long long trunc_need_doubles(int um, int vm, int R);
-cudaError_t launch_trunc(const TruncArgs& a, int nelem, size_t smem_bytes,
-                         cudaStream_t st);
+int trunc_warp_pool_doubles();
+// warp-per-task recompression; tasks too large for the warp pool are queued
+// to bigq and processed by a persistent block-level kernel (may_big)
+// direct: one 512-thread CTA per (task, element) -- small, latency-bound
+// launches; otherwise warp kernel, with oversized tasks queued to bigq
+cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
+                         int* bigq, int* bigcount, cudaStream_t st);
+int trunc_direct_max();
+long long warp_need_doubles(int um, int vm, int R);
 
 // leaf kernels (k_leaf.cu)
 cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,

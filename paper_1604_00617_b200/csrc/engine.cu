@@ -9,6 +9,7 @@
 // are decided per block on the device from device-resident ranks.  The
 // truncation schedule is the reference's.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -47,6 +48,8 @@ struct InternalError : std::runtime_error {
 // ---------------------------------------------------------------------------
 // stream-ordered device memory
 // ---------------------------------------------------------------------------
+static long long g_live = 0, g_peak = 0;   // bytes held through Dev
+
 struct Dev {
   void* p = nullptr;
   size_t n = 0;
@@ -57,10 +60,17 @@ struct Dev {
     release();
     st = s;
     n = bytes;
-    if (bytes) CK(cudaMallocAsync(&p, bytes, s));
+    if (bytes) {
+      CK(cudaMallocAsync(&p, bytes, s));
+      g_live += (long long)bytes;
+      if (g_live > g_peak) g_peak = g_live;
+    }
   }
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) {
+      cudaFreeAsync(p, st);
+      g_live -= (long long)n;
+    }
     p = nullptr;
     n = 0;
   }
@@ -366,6 +376,7 @@ struct Plan {
   double fms = 0, sms = 0;
   long long launches = 0;
   bool factored = false;
+  long long reserved = 0;
   std::string err;
   // per-kernel-class instrumentation (option 2)
   bool prof_on = false;
@@ -453,7 +464,8 @@ struct Plan {
     return t;
   }
 
-  // ---- truncation launcher: split by depth, size smem / global scratch ----
+  // ---- truncation launcher: warp kernel + persistent block kernel for
+  //      tasks that exceed the per-CTA smem pool ----
   void run_trunc(TruncArgs a, int t0, int t1, const HB* out, int nelem, int Ra,
                  int Rb) {
     if (t1 <= t0 || nelem <= 0) return;
@@ -462,58 +474,40 @@ struct Plan {
     a.eps = eps;
     a.cap = cap;
     a.overflow = ovf.as<int>();
+    a.tasks = dt.d_listA + 3 * t0;
+    a.ntasks = t1 - t0;
+    a.ctr = prof_on ? dctr.as<unsigned long long>() : nullptr;
     const int Rw = (a.mode == TM_TRUNCATE) ? Ra : Ra + Rb;
-    int i = t0;
-    while (i < t1) {
-      int b = ht.listA[i * 3 + 1];
-      int d = ht.depth[b];
-      int j = i;
-      long long worst = 0;
-      while (j < t1 && ht.depth[ht.listA[j * 3 + 1]] == d) {
-        int bb = ht.listA[j * 3 + 1];
-        int um = ht.mid[bb] - ht.lo[bb], vm = ht.hi[bb] - ht.mid[bb];
-        worst = std::max(worst, trunc_need_doubles(std::max(um, vm), std::max(um, vm), Rw));
-        ++j;
-      }
-      TruncArgs A = a;
-      A.tasks = dt.d_listA + 3 * i;
-      A.ntasks = j - i;
-      long long wb = worst * 8 + 64;
-      if (wb <= SMEM_MAX_BYTES) {
-        A.smem_doubles = (int)worst;
-        A.gscr = nullptr;
-        A.gscr_ntasks = 0;
-        A.gscr_stride = 0;
-        A.ctr = prof_on ? dctr.as<unsigned long long>() : nullptr;
-        kbegin(0);
-        CK(launch_trunc(A, nelem, (size_t)wb, st));
-        kend();
-        ++launches;
-      } else {
-        // global work areas; chunk elements to bound the scratch
-        long long per_elem = worst * (long long)A.ntasks * 8;
-        int chunk = (int)std::max<long long>(1, GSCR_BUDGET_BYTES / per_elem);
-        chunk = std::min(chunk, nelem);
-        double* g = scratch<double>(10, (size_t)worst * A.ntasks * chunk);
-        A.gscr = g;
-        A.gscr_stride = worst;
-        A.gscr_ntasks = A.ntasks;
-        A.smem_doubles = (int)(48 * 1024 / 8);
-        for (int e0 = 0; e0 < nelem; e0 += chunk) {
-          int ce = std::min(chunk, nelem - e0);
-          TruncArgs B = A;
-          B.out = out + e0;
-          offset_op(B.a, e0);
-          offset_op(B.b, e0);
-          B.ctr = prof_on ? dctr.as<unsigned long long>() : nullptr;
-          kbegin(0);
-          CK(launch_trunc(B, ce, 48 * 1024, st));
-          kend();
-          ++launches;
-        }
-      }
-      i = j;
+    long long wworst = 0, bworst = 0;
+    for (int i = t0; i < t1; ++i) {
+      int bb = ht.listA[i * 3 + 1];
+      int um = ht.mid[bb] - ht.lo[bb], vm = ht.hi[bb] - ht.mid[bb];
+      wworst = std::max(wworst, warp_need_doubles(um, vm, Rw));
+      bworst = std::max(bworst, trunc_need_doubles(um, vm, Rw));
     }
+    const int nitems = a.ntasks * nelem;
+    const bool direct = nitems <= trunc_direct_max();
+    const bool may_big = !direct && wworst > trunc_warp_pool_doubles();
+    int* q = nullptr;
+    int* qc = nullptr;
+    const long long SMD = 24576;                 // 192 KB of doubles
+    a.smem_doubles = (int)std::min(bworst, SMD);
+    a.gscr = nullptr;
+    a.gscr_stride = 0;
+    a.gscr_ntasks = 0;
+    if (may_big) {
+      q = scratch<int>(13, (size_t)nitems + 1);
+      qc = scratch<int>(14, 4);
+    }
+    if ((direct || may_big) && bworst > SMD) {
+      const int nblk = direct ? nitems : std::min(nitems, 148);
+      a.gscr = scratch<double>(10, (size_t)nblk * bworst);
+      a.gscr_stride = bworst;
+    }
+    kbegin(0);
+    CK(launch_trunc(a, nelem, direct, may_big, q, qc, st));
+    kend();
+    launches += may_big ? 2 : 1;
   }
 
   static void offset_src(Src& s, int e0) {
@@ -928,8 +922,13 @@ struct Plan {
                ht.lo[v], ht.hi[v], lvl, 2 * bad);
       throw SingularError(buf);
     }
-    if (dbg())
-      fprintf(stderr, "[acr] level %d m=%d Rout=%d overflow=%d\n", lvl, mm, Rout, h_ovf);
+    if (dbg()) {
+      static auto t_prev = std::chrono::steady_clock::now();
+      auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[acr] level %d m=%d Rout=%d overflow=%d host_ms=%.2f\n", lvl, mm, Rout,
+              h_ovf, std::chrono::duration<double, std::milli>(now - t_prev).count());
+      t_prev = now;
+    }
     if (h_ovf) {
       if (h_ovf >= (1 << 29)) throw InternalError("truncation work area too small");
       if (h_ovf > 4 * n + 64) throw InternalError("implausible rank " + std::to_string(h_ovf));
@@ -956,6 +955,18 @@ struct Plan {
     if (!ev0) {
       CK(cudaEventCreate(&ev0));
       CK(cudaEventCreate(&ev1));
+    }
+    // keep the stream-ordered pool at the footprint of the previous factor so
+    // later factors never map new memory in the middle of a level
+    if (g_peak > 0 && reserved < g_peak) {
+      void* r = nullptr;
+      size_t want = (size_t)(g_peak - g_live) + ((size_t)g_peak >> 3);
+      if (cudaMallocAsync(&r, want, st) == cudaSuccess) {
+        cudaFreeAsync(r, st);
+        reserved = g_peak;
+      } else {
+        cudaGetLastError();
+      }
     }
     CK(cudaEventRecord(ev0, st));
     Level L;
@@ -1486,18 +1497,13 @@ int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
     a.cap = max_rank_cap;
     a.overflow = ovf.as<int>();
     long long need = acr::trunc_need_doubles(m, k, Rc);
-    acr::Dev g;
-    if (need * 8 + 64 <= acr::SMEM_MAX_BYTES) {
-      a.smem_doubles = (int)need;
-      CK(acr::launch_trunc(a, 1, need * 8 + 64, st));
-    } else {
-      g.alloc(sizeof(double) * need, st);
-      a.gscr = g.as<double>();
-      a.gscr_stride = need;
-      a.gscr_ntasks = 1;
-      a.smem_doubles = 0;
-      CK(acr::launch_trunc(a, 1, 64, st));
-    }
+    acr::Dev g(sizeof(double) * std::max<long long>(need, 1) * 148, st);
+    acr::Dev q(sizeof(int) * 4, st), qc(sizeof(int) * 4, st);
+    a.smem_doubles = 24576;
+    a.gscr = g.as<double>();
+    a.gscr_stride = need;
+    a.smem_doubles = (int)std::min<long long>(need, 24576);
+    CK(acr::launch_trunc(a, 1, true, false, q.as<int>(), qc.as<int>(), st));
     int hr2[6];
     CK(cudaMemcpyAsync(hr2, rk.p, sizeof(hr2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -18,23 +18,29 @@ static constexpr int LT = 128;
 
 // ---------------------------------------------------------------------------
 // leaf inverse: in-place Gauss-Jordan with row partial pivoting (the pivot
-// sequence equals getrf's), column swaps undone at the end.
+// sequence equals getrf's: first index of the largest |a_ik|), column swaps
+// undone at the end.  256 threads; thread t owns column (t mod cp) of rows
+// (t / cp) + k*rs, so no runtime division in the O(s^3) loop.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(LT) k_leafinv(TreeDev T, const HB* H, int leaf,
+static constexpr int IT = 256;
+
+__global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf,
                                                 int* sing) {
   extern __shared__ double sm[];
   const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
   const int ld = s + 1;
   double* A = sm;
-  int* piv = reinterpret_cast<int*>(A + s * ld);
-  __shared__ double pv;
+  double* colk = A + s * ld;
+  int* piv = reinterpret_cast<int*>(colk + s);
+  __shared__ double pv, akk;
   __shared__ int pidx, bad;
+  const int cp = s <= 32 ? 32 : (s <= 64 ? 64 : 128);
+  const int rs = IT / cp;
+  const int tj = tid & (cp - 1), ti0 = tid / cp;
   double* L = H[g].leaf + (long long)lo * bw;
-  for (int idx = tid; idx < s * s; idx += LT) {
-    int i = idx / s, j = idx - i * s;
-    A[i * ld + j] = L[(long long)i * bw + j];
-  }
+  if (tj < s)
+    for (int i = ti0; i < s; i += rs) A[i * ld + tj] = L[(long long)i * bw + tj];
   if (tid == 0) bad = 0;
   __syncthreads();
   for (int k = 0; k < s; ++k) {
@@ -55,39 +61,38 @@ __global__ void __launch_bounds__(LT) k_leafinv(TreeDev T, const HB* H, int leaf
         pidx = bi;
         piv[k] = bi;
         pv = A[bi * ld + k];
+        akk = A[k * ld + k];
         if (pv == 0.0) bad = 1;
       }
     }
     __syncthreads();
     if (bad) break;
     const int p = pidx;
-    if (p != k)
-      for (int j = tid; j < s; j += LT) {
-        double t = A[k * ld + j];
-        A[k * ld + j] = A[p * ld + j];
-        A[p * ld + j] = t;
-      }
-    __syncthreads();
     const double inv = 1.0 / pv;
-    if (tid == 0) A[k * ld + k] = 1.0;
-    __syncthreads();
-    for (int j = tid; j < s; j += LT) A[k * ld + j] *= inv;
-    __syncthreads();
-    for (int idx = tid; idx < s * s; idx += LT) {
-      int i = idx / s, j = idx - i * s;
-      if (i == k || j == k) continue;
-      A[i * ld + j] -= A[i * ld + k] * A[k * ld + j];
+    // swap rows k <-> p and scale the new pivot row; save column k
+    for (int j = tid; j < s; j += IT) {
+      double rk = A[k * ld + j], rp = A[p * ld + j];
+      if (p != k) A[p * ld + j] = rk;
+      A[k * ld + j] = (j == k) ? inv : rp * inv;
     }
+    for (int i = tid; i < s; i += IT)
+      colk[i] = (i == k) ? 0.0 : (i == p ? akk : A[i * ld + k]);
     __syncthreads();
-    for (int i = tid; i < s; i += LT)
-      if (i != k) A[i * ld + k] = -A[i * ld + k] * A[k * ld + k];
+    if (tj < s) {
+      const double akj = A[k * ld + tj];
+      for (int i = ti0; i < s; i += rs) {
+        if (i == k) continue;
+        if (tj != k) A[i * ld + tj] -= colk[i] * akj;
+        else A[i * ld + k] = -colk[i] * akj;
+      }
+    }
     __syncthreads();
   }
   if (!bad) {
     for (int k = s - 1; k >= 0; --k) {
       int p = piv[k];
       if (p != k)
-        for (int i = tid; i < s; i += LT) {
+        for (int i = tid; i < s; i += IT) {
           double t = A[i * ld + k];
           A[i * ld + k] = A[i * ld + p];
           A[i * ld + p] = t;
@@ -95,12 +100,12 @@ __global__ void __launch_bounds__(LT) k_leafinv(TreeDev T, const HB* H, int leaf
       __syncthreads();
     }
     int nf = 0;
-    for (int idx = tid; idx < s * s; idx += LT) {
-      int i = idx / s, j = idx - i * s;
-      double v = A[i * ld + j];
-      if (!isfinite(v)) nf = 1;
-      L[(long long)i * bw + j] = v;
-    }
+    if (tj < s)
+      for (int i = ti0; i < s; i += rs) {
+        double v = A[i * ld + tj];
+        if (!isfinite(v)) nf = 1;
+        L[(long long)i * bw + tj] = v;
+      }
     if (__syncthreads_or(nf) && tid == 0) bad = 1;
   }
   __syncthreads();
@@ -117,14 +122,14 @@ cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
                            int* sing, cudaStream_t st) {
   if (!nelem) return cudaSuccess;
   int s = T.bw;
-  size_t smem = (size_t)s * (s + 1) * 8 + (size_t)s * 4 + 16;
+  size_t smem = (size_t)s * (s + 1) * 8 + (size_t)s * 8 + (size_t)s * 4 + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_leafinv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr = true;
   }
-  k_leafinv<<<nelem, LT, smem, st>>>(T, H, leaf, sing);
+  k_leafinv<<<nelem, IT, smem, st>>>(T, H, leaf, sing);
   return cudaGetLastError();
 }
 

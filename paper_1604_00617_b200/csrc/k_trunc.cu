@@ -17,7 +17,8 @@
 
 namespace acr {
 
-static constexpr int TT = 128;   // threads per truncation CTA
+static constexpr int TT = 512;   // threads per block-path truncation CTA
+static constexpr int NWB = TT / 32;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -30,7 +31,10 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  return red[0] + red[1] + red[2] + red[3];
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < NWB; ++w) s += red[w];   // fixed order
+  return s;
 }
 
 struct OpRes {
@@ -137,61 +141,78 @@ __device__ void block_apply_q(const double* W, int mr, int p, const double* tau,
 
 // Round-robin (circle method) pairing of np players (np even).
 __device__ __forceinline__ int rr_player(int step, int x, int np) {
-  return x == 0 ? 0 : 1 + ((x - 1 + step) % (np - 1));
+  if (x == 0) return 0;
+  int t = x - 1 + step;              // < 2 (np - 1): one conditional wrap
+  if (t >= np - 1) t -= np - 1;
+  return 1 + t;
 }
 
 // One-sided Jacobi on B (pr x pc, column-major ld pr) accumulating J (pc x pc).
+// The disjoint pairs of one round-robin step are spread over lane groups of
+// size gs (power of two) across the whole CTA.
 __device__ void block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   for (int i = tid; i < pc * pc; i += TT) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
-  const int np = pc + (pc & 1);
-  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
   __syncthreads();
   if (pc < 2) return;
+  const int np = pc + (pc & 1), npairs = np / 2;
+  int gs = 32;
+  while (gs > 1 && gs * npairs > TT) gs >>= 1;
+  const int per = TT / gs;
+  const int sub = tid & (gs - 1), grp = tid / gs;
+  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  (void)flag;
   for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) *flag = 0;
-    __syncthreads();
+    int rot = 0;
     for (int step = 0; step < np - 1; ++step) {
-      for (int k = warp; k < np / 2; k += TT / 32) {
-        int i = rr_player(step, k, np), j = rr_player(step, np - 1 - k, np);
-        if (i >= pc || j >= pc) continue;
+      for (int base = 0; base < npairs; base += per) {
+        const int k = base + grp;
+        int i = 0, j = 0;
+        bool valid = k < npairs;
+        if (valid) {
+          i = rr_player(step, k, np);
+          j = rr_player(step, np - 1 - k, np);
+          valid = i < pc && j < pc;
+        }
+        double a = 0.0, b = 0.0, c = 0.0;
         double* bi = B + (long long)i * pr;
         double* bj = B + (long long)j * pr;
-        double a = 0.0, b = 0.0, c = 0.0;
-        for (int r = lane; r < pr; r += 32) {
-          double x = bi[r], y = bj[r];
-          a += x * x;
-          b += y * y;
-          c += x * y;
+        if (valid)
+          for (int r = sub; r < pr; r += gs) {
+            double x = bi[r], y = bj[r];
+            a += x * x;
+            b += y * y;
+            c += x * y;
+          }
+        for (int o = gs >> 1; o; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          c += __shfl_xor_sync(0xffffffffu, c, o);
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        c = warp_sum(c);
-        if (a == 0.0 || b == 0.0 || c == 0.0) continue;
-        if (fabs(c) <= tol * sqrt(a) * sqrt(b)) continue;
-        double zeta = (b - a) / (2.0 * c);
-        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double cs = 1.0 / sqrt(1.0 + t * t);
-        double sn = cs * t;
-        for (int r = lane; r < pr; r += 32) {
-          double x = bi[r], y = bj[r];
-          bi[r] = cs * x - sn * y;
-          bj[r] = sn * x + cs * y;
+        if (valid && a != 0.0 && b != 0.0 && c != 0.0 &&
+            fabs(c) > tol * sqrt(a) * sqrt(b)) {
+          double zeta = (b - a) / (2.0 * c);
+          double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double cs = 1.0 / sqrt(1.0 + t * t);
+          double sn = cs * t;
+          for (int r = sub; r < pr; r += gs) {
+            double x = bi[r], y = bj[r];
+            bi[r] = cs * x - sn * y;
+            bj[r] = sn * x + cs * y;
+          }
+          double* ji = J + (long long)i * pc;
+          double* jj = J + (long long)j * pc;
+          for (int r = sub; r < pc; r += gs) {
+            double x = ji[r], y = jj[r];
+            ji[r] = cs * x - sn * y;
+            jj[r] = sn * x + cs * y;
+          }
+          rot = 1;
         }
-        double* ji = J + (long long)i * pc;
-        double* jj = J + (long long)j * pc;
-        for (int r = lane; r < pc; r += 32) {
-          double x = ji[r], y = jj[r];
-          ji[r] = cs * x - sn * y;
-          jj[r] = sn * x + cs * y;
-        }
-        if (lane == 0) *flag = 1;
+        __syncthreads();
       }
-      __syncthreads();
     }
-    int f = *flag;
-    __syncthreads();
-    if (!f) break;
+    if (!__syncthreads_or(rot)) break;
   }
 }
 
@@ -208,85 +229,75 @@ __device__ void copy_factor(const OpRes& s, double* Uo, double* Vo, int um,
   }
 }
 
-__global__ void __launch_bounds__(TT) k_trunc(TruncArgs A) {
-  extern __shared__ double sm[];
-  __shared__ double red[8];
-  __shared__ int iflag[2];
-  const int task = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+// ---------------------------------------------------------------------------
+// task resolution shared by the warp and block paths
+// ---------------------------------------------------------------------------
+struct TaskCtx {
+  OpRes a, b;
+  int um, vm;
+  double* Uo;
+  double* Vo;
+  int* ro;
+  int Rout;
+};
+
+__device__ __forceinline__ TaskCtx resolve_task(const TruncArgs& A, int task, int g) {
   const TreeDev& T = A.T;
   const int n = T.n;
   const int beta = A.tasks[task * 3 + 1], side = A.tasks[task * 3 + 2];
   const int lo = T.lo[beta], hi = T.hi[beta], mid = T.mid[beta];
-  const int urow = side ? mid : lo, um = side ? hi - mid : mid - lo;
-  const int vrow = side ? lo : mid, vm = side ? mid - lo : hi - mid;
-  OpRes a = resolve_op(A.a, T, g, beta, side, urow, vrow);
-  OpRes b;
-  b.r = 0;
-  b.U = b.V = nullptr;
-  b.sc = 1.0;
-  if (A.mode != TM_TRUNCATE) b = resolve_op(A.b, T, g, beta, side, urow, vrow);
+  const int urow = side ? mid : lo;
+  const int vrow = side ? lo : mid;
+  TaskCtx c;
+  c.um = side ? hi - mid : mid - lo;
+  c.vm = side ? mid - lo : hi - mid;
+  c.a = resolve_op(A.a, T, g, beta, side, urow, vrow);
+  c.b.r = 0;
+  c.b.U = c.b.V = nullptr;
+  c.b.sc = 1.0;
+  if (A.mode != TM_TRUNCATE) c.b = resolve_op(A.b, T, g, beta, side, urow, vrow);
   if (A.mode == TM_COMBINE_SWAP1 && side == 1) {
-    OpRes t = a;
-    a = b;
-    b = t;
+    OpRes t = c.a;
+    c.a = c.b;
+    c.b = t;
   }
   const HB out = A.out[g];
   const long long oslot = (long long)T.depth[beta] * out.R * n;
-  double* Uo = out.U + oslot + urow;
-  double* Vo = out.V + oslot + vrow;
-  int* ro = out.rk + beta * 2 + side;
-  __syncthreads();   // every thread has read the ranks before any write
+  c.Uo = out.U + oslot + urow;
+  c.Vo = out.V + oslot + vrow;
+  c.ro = out.rk + beta * 2 + side;
+  c.Rout = out.R;
+  return c;
+}
 
-  if (A.mode != TM_TRUNCATE) {
-    if (a.r == 0 || b.r == 0) {                      // algebra.py:93-96
-      const OpRes& s = a.r ? a : b;
-      int r = s.r;
-      if (r > out.R) {
-        if (tid == 0) atomicMax(A.overflow, r);
-        r = out.R;
-      }
-      if (r) copy_factor(s, Uo, Vo, um, vm, n, r);
-      if (tid == 0) {
-        *ro = r;
-        if (A.ctr && r && !(s.U == Uo && s.V == Vo && s.sc == 1.0))
-          atomicAdd(A.ctr + 1, 16ull * (um + vm) * r);
-      }
-      return;
-    }
-  } else {
-    if (a.r == 0) {
-      if (tid == 0) *ro = 0;
-      return;
-    }
-    if (a.r == 1) {                                   // hodlr.py:181-185
-      double nzu = 0.0, nzv = 0.0;
-      for (int i = tid; i < um; i += TT) nzu += (a.U[i] != 0.0) ? 1.0 : 0.0;
-      for (int i = tid; i < vm; i += TT) nzv += (a.V[i] != 0.0) ? 1.0 : 0.0;
-      nzu = block_sum(nzu, red);
-      nzv = block_sum(nzv, red);
-      int r = (nzu > 0.0 && nzv > 0.0) ? 1 : 0;
-      if (r > out.R) {
-        if (tid == 0) atomicMax(A.overflow, r);
-        r = 0;
-      }
-      if (r) copy_factor(a, Uo, Vo, um, vm, n, 1);
-      if (tid == 0) *ro = r;
-      return;
-    }
-  }
+// 0: nothing to compute beyond a copy / zero (handled by the caller), 1: full
+__device__ __forceinline__ bool task_is_full(const TruncArgs& A, const TaskCtx& c) {
+  if (A.mode != TM_TRUNCATE) return c.a.r > 0 && c.b.r > 0;
+  return c.a.r >= 2;
+}
 
-  // ---- full truncation of [a | b] -------------------------------------
+__host__ __device__ long long trunc_need_doubles(int um, int vm, int R) {
+  return 2LL * (um + vm) * R + 2LL * R * R + 4LL * R + 8;
+}
+
+__host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
+  return (long long)(um + vm) * R + 2LL * R * R + 4LL * R + (um > vm ? um : vm) + 8;
+}
+
+// ---------------------------------------------------------------------------
+// block path (one CTA per queued task; used for tasks too large for a warp)
+// ---------------------------------------------------------------------------
+__device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
+                                 double* red, int* iflag) {
+  const int tid = threadIdx.x, n = A.T.n;
+  const OpRes& a = tc.a;
+  const OpRes& b = tc.b;
+  const int um = tc.um, vm = tc.vm;
+  double* Uo = tc.Uo;
+  double* Vo = tc.Vo;
+  int* ro = tc.ro;
   const int R = a.r + b.r;
   const int pu = um < R ? um : R, pv = vm < R ? vm : R;
-  const long long need = 2LL * (um + vm) * R + 2LL * R * R + 4LL * R + 8;
-  double* wk = sm;
-  if (need > A.smem_doubles) {
-    if (task >= A.gscr_ntasks || A.gscr == nullptr) {
-      if (tid == 0) atomicMax(A.overflow, 1 << 29);
-      return;
-    }
-    wk = A.gscr + ((long long)g * A.gscr_ntasks + task) * A.gscr_stride;
-  }
   double* Uw = wk;
   double* Vw = Uw + (long long)um * R;
   double* Ou = Vw + (long long)vm * R;
@@ -308,8 +319,8 @@ __global__ void __launch_bounds__(TT) k_trunc(TruncArgs A) {
     Vw[idx] = c < a.r ? a.V[(long long)c * n + i] : b.V[(long long)(c - a.r) * n + i];
   }
   __syncthreads();
-  block_qr(Uw, um, R, tauU, red, red + 4);
-  block_qr(Vw, vm, R, tauV, red, red + 4);
+  block_qr(Uw, um, R, tauU, red, red + NWB);
+  block_qr(Vw, vm, R, tauV, red, red + NWB);
 
   // Frobenius norms of the triangular factors (hodlr.py:191-192)
   double nu2 = 0.0, nv2 = 0.0;
@@ -363,7 +374,7 @@ __global__ void __launch_bounds__(TT) k_trunc(TruncArgs A) {
     for (int i = 0; i < pc; ++i) keep += sig[i] >= thr;
     if (A.cap > 0 && keep > A.cap) keep = A.cap;
   }
-  if (keep > out.R) {
+  if (keep > tc.Rout) {
     if (tid == 0) atomicMax(A.overflow, keep);
     keep = 0;
   }
@@ -406,22 +417,450 @@ __global__ void __launch_bounds__(TT) k_trunc(TruncArgs A) {
   if (tid == 0) *ro = keep;
 }
 
-long long trunc_need_doubles(int um, int vm, int R) {
-  return 2LL * (um + vm) * R + 2LL * R * R + 4LL * R + 8;
+
+// rank-0 / passthrough / rank-1 shortcut cases, whole CTA (uniform branch)
+__device__ bool block_trivial(const TruncArgs& A, const TaskCtx& c, double* red) {
+  const int tid = threadIdx.x, n = A.T.n;
+  if (A.mode != TM_TRUNCATE && (c.a.r == 0 || c.b.r == 0)) {   // algebra.py:93-96
+    const OpRes& s = c.a.r ? c.a : c.b;
+    int r = s.r;
+    if (r > c.Rout) {
+      if (tid == 0) atomicMax(A.overflow, r);
+      r = c.Rout;
+    }
+    if (r) copy_factor(s, c.Uo, c.Vo, c.um, c.vm, n, r);
+    if (tid == 0) {
+      *c.ro = r;
+      if (A.ctr && r && !(s.U == c.Uo && s.V == c.Vo && s.sc == 1.0))
+        atomicAdd(A.ctr + 1, 16ull * (c.um + c.vm) * r);
+    }
+    return true;
+  }
+  if (A.mode == TM_TRUNCATE && c.a.r < 2) {
+    int r = 0;
+    if (c.a.r == 1) {                                           // hodlr.py:181-185
+      double nzu = 0.0, nzv = 0.0;
+      for (int i = tid; i < c.um; i += TT) nzu += (c.a.U[i] != 0.0) ? 1.0 : 0.0;
+      for (int i = tid; i < c.vm; i += TT) nzv += (c.a.V[i] != 0.0) ? 1.0 : 0.0;
+      nzu = block_sum(nzu, red);
+      nzv = block_sum(nzv, red);
+      r = (nzu > 0.0 && nzv > 0.0) ? 1 : 0;
+      if (r > c.Rout) {
+        if (tid == 0) atomicMax(A.overflow, r);
+        r = 0;
+      }
+      if (r) copy_factor(c.a, c.Uo, c.Vo, c.um, c.vm, n, 1);
+    }
+    if (tid == 0) *c.ro = r;
+    return true;
+  }
+  return false;
 }
 
-cudaError_t launch_trunc(const TruncArgs& a, int nelem, size_t smem_bytes,
-                         cudaStream_t st) {
+// q == nullptr: direct mode, one CTA per item (small launches, latency bound)
+// otherwise: persistent CTAs over the queue of tasks the warp path rejected
+__global__ void __launch_bounds__(TT) k_trunc_big(TruncArgs A, const int* q,
+                                                  const int* qcount, int nitems) {
+  extern __shared__ double sm[];
+  __shared__ double red[NWB + 4];
+  __shared__ int iflag[2];
+  const int cnt = q ? *qcount : nitems;
+  for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+    const int item = q ? q[i] : i;
+    const int task = item % A.ntasks, g = item / A.ntasks;
+    TaskCtx c = resolve_task(A, task, g);
+    __syncthreads();
+    if (!q && block_trivial(A, c, red)) {
+      __syncthreads();
+      continue;
+    }
+    const int R = c.a.r + c.b.r;
+    const long long need = trunc_need_doubles(c.um, c.vm, R);
+    double* wk = sm;
+    if (need > A.smem_doubles) {
+      if (A.gscr == nullptr || need > A.gscr_stride) {
+        if (threadIdx.x == 0) atomicMax(A.overflow, 1 << 29);
+        continue;
+      }
+      wk = A.gscr + (long long)blockIdx.x * A.gscr_stride;
+    }
+    trunc_block_full(A, c, wk, red, iflag);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// warp path: one warp per task, work area carved from a per-CTA smem pool
+// ---------------------------------------------------------------------------
+static constexpr int TW = 16;          // warps per CTA
+static constexpr int SLOT = 512;       // doubles per slot
+static constexpr int NSLOT = 48;       // 192 KB pool
+static constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns) {
+  const unsigned long long want = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
+  while (true) {
+    unsigned long long m = atomicAdd(mask, 0ull);
+    int s = -1;
+    for (int k = 0; k + ns <= NSLOT; ++k)
+      if (((m >> k) & want) == 0ull) { s = k; break; }
+    if (s >= 0) {
+      unsigned long long w = want << s;
+      if (atomicCAS(mask, m, m | w) == m) return s;
+      continue;
+    }
+    __nanosleep(128);
+  }
+}
+
+__device__ __forceinline__ void warp_copy_factor(const OpRes& s, double* Uo, double* Vo,
+                                                 int um, int vm, int n, int r, int lane) {
+  if (s.U == Uo && s.V == Vo && s.sc == 1.0) return;
+  for (int c = 0; c < r; ++c) {
+    const double* su = s.U + (long long)c * n;
+    double* du = Uo + (long long)c * n;
+    for (int i = lane; i < um; i += 32) du[i] = s.sc * su[i];
+    const double* sv = s.V + (long long)c * n;
+    double* dv = Vo + (long long)c * n;
+    for (int i = lane; i < vm; i += 32) dv[i] = sv[i];
+  }
+}
+
+// Householder QR of W (mr x R, col-major ld mr) by one warp
+__device__ void warp_qr(double* W, int mr, int R, double* tau, int lane) {
+  const int p = mr < R ? mr : R;
+  for (int j = 0; j < p; ++j) {
+    double* cj = W + (long long)j * mr;
+    double ss = 0.0;
+    for (int i = j + 1 + lane; i < mr; i += 32) ss += cj[i] * cj[i];
+    ss = warp_sum(ss);
+    const double alpha = cj[j];
+    double tj = 0.0, scal = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncwarp();
+    if (tj != 0.0) {
+      for (int i = j + 1 + lane; i < mr; i += 32) cj[i] *= scal;
+      if (lane == 0) cj[j] = beta;
+    }
+    if (lane == 0) tau[j] = tj;
+    __syncwarp();
+    if (tj != 0.0) {
+      for (int c = j + 1; c < R; ++c) {
+        double* cc = W + (long long)c * mr;
+        double w = 0.0;
+        for (int i = j + 1 + lane; i < mr; i += 32) w += cj[i] * cc[i];
+        w = (warp_sum(w) + cc[j]) * tj;
+        for (int i = j + 1 + lane; i < mr; i += 32) cc[i] -= w * cj[i];
+        if (lane == 0) cc[j] -= w;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// x (length mr) := Q x,  Q = H_0 ... H_{p-1}
+__device__ void warp_apply_q(const double* W, int mr, int p, const double* tau,
+                             double* x, int lane) {
+  for (int j = p - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double* v = W + (long long)j * mr;
+    double w = 0.0;
+    for (int i = j + 1 + lane; i < mr; i += 32) w += v[i] * x[i];
+    w = (warp_sum(w) + x[j]) * tj;
+    for (int i = j + 1 + lane; i < mr; i += 32) x[i] -= w * v[i];
+    __syncwarp();
+    if (lane == 0) x[j] -= w;
+    __syncwarp();
+  }
+}
+
+// one-sided Jacobi on B (pr x pc col-major), J (pc x pc); pairs of a
+// round-robin step are spread over lane groups of size gs
+__device__ void warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
+  for (int i = lane; i < pc * pc; i += 32) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
+  __syncwarp();
+  if (pc < 2) return;
+  const int np = pc + (pc & 1), npairs = np / 2;
+  int gs = 32;
+  while (gs > 1 && gs * npairs > 32) gs >>= 1;
+  const int per = 32 / gs;                 // pairs per pass
+  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  const int sub = lane & (gs - 1), grp = lane / gs;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rot = false;
+    for (int step = 0; step < np - 1; ++step) {
+      for (int base = 0; base < npairs; base += per) {
+        const int k = base + grp;
+        int i = 0, j = 0;
+        bool valid = k < npairs;
+        if (valid) {
+          i = rr_player(step, k, np);
+          j = rr_player(step, np - 1 - k, np);
+          valid = i < pc && j < pc;
+        }
+        double a = 0.0, b = 0.0, c = 0.0;
+        double* bi = B + (long long)i * pr;
+        double* bj = B + (long long)j * pr;
+        if (valid)
+          for (int r = sub; r < pr; r += gs) {
+            double x = bi[r], y = bj[r];
+            a += x * x;
+            b += y * y;
+            c += x * y;
+          }
+        for (int o = gs >> 1; o; o >>= 1) {
+          a += __shfl_xor_sync(FULL, a, o);
+          b += __shfl_xor_sync(FULL, b, o);
+          c += __shfl_xor_sync(FULL, c, o);
+        }
+        if (valid && a != 0.0 && b != 0.0 && c != 0.0 &&
+            fabs(c) > tol * sqrt(a) * sqrt(b)) {
+          double zeta = (b - a) / (2.0 * c);
+          double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double cs = 1.0 / sqrt(1.0 + t * t);
+          double sn = cs * t;
+          for (int r = sub; r < pr; r += gs) {
+            double x = bi[r], y = bj[r];
+            bi[r] = cs * x - sn * y;
+            bj[r] = sn * x + cs * y;
+          }
+          double* ji = J + (long long)i * pc;
+          double* jj = J + (long long)j * pc;
+          for (int r = sub; r < pc; r += gs) {
+            double x = ji[r], y = jj[r];
+            ji[r] = cs * x - sn * y;
+            jj[r] = sn * x + cs * y;
+          }
+          rot = true;
+        }
+        __syncwarp();
+      }
+    }
+    if (!__any_sync(FULL, rot)) break;
+  }
+}
+
+__device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
+                                int lane) {
+  const int n = A.T.n;
+  const OpRes& a = tc.a;
+  const OpRes& b = tc.b;
+  const int um = tc.um, vm = tc.vm;
+  const int R = a.r + b.r;
+  const int pu = um < R ? um : R, pv = vm < R ? vm : R;
+  double* Uw = wk;
+  double* Vw = Uw + (long long)um * R;
+  double* Bm = Vw + (long long)vm * R;
+  double* Jm = Bm + (long long)R * R;
+  double* tauU = Jm + (long long)R * R;
+  double* tauV = tauU + R;
+  double* sig = tauV + R;
+  int* ord = reinterpret_cast<int*>(sig + R);
+  double* ob = sig + 2 * R;
+  for (int c = 0; c < R; ++c) {
+    const bool fa = c < a.r;
+    const double* su = fa ? a.U + (long long)c * n : b.U + (long long)(c - a.r) * n;
+    const double sc = fa ? a.sc : b.sc;
+    for (int i = lane; i < um; i += 32) Uw[(long long)c * um + i] = sc * su[i];
+    const double* sv = fa ? a.V + (long long)c * n : b.V + (long long)(c - a.r) * n;
+    for (int i = lane; i < vm; i += 32) Vw[(long long)c * vm + i] = sv[i];
+  }
+  __syncwarp();
+  warp_qr(Uw, um, R, tauU, lane);
+  warp_qr(Vw, vm, R, tauV, lane);
+  double nu2 = 0.0, nv2 = 0.0;
+  for (int idx = lane; idx < pu * R; idx += 32) {
+    int l = idx / pu, i = idx - l * pu;
+    if (l >= i) { double x = Uw[(long long)l * um + i]; nu2 += x * x; }
+  }
+  for (int idx = lane; idx < pv * R; idx += 32) {
+    int l = idx / pv, i = idx - l * pv;
+    if (l >= i) { double x = Vw[(long long)l * vm + i]; nv2 += x * x; }
+  }
+  nu2 = warp_sum(nu2);
+  nv2 = warp_sum(nv2);
+  const bool tr = pu < pv;
+  const int pr = tr ? pv : pu, pc = tr ? pu : pv;
+  for (int idx = lane; idx < pu * pv; idx += 32) {
+    int i = idx / pv, j = idx - i * pv;
+    int l0 = i > j ? i : j;
+    double s = 0.0;
+    for (int l = l0; l < R; ++l) s += Uw[(long long)l * um + i] * Vw[(long long)l * vm + j];
+    if (!tr) Bm[(long long)j * pr + i] = s;
+    else Bm[(long long)i * pr + j] = s;
+  }
+  __syncwarp();
+  warp_jacobi(Bm, pr, pc, Jm, lane);
+  for (int j = lane; j < pc; j += 32) {
+    double s = 0.0;
+    const double* bj = Bm + (long long)j * pr;
+    for (int r = 0; r < pr; ++r) s += bj[r] * bj[r];
+    sig[j] = sqrt(s);
+  }
+  __syncwarp();
+  for (int j = lane; j < pc; j += 32) {
+    double sj = sig[j];
+    int rnk = 0;
+    for (int i = 0; i < pc; ++i) {
+      double si = sig[i];
+      rnk += (si > sj) || (si == sj && i < j);
+    }
+    ord[rnk] = j;
+  }
+  __syncwarp();
+  const double s1 = sig[ord[0]];
+  const double guard = (double)R * 2.220446049250313e-16 * sqrt(nu2) * sqrt(nv2);
+  int keep = 0;
+  if (s1 > guard) {
+    const double thr = A.eps * s1;
+    for (int i = 0; i < pc; ++i) keep += sig[i] >= thr;
+    if (A.cap > 0 && keep > A.cap) keep = A.cap;
+  }
+  if (keep > tc.Rout) {
+    if (lane == 0) atomicMax(A.overflow, keep);
+    keep = 0;
+  }
+  if (A.ctr && lane == 0) {   // census formulas of SURVEY.md Appendix C
+    unsigned long long fl = 4ull * um * R * R + 4ull * vm * R * R + 24ull * R * R * R +
+                            2ull * (um + vm) * R * keep;
+    atomicAdd(A.ctr, fl);
+    atomicAdd(A.ctr + 1, 8ull * ((unsigned long long)um * R + vm * R + um * keep + vm * keep));
+  }
+  for (int c = 0; c < keep; ++c) {
+    const int j = ord[c];
+    for (int i = lane; i < um; i += 32) {
+      double v = 0.0;
+      if (i < pu) v = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
+      ob[i] = v;
+    }
+    __syncwarp();
+    warp_apply_q(Uw, um, pu, tauU, ob, lane);
+    double* du = tc.Uo + (long long)c * n;
+    for (int i = lane; i < um; i += 32) du[i] = ob[i];
+    __syncwarp();
+    for (int i = lane; i < vm; i += 32) {
+      double v = 0.0;
+      if (i < pv) v = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
+      ob[i] = v;
+    }
+    __syncwarp();
+    warp_apply_q(Vw, vm, pv, tauV, ob, lane);
+    double* dv = tc.Vo + (long long)c * n;
+    for (int i = lane; i < vm; i += 32) dv[i] = ob[i];
+    __syncwarp();
+  }
+  if (lane == 0) *tc.ro = keep;
+}
+
+__global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nitems,
+                                                          int* bigq, int* bigcount) {
+  extern __shared__ double pool[];
+  __shared__ unsigned long long mask;
+  if (threadIdx.x == 0) mask = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = A.T.n;
+  for (int item = blockIdx.x * TW + warp; item < nitems; item += gridDim.x * TW) {
+    const int task = item % A.ntasks, g = item / A.ntasks;
+    TaskCtx tc = resolve_task(A, task, g);
+    __syncwarp();
+    const OpRes& a = tc.a;
+    const OpRes& b = tc.b;
+    if (A.mode != TM_TRUNCATE && (a.r == 0 || b.r == 0)) {   // algebra.py:93-96
+      const OpRes& s = a.r ? a : b;
+      int r = s.r;
+      if (r > tc.Rout) {
+        if (lane == 0) atomicMax(A.overflow, r);
+        r = tc.Rout;
+      }
+      if (r) warp_copy_factor(s, tc.Uo, tc.Vo, tc.um, tc.vm, n, r, lane);
+      if (lane == 0) {
+        *tc.ro = r;
+        if (A.ctr && r && !(s.U == tc.Uo && s.V == tc.Vo && s.sc == 1.0))
+          atomicAdd(A.ctr + 1, 16ull * (tc.um + tc.vm) * r);
+      }
+      continue;
+    }
+    if (A.mode == TM_TRUNCATE && a.r < 2) {
+      int r = 0;
+      if (a.r == 1) {                                           // hodlr.py:181-185
+        bool nzu = false, nzv = false;
+        for (int i = lane; i < tc.um; i += 32) nzu |= a.U[i] != 0.0;
+        for (int i = lane; i < tc.vm; i += 32) nzv |= a.V[i] != 0.0;
+        nzu = __any_sync(FULL, nzu);
+        nzv = __any_sync(FULL, nzv);
+        r = (nzu && nzv) ? 1 : 0;
+        if (r > tc.Rout) {
+          if (lane == 0) atomicMax(A.overflow, r);
+          r = 0;
+        }
+        if (r) warp_copy_factor(a, tc.Uo, tc.Vo, tc.um, tc.vm, n, 1, lane);
+      }
+      if (lane == 0) *tc.ro = r;
+      continue;
+    }
+    const int R = a.r + b.r;
+    const long long need = warp_need_doubles(tc.um, tc.vm, R);
+    if (need > (long long)NSLOT * SLOT) {
+      if (lane == 0) bigq[atomicAdd(bigcount, 1)] = item;
+      continue;
+    }
+    const int ns = (int)((need + SLOT - 1) / SLOT);
+    int s0 = 0;
+    if (lane == 0) s0 = acquire_slots(&mask, ns);
+    s0 = __shfl_sync(FULL, s0, 0);
+    trunc_warp_full(A, tc, pool + (long long)s0 * SLOT, lane);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) {
+      const unsigned long long want = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
+      atomicAnd(&mask, ~(want << s0));
+    }
+  }
+}
+
+int trunc_warp_pool_doubles() { return NSLOT * SLOT; }
+
+cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
+                         int* bigq, int* bigcount, cudaStream_t st) {
   if (a.ntasks == 0 || nelem == 0) return cudaSuccess;
   static bool attr = false;
+  static int nsm = 148;
   if (!attr) {
-    cudaFuncSetAttribute(k_trunc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_trunc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         NSLOT * SLOT * 8);
+    cudaFuncSetAttribute(k_trunc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
-  dim3 grid(a.ntasks, nelem);
-  k_trunc<<<grid, TT, smem_bytes, st>>>(a);
+  const int nitems = a.ntasks * nelem;
+  const size_t bsm = (size_t)a.smem_doubles * 8 + 64;
+  if (direct) {
+    k_trunc_big<<<nitems, TT, bsm, st>>>(a, nullptr, nullptr, nitems);
+    return cudaGetLastError();
+  }
+  if (may_big) {
+    cudaError_t e = cudaMemsetAsync(bigcount, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
+  int blocks = (nitems + TW - 1) / TW;
+  if (blocks > nsm) blocks = nsm;
+  k_trunc_warp<<<blocks, TW * 32, NSLOT * SLOT * 8, st>>>(a, nitems, bigq, bigcount);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !may_big) return e;
+  int bb = nitems < nsm ? nitems : nsm;
+  k_trunc_big<<<bb, TT, bsm, st>>>(a, bigq, bigcount, nitems);
   return cudaGetLastError();
 }
+
+int trunc_direct_max() { return 2 * 148; }
 
 }  // namespace acr
