@@ -108,26 +108,42 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel(double* A, int N, int j0,
       for (int i = j + 1 + tid; i < N; i += LU_PT) A[(long long)i * N + j] *= rinv;
     }
     __syncthreads();
-    // rank-1 update inside the panel
+    // rank-1 update inside the panel: lane -> column, warp -> row stride
     const int w = j0 + jb - j - 1;
-    if (w > 0)
-      for (long long idx = tid; idx < (long long)(N - j - 1) * w; idx += LU_PT) {
-        int i = j + 1 + (int)(idx / w), c = j + 1 + (int)(idx % w);
-        A[(long long)i * N + c] -= A[(long long)i * N + j] * A[(long long)j * N + c];
-      }
+    if (w > 0 && lane < w) {
+      const int c = j + 1 + lane;
+      const double ajc = A[(long long)j * N + c];
+      for (int i = j + 1 + warp; i < N; i += LU_PT / 32)
+        A[(long long)i * N + c] -= A[(long long)i * N + j] * ajc;
+    }
     __syncthreads();
   }
 }
 
-// A12 := L11^{-1} A12 (unit lower), one thread per column
+// A12 := L11^{-1} A12 (unit lower), one thread per column, L11 in smem
 __global__ void k_lu_trsm(double* A, int N, int j0, int jb) {
+  __shared__ double L[LU_NB][LU_NB + 1];
+  for (int idx = threadIdx.x; idx < jb * jb; idx += blockDim.x) {
+    int i = idx / jb, k = idx - i * jb;
+    L[i][k] = A[(long long)(j0 + i) * N + j0 + k];
+  }
+  __syncthreads();
   int c = j0 + jb + blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
-  for (int i = j0; i < j0 + jb; ++i) {
-    double x = A[(long long)i * N + c];
-    for (int k = j0; k < i; ++k) x -= A[(long long)i * N + k] * A[(long long)k * N + c];
-    A[(long long)i * N + c] = x;
+  double x[LU_NB];
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i)
+    x[i] = i < jb ? A[(long long)(j0 + i) * N + c] : 0.0;
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i) {
+    double v = x[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v -= L[i][k] * x[k];
+    x[i] = v;
   }
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i)
+    if (i < jb) A[(long long)(j0 + i) * N + c] = x[i];
 }
 
 // A22 -= A21 A12, 64x64 tiles, k = jb <= 32
@@ -180,7 +196,7 @@ cudaError_t lu_factor(double* A, int N, int* piv, int* info, cudaStream_t st) {
     k_lu_panel<<<1, LU_PT, 0, st>>>(A, N, j0, jb, piv, info);
     int rest = N - j0 - jb;
     if (rest > 0) {
-      k_lu_trsm<<<(rest + 127) / 128, 128, 0, st>>>(A, N, j0, jb);
+      k_lu_trsm<<<(rest + 63) / 64, 64, 0, st>>>(A, N, j0, jb);
       dim3 g((rest + 63) / 64, (rest + 63) / 64);
       k_lu_gemm<<<g, 256, 0, st>>>(A, N, j0, jb);
     }

@@ -161,8 +161,19 @@ __device__ void block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
   const int per = TT / gs;
   const int sub = tid & (gs - 1), grp = tid / gs;
   const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  // columns below eps64 * |B|_F cannot move any singular value that a
+  // relative threshold >= 1e-14 keeps: rotations involving them are skipped
+  double nb = 0.0;
+  for (int i = tid; i < pr * pc; i += TT) nb += B[i] * B[i];
+  __shared__ double s_nb[NWB];
+  nb = warp_sum(nb);
+  if ((tid & 31) == 0) s_nb[tid >> 5] = nb;
+  __syncthreads();
+  nb = 0.0;
+  for (int w = 0; w < NWB; ++w) nb += s_nb[w];
+  const double tiny = nb * 4.930380657631324e-32;   // (eps64 |B|_F)^2
   (void)flag;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  for (int sweep = 0; sweep < 40; ++sweep) {
     int rot = 0;
     for (int step = 0; step < np - 1; ++step) {
       for (int base = 0; base < npairs; base += per) {
@@ -189,7 +200,7 @@ __device__ void block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
           b += __shfl_xor_sync(0xffffffffu, b, o);
           c += __shfl_xor_sync(0xffffffffu, c, o);
         }
-        if (valid && a != 0.0 && b != 0.0 && c != 0.0 &&
+        if (valid && a > tiny && b > tiny && c != 0.0 &&
             fabs(c) > tol * sqrt(a) * sqrt(b)) {
           double zeta = (b - a) / (2.0 * c);
           double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -591,7 +602,10 @@ __device__ void warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
   const int per = 32 / gs;                 // pairs per pass
   const double tol = sqrt((double)pr) * 2.220446049250313e-16;
   const int sub = lane & (gs - 1), grp = lane / gs;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  double nb = 0.0;
+  for (int i = lane; i < pr * pc; i += 32) nb += B[i] * B[i];
+  const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  for (int sweep = 0; sweep < 40; ++sweep) {
     bool rot = false;
     for (int step = 0; step < np - 1; ++step) {
       for (int base = 0; base < npairs; base += per) {
@@ -618,7 +632,7 @@ __device__ void warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
           b += __shfl_xor_sync(FULL, b, o);
           c += __shfl_xor_sync(FULL, c, o);
         }
-        if (valid && a != 0.0 && b != 0.0 && c != 0.0 &&
+        if (valid && a > tiny && b > tiny && c != 0.0 &&
             fabs(c) > tol * sqrt(a) * sqrt(b)) {
           double zeta = (b - a) / (2.0 * c);
           double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -806,7 +820,7 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     }
     const int R = a.r + b.r;
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
-    if (need > (long long)NSLOT * SLOT) {
+    if (need > (long long)NSLOT * SLOT / 4) {   // large: 512-thread block path
       if (lane == 0) bigq[atomicAdd(bigcount, 1)] = item;
       continue;
     }
@@ -824,7 +838,7 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
   }
 }
 
-int trunc_warp_pool_doubles() { return NSLOT * SLOT; }
+int trunc_warp_pool_doubles() { return NSLOT * SLOT / 4; }
 
 cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
                          int* bigq, int* bigcount, cudaStream_t st) {
