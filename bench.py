@@ -265,7 +265,7 @@ def run_ours(args):
     for cls, name in enumerate(["k_trunc", "k_leafinv", "k_leafgemm", "k_hmat"]):
         nl = C.c_longlong()
         kms = C.c_double()
-        ctr = (C.c_ulonglong * 2)()
+        ctr = (C.c_ulonglong * 16)()
         solver.lib.acr_kernel_stats(solver.plan, cls, C.byref(nl), C.byref(kms), ctr)
         stats[name] = {"launches": nl.value, "ms": kms.value,
                        "flops": ctr[0], "bytes": ctr[1]}

@@ -71,8 +71,12 @@ double acr_factor_ms(const acr_plan_t* p);
 double acr_solve_ms(const acr_plan_t* p);
 long long acr_kernel_launches(const acr_plan_t* p);
 /* Instrumented factor only (option 2): class 0 recompression (k_trunc),
- * 1 leaf inverse, 2 leaf GEMM, 3 HODLR x panel.  counters (class 0):
- * [0] algorithmic FLOPs, [1] algorithmic bytes. */
+ * 1 leaf inverse, 2 leaf GEMM, 3 HODLR x panel.  counters[16] (class 0):
+ * [0] algorithmic FLOPs, [1] algorithmic bytes,
+ * [2..7] block-path clock64 cycles per phase (load, QR, core, Jacobi, select,
+ * output), [8] block-path full tasks, [9] warp-path full tasks, [10]/[11]
+ * Jacobi sweeps (block / warp), [12..15] warp-path cycles (load, QR, core,
+ * Jacobi+rest). */
 int acr_kernel_stats(const acr_plan_t* p, int cls, long long* launches,
                      double* ms, unsigned long long* counters);
 int acr_last_error(const acr_plan_t* p, char* buf, int len);

@@ -9,6 +9,8 @@
 // are decided per block on the device from device-resident ranks.  The
 // truncation schedule is the reference's.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <chrono>
 #include <climits>
 #include <cstdio>
@@ -50,9 +52,65 @@ struct InternalError : std::runtime_error {
 // ---------------------------------------------------------------------------
 static long long g_live = 0, g_peak = 0;   // bytes held through Dev
 
+// Size-class caching allocator.  A factor requests the same sizes in the
+// same order every time, so after the first factor every request is served
+// from the cache (no new device mappings inside a timed factor).  All work of
+// a plan is on one stream, so handing a cached block to a later request is
+// stream-ordered.  Blocks are returned to the driver when the last plan dies.
+struct DevCache {
+  std::mutex mu;
+  std::multimap<std::pair<size_t, cudaStream_t>, void*> free_;
+  std::vector<void*> all;
+  int plans = 0;
+  static size_t cls(size_t b) {
+    if (b <= 4096) return (b + 255) & ~size_t(255);
+    int lg = 63 - __builtin_clzll(b);
+    size_t step = size_t(1) << (lg > 3 ? lg - 3 : 0);   // 8 classes per octave
+    return (b + step - 1) & ~(step - 1);
+  }
+  void* get(size_t bytes, size_t* cap, cudaStream_t s) {
+    size_t c = cls(bytes);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_.find({c, s});
+      if (it != free_.end()) {
+        void* p = it->second;
+        free_.erase(it);
+        *cap = c;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, c, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      trim(s);                       // give cached blocks back, retry once
+      CK(cudaMallocAsync(&p, c, s));
+    }
+    std::lock_guard<std::mutex> g(mu);
+    all.push_back(p);
+    *cap = c;
+    return p;
+  }
+  void put(void* p, size_t cap, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    free_.emplace(std::make_pair(cap, s), p);
+  }
+  void trim(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : free_) {
+      cudaFreeAsync(kv.second, s);
+      all.erase(std::find(all.begin(), all.end(), kv.second));
+    }
+    free_.clear();
+  }
+};
+static DevCache g_cache;
+
 struct Dev {
   void* p = nullptr;
   size_t n = 0;
+  size_t cap = 0;
   cudaStream_t st = 0;
   Dev() {}
   Dev(size_t bytes, cudaStream_t s) { alloc(bytes, s); }
@@ -61,31 +119,38 @@ struct Dev {
     st = s;
     n = bytes;
     if (bytes) {
-      CK(cudaMallocAsync(&p, bytes, s));
-      g_live += (long long)bytes;
+      p = g_cache.get(bytes, &cap, s);
+      g_live += (long long)cap;
       if (g_live > g_peak) g_peak = g_live;
     }
   }
   void release() {
     if (p) {
-      cudaFreeAsync(p, st);
-      g_live -= (long long)n;
+      g_cache.put(p, cap, st);
+      g_live -= (long long)cap;
     }
     p = nullptr;
     n = 0;
+    cap = 0;
   }
   ~Dev() { release(); }
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;
-  Dev(Dev&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
+  Dev(Dev&& o) noexcept : p(o.p), n(o.n), cap(o.cap), st(o.st) {
+    o.p = nullptr;
+    o.n = 0;
+    o.cap = 0;
+  }
   Dev& operator=(Dev&& o) noexcept {
     if (this != &o) {
       release();
       p = o.p;
       n = o.n;
+      cap = o.cap;
       st = o.st;
       o.p = nullptr;
       o.n = 0;
+      o.cap = 0;
     }
     return *this;
   }
@@ -386,7 +451,7 @@ struct Plan {
   std::vector<std::pair<int, size_t>> evmarks;   // (class, index of start event)
   double kms[NCLS] = {0};
   long long kcnt[NCLS] = {0};
-  unsigned long long kctr[2] = {0, 0};
+  unsigned long long kctr[16] = {0};
   Dev dctr;
   // scratch pool
   std::vector<Dev> scr;
@@ -426,10 +491,10 @@ struct Plan {
     evused = 0;
     evmarks.clear();
     for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; }
-    kctr[0] = kctr[1] = 0;
+    for (auto& c : kctr) c = 0;
     if (prof_on) {
-      if (!dctr.p) dctr.alloc(2 * sizeof(unsigned long long), st);
-      CK(cudaMemsetAsync(dctr.p, 0, 2 * sizeof(unsigned long long), st));
+      if (!dctr.p) dctr.alloc(16 * sizeof(unsigned long long), st);
+      CK(cudaMemsetAsync(dctr.p, 0, 16 * sizeof(unsigned long long), st));
     }
   }
   void prof_collect() {   // after a stream sync
@@ -956,18 +1021,6 @@ struct Plan {
       CK(cudaEventCreate(&ev0));
       CK(cudaEventCreate(&ev1));
     }
-    // keep the stream-ordered pool at the footprint of the previous factor so
-    // later factors never map new memory in the middle of a level
-    if (g_peak > 0 && reserved < g_peak) {
-      void* r = nullptr;
-      size_t want = (size_t)(g_peak - g_live) + ((size_t)g_peak >> 3);
-      if (cudaMallocAsync(&r, want, st) == cudaSuccess) {
-        cudaFreeAsync(r, st);
-        reserved = g_peak;
-      } else {
-        cudaGetLastError();
-      }
-    }
     CK(cudaEventRecord(ev0, st));
     Level L;
     L.m = m;
@@ -1257,6 +1310,7 @@ int acr_plan_create(int m, int n, int leaf_size, double eps, int max_rank_cap,
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     h->p->dt.upload(h->p->ht, 0);
+    acr::g_cache.plans++;
   } catch (const std::exception& e) {
     g_err = e.what();
     delete h->p;
@@ -1270,8 +1324,13 @@ int acr_plan_create(int m, int n, int leaf_size, double eps, int max_rank_cap,
 void acr_plan_destroy(acr_plan_t* h) {
   if (!h) return;
   if (h->p) {
-    cudaStreamSynchronize(h->p->st);
+    cudaStream_t st = h->p->st;
+    cudaStreamSynchronize(st);
     delete h->p;
+    if (--acr::g_cache.plans <= 0) {
+      acr::g_cache.trim(st);
+      cudaStreamSynchronize(st);
+    }
   }
   delete h;
 }
@@ -1346,10 +1405,8 @@ int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
   const Plan& P = *h->p;
   *launches = P.kcnt[cls];
   *ms = P.kms[cls];
-  if (counters) {
-    counters[0] = cls == 0 ? P.kctr[0] : 0;
-    counters[1] = cls == 0 ? P.kctr[1] : 0;
-  }
+  if (counters)
+    for (int i = 0; i < 16; ++i) counters[i] = cls == 0 ? P.kctr[i] : 0;
   return ACR_OK;
 }
 

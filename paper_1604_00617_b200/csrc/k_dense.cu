@@ -59,7 +59,7 @@ cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
 // blocked right-looking LU, nb = 32, row-major N x N
 // ---------------------------------------------------------------------------
 static constexpr int LU_NB = 32;
-static constexpr int LU_PT = 512;
+static constexpr int LU_PT = 1024;
 
 __global__ void __launch_bounds__(LU_PT) k_lu_panel(double* A, int N, int j0,
                                                     int jb, int* piv, int* info) {
@@ -113,8 +113,19 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel(double* A, int N, int j0,
     if (w > 0 && lane < w) {
       const int c = j + 1 + lane;
       const double ajc = A[(long long)j * N + c];
-      for (int i = j + 1 + warp; i < N; i += LU_PT / 32)
-        A[(long long)i * N + c] -= A[(long long)i * N + j] * ajc;
+      constexpr int ST = LU_PT / 32;
+      int i = j + 1 + warp;
+      for (; i + 3 * ST < N; i += 4 * ST) {      // 4 independent rows in flight
+        double l0 = A[(long long)i * N + j], l1 = A[(long long)(i + ST) * N + j];
+        double l2 = A[(long long)(i + 2 * ST) * N + j], l3 = A[(long long)(i + 3 * ST) * N + j];
+        double a0 = A[(long long)i * N + c], a1 = A[(long long)(i + ST) * N + c];
+        double a2 = A[(long long)(i + 2 * ST) * N + c], a3 = A[(long long)(i + 3 * ST) * N + c];
+        A[(long long)i * N + c] = a0 - l0 * ajc;
+        A[(long long)(i + ST) * N + c] = a1 - l1 * ajc;
+        A[(long long)(i + 2 * ST) * N + c] = a2 - l2 * ajc;
+        A[(long long)(i + 3 * ST) * N + c] = a3 - l3 * ajc;
+      }
+      for (; i < N; i += ST) A[(long long)i * N + c] -= A[(long long)i * N + j] * ajc;
     }
     __syncthreads();
   }

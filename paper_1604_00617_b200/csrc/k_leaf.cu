@@ -118,10 +118,142 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
   }
 }
 
+// Register-tiled Gauss-Jordan for leaves of size <= S (S in {16, 32, 64}):
+// (S/4)^2 threads, each owning a 4x4 tile in registers, plus a double-buffered
+// shared copy of the matrix.  Every warp computes the pivot (first index of the
+// largest |a_ik|, getrf's rule) redundantly from the shared copy, so one
+// barrier per pivot step suffices.  Singular / non-finite detection as the
+// reference's LAPACK call (algebra.py:199-207).
+template <int S>
+__global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, const HB* H,
+                                                                  int leaf, int* sing) {
+  constexpr int TG = S / 4, LD = S + 1;
+  extern __shared__ double buf[];              // [2][S][LD]
+  __shared__ int piv[S], inv_[S];
+  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int ty = tid / TG, tx = tid - ty * TG;
+  const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
+  double* L = H[g].leaf + (long long)lo * bw;
+  double x[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = ty * 4 + a, c = tx * 4 + b;
+      x[a][b] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
+      buf[r * LD + c] = x[a][b];
+    }
+  bool bad = false;
+  for (int k = 0; k < s; ++k) {
+    const double* cur = buf + (k & 1) * S * LD;
+    double* nxt = buf + ((k + 1) & 1) * S * LD;
+    __syncthreads();
+    double best = -1.0;
+    int p = k;
+    for (int i = k + lane; i < s; i += 32) {
+      double v = fabs(cur[i * LD + k]);
+      if (v > best) { best = v; p = i; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, p, o);
+      if (ov > best || (ov == best && oi < p)) { best = ov; p = oi; }
+    }
+    const double pv = cur[p * LD + k];
+    if (pv == 0.0) { bad = true; break; }     // uniform: every warp sees the same
+    if (tid == 0) piv[k] = p;
+    const double inv = 1.0 / pv;
+    double rk[4], ok[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = tx * 4 + b;
+      rk[b] = (c == k) ? inv : cur[p * LD + c] * inv;   // new row k = old row p / pv
+      ok[b] = cur[k * LD + c];                           // old row k -> row p
+    }
+    const double fk = cur[k * LD + k];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = ty * 4 + a;
+      if (r == k) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) x[a][b] = rk[b];
+      } else {
+        const bool isp = (r == p);
+        const double f = isp ? fk : cur[r * LD + k];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int c = tx * 4 + b;
+          const double src = isp ? ok[b] : x[a][b];
+          x[a][b] = (c == k) ? -f * inv : src - f * rk[b];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) nxt[r * LD + tx * 4 + b] = x[a][b];
+    }
+  }
+  if (bad) {
+    if (tid == 0) {
+      int ps = 0;
+      for (int v = 0; v < T.nnodes; ++v)
+        if (T.isleaf[v] && T.lo[v] < lo) ++ps;
+      atomicMin(sing + g, ps);
+    }
+    return;
+  }
+  __syncthreads();
+  // A^{-1} = X P: undo the column swaps in reverse order
+  if (tid == 0) {
+    int* pos = reinterpret_cast<int*>(buf);
+    for (int j = 0; j < s; ++j) pos[j] = j;
+    for (int k = s - 1; k >= 0; --k) {
+      int t = pos[k];
+      pos[k] = pos[piv[k]];
+      pos[piv[k]] = t;
+    }
+    for (int j = 0; j < s; ++j) inv_[pos[j]] = j;
+  }
+  __syncthreads();
+  int nf = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = ty * 4 + a, c = tx * 4 + b;
+      if (r < s && c < s) {
+        if (!isfinite(x[a][b])) nf = 1;
+        L[(long long)r * bw + inv_[c]] = x[a][b];
+      }
+    }
+  if (__syncthreads_or(nf) && tid == 0) {
+    int ps = 0;
+    for (int v = 0; v < T.nnodes; ++v)
+      if (T.isleaf[v] && T.lo[v] < lo) ++ps;
+    atomicMin(sing + g, ps);
+  }
+}
+
+template <int S>
+static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int leaf,
+                               int* sing, cudaStream_t st) {
+  const size_t smem = 2ull * S * (S + 1) * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_leafinv_reg<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k_leafinv_reg<S><<<nelem, (S / 4) * (S / 4), smem, st>>>(T, H, leaf, sing);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
                            int* sing, cudaStream_t st) {
   if (!nelem) return cudaSuccess;
   int s = T.bw;
+  if (s <= 16) return leafinv_reg<16>(T, H, nelem, leaf, sing, st);
+  if (s <= 32) return leafinv_reg<32>(T, H, nelem, leaf, sing, st);
+  if (s <= 64) return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
   size_t smem = (size_t)s * (s + 1) * 8 + (size_t)s * 8 + (size_t)s * 4 + 16;
   static bool attr = false;
   if (!attr) {

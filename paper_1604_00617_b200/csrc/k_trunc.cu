@@ -150,11 +150,11 @@ __device__ __forceinline__ int rr_player(int step, int x, int np) {
 // One-sided Jacobi on B (pr x pc, column-major ld pr) accumulating J (pc x pc).
 // The disjoint pairs of one round-robin step are spread over lane groups of
 // size gs (power of two) across the whole CTA.
-__device__ void block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
+__device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
   const int tid = threadIdx.x;
   for (int i = tid; i < pc * pc; i += TT) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
   __syncthreads();
-  if (pc < 2) return;
+  if (pc < 2) return 0;
   const int np = pc + (pc & 1), npairs = np / 2;
   int gs = 32;
   while (gs > 1 && gs * npairs > TT) gs >>= 1;
@@ -223,8 +223,9 @@ __device__ void block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
         __syncthreads();
       }
     }
-    if (!__syncthreads_or(rot)) break;
+    if (!__syncthreads_or(rot)) return sweep + 1;
   }
+  return 40;
 }
 
 __device__ void copy_factor(const OpRes& s, double* Uo, double* Vo, int um,
@@ -320,6 +321,9 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   double* sig = tauV + R;
   int* ord = reinterpret_cast<int*>(sig + R);
 
+  long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long t_ph = clock64();
+#define ACR_PH(i) do { if (A.ctr) { long long t_ = clock64(); ph[i] += t_ - t_ph; t_ph = t_; } } while (0)
   for (int idx = tid; idx < um * R; idx += TT) {
     int c = idx / um, i = idx - c * um;
     Uw[idx] = c < a.r ? a.sc * a.U[(long long)c * n + i]
@@ -330,8 +334,10 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     Vw[idx] = c < a.r ? a.V[(long long)c * n + i] : b.V[(long long)(c - a.r) * n + i];
   }
   __syncthreads();
+  ACR_PH(0);
   block_qr(Uw, um, R, tauU, red, red + NWB);
   block_qr(Vw, vm, R, tauV, red, red + NWB);
+  ACR_PH(1);
 
   // Frobenius norms of the triangular factors (hodlr.py:191-192)
   double nu2 = 0.0, nv2 = 0.0;
@@ -359,7 +365,9 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     else Bm[(long long)i * pr + j] = s;
   }
   __syncthreads();
-  block_jacobi(Bm, pr, pc, Jm, iflag);
+  ACR_PH(2);
+  const int sweeps = block_jacobi(Bm, pr, pc, Jm, iflag);
+  ACR_PH(3);
   for (int j = tid; j < pc; j += TT) {
     double s = 0.0;
     const double* bj = Bm + (long long)j * pr;
@@ -389,14 +397,19 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     if (tid == 0) atomicMax(A.overflow, keep);
     keep = 0;
   }
+  ACR_PH(4);
   if (A.ctr && tid == 0) {   // census formulas of SURVEY.md Appendix C
     unsigned long long fl = 4ull * um * R * R + 4ull * vm * R * R + 24ull * R * R * R +
                             2ull * (um + vm) * R * keep;
     atomicAdd(A.ctr, fl);
     atomicAdd(A.ctr + 1, 8ull * ((unsigned long long)um * R + vm * R + um * keep + vm * keep));
+    atomicAdd(A.ctr + 8, 1ull);
+    atomicAdd(A.ctr + 10, (unsigned long long)sweeps);
   }
   if (keep == 0) {
     if (tid == 0) *ro = 0;
+    if (A.ctr && tid == 0)
+      for (int i = 0; i < 5; ++i) atomicAdd(A.ctr + 2 + i, (unsigned long long)ph[i]);
     return;
   }
   // left/right factors padded with zeros, then Q applied
@@ -426,6 +439,9 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     Vo[(long long)c * n + i] = Ov[idx];
   }
   if (tid == 0) *ro = keep;
+  ACR_PH(5);
+  if (A.ctr && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 2 + i, (unsigned long long)ph[i]);
 }
 
 
@@ -504,8 +520,8 @@ __global__ void __launch_bounds__(TT) k_trunc_big(TruncArgs A, const int* q,
 // warp path: one warp per task, work area carved from a per-CTA smem pool
 // ---------------------------------------------------------------------------
 static constexpr int TW = 16;          // warps per CTA
-static constexpr int SLOT = 512;       // doubles per slot
-static constexpr int NSLOT = 48;       // 192 KB pool
+static constexpr int SLOT = 384;       // doubles per slot (3 KB)
+static constexpr int NSLOT = 64;       // 192 KB pool, one 64-bit occupancy mask
 static constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns) {
@@ -592,10 +608,10 @@ __device__ void warp_apply_q(const double* W, int mr, int p, const double* tau,
 
 // one-sided Jacobi on B (pr x pc col-major), J (pc x pc); pairs of a
 // round-robin step are spread over lane groups of size gs
-__device__ void warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
+__device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
   for (int i = lane; i < pc * pc; i += 32) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
   __syncwarp();
-  if (pc < 2) return;
+  if (pc < 2) return 0;
   const int np = pc + (pc & 1), npairs = np / 2;
   int gs = 32;
   while (gs > 1 && gs * npairs > 32) gs >>= 1;
@@ -655,7 +671,33 @@ __device__ void warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
         __syncwarp();
       }
     }
-    if (!__any_sync(FULL, rot)) break;
+    if (!__any_sync(FULL, rot)) return sweep + 1;
+  }
+  return 40;
+}
+
+// W[c*m + i] = [sa*A | sb*B] columns, global -> smem, 4 loads in flight
+__device__ __forceinline__ void warp_load_cols(double* __restrict__ W, int m,
+                                               const double* __restrict__ A, int ra,
+                                               double sa, const double* __restrict__ B,
+                                               int rb, double sb, int n, int lane) {
+  const int R = ra + rb;
+  for (int i = lane; i < m; i += 32) {
+    int c = 0;
+    for (; c + 4 <= R; c += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int cc = c + u;
+        v[u] = cc < ra ? sa * __ldg(A + (long long)cc * n + i)
+                       : sb * __ldg(B + (long long)(cc - ra) * n + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) W[(long long)(c + u) * m + i] = v[u];
+    }
+    for (; c < R; ++c)
+      W[(long long)c * m + i] = c < ra ? sa * __ldg(A + (long long)c * n + i)
+                                       : sb * __ldg(B + (long long)(c - ra) * n + i);
   }
 }
 
@@ -676,17 +718,16 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   double* sig = tauV + R;
   int* ord = reinterpret_cast<int*>(sig + R);
   double* ob = sig + 2 * R;
-  for (int c = 0; c < R; ++c) {
-    const bool fa = c < a.r;
-    const double* su = fa ? a.U + (long long)c * n : b.U + (long long)(c - a.r) * n;
-    const double sc = fa ? a.sc : b.sc;
-    for (int i = lane; i < um; i += 32) Uw[(long long)c * um + i] = sc * su[i];
-    const double* sv = fa ? a.V + (long long)c * n : b.V + (long long)(c - a.r) * n;
-    for (int i = lane; i < vm; i += 32) Vw[(long long)c * vm + i] = sv[i];
-  }
+  // operand load: all global reads of a lane issued before its smem stores
+  long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long t_ph = clock64();
+  warp_load_cols(Uw, um, a.U, a.r, a.sc, b.U, b.r, b.sc, n, lane);
+  warp_load_cols(Vw, vm, a.V, a.r, 1.0, b.V, b.r, 1.0, n, lane);
   __syncwarp();
+  ACR_PH(0);
   warp_qr(Uw, um, R, tauU, lane);
   warp_qr(Vw, vm, R, tauV, lane);
+  ACR_PH(1);
   double nu2 = 0.0, nv2 = 0.0;
   for (int idx = lane; idx < pu * R; idx += 32) {
     int l = idx / pu, i = idx - l * pu;
@@ -709,7 +750,9 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     else Bm[(long long)i * pr + j] = s;
   }
   __syncwarp();
-  warp_jacobi(Bm, pr, pc, Jm, lane);
+  ACR_PH(2);
+  const int sweeps = warp_jacobi(Bm, pr, pc, Jm, lane);
+  ACR_PH(3);
   for (int j = lane; j < pc; j += 32) {
     double s = 0.0;
     const double* bj = Bm + (long long)j * pr;
@@ -739,11 +782,14 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     if (lane == 0) atomicMax(A.overflow, keep);
     keep = 0;
   }
+  ACR_PH(4);
   if (A.ctr && lane == 0) {   // census formulas of SURVEY.md Appendix C
     unsigned long long fl = 4ull * um * R * R + 4ull * vm * R * R + 24ull * R * R * R +
                             2ull * (um + vm) * R * keep;
     atomicAdd(A.ctr, fl);
     atomicAdd(A.ctr + 1, 8ull * ((unsigned long long)um * R + vm * R + um * keep + vm * keep));
+    atomicAdd(A.ctr + 9, 1ull);
+    atomicAdd(A.ctr + 11, (unsigned long long)sweeps);
   }
   for (int c = 0; c < keep; ++c) {
     const int j = ord[c];
@@ -769,6 +815,9 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     __syncwarp();
   }
   if (lane == 0) *tc.ro = keep;
+  ACR_PH(5);
+  if (A.ctr && lane == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 12 + (i < 4 ? i : 3), (unsigned long long)ph[i]);
 }
 
 __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nitems,
@@ -820,7 +869,7 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     }
     const int R = a.r + b.r;
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
-    if (need > (long long)NSLOT * SLOT / 4) {   // large: 512-thread block path
+    if (need > (long long)NSLOT * SLOT / 8) {   // large: 512-thread block path
       if (lane == 0) bigq[atomicAdd(bigcount, 1)] = item;
       continue;
     }
@@ -838,7 +887,7 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
   }
 }
 
-int trunc_warp_pool_doubles() { return NSLOT * SLOT / 4; }
+int trunc_warp_pool_doubles() { return NSLOT * SLOT / 8; }
 
 cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
                          int* bigq, int* bigcount, cudaStream_t st) {

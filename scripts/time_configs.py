@@ -27,3 +27,16 @@ for name in cfgs:
                           max_rank=max(p.max_rank for p in prof), launches=sol.kernel_launches,
                           storage=sol.storage_bytes(s.n_rhs),
                           unknowns_per_s=s.n_unknowns / (min(times) / 1e3))), flush=True)
+    if __import__("os").environ.get("PROF"):
+        import ctypes as C
+        sol.lib.acr_plan_set_option(sol.plan, 2, 1)
+        sol.factor(bands)
+        sol.lib.acr_plan_set_option(sol.plan, 2, 0)
+        st = {}
+        for cls, nm in enumerate(["trunc", "leafinv", "leafgemm", "hmat"]):
+            nl = C.c_longlong(); ms = C.c_double(); ctr = (C.c_ulonglong * 16)()
+            sol.lib.acr_kernel_stats(sol.plan, cls, C.byref(nl), C.byref(ms), ctr)
+            st[nm] = (nl.value, round(ms.value, 1))
+            if cls == 0:
+                st["trunc_ctr"] = list(ctr)
+        print(json.dumps(dict(cfg=name, instrumented_factor_ms=round(sol.factor_ms, 1), classes=st)), flush=True)
