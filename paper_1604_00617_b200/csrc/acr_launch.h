@@ -20,8 +20,9 @@ long long warp_need_doubles(int um, int vm, int R);
 // leaf kernels (k_leaf.cu)
 cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
                            int* sing, cudaStream_t st);
+// diag: 0 general (DMMA), 1 A diagonal, 2 B diagonal (exact fast path)
 cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
-                            const HB* C, int nelem, Src PX, RankRef xr,
+                            const HB* C, int nelem, Src PX, RankRef xr, int diag,
                             cudaStream_t st);
 cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
                             int nleaf, Src U, Src V, RankRef rr, int node,

@@ -451,7 +451,7 @@ struct Plan {
   std::vector<std::pair<int, size_t>> evmarks;   // (class, index of start event)
   double kms[NCLS] = {0};
   long long kcnt[NCLS] = {0};
-  unsigned long long kctr[16] = {0};
+  unsigned long long kctr[72] = {0};
   Dev dctr;
   // scratch pool
   std::vector<Dev> scr;
@@ -493,8 +493,8 @@ struct Plan {
     for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; }
     for (auto& c : kctr) c = 0;
     if (prof_on) {
-      if (!dctr.p) dctr.alloc(16 * sizeof(unsigned long long), st);
-      CK(cudaMemsetAsync(dctr.p, 0, 16 * sizeof(unsigned long long), st));
+      if (!dctr.p) dctr.alloc(72 * sizeof(unsigned long long), st);
+      CK(cudaMemsetAsync(dctr.p, 0, 72 * sizeof(unsigned long long), st));
     }
   }
   void prof_collect() {   // after a stream sync
@@ -592,7 +592,7 @@ struct Plan {
 
   // ---- multiply: C = A B for G elements (reference algebra.py:159-185) ----
   void multiply(const HB* A, const HB* B, const HB* C, int G, int RA, int RB,
-                int RC) {
+                int RC, int diag = 0) {
     if (G <= 0) return;
     const int nd = std::max(ht.nd, 1), nn = ht.nnodes;
     const int nA1 = ht.nA(1, nn);
@@ -601,12 +601,12 @@ struct Plan {
     int chunk = (int)std::max<long long>(1, (4LL << 30) / std::max<long long>(per, 1));
     for (int g0 = 0; g0 < G; g0 += chunk) {
       int cg = std::min(chunk, G - g0);
-      multiply_chunk(A + g0, B + g0, C + g0, cg, RA, RB, RC);
+      multiply_chunk(A + g0, B + g0, C + g0, cg, RA, RB, RC, diag);
     }
   }
 
   void multiply_chunk(const HB* A, const HB* B, const HB* C, int G, int RA,
-                      int RB, int RC) {
+                      int RB, int RC, int diag) {
     const int nd = std::max(ht.nd, 1), nn = ht.nnodes;
     const long long ps = (long long)nd * n;
     double* PX = scratch<double>(0, (size_t)G * ps * RB);
@@ -640,7 +640,8 @@ struct Plan {
       ++launches;
     }
     kbegin(2);
-    CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), st));
+    CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), diag,
+                       st));
     kend();
     ++launches;
     if (ht.branches.empty()) return;
@@ -927,7 +928,8 @@ struct Plan {
       Dev tA = make_tab({{&L.E, 1, 2, no}, {&L.F, 1, 2, nq}});
       Dev tB = make_tab({{&rec.Dinv, 0, 1, no}, {&rec.Dinv, 1, 1, nq}});
       Dev tC = make_tab({{&PQ, 0, 1, no + nq}});
-      multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), no + nq, L.R, rec.Dinv.R, PQ.R);
+      multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), no + nq, L.R, rec.Dinv.R, PQ.R,
+               lvl == 0 ? 1 : 0);
     }
     // 3. X = P F_{j-1}, Y = Q E_{j+1}, E' = -P E_{j-1}, F' = -Q F_{j+1}
     nx.m = no;
@@ -944,7 +946,8 @@ struct Plan {
                          {&L.F, 2, 2, nf}});
       Dev tC = make_tab({{&XY, 0, 1, no + nq}, {&nx.E, 1, 1, no - 1}, {&nx.F, 0, 1, nf}});
       int G = no + nq + std::max(no - 1, 0) + nf;
-      multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), G, PQ.R, L.R, Rout);
+      multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), G, PQ.R, L.R, Rout,
+               lvl == 0 ? 2 : 0);
       Dev tE = make_tab({{&nx.E, 1, 1, no - 1}, {&nx.F, 0, 1, nf}});
       CK(launch_negate(dt.T, tE.as<HB>(), std::max(no - 1, 0) + nf, st));
       ++launches;
@@ -1401,12 +1404,14 @@ long long acr_kernel_launches(const acr_plan_t* h) { return h && h->p ? h->p->la
 
 int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
                      double* ms, unsigned long long* counters) {
-  if (!h || !h->p || cls < 0 || cls >= Plan::NCLS) return ACR_EARG;
+  if (!h || !h->p || cls < 0 || (cls >= Plan::NCLS && cls != 100)) return ACR_EARG;
   const Plan& P = *h->p;
-  *launches = P.kcnt[cls];
-  *ms = P.kms[cls];
+  *launches = cls == 100 ? 0 : P.kcnt[cls];
+  *ms = cls == 100 ? 0.0 : P.kms[cls];
   if (counters)
     for (int i = 0; i < 16; ++i) counters[i] = cls == 0 ? P.kctr[i] : 0;
+  if (counters && cls == 100)
+    for (int i = 0; i < 72; ++i) counters[i] = P.kctr[i];
   return ACR_OK;
 }
 

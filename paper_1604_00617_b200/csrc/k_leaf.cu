@@ -307,18 +307,140 @@ __global__ void __launch_bounds__(LT) k_leafgemm(TreeDev T, const HB* A,
   }
 }
 
+// ---------------------------------------------------------------------------
+// leaf GEMM on the FP64 tensor pipe: mma.sync.m8n8k4.f64 (SASS DMMA).
+// One CTA of 8 warps per (leaf, element); the leaf is zero-padded to S (a
+// multiple of 8, <= 64) in shared memory, A row-major and B column-major so
+// both fragments are 8x4 row-contiguous reads.  Ancestor cross terms
+// (P Q^T, rank r, deepest first) are separate tensor-core products added to
+// C one at a time, the reference's order (algebra.py:165-168, 134-135).
+// diag: 1 = A diagonal, 2 = B diagonal (level 0, exact fast path).
+// ---------------------------------------------------------------------------
+static constexpr int GT = 256;
+static constexpr int GLD = 68;           // padded leading dimension (doubles)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+               "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(GT) k_leafgemm_tc(TreeDev T, const HB* A, const HB* B,
+                                                   const HB* C, Src PX, RankRef xr,
+                                                   int diag) {
+  extern __shared__ double sm[];
+  double* sa = sm;                 // [64][GLD]  A rows       (also P for cross terms)
+  double* sb = sa + 64 * GLD;      // [64][GLD]  B columns    (also Q for cross terms)
+  const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
+  const int lo = T.lo[lam], s = T.hi[lam] - lo, bw = T.bw, n = T.n;
+  const int S = (s + 7) & ~7;
+  const double* La = A[g].leaf + (long long)lo * bw;
+  const double* Lb = B[g].leaf + (long long)lo * bw;
+  double* Lc = C[g].leaf + (long long)lo * bw;
+  if (diag) {                      // exact: C = diag(a) B or A diag(b)
+    for (int idx = tid; idx < s * s; idx += GT) {
+      const int i = idx / s, j = idx - i * s;
+      Lc[(long long)i * bw + j] = diag == 1
+          ? La[(long long)i * bw + i] * Lb[(long long)i * bw + j]
+          : La[(long long)i * bw + j] * Lb[(long long)j * bw + j];
+    }
+    // level-0 couplings have rank-0 factors: no cross terms
+    return;
+  }
+  for (int idx = tid; idx < S * S; idx += GT) {
+    const int i = idx / S, j = idx - i * S;
+    const bool in = i < s && j < s;
+    sa[i * GLD + j] = in ? La[(long long)i * bw + j] : 0.0;          // A[i][j]
+    sb[j * GLD + i] = in ? Lb[(long long)i * bw + j] : 0.0;          // B[i][j] -> col j
+  }
+  __syncthreads();
+  // warp w owns tiles (tm, tn) with t = w, w+8, ... over (S/8)^2 tiles
+  const int nt = S / 8, ntt = nt * nt;
+  const int gi = lane >> 2, ti = lane & 3;
+  double acc[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t = warp + q * 8;
+    if (t < ntt) {
+      const int tm = t / nt, tn = t - tm * nt;
+      const double* ar = sa + (tm * 8 + gi) * GLD + ti;
+      const double* bc = sb + (tn * 8 + gi) * GLD + ti;
+      for (int k = 0; k < S; k += 4) dmma(acc[q][0], acc[q][1], ar[k], bc[k]);
+    }
+  }
+  // ancestor cross terms, parent first
+  const HB bb = B[g];
+  const int* cr = rank_base(xr, g);
+  int child = lam;
+  for (int al = T.parent[lam]; al >= 0; child = al, al = T.parent[al]) {
+    const int r = cr[al * 2 + (child == T.c0[al] ? 0 : 1)];
+    if (!r) continue;
+    const int rp = (r + 3) & ~3;
+    const int slot = T.depth[al];
+    const double* P = src_col(PX, n, g, slot, 0) + lo;
+    const double* Q = bb.V + (long long)slot * bb.R * n + lo;
+    __syncthreads();
+    for (int idx = tid; idx < S * rp; idx += GT) {
+      const int i = idx / rp, c = idx - i * rp;
+      const bool in = i < s && c < r;
+      sa[i * GLD + c] = in ? P[(long long)c * n + i] : 0.0;   // P[i][c]
+      sb[i * GLD + c] = in ? Q[(long long)c * n + i] : 0.0;   // Q[i][c] = (Q^T)[c][i]
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = warp + q * 8;
+      if (t < ntt) {
+        const int tm = t / nt, tn = t - tm * nt;
+        const double* pr = sa + (tm * 8 + gi) * GLD + ti;
+        const double* qc = sb + (tn * 8 + gi) * GLD + ti;
+        double z0 = 0.0, z1 = 0.0;
+        for (int k = 0; k < rp; k += 4) dmma(z0, z1, pr[k], qc[k]);
+        acc[q][0] = acc[q][0] + z0;
+        acc[q][1] = acc[q][1] + z1;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t = warp + q * 8;
+    if (t < ntt) {
+      const int tm = t / nt, tn = t - tm * nt;
+      const int i = tm * 8 + gi, j = tn * 8 + ti * 2;
+      if (i < s) {
+        if (j < s) Lc[(long long)i * bw + j] = acc[q][0];
+        if (j + 1 < s) Lc[(long long)i * bw + j + 1] = acc[q][1];
+      }
+    }
+  }
+}
+
 cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
-                            const HB* C, int nelem, Src PX, RankRef xr,
+                            const HB* C, int nelem, Src PX, RankRef xr, int diag,
                             cudaStream_t st) {
   if (!nelem) return cudaSuccess;
+  dim3 grid(T.nleaves, nelem);
+  if (T.bw <= 64) {
+    const size_t smem = 2ull * 64 * GLD * 8;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_leafgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = true;
+    }
+    k_leafgemm_tc<<<grid, GT, smem, st>>>(T, A, B, C, PX, xr, diag);
+    return cudaGetLastError();
+  }
   size_t smem = 2ull * T.bw * T.bw * 8;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr2 = false;
+  if (!attr2) {
     cudaFuncSetAttribute(k_leafgemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr = true;
+    attr2 = true;
   }
-  dim3 grid(T.nleaves, nelem);
   k_leafgemm<<<grid, LT, smem, st>>>(T, A, B, C, PX, xr);
   return cudaGetLastError();
 }

@@ -816,8 +816,17 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   }
   if (lane == 0) *tc.ro = keep;
   ACR_PH(5);
-  if (A.ctr && lane == 0)
+  if (A.ctr && lane == 0) {
     for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 12 + (i < 4 ? i : 3), (unsigned long long)ph[i]);
+    // histogram: R bucket (<=4, <=8, <=16, <=32, >32) x m bucket (<=32, 64, 128, 256, >256)
+    const int rb = R <= 4 ? 0 : R <= 8 ? 1 : R <= 16 ? 2 : R <= 32 ? 3 : 4;
+    const int mm = um > vm ? um : vm;
+    const int mb = mm <= 32 ? 0 : mm <= 64 ? 1 : mm <= 128 ? 2 : mm <= 256 ? 3 : 4;
+    long long tot = 0;
+    for (int i = 0; i < 6; ++i) tot += ph[i];
+    atomicAdd(A.ctr + 16 + rb * 5 + mb, 1ull);
+    atomicAdd(A.ctr + 41 + rb * 5 + mb, (unsigned long long)tot);
+  }
 }
 
 __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nitems,

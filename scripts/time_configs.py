@@ -40,3 +40,10 @@ for name in cfgs:
             if cls == 0:
                 st["trunc_ctr"] = list(ctr)
         print(json.dumps(dict(cfg=name, instrumented_factor_ms=round(sol.factor_ms, 1), classes=st)), flush=True)
+        nl = C.c_longlong(); ms = C.c_double(); ctr = (C.c_ulonglong * 72)()
+        sol.lib.acr_kernel_stats(sol.plan, 100, C.byref(nl), C.byref(ms), ctr)
+        cnt = list(ctr)[16:41]; cyc = list(ctr)[41:66]
+        tot = sum(cyc) or 1
+        print("warp-path histogram (rows R<=4,8,16,32,>32; cols m<=32,64,128,256,>256): count / %cycles / kcyc-per-task")
+        for rb in range(5):
+            print("  ", " | ".join(f"{cnt[rb*5+mb]:8d} {100*cyc[rb*5+mb]/tot:5.1f}% {cyc[rb*5+mb]/max(cnt[rb*5+mb],1)/1e3:6.1f}" for mb in range(5)))
