@@ -126,6 +126,77 @@ __global__ void __launch_bounds__(HT) k_hmatB(TreeDev T, MMJobs2 JJ, int nBmax) 
   }
 }
 
+// Phase B for jobs whose subtree roots are every non-root node (multiply M1):
+// one CTA per (leaf, element, job) serves all roots mu on the leaf's path, so
+// the leaf block is read once instead of once per ancestor.
+__global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
+  extern __shared__ double sm[];
+  const MMJob& J = JJ.j[blockIdx.z];
+  const int g = blockIdx.y, n = T.n, bw = T.bw;
+  const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
+  const int lo = T.lo[lam], s = T.hi[lam] - lo;
+  const HB h = J.H[g];
+  const int* an = T.anc + lam * (T.maxdepth + 1);
+  const int dl = T.depth[lam];
+  double* L = sm;
+  double* X = L + s * s;
+  // columns of each root on the path (t = 0: lam itself ... dl-1)
+  int cnt = 0;
+  int off[16], cols[16], mus[16];
+  for (int t = 0; t < dl && t < 16; ++t) {
+    const int mu = an[t];
+    if (mu < J.mu0 || mu >= J.mu1) continue;
+    const int c = mm_cols(J, T, g, mu);
+    mus[cnt] = mu;
+    cols[cnt] = c;
+    off[cnt] = cnt == 0 ? 0 : off[cnt - 1] + cols[cnt - 1];
+    ++cnt;
+  }
+  const int ctot = cnt ? off[cnt - 1] + cols[cnt - 1] : 0;
+  if (!ctot) return;
+  const double* Lg = h.leaf + (long long)lo * bw;
+  for (int idx = threadIdx.x; idx < s * s; idx += HT) {
+    int i = idx / s, j = idx - i * s;
+    L[idx] = Lg[(long long)i * bw + j];
+  }
+  for (int q = 0; q < cnt; ++q) {
+    const int slot = mm_slot(T, mus[q]);
+    for (int idx = threadIdx.x; idx < s * cols[q]; idx += HT) {
+      int b = idx / s, i = idx - b * s;
+      X[(off[q] + b) * s + i] = src_col(J.X, n, g, slot, b)[lo + i];
+    }
+  }
+  __syncthreads();
+  const int eA0 = T.startA[J.mu0];
+  for (int idx = threadIdx.x; idx < s * ctot; idx += HT) {
+    const int bb = idx / s, i = idx - bb * s;
+    int q = 0;
+    while (q + 1 < cnt && off[q + 1] <= bb) ++q;
+    const int mu = mus[q], b = bb - off[q];
+    double y = 0.0;
+    const double* xb = X + bb * s;
+    if (!J.trans)
+      for (int j = 0; j < s; ++j) y += L[i * s + j] * xb[j];
+    else
+      for (int j = 0; j < s; ++j) y += L[j * s + i] * xb[j];
+    for (int be = lam; be != mu;) {
+      be = T.parent[be];
+      const int bmid = T.mid[be];
+      const bool top = lo < bmid;
+      const int sd = J.trans ? (top ? 1 : 0) : (top ? 0 : 1);
+      const int r = h.rk[be * 2 + sd];
+      if (!r) continue;
+      const int e = T.startA[mu] + 2 * T.posA[mu * T.nnodes + be] + sd - eA0;
+      const double* t = J.tbuf + ((long long)g * J.nA + e) * J.RT * J.CT;
+      const double* F = (J.trans ? h.V : h.U) + (long long)T.depth[be] * h.R * n + lo + i;
+      double z = 0.0;
+      for (int a = 0; a < r; ++a) z += F[(long long)a * n] * t[a * J.CT + b];
+      y = y + z;
+    }
+    src_col(J.Y, n, g, mm_slot(T, mu), b)[lo + i] = J.alpha * y;
+  }
+}
+
 cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
                         int nelem, cudaStream_t st) {
   if (!nelem || !njobs) return cudaSuccess;
@@ -144,13 +215,21 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  size_t smem = ((size_t)T.bw * T.bw + (size_t)T.bw * cmax) * 8;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_hmatB, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_path, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr = true;
   }
+  if (jobs[0].mu0 == 1 && jobs[0].mu1 == T.nnodes && T.maxdepth <= 16) {
+    size_t smem = ((size_t)T.bw * T.bw + (size_t)T.bw * cmax * T.maxdepth) * 8;
+    dim3 g(T.nleaves, nelem, njobs);
+    k_hmatB_path<<<g, HT, smem, st>>>(T, JJ);
+    return cudaGetLastError();
+  }
+  size_t smem = ((size_t)T.bw * T.bw + (size_t)T.bw * cmax) * 8;
   dim3 g(nB, nelem, njobs);
   k_hmatB<<<g, HT, smem, st>>>(T, JJ, nB);
   return cudaGetLastError();

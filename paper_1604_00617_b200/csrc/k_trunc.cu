@@ -74,6 +74,82 @@ __device__ __forceinline__ OpRes resolve_op(const TOp& op, const TreeDev& T,
   return o;
 }
 
+// Half-CTA thread group with its own named barrier (ids 1, 2), so the QR of
+// U and of V (and later the two Q applications) run concurrently.
+struct Grp {
+  int id, nt, t, nw, w, lane;
+  double* red;
+  double* bc;
+};
+
+__device__ __forceinline__ void gbar(const Grp& g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g.id), "r"(g.nt) : "memory");
+}
+
+__device__ __forceinline__ double gsum(double v, const Grp& g) {
+  v = warp_sum(v);
+  gbar(g);
+  if (g.lane == 0) g.red[g.w] = v;
+  gbar(g);
+  double s = 0.0;
+  for (int w = 0; w < g.nw; ++w) s += g.red[w];   // fixed order
+  return s;
+}
+
+__device__ void group_qr(double* W, int mr, int R, double* tau, const Grp& g) {
+  const int p = mr < R ? mr : R;
+  for (int j = 0; j < p; ++j) {
+    double* cj = W + (long long)j * mr;
+    double ss = 0.0;
+    for (int i = j + 1 + g.t; i < mr; i += g.nt) ss += cj[i] * cj[i];
+    ss = gsum(ss, g);
+    const double alpha = cj[j];
+    double tj = 0.0, scal = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    gbar(g);                                  // everyone has read cj[j]
+    if (tj != 0.0) {
+      for (int i = j + 1 + g.t; i < mr; i += g.nt) cj[i] *= scal;
+      if (g.t == 0) cj[j] = beta;
+    }
+    if (g.t == 0) tau[j] = tj;
+    gbar(g);
+    if (tj != 0.0) {
+      for (int c = j + 1 + g.w; c < R; c += g.nw) {
+        double* cc = W + (long long)c * mr;
+        double w = 0.0;
+        for (int i = j + 1 + g.lane; i < mr; i += 32) w += cj[i] * cc[i];
+        w = (warp_sum(w) + cc[j]) * tj;
+        for (int i = j + 1 + g.lane; i < mr; i += 32) cc[i] -= w * cj[i];
+        if (g.lane == 0) cc[j] -= w;
+      }
+      gbar(g);
+    }
+  }
+}
+
+__device__ void group_apply_q(const double* W, int mr, int p, const double* tau,
+                              double* X, int nc, const Grp& g) {
+  for (int j = p - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj != 0.0) {
+      const double* v = W + (long long)j * mr;
+      for (int c = g.w; c < nc; c += g.nw) {
+        double* xc = X + (long long)c * mr;
+        double w = 0.0;
+        for (int i = j + 1 + g.lane; i < mr; i += 32) w += v[i] * xc[i];
+        w = (warp_sum(w) + xc[j]) * tj;
+        for (int i = j + 1 + g.lane; i < mr; i += 32) xc[i] -= w * v[i];
+        if (g.lane == 0) xc[j] -= w;
+      }
+      gbar(g);
+    }
+  }
+}
+
 // Householder QR of W (mr x R, column-major, ld = mr), in place.  On exit
 // the upper trapezoid holds R, below-diagonal the reflector tails, tau[j].
 __device__ void block_qr(double* W, int mr, int R, double* tau, double* red,
@@ -293,7 +369,7 @@ __host__ __device__ long long trunc_need_doubles(int um, int vm, int R) {
 }
 
 __host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
-  return (long long)(um + vm) * R + 2LL * R * R + 4LL * R + (um > vm ? um : vm) + 8;
+  return (long long)(um + vm) * R + 2LL * R * R + 4LL * R + um + vm + 8;
 }
 
 // ---------------------------------------------------------------------------
@@ -335,8 +411,15 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   }
   __syncthreads();
   ACR_PH(0);
-  block_qr(Uw, um, R, tauU, red, red + NWB);
-  block_qr(Vw, vm, R, tauV, red, red + NWB);
+  {
+    const int half = tid >= TT / 2 ? 1 : 0;
+    const int t = tid - half * (TT / 2);
+    Grp g{1 + half, TT / 2, t, NWB / 2, t >> 5, tid & 31, red + half * (NWB / 2),
+          nullptr};
+    if (!half) group_qr(Uw, um, R, tauU, g);
+    else group_qr(Vw, vm, R, tauV, g);
+  }
+  __syncthreads();
   ACR_PH(1);
 
   // Frobenius norms of the triangular factors (hodlr.py:191-192)
@@ -428,8 +511,15 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     Ov[idx] = v;
   }
   __syncthreads();
-  block_apply_q(Uw, um, pu, tauU, Ou, keep);
-  block_apply_q(Vw, vm, pv, tauV, Ov, keep);
+  {
+    const int half = tid >= TT / 2 ? 1 : 0;
+    const int t = tid - half * (TT / 2);
+    Grp g{1 + half, TT / 2, t, NWB / 2, t >> 5, tid & 31, red + half * (NWB / 2),
+          nullptr};
+    if (!half) group_apply_q(Uw, um, pu, tauU, Ou, keep, g);
+    else group_apply_q(Vw, vm, pv, tauV, Ov, keep, g);
+  }
+  __syncthreads();
   for (int idx = tid; idx < um * keep; idx += TT) {
     int c = idx / um, i = idx - c * um;
     Uo[(long long)c * n + i] = Ou[idx];
@@ -553,55 +643,109 @@ __device__ __forceinline__ void warp_copy_factor(const OpRes& s, double* Uo, dou
   }
 }
 
-// Householder QR of W (mr x R, col-major ld mr) by one warp
-__device__ void warp_qr(double* W, int mr, int R, double* tau, int lane) {
-  const int p = mr < R ? mr : R;
-  for (int j = 0; j < p; ++j) {
-    double* cj = W + (long long)j * mr;
-    double ss = 0.0;
-    for (int i = j + 1 + lane; i < mr; i += 32) ss += cj[i] * cj[i];
-    ss = warp_sum(ss);
-    const double alpha = cj[j];
-    double tj = 0.0, scal = 0.0, beta = alpha;
-    if (ss != 0.0) {
-      beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
-      tj = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    __syncwarp();
-    if (tj != 0.0) {
-      for (int i = j + 1 + lane; i < mr; i += 32) cj[i] *= scal;
-      if (lane == 0) cj[j] = beta;
-    }
-    if (lane == 0) tau[j] = tj;
-    __syncwarp();
-    if (tj != 0.0) {
-      for (int c = j + 1; c < R; ++c) {
-        double* cc = W + (long long)c * mr;
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < mr; i += 32) w += cj[i] * cc[i];
-        w = (warp_sum(w) + cc[j]) * tj;
-        for (int i = j + 1 + lane; i < mr; i += 32) cc[i] -= w * cj[i];
-        if (lane == 0) cc[j] -= w;
-      }
-      __syncwarp();
-    }
+// Householder QR of U (mu x R) and V (mv x R) by one warp, interleaved: the
+// two factorisations are independent, so their reduction chains overlap.
+__device__ __forceinline__ void warp_reflector(double* cj, int j, int mr, double ss,
+                                               double& tj, int lane) {
+  const double alpha = cj[j];
+  double scal = 0.0, beta = alpha;
+  tj = 0.0;
+  if (ss != 0.0) {
+    beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+    tj = (beta - alpha) / beta;
+    scal = 1.0 / (alpha - beta);
+  }
+  __syncwarp();
+  if (tj != 0.0) {
+    for (int i = j + 1 + lane; i < mr; i += 32) cj[i] *= scal;
+    if (lane == 0) cj[j] = beta;
   }
 }
 
-// x (length mr) := Q x,  Q = H_0 ... H_{p-1}
-__device__ void warp_apply_q(const double* W, int mr, int p, const double* tau,
-                             double* x, int lane) {
-  for (int j = p - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* v = W + (long long)j * mr;
-    double w = 0.0;
-    for (int i = j + 1 + lane; i < mr; i += 32) w += v[i] * x[i];
-    w = (warp_sum(w) + x[j]) * tj;
-    for (int i = j + 1 + lane; i < mr; i += 32) x[i] -= w * v[i];
+__device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, double* tv,
+                         int R, int lane) {
+  const int pu = mu < R ? mu : R, pv = mv < R ? mv : R;
+  const int p = pu > pv ? pu : pv;
+  for (int j = 0; j < p; ++j) {
+    const bool du = j < pu, dv = j < pv;
+    double* cu = Wu + (long long)j * mu;
+    double* cv = Wv + (long long)j * mv;
+    double su = 0.0, sv = 0.0;
+    if (du) for (int i = j + 1 + lane; i < mu; i += 32) su += cu[i] * cu[i];
+    if (dv) for (int i = j + 1 + lane; i < mv; i += 32) sv += cv[i] * cv[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      su += __shfl_xor_sync(FULL, su, o);
+      sv += __shfl_xor_sync(FULL, sv, o);
+    }
+    double tju = 0.0, tjv = 0.0;
+    if (du) warp_reflector(cu, j, mu, su, tju, lane);
+    if (dv) warp_reflector(cv, j, mv, sv, tjv, lane);
+    if (lane == 0) {
+      if (du) tu[j] = tju;
+      if (dv) tv[j] = tjv;
+    }
     __syncwarp();
-    if (lane == 0) x[j] -= w;
+    const bool au = du && tju != 0.0, av = dv && tjv != 0.0;
+    if (!au && !av) continue;
+    for (int c = j + 1; c < R; ++c) {
+      double* ccu = Wu + (long long)c * mu;
+      double* ccv = Wv + (long long)c * mv;
+      double wu = 0.0, wv = 0.0;
+      if (au) for (int i = j + 1 + lane; i < mu; i += 32) wu += cu[i] * ccu[i];
+      if (av) for (int i = j + 1 + lane; i < mv; i += 32) wv += cv[i] * ccv[i];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        wu += __shfl_xor_sync(FULL, wu, o);
+        wv += __shfl_xor_sync(FULL, wv, o);
+      }
+      if (au) {
+        wu = (wu + ccu[j]) * tju;
+        for (int i = j + 1 + lane; i < mu; i += 32) ccu[i] -= wu * cu[i];
+        if (lane == 0) ccu[j] -= wu;
+      }
+      if (av) {
+        wv = (wv + ccv[j]) * tjv;
+        for (int i = j + 1 + lane; i < mv; i += 32) ccv[i] -= wv * cv[i];
+        if (lane == 0) ccv[j] -= wv;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// xu := Qu xu and xv := Qv xv, interleaved
+__device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu,
+                              double* xu, const double* Wv, int mv, int pv,
+                              const double* tv, double* xv, int lane) {
+  const int p = pu > pv ? pu : pv;
+  for (int j = p - 1; j >= 0; --j) {
+    const double tju = j < pu ? tu[j] : 0.0;
+    const double tjv = j < pv ? tv[j] : 0.0;
+    if (tju == 0.0 && tjv == 0.0) continue;
+    const double* vu = Wu + (long long)j * mu;
+    const double* vv = Wv + (long long)j * mv;
+    double wu = 0.0, wv = 0.0;
+    if (tju != 0.0) for (int i = j + 1 + lane; i < mu; i += 32) wu += vu[i] * xu[i];
+    if (tjv != 0.0) for (int i = j + 1 + lane; i < mv; i += 32) wv += vv[i] * xv[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      wu += __shfl_xor_sync(FULL, wu, o);
+      wv += __shfl_xor_sync(FULL, wv, o);
+    }
+    if (tju != 0.0) {
+      wu = (wu + xu[j]) * tju;
+      for (int i = j + 1 + lane; i < mu; i += 32) xu[i] -= wu * vu[i];
+    }
+    if (tjv != 0.0) {
+      wv = (wv + xv[j]) * tjv;
+      for (int i = j + 1 + lane; i < mv; i += 32) xv[i] -= wv * vv[i];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (tju != 0.0) xu[j] -= wu;
+      if (tjv != 0.0) xv[j] -= wv;
+    }
     __syncwarp();
   }
 }
@@ -725,8 +869,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   warp_load_cols(Vw, vm, a.V, a.r, 1.0, b.V, b.r, 1.0, n, lane);
   __syncwarp();
   ACR_PH(0);
-  warp_qr(Uw, um, R, tauU, lane);
-  warp_qr(Vw, vm, R, tauV, lane);
+  warp_qr2(Uw, um, tauU, Vw, vm, tauV, R, lane);
   ACR_PH(1);
   double nu2 = 0.0, nv2 = 0.0;
   for (int idx = lane; idx < pu * R; idx += 32) {
@@ -791,6 +934,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     atomicAdd(A.ctr + 9, 1ull);
     atomicAdd(A.ctr + 11, (unsigned long long)sweeps);
   }
+  double* ob2 = ob + um;
   for (int c = 0; c < keep; ++c) {
     const int j = ord[c];
     for (int i = lane; i < um; i += 32) {
@@ -798,20 +942,17 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
       if (i < pu) v = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
       ob[i] = v;
     }
-    __syncwarp();
-    warp_apply_q(Uw, um, pu, tauU, ob, lane);
-    double* du = tc.Uo + (long long)c * n;
-    for (int i = lane; i < um; i += 32) du[i] = ob[i];
-    __syncwarp();
     for (int i = lane; i < vm; i += 32) {
       double v = 0.0;
       if (i < pv) v = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
-      ob[i] = v;
+      ob2[i] = v;
     }
     __syncwarp();
-    warp_apply_q(Vw, vm, pv, tauV, ob, lane);
+    warp_apply_q2(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
+    double* du = tc.Uo + (long long)c * n;
+    for (int i = lane; i < um; i += 32) du[i] = ob[i];
     double* dv = tc.Vo + (long long)c * n;
-    for (int i = lane; i < vm; i += 32) dv[i] = ob[i];
+    for (int i = lane; i < vm; i += 32) dv[i] = ob2[i];
     __syncwarp();
   }
   if (lane == 0) *tc.ro = keep;
