@@ -88,12 +88,13 @@ __global__ void __launch_bounds__(HT) k_hmatB(TreeDev T, MMJobs2 JJ, int nBmax) 
   const HB h = J.H[g];
   const int lo = T.lo[lam], s = T.hi[lam] - lo;
   const int slot = mm_slot(T, mu);
-  double* L = sm;                 // s x s
-  double* X = L + s * s;          // c x s (column-major panel)
+  const int ld = s + 1;            // padded: conflict-free column reads
+  double* L = sm;                 // s x ld
+  double* X = L + s * ld;         // c x s (column-major panel)
   const double* Lg = h.leaf + (long long)lo * bw;
   for (int idx = threadIdx.x; idx < s * s; idx += HT) {
     int i = idx / s, j = idx - i * s;
-    L[idx] = Lg[(long long)i * bw + j];
+    L[i * ld + j] = Lg[(long long)i * bw + j];
   }
   for (int idx = threadIdx.x; idx < s * c; idx += HT) {
     int b = idx / s, i = idx - b * s;
@@ -105,9 +106,9 @@ __global__ void __launch_bounds__(HT) k_hmatB(TreeDev T, MMJobs2 JJ, int nBmax) 
     int b = idx / s, i = idx - b * s;
     double y = 0.0;
     if (!J.trans)
-      for (int j = 0; j < s; ++j) y += L[i * s + j] * X[b * s + j];
+      for (int j = 0; j < s; ++j) y += L[i * ld + j] * X[b * s + j];
     else
-      for (int j = 0; j < s; ++j) y += L[j * s + i] * X[b * s + j];
+      for (int j = 0; j < s; ++j) y += L[j * ld + i] * X[b * s + j];
     for (int be = lam; be != mu;) {
       be = T.parent[be];
       int bmid = T.mid[be];
@@ -138,8 +139,9 @@ __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
   const HB h = J.H[g];
   const int* an = T.anc + lam * (T.maxdepth + 1);
   const int dl = T.depth[lam];
+  const int ld = s + 1;            // padded: conflict-free column reads
   double* L = sm;
-  double* X = L + s * s;
+  double* X = L + s * ld;
   // columns of each root on the path (t = 0: lam itself ... dl-1)
   int cnt = 0;
   int off[16], cols[16], mus[16];
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
   const double* Lg = h.leaf + (long long)lo * bw;
   for (int idx = threadIdx.x; idx < s * s; idx += HT) {
     int i = idx / s, j = idx - i * s;
-    L[idx] = Lg[(long long)i * bw + j];
+    L[i * ld + j] = Lg[(long long)i * bw + j];
   }
   for (int q = 0; q < cnt; ++q) {
     const int slot = mm_slot(T, mus[q]);
@@ -176,9 +178,9 @@ __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
     double y = 0.0;
     const double* xb = X + bb * s;
     if (!J.trans)
-      for (int j = 0; j < s; ++j) y += L[i * s + j] * xb[j];
+      for (int j = 0; j < s; ++j) y += L[i * ld + j] * xb[j];
     else
-      for (int j = 0; j < s; ++j) y += L[j * s + i] * xb[j];
+      for (int j = 0; j < s; ++j) y += L[j * ld + i] * xb[j];
     for (int be = lam; be != mu;) {
       be = T.parent[be];
       const int bmid = T.mid[be];
@@ -224,12 +226,12 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     attr = true;
   }
   if (jobs[0].mu0 == 1 && jobs[0].mu1 == T.nnodes && T.maxdepth <= 16) {
-    size_t smem = ((size_t)T.bw * T.bw + (size_t)T.bw * cmax * T.maxdepth) * 8;
+    size_t smem = ((size_t)T.bw * (T.bw + 1) + (size_t)T.bw * cmax * T.maxdepth) * 8;
     dim3 g(T.nleaves, nelem, njobs);
     k_hmatB_path<<<g, HT, smem, st>>>(T, JJ);
     return cudaGetLastError();
   }
-  size_t smem = ((size_t)T.bw * T.bw + (size_t)T.bw * cmax) * 8;
+  size_t smem = ((size_t)T.bw * (T.bw + 1) + (size_t)T.bw * cmax) * 8;
   dim3 g(nB, nelem, njobs);
   k_hmatB<<<g, HT, smem, st>>>(T, JJ, nB);
   return cudaGetLastError();
