@@ -270,11 +270,23 @@ __global__ void __launch_bounds__(HT) k_gp(TreeDev T, GPJobs2 JJ, const int* nod
     if (lane == 0) K[a * ry + b] = s;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < l2 * ry; idx += HT) {
-    int b = idx / l2, i = idx - b * l2;
-    double z = 0.0;
-    for (int a = 0; a < rx; ++a) z += src_col(J.W, n, g, slot, a)[r2 + i] * K[a * ry + b];
-    src_col(J.Z, n, g, slot, b)[r2 + i] = J.alpha * z;
+  // thread per output row: W[i][:] loaded once, all ry outputs of the row
+  for (int i = threadIdx.x; i < l2; i += HT) {
+    double w[32];
+    for (int a0 = 0; a0 < rx; a0 += 32) {
+      const int na = rx - a0 < 32 ? rx - a0 : 32;
+#pragma unroll
+      for (int a = 0; a < 32; ++a)
+        if (a < na) w[a] = src_col(J.W, n, g, slot, a0 + a)[r2 + i];
+      for (int b = 0; b < ry; ++b) {
+        double z = 0.0;
+#pragma unroll
+        for (int a = 0; a < 32; ++a)
+          if (a < na) z += w[a] * K[(a0 + a) * ry + b];
+        if (a0 == 0) src_col(J.Z, n, g, slot, b)[r2 + i] = J.alpha * z;
+        else src_col(J.Z, n, g, slot, b)[r2 + i] += J.alpha * z;
+      }
+    }
   }
   if (J.orank && threadIdx.x == 0) J.orank[g * J.ors + nu * 2 + J.oside] = ry;
 }

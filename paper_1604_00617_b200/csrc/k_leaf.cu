@@ -451,6 +451,7 @@ cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
 __global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
                                                Src Us, Src Vs, RankRef rr,
                                                int node, int fside) {
+  extern __shared__ double sm[];
   const int g = blockIdx.y, tid = threadIdx.x, n = T.n, bw = T.bw;
   const int* rb = rank_base(rr, g);
   int r = rb[node * 2 + fside];
@@ -461,22 +462,38 @@ __global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
   const int slot = T.depth[node];
   const double* U = src_col(Us, n, g, slot, 0) + lo;
   const double* V = src_col(Vs, n, g, slot, 0) + lo;
+  // stage the leaf rows of U and V (r columns) once: u[c][i], v[c][j]
+  double* u = sm;
+  double* v = u + r * s;
+  for (int idx = tid; idx < r * s; idx += LT) {
+    const int c = idx / s, i = idx - c * s;
+    u[idx] = U[(long long)c * n + i];
+    v[idx] = V[(long long)c * n + i];
+  }
+  __syncthreads();
   double* L = H[g].leaf + (long long)lo * bw;
   for (int idx = tid; idx < s * s; idx += LT) {
     int i = idx / s, j = idx - i * s;
     double z = 0.0;
-    for (int c = 0; c < r; ++c) z += U[(long long)c * n + i] * V[(long long)c * n + j];
+    for (int c = 0; c < r; ++c) z += u[c * s + i] * v[c * s + j];
     L[(long long)i * bw + j] = L[(long long)i * bw + j] + z;
   }
 }
 
-// variant with explicit leaf count (host knows the tree)
 cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
                             int nleaf, Src U, Src V, RankRef rr, int node,
                             int fside, cudaStream_t st) {
   if (!nelem || !nleaf) return cudaSuccess;
   dim3 grid(nleaf, nelem);
-  k_leaflr<<<grid, LT, 0, st>>>(T, H, mu, U, V, rr, node, fside);
+  const int cap = U.kind >= 2 ? 256 : (U.C > 0 ? U.C : 256);   // rank bound
+  size_t smem = 2ull * T.bw * (size_t)cap * 8;
+  if (smem > 200 * 1024) smem = 200 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_leaflr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_leaflr<<<grid, LT, smem, st>>>(T, H, mu, U, V, rr, node, fside);
   return cudaGetLastError();
 }
 
