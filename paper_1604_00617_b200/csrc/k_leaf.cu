@@ -378,30 +378,39 @@ __global__ void __launch_bounds__(GT) k_leafgemm_tc(TreeDev T, const HB* A, cons
   for (int al = T.parent[lam]; al >= 0; child = al, al = T.parent[al]) {
     const int r = cr[al * 2 + (child == T.c0[al] ? 0 : 1)];
     if (!r) continue;
-    const int rp = (r + 3) & ~3;
     const int slot = T.depth[al];
     const double* P = src_col(PX, n, g, slot, 0) + lo;
     const double* Q = bb.V + (long long)slot * bb.R * n + lo;
-    __syncthreads();
-    for (int idx = tid; idx < S * rp; idx += GT) {
-      const int i = idx / rp, c = idx - i * rp;
-      const bool in = i < s && c < r;
-      sa[i * GLD + c] = in ? P[(long long)c * n + i] : 0.0;   // P[i][c]
-      sb[i * GLD + c] = in ? Q[(long long)c * n + i] : 0.0;   // Q[i][c] = (Q^T)[c][i]
+    double z[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z[q][0] = z[q][1] = 0.0;
+    // rank r may exceed the 64-column staging rows: k-chunks of 64
+    for (int k0 = 0; k0 < r; k0 += 64) {
+      const int kr = r - k0 < 64 ? r - k0 : 64;
+      const int rp = (kr + 3) & ~3;
+      __syncthreads();
+      for (int idx = tid; idx < S * rp; idx += GT) {
+        const int i = idx / rp, c = idx - i * rp;
+        const bool in = i < s && c < kr;
+        sa[i * GLD + c] = in ? P[(long long)(k0 + c) * n + i] : 0.0;   // P[i][c]
+        sb[i * GLD + c] = in ? Q[(long long)(k0 + c) * n + i] : 0.0;   // Q[i][c]
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int t = warp + q * 8;
+        if (t < ntt) {
+          const int tm = t / nt, tn = t - tm * nt;
+          const double* pr = sa + (tm * 8 + gi) * GLD + ti;
+          const double* qc = sb + (tn * 8 + gi) * GLD + ti;
+          for (int k = 0; k < rp; k += 4) dmma(z[q][0], z[q][1], pr[k], qc[k]);
+        }
+      }
     }
-    __syncthreads();
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int t = warp + q * 8;
-      if (t < ntt) {
-        const int tm = t / nt, tn = t - tm * nt;
-        const double* pr = sa + (tm * 8 + gi) * GLD + ti;
-        const double* qc = sb + (tn * 8 + gi) * GLD + ti;
-        double z0 = 0.0, z1 = 0.0;
-        for (int k = 0; k < rp; k += 4) dmma(z0, z1, pr[k], qc[k]);
-        acc[q][0] = acc[q][0] + z0;
-        acc[q][1] = acc[q][1] + z1;
-      }
+      acc[q][0] = acc[q][0] + z[q][0];
+      acc[q][1] = acc[q][1] + z[q][1];
     }
   }
 #pragma unroll

@@ -229,3 +229,30 @@ def test_single_block_and_cutoff(solver_mod):
     uo, ro = O.acr_solve(s, Tolerance(1e-12), cutoff_blocks=3, leaf_size=4)
     assert rep.levels == ro.levels and rep.cutoff_blocks == ro.cutoff_blocks
     assert _rel(u, uo) <= 1e-11
+
+
+def test_config4_residual_against_reference(solver_mod):
+    """Config 4 (Helmholtz, 10 ppw) is ill-conditioned for the method: the
+    reference moves by 24.8 x eps under a 1e-15 input perturbation (SURVEY
+    section 0, fact 7), so only the residual criterion is meaningful."""
+    z = load_npz("cfg4.npz")
+    c = P.CONFIGS["cfg4"]
+    u, rep = solver_mod.acr_solve(P.make_config("cfg4"), Tolerance(c["eps"]),
+                                  leaf_size=c["leaf"])
+    assert rep.residual <= 2 * float(z["residual"])
+    assert rep.levels == int(z["levels"])
+    prof = golden_profiles(z, "")
+    assert all(abs(max(p.max_by_depth) - max(q[0])) <= 2
+               for p, q in zip(rep.per_level_ranks, prof))
+
+
+def test_config5_column0_against_reference(solver_mod):
+    """BASELINE config 5 (2048^2, leaf 64) against the reference's own
+    single-column run (10 min on the host; tests/golden/cfg5.npz)."""
+    z = load_npz("cfg5.npz")
+    c = P.CONFIGS["cfg5"]
+    u, rep = solver_mod.acr_solve(P.make_config("cfg5", nrhs=1), Tolerance(c["eps"]),
+                                  leaf_size=c["leaf"])
+    stride = int(z["u_stride"])
+    _check_against_golden(rep, u, z, "", c["eps"], stride=stride,
+                          shape=(c["n"], c["n"], c["leaf"]))
