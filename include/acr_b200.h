@@ -36,6 +36,26 @@ int acr_plan_create(int m, int n, int leaf_size, double eps, int max_rank_cap,
                     int cutoff_blocks, acr_plan_t** out);
 void acr_plan_destroy(acr_plan_t* p);
 
+/* Sharded plan: rank `rank` of `nranks` owns global block
+ * rows [bnd0[rank], bnd0[rank+1]) (bnd0: nranks+1 host ints, bnd0[0] = 0,
+ * bnd0[nranks] = m, even starts).  Per level a rank sends its first even
+ * block's {Dinv, E, F} to rank-1 over NCCL; the top levels are gathered on
+ * rank 0.  nccl_id: 128 bytes from acr_nccl_unique_id() on rank 0,
+ * broadcast by the caller.  acr_factor / acr_solve then take the GLOBAL band,
+ * rhs and u arrays (each rank writes its own rows of u). */
+int acr_nccl_unique_id(void* out128);
+int acr_plan_create_dist(int m, int n, int leaf_size, double eps, int max_rank_cap,
+                         int cutoff_blocks, int rank, int nranks, const int* bnd0,
+                         const void* nccl_id, acr_plan_t** out);
+/* The same sharded factor + solve with `nranks` virtual ranks as threads of
+ * this process on the current GPU (loopback transport; tests the sharded
+ * path on one GPU).  factor_ms: max over ranks. */
+int acr_loopback_solve(int nranks, const int* bnd0, int m, int n, int leaf_size,
+                       double eps, int max_rank_cap, int cutoff_blocks,
+                       const double* D_sub, const double* D_diag, const double* D_sup,
+                       const double* E, const double* F, const double* rhs, int nrhs,
+                       double* u, double* factor_ms);
+
 /* option 1: keep every level's D blocks for export (tests); value 0/1
  * option 2: per-kernel-class instrumentation (CUDA events around every
  *           launch of a class + algorithmic FLOP/byte counters); 0/1 */

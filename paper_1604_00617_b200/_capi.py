@@ -18,6 +18,13 @@ _SIGS = [
     ("acr_plan_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                   C.c_int, C.POINTER(C.c_void_p)]),
     ("acr_plan_destroy", None, [C.c_void_p]),
+    ("acr_nccl_unique_id", C.c_int, [C.c_void_p]),
+    ("acr_plan_create_dist", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                       C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                       C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("acr_loopback_solve", C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int,
+                                     C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 6 +
+     [C.c_int, C.c_void_p, C.POINTER(C.c_double)]),
     ("acr_plan_set_option", C.c_int, [C.c_void_p, C.c_int, C.c_longlong]),
     ("acr_factor", C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int, C.c_void_p]),
     ("acr_solve", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),

@@ -17,11 +17,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
 #include "acr_launch.h"
 #include "acr_types.cuh"
+#include "dist.h"
 #include "../../include/acr_b200.h"
 
 namespace acr {
@@ -349,14 +351,18 @@ struct Seg {
   int first, step, count;
 };
 
+// A level is a window [first, first+m) of a global level of mg blocks (one
+// GPU: first = 0, m = mg).  E of global block 0 and F of global block mg-1
+// are unused (rank 0).
 struct Level {
-  int m = 0;
+  int m = 0, first = 0, mg = 0;
   int R = 1;
-  Batch D, E, F;   // E element 0 and F element m-1 unused (rank 0)
+  Batch D, E, F;
 };
 
 struct Record {
-  int m = 0;
+  int m = 0, first = 0, mg = 0;
+  bool right = false;               // a right neighbour (other rank) exists
   Batch Dinv, E, F;
   std::vector<int> hDinv, hE, hF;   // host ranks (storage accounting)
 };
@@ -443,6 +449,12 @@ struct Plan {
   bool factored = false;
   long long reserved = 0;
   std::string err;
+  // sharding: level-0 block boundaries of every rank
+  Transport* tp = nullptr;
+  bool own_tp = false;
+  std::vector<int> bnd0;
+  int Ld = 0;                 // number of distributed levels (then rank 0 alone)
+  int first0 = 0, mloc0 = 0;  // this rank's level-0 window
   // per-kernel-class instrumentation (option 2)
   bool prof_on = false;
   enum { NCLS = 8 };
@@ -467,6 +479,49 @@ struct Plan {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : evpool) cudaEventDestroy(e);
+    if (own_tp) delete tp;
+  }
+
+  int nranks() const { return tp ? tp->size() : 1; }
+  int me() const { return tp ? tp->rank() : 0; }
+
+  // block boundaries of every rank at level l (b[P] = global block count)
+  std::vector<int> bounds(int l) const {
+    const int P = nranks();
+    std::vector<int> b(P + 1);
+    int mg = m;
+    for (int t = 0; t < l; ++t) mg /= 2;
+    for (int r = 0; r < P; ++r) b[r] = bnd0.empty() ? 0 : (bnd0[r] >> l);
+    b[P] = mg;
+    return b;
+  }
+  // level l can be reduced distributed: every window starts even, has >= 2
+  // blocks and (except the last) an even length
+  bool dist_ok(int l) const {
+    const int P = nranks();
+    if (P <= 1) return false;
+    std::vector<int> b = bounds(l);
+    for (int r = 0; r < P; ++r) {
+      const int c = b[r + 1] - b[r];
+      if ((b[r] & 1) || c < 2) return false;
+      if (r < P - 1 && (c & 1)) return false;
+    }
+    return true;
+  }
+
+  void block_msgs(std::vector<Msg>& msgs, const Batch& b, int e, int peer, bool send) {
+    msgs.push_back({peer, b.leaf.as<double>() + e * b.sl, sizeof(double) * b.sl, send});
+    msgs.push_back({peer, b.U.as<double>() + e * b.sf, sizeof(double) * b.sf, send});
+    msgs.push_back({peer, b.V.as<double>() + e * b.sf, sizeof(double) * b.sf, send});
+    msgs.push_back({peer, b.rk.as<int>() + e * b.sr, sizeof(int) * b.sr, send});
+  }
+  void range_msgs(std::vector<Msg>& msgs, const Batch& b, int e0, int cnt, int peer,
+                  bool send) {
+    if (cnt <= 0) return;
+    msgs.push_back({peer, b.leaf.as<double>() + e0 * b.sl, sizeof(double) * b.sl * cnt, send});
+    msgs.push_back({peer, b.U.as<double>() + e0 * b.sf, sizeof(double) * b.sf * cnt, send});
+    msgs.push_back({peer, b.V.as<double>() + e0 * b.sf, sizeof(double) * b.sf * cnt, send});
+    msgs.push_back({peer, b.rk.as<int>() + e0 * b.sr, sizeof(int) * b.sr * cnt, send});
   }
 
   cudaEvent_t next_event() {
@@ -896,14 +951,20 @@ struct Plan {
   }
 
   // ---- one reduction level (reference reduction.py:173-232) ----
+  // Local window [first, first+m) of a global level of mg blocks; the last
+  // local odd block takes {Dinv, E, F} of the right neighbour's first block.
   bool reduce(Level& L, int Rout, int lvl, int order, Level& nx, Record& rec,
-              int& need) {
-    const int mm = L.m, ne = (mm + 1) / 2, no = mm / 2;
-    int nq = 0, nf = 0;
+              int& need, bool dlev) {
+    const int mm = L.m, first = L.first, mg = L.mg, ne = (mm + 1) / 2, no = mm / 2;
+    const bool right = first + mm < mg;
+    int nq = 0, nq_loc = 0, nq_h = 0, nf = 0, nf_loc = 0, nf_h = 0;
     for (int j = 1; j < mm; j += 2) {
-      if (j + 1 <= mm - 1) ++nq;
-      if (j + 2 <= mm - 1) ++nf;
+      const int jg = first + j;
+      if (jg + 1 <= mg - 1) { ++nq; if (j + 1 < mm) ++nq_loc; else ++nq_h; }
+      if (jg + 2 <= mg - 1) { ++nf; if (j + 1 < mm) ++nf_loc; else ++nf_h; }
     }
+    const int i0 = first >= 2 ? 0 : 1;        // first new block with an E' (jg >= 2)
+    const int nep = std::max(no - i0, 0);
     CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
     int* sg = sing.as<int>();
     {
@@ -913,6 +974,9 @@ struct Plan {
     }
     // 1. Dinv of the even blocks
     rec.m = mm;
+    rec.first = first;
+    rec.mg = mg;
+    rec.right = right;
     rec.Dinv.alloc(ht, ne, Rout, st);
     {
       Dev tDe = make_tab({{&L.D, 0, 2, ne}});
@@ -921,18 +985,39 @@ struct Plan {
       ++launches;
       invert(tDi.as<HB>(), ne, rec.Dinv.R, sg);
     }
+    // 1b. halo: our first even block to the left, the right neighbour's to us
+    Batch hDi, hE, hF;
+    if (dlev) {
+      std::vector<Msg> msgs;
+      if (first > 0) {
+        block_msgs(msgs, rec.Dinv, 0, me() - 1, true);
+        block_msgs(msgs, L.E, 0, me() - 1, true);
+        block_msgs(msgs, L.F, 0, me() - 1, true);
+      }
+      if (right) {
+        hDi.alloc(ht, 1, Rout, st);
+        hE.alloc(ht, 1, L.R, st);
+        hF.alloc(ht, 1, L.R, st);
+        block_msgs(msgs, hDi, 0, me() + 1, false);
+        block_msgs(msgs, hE, 0, me() + 1, false);
+        block_msgs(msgs, hF, 0, me() + 1, false);
+      }
+      tp->exchange(msgs, st);
+    }
     // 2. P_j = E_j Dinv_{j-1}, Q_j = F_j Dinv_{j+1}
     Batch PQ;
     PQ.alloc(ht, no + nq, Rout, st);
     {
       Dev tA = make_tab({{&L.E, 1, 2, no}, {&L.F, 1, 2, nq}});
-      Dev tB = make_tab({{&rec.Dinv, 0, 1, no}, {&rec.Dinv, 1, 1, nq}});
+      Dev tB = make_tab({{&rec.Dinv, 0, 1, no}, {&rec.Dinv, 1, 1, nq_loc}, {&hDi, 0, 1, nq_h}});
       Dev tC = make_tab({{&PQ, 0, 1, no + nq}});
       multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), no + nq, L.R, rec.Dinv.R, PQ.R,
                lvl == 0 ? 1 : 0);
     }
     // 3. X = P F_{j-1}, Y = Q E_{j+1}, E' = -P E_{j-1}, F' = -Q F_{j+1}
     nx.m = no;
+    nx.first = first / 2;
+    nx.mg = mg / 2;
     nx.R = Rout;
     nx.D.alloc(ht, no, Rout, st);
     nx.E.alloc(ht, no, Rout, st);
@@ -940,19 +1025,20 @@ struct Plan {
     Batch XY;
     XY.alloc(ht, no + nq, Rout, st);
     {
-      Dev tA = make_tab({{&PQ, 0, 1, no}, {&PQ, no, 1, nq}, {&PQ, 1, 1, no - 1},
+      Dev tA = make_tab({{&PQ, 0, 1, no}, {&PQ, no, 1, nq}, {&PQ, i0, 1, nep},
                          {&PQ, no, 1, nf}});
-      Dev tB = make_tab({{&L.F, 0, 2, no}, {&L.E, 2, 2, nq}, {&L.E, 2, 2, no - 1},
-                         {&L.F, 2, 2, nf}});
-      Dev tC = make_tab({{&XY, 0, 1, no + nq}, {&nx.E, 1, 1, no - 1}, {&nx.F, 0, 1, nf}});
-      int G = no + nq + std::max(no - 1, 0) + nf;
+      Dev tB = make_tab({{&L.F, 0, 2, no}, {&L.E, 2, 2, nq_loc}, {&hE, 0, 1, nq_h},
+                         {&L.E, 2 * i0, 2, nep}, {&L.F, 2, 2, nf_loc}, {&hF, 0, 1, nf_h}});
+      Dev tC = make_tab({{&XY, 0, 1, no + nq}, {&nx.E, i0, 1, nep}, {&nx.F, 0, 1, nf}});
+      int G = no + nq + nep + nf;
       multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), G, PQ.R, L.R, Rout,
                lvl == 0 ? 2 : 0);
-      Dev tE = make_tab({{&nx.E, 1, 1, no - 1}, {&nx.F, 0, 1, nf}});
-      CK(launch_negate(dt.T, tE.as<HB>(), std::max(no - 1, 0) + nf, st));
+      Dev tE = make_tab({{&nx.E, i0, 1, nep}, {&nx.F, 0, 1, nf}});
+      CK(launch_negate(dt.T, tE.as<HB>(), nep + nf, st));
       ++launches;
-      Dev tZ = make_tab({{&nx.E, 0, 1, no > 0 ? 1 : 0}, {&nx.F, nf, 1, no - nf}});
-      CK(launch_zerohb(dt.T, tZ.as<HB>(), (no > 0 ? 1 : 0) + std::max(no - nf, 0), st));
+      const int nz_e = std::min(i0, no);
+      Dev tZ = make_tab({{&nx.E, 0, 1, nz_e}, {&nx.F, nf, 1, no - nf}});
+      CK(launch_zerohb(dt.T, tZ.as<HB>(), nz_e + std::max(no - nf, 0), st));
       ++launches;
     }
     // 4. D' = add(add(D_j, -X), -Y)
@@ -977,6 +1063,12 @@ struct Plan {
       int e = order ? ne - 1 - k : k;
       if (hs[e] != INT_MAX) { bad = e; break; }
     }
+    if (dlev) {
+      // every rank learns of a singular pivot anywhere; capacities agree
+      const long long any = tp->allreduce_max(bad >= 0 ? 1 : 0, st);
+      if (any && bad < 0) throw SingularError("singular dense leaf on another rank");
+      h_ovf = (int)tp->allreduce_max(h_ovf, st);
+    }
     if (bad >= 0) {
       int pos = hs[bad];
       std::vector<int> lv;
@@ -987,14 +1079,15 @@ struct Plan {
       char buf[256];
       snprintf(buf, sizeof(buf),
                "singular dense leaf on index range [%d,%d): level %d, pivot block %d",
-               ht.lo[v], ht.hi[v], lvl, 2 * bad);
+               ht.lo[v], ht.hi[v], lvl, first + 2 * bad);
       throw SingularError(buf);
     }
     if (dbg()) {
       static auto t_prev = std::chrono::steady_clock::now();
       auto now = std::chrono::steady_clock::now();
-      fprintf(stderr, "[acr] level %d m=%d Rout=%d overflow=%d host_ms=%.2f\n", lvl, mm, Rout,
-              h_ovf, std::chrono::duration<double, std::milli>(now - t_prev).count());
+      fprintf(stderr, "[acr r%d] level %d m=%d/%d Rout=%d overflow=%d host_ms=%.2f\n", me(), lvl,
+              mm, mg, Rout, h_ovf,
+              std::chrono::duration<double, std::milli>(now - t_prev).count());
       t_prev = now;
     }
     if (h_ovf) {
@@ -1009,6 +1102,50 @@ struct Plan {
     return true;
   }
 
+  // gather every rank's window of level l onto rank 0 (rank 0 continues alone)
+  void consolidate(Level& L, int l) {
+    std::vector<int> b = bounds(l);
+    const int P = nranks();
+    std::vector<Msg> msgs;
+    Level F;
+    if (me() == 0) {
+      F.m = L.mg;
+      F.first = 0;
+      F.mg = L.mg;
+      F.R = L.R;
+      F.D.alloc(ht, F.m, F.R, st);
+      F.E.alloc(ht, F.m, F.R, st);
+      F.F.alloc(ht, F.m, F.R, st);
+      auto cp = [&](Batch& dst, const Batch& src, int cnt) {
+        CK(cudaMemcpyAsync(dst.leaf.p, src.leaf.p, sizeof(double) * src.sl * cnt,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.U.p, src.U.p, sizeof(double) * src.sf * cnt,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.V.p, src.V.p, sizeof(double) * src.sf * cnt,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.rk.p, src.rk.p, sizeof(int) * src.sr * cnt,
+                           cudaMemcpyDeviceToDevice, st));
+      };
+      cp(F.D, L.D, L.m);
+      cp(F.E, L.E, L.m);
+      cp(F.F, L.F, L.m);
+      for (int r = 1; r < P; ++r) {
+        const int c = b[r + 1] - b[r];
+        range_msgs(msgs, F.D, b[r], c, r, false);
+        range_msgs(msgs, F.E, b[r], c, r, false);
+        range_msgs(msgs, F.F, b[r], c, r, false);
+      }
+    } else {
+      range_msgs(msgs, L.D, 0, L.m, 0, true);
+      range_msgs(msgs, L.E, 0, L.m, 0, true);
+      range_msgs(msgs, L.F, 0, L.m, 0, true);
+    }
+    tp->exchange(msgs, st);
+    CK(cudaStreamSynchronize(st));
+    if (me() == 0) L = std::move(F);
+    else L = Level();
+  }
+
   // ---- factor ----
   void factor(const double* sub, const double* diag, const double* sup,
               const double* E, const double* F, int order) {
@@ -1018,6 +1155,7 @@ struct Plan {
     launches = 0;
     prof_reset();
     factored = false;
+    Ld = 0;
     if (!ovf.p) ovf.alloc(sizeof(int), st);
     sing.alloc(sizeof(int) * std::max(m, 1), st);
     if (!ev0) {
@@ -1025,21 +1163,32 @@ struct Plan {
       CK(cudaEventCreate(&ev1));
     }
     CK(cudaEventRecord(ev0, st));
+    const int P = nranks();
+    std::vector<int> b0 = bounds(0);
+    first0 = P > 1 ? b0[me()] : 0;
+    mloc0 = P > 1 ? b0[me() + 1] - b0[me()] : m;
     Level L;
-    L.m = m;
+    L.m = mloc0;
+    L.first = first0;
+    L.mg = m;
     L.R = 1;
-    L.D.alloc(ht, m, 1, st);
-    L.E.alloc(ht, m, 1, st);
-    L.F.alloc(ht, m, 1, st);
+    L.D.alloc(ht, L.m, 1, st);
+    L.E.alloc(ht, L.m, 1, st);
+    L.F.alloc(ht, L.m, 1, st);
     {
-      Dev tD = make_tab({{&L.D, 0, 1, m}});
-      CK(launch_lift(dt.T, sub, diag, sup, tD.as<HB>(), m, st));
-      Dev tE = make_tab({{&L.E, 1, 1, m - 1}});
-      CK(launch_liftdiag(dt.T, E, tE.as<HB>(), m - 1, st));
-      Dev tF = make_tab({{&L.F, 0, 1, m - 1}});
-      CK(launch_liftdiag(dt.T, F, tF.as<HB>(), m - 1, st));
-      Dev tZ = make_tab({{&L.E, 0, 1, 1}, {&L.F, m - 1, 1, 1}});
-      CK(launch_zerohb(dt.T, tZ.as<HB>(), 2, st));
+      // bands of the global blocks [first0, first0 + mloc0)
+      const int e0 = first0 == 0 ? 1 : 0;                       // E exists for g >= 1
+      const int ne_ = L.m - e0;
+      const int nf_ = std::min(L.m, m - 1 - first0);            // F exists for g <= m-2
+      Dev tD = make_tab({{&L.D, 0, 1, L.m}});
+      CK(launch_lift(dt.T, sub + (long long)first0 * (n - 1), diag + (long long)first0 * n,
+                     sup + (long long)first0 * (n - 1), tD.as<HB>(), L.m, st));
+      Dev tE = make_tab({{&L.E, e0, 1, ne_}});
+      CK(launch_liftdiag(dt.T, E + (long long)(first0 + e0 - 1) * n, tE.as<HB>(), ne_, st));
+      Dev tF = make_tab({{&L.F, 0, 1, nf_}});
+      CK(launch_liftdiag(dt.T, F + (long long)first0 * n, tF.as<HB>(), nf_, st));
+      Dev tZ = make_tab({{&L.E, 0, 1, e0}, {&L.F, nf_, 1, L.m - nf_}});
+      CK(launch_zerohb(dt.T, tZ.as<HB>(), e0 + L.m - nf_, st));
       launches += 4;
     }
     std::vector<int> dR, eR, fR;
@@ -1050,15 +1199,29 @@ struct Plan {
     profile_level(L.m, dR, eR, fR);
     int maxr = std::max(max_rank_of(dR), 1);
     int lvl = 0;
-    while (L.m > cutoff) {
+    bool distributed = P > 1;
+    while (L.mg > cutoff || distributed) {
+      if (distributed && (L.mg <= cutoff || !dist_ok(lvl))) {
+        consolidate(L, lvl);
+        distributed = false;
+        Ld = lvl;
+        if (me() != 0) break;
+        fetch_ranks(L.D, dR);
+        fetch_ranks(L.E, eR);
+        fetch_ranks(L.F, fR);
+        CK(cudaStreamSynchronize(st));
+        maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
+        continue;
+      }
       int Rout = std::max(4, (3 * maxr + 1) / 2 + 4);
       if (cap > 0) Rout = std::min(Rout, std::max(cap, 1) + 0);
       Rout = std::max(Rout, L.R);
+      if (distributed) Rout = (int)tp->allreduce_max(Rout, st);
       Record rec;
       Level nx;
       int need = 0;
       int tries = 0;
-      while (!reduce(L, Rout, lvl, order, nx, rec, need)) {
+      while (!reduce(L, Rout, lvl, order, nx, rec, need, distributed)) {
         Rout = std::max(need, 2 * Rout);
         rec = Record();
         nx = Level();
@@ -1077,6 +1240,19 @@ struct Plan {
       recs.push_back(std::move(rec));
       L = std::move(nx);
       ++lvl;
+    }
+    if (P > 1 && me() != 0) {
+      // this rank's part ends at the consolidation level
+      CK(cudaEventRecord(ev1, st));
+      CK(cudaStreamSynchronize(st));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      fms = ms;
+      prof_collect();
+      lastR = {{}, {}, {}};
+      last = Level();
+      factored = true;
+      return;
     }
     lastR = {dR, eR, fR};
     // cutoff: dense LU of the remaining system
@@ -1142,37 +1318,85 @@ struct Plan {
     CK(cudaEventRecord(ev0, st));
     const long long kn = (long long)k * n;
     const int L = (int)recs.size();
+    const int P = nranks();
+    const bool root = me() == 0;
     std::vector<Dev> f(L + 1);
-    f[0].alloc(sizeof(double) * kn * m, st);
-    CK(launch_rhs_in(rhs, m * n, k, n, f[0].as<double>(), st));
+    f[0].alloc(sizeof(double) * kn * std::max(mloc0, 1), st);
+    CK(launch_rhs_in(rhs + (long long)first0 * n * k, mloc0 * n, k, n, f[0].as<double>(), st));
     ++launches;
     for (int l = 0; l < L; ++l) {
+      if (P > 1 && l == Ld) {
+        // gather the consolidation level's right-hand side on rank 0
+        std::vector<int> b = bounds(l);
+        std::vector<Msg> msgs;
+        if (root) {
+          Dev full(sizeof(double) * kn * b[P], st);
+          CK(cudaMemcpyAsync(full.p, f[l].p, sizeof(double) * kn * (b[1] - b[0]),
+                             cudaMemcpyDeviceToDevice, st));
+          for (int r = 1; r < P; ++r)
+            msgs.push_back({r, full.as<double>() + kn * b[r],
+                            sizeof(double) * kn * (b[r + 1] - b[r]), false});
+          tp->exchange(msgs, st);
+          f[l] = std::move(full);
+        } else {
+          msgs.push_back({0, f[l].p, sizeof(double) * kn * (b[me() + 1] - b[me()]), true});
+          tp->exchange(msgs, st);
+        }
+      }
       Record& r = recs[l];
       const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
-      int nq = 0;
-      for (int j = 1; j + 1 <= mm - 1; j += 2) ++nq;
+      int nq = 0, nq_loc = 0;
+      for (int j = 1; j < mm; j += 2)
+        if (r.first + j + 1 <= r.mg - 1) { ++nq; if (j + 1 < mm) ++nq_loc; }
+      const int nq_h = nq - nq_loc;
       double* fl = f[l].as<double>();
-      Dev z(sizeof(double) * kn * std::max(ne, 1), st);
+      Dev z(sizeof(double) * kn * (std::max(ne, 1) + 1), st);   // + halo slot
       Dev a(sizeof(double) * kn * std::max(no, 1), st);
-      Dev b(sizeof(double) * kn * std::max(nq, 1), st);
+      Dev bb(sizeof(double) * kn * std::max(nq, 1), st);
       Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
       hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl, 2 * kn, k), s_pan(z.as<double>(), kn, k), k);
+      if (P > 1 && l < Ld) {
+        std::vector<Msg> msgs;
+        if (r.first > 0) msgs.push_back({me() - 1, z.p, sizeof(double) * kn, true});
+        if (r.right) msgs.push_back({me() + 1, z.as<double>() + kn * ne, sizeof(double) * kn, false});
+        tp->exchange(msgs, st);
+      }
       Dev tE = make_tab({{&r.E, 1, 2, no}});
       hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
+      // F_j z_{j+1}: z index i+1 (the halo slot ne for the right neighbour's block)
       Dev tF = make_tab({{&r.F, 1, 2, nq}});
-      hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k), s_pan(b.as<double>(), kn, k), k);
+      hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k), s_pan(bb.as<double>(), kn, k), k);
+      (void)nq_h;
       f[l + 1].alloc(sizeof(double) * kn * std::max(no, 1), st);
       double* fn = f[l + 1].as<double>();
-      CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, b.as<double>(), kn, fn, kn, nq, (int)kn, st));
+      CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, bb.as<double>(), kn, fn, kn, nq, (int)kn, st));
       CK(launch_rhs_combine(fl + kn + 2 * kn * nq, 2 * kn, a.as<double>() + kn * nq, kn, nullptr, 0,
                             fn + kn * nq, kn, no - nq, (int)kn, st));
       launches += 2;
     }
-    // cutoff solve
-    const int mc = last.m;
+    if (P > 1 && L == Ld) {
+      // distributed levels only reach the cutoff: gather for the dense solve
+      std::vector<int> b = bounds(L);
+      std::vector<Msg> msgs;
+      if (root) {
+        Dev full(sizeof(double) * kn * b[P], st);
+        CK(cudaMemcpyAsync(full.p, f[L].p, sizeof(double) * kn * (b[1] - b[0]),
+                           cudaMemcpyDeviceToDevice, st));
+        for (int r = 1; r < P; ++r)
+          msgs.push_back({r, full.as<double>() + kn * b[r],
+                          sizeof(double) * kn * (b[r + 1] - b[r]), false});
+        tp->exchange(msgs, st);
+        f[L] = std::move(full);
+      } else {
+        msgs.push_back({0, f[L].p, sizeof(double) * kn * (b[me() + 1] - b[me()]), true});
+        tp->exchange(msgs, st);
+      }
+    }
     std::vector<Dev> uu(L + 1);
-    uu[L].alloc(sizeof(double) * kn * std::max(mc, 1), st);
-    {
+    if (root) {
+      // cutoff solve
+      const int mc = last.m;
+      uu[L].alloc(sizeof(double) * kn * std::max(mc, 1), st);
       Dev B(sizeof(double) * (size_t)Nc * k, st);
       for (int i = 0; i < mc; ++i)
         CK(cudaMemcpy2DAsync(B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
@@ -1186,7 +1410,30 @@ struct Plan {
                              sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
     }
     // back-substitution
-    for (int l = L - 1; l >= 0; --l) {
+    for (int l = L - 1; l >= -1; --l) {
+      if (P > 1 && l + 1 == Ld) {
+        // scatter the consolidation level's solution back to the owners
+        std::vector<int> b = bounds(Ld);
+        std::vector<Msg> msgs;
+        const int c = b[me() + 1] - b[me()];
+        if (root) {
+          for (int r = 1; r < P; ++r)
+            msgs.push_back({r, uu[Ld].as<double>() + kn * b[r],
+                            sizeof(double) * kn * (b[r + 1] - b[r]), true});
+          tp->exchange(msgs, st);
+          Dev mine(sizeof(double) * kn * std::max(c, 1), st);
+          CK(cudaMemcpyAsync(mine.p, uu[Ld].p, sizeof(double) * kn * c,
+                             cudaMemcpyDeviceToDevice, st));
+          CK(cudaStreamSynchronize(st));
+          uu[Ld] = std::move(mine);
+        } else {
+          uu[Ld].alloc(sizeof(double) * kn * std::max(c, 1), st);
+          msgs.push_back({0, uu[Ld].p, sizeof(double) * kn * c, false});
+          tp->exchange(msgs, st);
+        }
+      }
+      if (l < 0) break;
+      if (P > 1 && !root && l >= Ld) continue;
       Record& r = recs[l];
       const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
       uu[l].alloc(sizeof(double) * kn * mm, st);
@@ -1195,14 +1442,28 @@ struct Plan {
         CK(cudaMemcpy2DAsync(ul + kn, sizeof(double) * 2 * kn, uu[l + 1].as<double>(),
                              sizeof(double) * kn, sizeof(double) * kn, no,
                              cudaMemcpyDeviceToDevice, st));
+      Dev uleft(sizeof(double) * kn, st);
+      if (P > 1 && l < Ld) {
+        // the left neighbour's last odd block feeds our first even block
+        std::vector<Msg> msgs;
+        if (r.right) msgs.push_back({me() + 1, ul + kn * (mm - 1), sizeof(double) * kn, true});
+        if (r.first > 0) msgs.push_back({me() - 1, uleft.p, sizeof(double) * kn, false});
+        tp->exchange(msgs, st);
+      }
       int nb = 0;
-      for (int i = 0; i <= mm - 2; i += 2) ++nb;
+      for (int i = 0; i <= mm - 1; i += 2)
+        if (r.first + i <= r.mg - 2) ++nb;
       Dev a(sizeof(double) * kn * ne, st);
       Dev b(sizeof(double) * kn * ne, st);
       CK(cudaMemsetAsync(a.p, 0, sizeof(double) * kn * ne, st));
       CK(cudaMemsetAsync(b.p, 0, sizeof(double) * kn * ne, st));
       Dev tE = make_tab({{&r.E, 2, 2, ne - 1}});
       hmat_full(tE.as<HB>(), ne - 1, r.E.R, s_pan(ul + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
+      if (r.first > 0) {
+        Dev tE0 = make_tab({{&r.E, 0, 1, 1}});
+        hmat_full(tE0.as<HB>(), 1, r.E.R, s_pan(uleft.as<double>(), kn, k),
+                  s_pan(a.as<double>(), kn, k), k);
+      }
       Dev tF = make_tab({{&r.F, 0, 2, nb}});
       hmat_full(tF.as<HB>(), nb, r.F.R, s_pan(ul + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
       Dev rr(sizeof(double) * kn * ne, st);
@@ -1213,7 +1474,7 @@ struct Plan {
       hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(rr.as<double>(), kn, k), s_pan(ul, 2 * kn, k), k);
       uu[l + 1].release();
     }
-    CK(launch_u_out(uu[0].as<double>(), m * n, k, n, u, st));
+    CK(launch_u_out(uu[0].as<double>(), mloc0 * n, k, n, u + (long long)first0 * n * k, st));
     ++launches;
     CK(cudaEventRecord(ev1, st));
     CK(cudaStreamSynchronize(st));
@@ -1336,6 +1597,88 @@ void acr_plan_destroy(acr_plan_t* h) {
     }
   }
   delete h;
+}
+
+int acr_nccl_unique_id(void* out) {
+  std::string e;
+  if (acr::nccl_unique_id(out, &e)) return set_err(nullptr, ACR_ECUDA, e);
+  return ACR_OK;
+}
+
+static int check_bounds(int m, int nranks, const int* bnd) {
+  if (nranks < 1 || !bnd) return 0;
+  if (bnd[0] != 0 || bnd[nranks] != m) return 0;
+  for (int r = 0; r < nranks; ++r)
+    if (bnd[r + 1] - bnd[r] < 1 || (bnd[r] & 1)) return 0;
+  return 1;
+}
+
+int acr_plan_create_dist(int m, int n, int leaf_size, double eps, int max_rank_cap,
+                         int cutoff_blocks, int rank, int nranks, const int* bnd0,
+                         const void* nccl_id, acr_plan_t** out) {
+  if (!check_bounds(m, nranks, bnd0) || rank < 0 || rank >= nranks)
+    return set_err(nullptr, ACR_EARG, "bad rank partition");
+  int rc = acr_plan_create(m, n, leaf_size, eps, max_rank_cap, cutoff_blocks, out);
+  if (rc) return rc;
+  Plan& P = *(*out)->p;
+  P.bnd0.assign(bnd0, bnd0 + nranks + 1);
+  if (nranks > 1) {
+    std::string e;
+    P.tp = acr::make_nccl(nccl_id, rank, nranks, &e);
+    if (!P.tp) {
+      acr_plan_destroy(*out);
+      *out = nullptr;
+      return set_err(nullptr, ACR_ECUDA, e);
+    }
+    P.own_tp = true;
+  }
+  return ACR_OK;
+}
+
+int acr_loopback_solve(int nranks, const int* bnd0, int m, int n, int leaf_size,
+                       double eps, int max_rank_cap, int cutoff_blocks,
+                       const double* D_sub, const double* D_diag, const double* D_sup,
+                       const double* E, const double* F, const double* rhs, int nrhs,
+                       double* u, double* factor_ms) {
+  if (!check_bounds(m, nranks, bnd0)) return set_err(nullptr, ACR_EARG, "bad rank partition");
+  acr::LoopbackHub hub(nranks);
+  std::vector<int> rcs(nranks, 0);
+  std::vector<std::string> errs(nranks);
+  std::vector<double> fms(nranks, 0.0);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<std::thread> th;
+  for (int r = 0; r < nranks; ++r) {
+    th.emplace_back([&, r] {
+      cudaSetDevice(dev);
+      cudaStream_t st;
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      acr_plan_t* h = nullptr;
+      int rc = acr_plan_create(m, n, leaf_size, eps, max_rank_cap, cutoff_blocks, &h);
+      if (!rc) {
+        Plan& P = *h->p;
+        P.bnd0.assign(bnd0, bnd0 + nranks + 1);
+        P.tp = acr::make_loopback(&hub, r);
+        P.own_tp = true;
+        rc = acr_factor(h, D_sub, D_diag, D_sup, E, F, 0, st);
+        if (!rc) rc = acr_solve(h, rhs, nrhs, u, st);
+        fms[r] = P.fms;
+        if (rc) errs[r] = P.err;
+      }
+      rcs[r] = rc;
+      acr_plan_destroy(h);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    });
+  }
+  for (auto& t : th) t.join();
+  double mx = 0;
+  for (int r = 0; r < nranks; ++r) {
+    mx = std::max(mx, fms[r]);
+    if (rcs[r]) return set_err(nullptr, rcs[r], "rank " + std::to_string(r) + ": " + errs[r]);
+  }
+  if (factor_ms) *factor_ms = mx;
+  return ACR_OK;
 }
 
 int acr_plan_set_option(acr_plan_t* h, int option, long long value) {

@@ -109,3 +109,19 @@ def test_product_path_has_no_oracle_import():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert "oracle" not in re.sub(r'""".*?"""|#.*', "", src, flags=re.S), f
+
+
+def test_block_partition_rules():
+    from paper_1604_00617_b200.dist import (block_partition, distributed_levels,
+                                            distributed_ok, level_bounds)
+    assert block_partition(2048, 8) == [256 * r for r in range(8)] + [2048]
+    for m, Pn in [(2048, 2), (2048, 4), (2048, 8), (13, 3), (256, 8), (100, 7)]:
+        b = block_partition(m, Pn)
+        assert b[0] == 0 and b[-1] == m
+        assert all(x % 2 == 0 for x in b[:-1])
+        assert all(b[r + 1] > b[r] for r in range(Pn))
+    # cfg5 on 8 GPUs: 8 sharded levels (2048 -> 8 blocks), then rank 0
+    assert distributed_levels(2048, 8) == 8
+    assert distributed_levels(2048, 2) == 10
+    assert level_bounds(block_partition(2048, 8), 2048, 3) == [32 * r for r in range(8)] + [256]
+    assert not distributed_ok(block_partition(2048, 8), 2048, 8)
