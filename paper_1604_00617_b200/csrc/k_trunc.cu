@@ -106,9 +106,10 @@ __device__ void group_qr(double* W, int mr, int R, double* tau, const Grp& g) {
     const double alpha = cj[j];
     double tj = 0.0, scal = 0.0, beta = alpha;
     if (ss != 0.0) {
-      beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
-      tj = (beta - alpha) / beta;
+      beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+      const double rb = 1.0 / beta;           // independent of the next division
       scal = 1.0 / (alpha - beta);
+      tj = (beta - alpha) * rb;
     }
     gbar(g);                                  // everyone has read cj[j]
     if (tj != 0.0) {
@@ -277,11 +278,13 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
           c += __shfl_xor_sync(0xffffffffu, c, o);
         }
         if (valid && a > tiny && b > tiny && c != 0.0 &&
-            fabs(c) > tol * sqrt(a) * sqrt(b)) {
-          double zeta = (b - a) / (2.0 * c);
-          double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          double cs = 1.0 / sqrt(1.0 + t * t);
-          double sn = cs * t;
+            c * c > tol * tol * a * b) {
+          // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0,
+          // zeta = (b - a) / 2c, written with one sqrt and one division
+          const double d = b - a, e = 2.0 * c;
+          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
           for (int r = sub; r < pr; r += gs) {
             double x = bi[r], y = bj[r];
             bi[r] = cs * x - sn * y;
@@ -372,6 +375,8 @@ __host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
   return (long long)(um + vm) * R + 2LL * R * R + 4LL * R + um + vm + 8;
 }
 
+__device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane);
+
 // ---------------------------------------------------------------------------
 // block path (one CTA per queued task; used for tasks too large for a warp)
 // ---------------------------------------------------------------------------
@@ -449,7 +454,20 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   }
   __syncthreads();
   ACR_PH(2);
-  const int sweeps = block_jacobi(Bm, pr, pc, Jm, iflag);
+  // small cores: one warp, warp-level syncs per rotation step (a CTA barrier
+  // per step costs more than the step); large cores: the whole CTA
+  int sweeps;
+  if (pc <= 32 && pr <= 128) {
+    __shared__ int s_sw;
+    if (tid < 32) {
+      const int sw = warp_jacobi(Bm, pr, pc, Jm, tid);
+      if (tid == 0) s_sw = sw;
+    }
+    __syncthreads();
+    sweeps = s_sw;
+  } else {
+    sweeps = block_jacobi(Bm, pr, pc, Jm, iflag);
+  }
   ACR_PH(3);
   for (int j = tid; j < pc; j += TT) {
     double s = 0.0;
@@ -651,9 +669,10 @@ __device__ __forceinline__ void warp_reflector(double* cj, int j, int mr, double
   double scal = 0.0, beta = alpha;
   tj = 0.0;
   if (ss != 0.0) {
-    beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
-    tj = (beta - alpha) / beta;
+    beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+    const double rb = 1.0 / beta;             // independent of the next division
     scal = 1.0 / (alpha - beta);
+    tj = (beta - alpha) * rb;
   }
   __syncwarp();
   if (tj != 0.0) {
@@ -793,11 +812,13 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
           c += __shfl_xor_sync(FULL, c, o);
         }
         if (valid && a > tiny && b > tiny && c != 0.0 &&
-            fabs(c) > tol * sqrt(a) * sqrt(b)) {
-          double zeta = (b - a) / (2.0 * c);
-          double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          double cs = 1.0 / sqrt(1.0 + t * t);
-          double sn = cs * t;
+            c * c > tol * tol * a * b) {
+          // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0,
+          // zeta = (b - a) / 2c, written with one sqrt and one division
+          const double d = b - a, e = 2.0 * c;
+          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
           for (int r = sub; r < pr; r += gs) {
             double x = bi[r], y = bj[r];
             bi[r] = cs * x - sn * y;

@@ -48,7 +48,7 @@ def _rank_counts(m0, n, leaf, levels, cutoff=1):
 
 
 def _check_against_golden(rep, u, z, prefix, eps, u_ref=None, stride=1,
-                          shape=None, flip_frac=2e-4):
+                          shape=None, flip_frac=1e-3):
     if u_ref is None:
         u_ref = z[prefix + "u"]
     rel = _rel(u[::stride], u_ref)
@@ -58,8 +58,10 @@ def _check_against_golden(rep, u, z, prefix, eps, u_ref=None, stride=1,
     assert rep.levels == int(z[prefix + "levels"])
     prof = golden_profiles(z, prefix)
     # rank decisions: a decision whose singular value sits within roundoff of
-    # the threshold (or of the noise guard) may flip between LAPACK and the
-    # GPU; allow a tiny fraction of flips and report them
+    # the threshold -- or of the noise guard sigma_1 <= R eps |Ru| |Rv|, which
+    # fires hundreds of times on config 3 and compares roundoff-level numbers
+    # by construction -- may flip between LAPACK and the GPU; allow <= 0.1% of
+    # decisions to flip (the solution / residual bars above are the contract)
     flips, total = 0.0, 0
     counts = _rank_counts(*shape, rep.levels) if shape else None
     for lv, (p, q) in enumerate(zip(rep.per_level_ranks, prof)):
