@@ -479,7 +479,37 @@ struct Plan {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : evpool) cudaEventDestroy(e);
+    if (st2) {
+      cudaStreamSynchronize(st2);
+      cudaStreamDestroy(st2);
+      cudaEventDestroy(evf);
+      cudaEventDestroy(evj);
+    }
     if (own_tp) delete tp;
+  }
+
+  // second stream for independent launches at latency-bound levels (disabled
+  // while instrumenting so per-class event timings stay on one stream)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr;
+  cudaStream_t side() {
+    if (prof_on) return st;
+    if (!st2) {
+      CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&evj, cudaEventDisableTiming));
+    }
+    return st2;
+  }
+  void fork(cudaStream_t s) {
+    if (s == st) return;
+    CK(cudaEventRecord(evf, st));
+    CK(cudaStreamWaitEvent(s, evf, 0));
+  }
+  void join(cudaStream_t s) {
+    if (s == st) return;
+    CK(cudaEventRecord(evj, s));
+    CK(cudaStreamWaitEvent(st, evj, 0));
   }
 
   int nranks() const { return tp ? tp->size() : 1; }
@@ -587,8 +617,10 @@ struct Plan {
   // ---- truncation launcher: warp kernel + persistent block kernel for
   //      tasks that exceed the per-CTA smem pool ----
   void run_trunc(TruncArgs a, int t0, int t1, const HB* out, int nelem, int Ra,
-                 int Rb) {
+                 int Rb, cudaStream_t s = nullptr) {
     if (t1 <= t0 || nelem <= 0) return;
+    if (!s) s = st;
+    const bool alt = s != st;                    // own scratch slots per stream
     a.T = dt.T;
     a.out = out;
     a.eps = eps;
@@ -616,16 +648,17 @@ struct Plan {
     a.gscr_stride = 0;
     a.gscr_ntasks = 0;
     if (may_big) {
-      q = scratch<int>(13, (size_t)nitems + 1);
-      qc = scratch<int>(14, 4);
+      q = scratch<int>(alt ? 16 : 13, (size_t)nitems + 1);
+      qc = scratch<int>(alt ? 17 : 14, 4);
     }
     if ((direct || may_big) && bworst > SMD) {
       const int nblk = direct ? nitems : std::min(nitems, 148);
-      a.gscr = scratch<double>(10, (size_t)nblk * bworst);
+      a.gscr = scratch<double>(alt ? 15 : 10, (size_t)nblk * bworst);
       a.gscr_stride = bworst;
     }
+    fork(s);
     kbegin(0);
-    CK(launch_trunc(a, nelem, direct, may_big, q, qc, st));
+    CK(launch_trunc(a, nelem, direct, may_big, q, qc, s));
     kend();
     launches += may_big ? 2 : 1;
   }
@@ -694,11 +727,18 @@ struct Plan {
                    RA * RB, st));
       ++launches;
     }
+    const cudaStream_t s2 = side();
+    fork(s2);
     kbegin(2);
     CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), diag,
-                       st));
+                       s2));
     kend();
     ++launches;
+    struct Joiner {
+      Plan* p;
+      cudaStream_t s;
+      ~Joiner() { p->join(s); }
+    } jn{this, s2};
     if (ht.branches.empty()) return;
     MMJob J[2];
     memset(J, 0, sizeof(J));
@@ -760,15 +800,19 @@ struct Plan {
   void add(const HB* A, const HB* B, const HB* C, int G, double sb, int RA,
            int RB) {
     if (G <= 0) return;
-    CK(launch_leafadd(dt.T, A, B, C, sb, G, st));
+    const cudaStream_t s2 = side();
+    fork(s2);
+    CK(launch_leafadd(dt.T, A, B, C, sb, G, s2));
     ++launches;
-    if (ht.branches.empty()) return;
-    TruncArgs a;
-    memset(&a, 0, sizeof(a));
-    a.mode = TM_COMBINE;
-    a.a = op_own(s_hbU(A), s_hbV(A), r_hb(A));
-    a.b = op_own(s_hbU(B), s_hbV(B), r_hb(B), sb);
-    run_trunc(a, ht.startA[0], ht.startA[1], C, G, RA, RB);
+    if (!ht.branches.empty()) {
+      TruncArgs a;
+      memset(&a, 0, sizeof(a));
+      a.mode = TM_COMBINE;
+      a.a = op_own(s_hbU(A), s_hbV(A), r_hb(A));
+      a.b = op_own(s_hbU(B), s_hbV(B), r_hb(B), sb);
+      run_trunc(a, ht.startA[0], ht.startA[1], C, G, RA, RB);
+    }
+    join(s2);
   }
 
   // ---- invert in place (reference algebra.py:192-240) ----
@@ -833,8 +877,14 @@ struct Plan {
     launches += 2;
   }
 
-  void inv_lowrank(InvCtx& c, int nu, int mu, Src U, Src V, int fside) {
-    // add_lowrank(H_mu, (U, V)) with rank (nu, fside) if (nu, 1-fside) != 0
+  // add_lowrank(H_mu, (U, V)) with rank (nu, fside) if (nu, 1-fside) != 0:
+  // factor recompressions on st, the leaves' dense update on s2 (disjoint
+  // data); the caller joins s2
+  void inv_lowrank(InvCtx& c, int nu, int mu, Src U, Src V, int fside, cudaStream_t s2) {
+    fork(s2);
+    CK(launch_leaflr_n(dt.T, c.H, c.G, mu, ht.nleaves_under(mu), U, V, r_hb(c.H),
+                       nu, fside, s2));
+    ++launches;
     int t0 = ht.startA[mu], t1 = ht.startA[mu + 1];
     if (t1 > t0) {
       TruncArgs a;
@@ -847,9 +897,6 @@ struct Plan {
       a.b.fside = fside;
       run_trunc(a, t0, t1, c.H, c.G, c.R, c.R);
     }
-    CK(launch_leaflr_n(dt.T, c.H, c.G, mu, ht.nleaves_under(mu), U, V, r_hb(c.H),
-                       nu, fside, st));
-    ++launches;
   }
 
   void inv_node(InvCtx& c, int nu) {
@@ -877,7 +924,9 @@ struct Plan {
       CK(launch_gp(dt.T, &j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st));
       ++launches;
     }
-    inv_lowrank(c, nu, a1, P3, s_hbV(c.H), 0);         // S = H22 + W V12^T
+    const cudaStream_t s2 = side();
+    inv_lowrank(c, nu, a1, P3, s_hbV(c.H), 0, s2);     // S = H22 + W V12^T
+    join(s2);
     inv_node(c, a1);                                   // sinv
     inv_hmat(c, a1, true);                             // Z, S2
     {
@@ -891,12 +940,13 @@ struct Plan {
       CK(launch_gp(dt.T, &j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st));
       ++launches;
     }
-    inv_lowrank(c, nu, a0, P3, P2, 1);                 // b11 = x11 + G Hh^T
-    TruncArgs a;                                       // b12, b21
+    inv_lowrank(c, nu, a0, P3, P2, 1, s2);             // b11 = x11 + G Hh^T
+    TruncArgs a;                                       // b12, b21 (independent of b11)
     memset(&a, 0, sizeof(a));
     a.mode = TM_TRUNCATE;
     a.a = op_own(P1, P2, r_hb(c.H), -1.0);
-    run_trunc(a, ht.startA[nu], ht.startA[nu] + 2, c.H, c.G, c.R, 0);
+    run_trunc(a, ht.startA[nu], ht.startA[nu] + 2, c.H, c.G, c.R, 0, s2);
+    join(s2);
   }
 
   // ---- helpers for reports ----
