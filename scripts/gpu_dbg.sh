@@ -1,1 +1,1 @@
-ACR_DEBUG=1 REPS=5 python scripts/time_configs.py cfg5 > gpurun_out/dbg.log 2>&1
+ACR_DEBUG=1 REPS=3 python scripts/time_configs.py cfg5 > gpurun_out/dbg.log 2>&1
