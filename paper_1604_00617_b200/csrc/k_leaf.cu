@@ -325,12 +325,31 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(GT) k_leafgemm_tc(TreeDev T, const HB* A, const HB* B,
-                                                   const HB* C, Src PX, RankRef xr,
-                                                   int diag) {
+// warp tile block: 2 x 4 tiles of 8x8 (16 x 32 outputs); 8 warps cover 64x64.
+// A fragment: A[r][k] (row-major sa), B fragment: B[k][c] (row-major sb).
+__device__ __forceinline__ void dmma_block(double (&acc)[2][4][2], const double* sa,
+                                           const double* sb, int r0, int c0, int K,
+                                           int gi, int ti) {
+  for (int k = 0; k < K; k += 4) {
+    double a0 = sa[(r0 + gi) * GLD + k + ti];
+    double a1 = sa[(r0 + 8 + gi) * GLD + k + ti];
+    double b[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b[q] = sb[(k + ti) * GLD + c0 + q * 8 + gi];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      dmma(acc[0][q][0], acc[0][q][1], a0, b[q]);
+      dmma(acc[1][q][0], acc[1][q][1], a1, b[q]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, const HB* B,
+                                                      const HB* C, Src PX, RankRef xr,
+                                                      int diag) {
   extern __shared__ double sm[];
-  double* sa = sm;                 // [64][GLD]  A rows       (also P for cross terms)
-  double* sb = sa + 64 * GLD;      // [64][GLD]  B columns    (also Q for cross terms)
+  double* sa = sm;                 // [64][GLD]  A rows       (P for cross terms)
+  double* sb = sa + 64 * GLD;      // [64][GLD]  B rows       (Q^T for cross terms)
   const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
   const int lo = T.lo[lam], s = T.hi[lam] - lo, bw = T.bw, n = T.n;
@@ -345,33 +364,24 @@ __global__ void __launch_bounds__(GT) k_leafgemm_tc(TreeDev T, const HB* A, cons
           ? La[(long long)i * bw + i] * Lb[(long long)i * bw + j]
           : La[(long long)i * bw + j] * Lb[(long long)j * bw + j];
     }
-    // level-0 couplings have rank-0 factors: no cross terms
-    return;
+    return;                        // level-0 couplings have rank-0 factors
   }
-  for (int idx = tid; idx < S * S; idx += GT) {
-    const int i = idx / S, j = idx - i * S;
+  for (int idx = tid; idx < 64 * 64; idx += GT) {
+    const int i = idx >> 6, j = idx & 63;
     const bool in = i < s && j < s;
-    sa[i * GLD + j] = in ? La[(long long)i * bw + j] : 0.0;          // A[i][j]
-    sb[j * GLD + i] = in ? Lb[(long long)i * bw + j] : 0.0;          // B[i][j] -> col j
+    sa[i * GLD + j] = in ? La[(long long)i * bw + j] : 0.0;
+    sb[i * GLD + j] = in ? Lb[(long long)i * bw + j] : 0.0;
   }
   __syncthreads();
-  // warp w owns tiles (tm, tn) with t = w, w+8, ... over (S/8)^2 tiles
-  const int nt = S / 8, ntt = nt * nt;
   const int gi = lane >> 2, ti = lane & 3;
-  double acc[8][2];
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;   // 4 x 2 warp grid
+  double acc[2][4][2];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int t = warp + q * 8;
-    if (t < ntt) {
-      const int tm = t / nt, tn = t - tm * nt;
-      const double* ar = sa + (tm * 8 + gi) * GLD + ti;
-      const double* bc = sb + (tn * 8 + gi) * GLD + ti;
-      for (int k = 0; k < S; k += 4) dmma(acc[q][0], acc[q][1], ar[k], bc[k]);
-    }
-  }
-  // ancestor cross terms, parent first
+    for (int q = 0; q < 4; ++q) acc[a][q][0] = acc[a][q][1] = 0.0;
+  dmma_block(acc, sa, sb, r0, c0, S, gi, ti);
+  // ancestor cross terms, parent first: acc += P Q^T, one ancestor at a time
   const HB bb = B[g];
   const int* cr = rank_base(xr, g);
   int child = lam;
@@ -381,50 +391,42 @@ __global__ void __launch_bounds__(GT) k_leafgemm_tc(TreeDev T, const HB* A, cons
     const int slot = T.depth[al];
     const double* P = src_col(PX, n, g, slot, 0) + lo;
     const double* Q = bb.V + (long long)slot * bb.R * n + lo;
-    double z[8][2];
+    double z[2][4][2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) z[q][0] = z[q][1] = 0.0;
-    // rank r may exceed the 64-column staging rows: k-chunks of 64
-    for (int k0 = 0; k0 < r; k0 += 64) {
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) z[a][q][0] = z[a][q][1] = 0.0;
+    for (int k0 = 0; k0 < r; k0 += 64) {       // ranks above 64 in chunks
       const int kr = r - k0 < 64 ? r - k0 : 64;
       const int rp = (kr + 3) & ~3;
       __syncthreads();
-      for (int idx = tid; idx < S * rp; idx += GT) {
-        const int i = idx / rp, c = idx - i * rp;
+      for (int idx = tid; idx < 64 * rp; idx += GT) {
+        const int c = idx / 64, i = idx - c * 64;             // coalesced in i
         const bool in = i < s && c < kr;
         sa[i * GLD + c] = in ? P[(long long)(k0 + c) * n + i] : 0.0;   // P[i][c]
-        sb[i * GLD + c] = in ? Q[(long long)(k0 + c) * n + i] : 0.0;   // Q[i][c]
+        sb[c * GLD + i] = in ? Q[(long long)(k0 + c) * n + i] : 0.0;   // Q^T[c][i]
       }
       __syncthreads();
+      dmma_block(z, sa, sb, r0, c0, rp, gi, ti);
+    }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int t = warp + q * 8;
-        if (t < ntt) {
-          const int tm = t / nt, tn = t - tm * nt;
-          const double* pr = sa + (tm * 8 + gi) * GLD + ti;
-          const double* qc = sb + (tn * 8 + gi) * GLD + ti;
-          for (int k = 0; k < rp; k += 4) dmma(z[q][0], z[q][1], pr[k], qc[k]);
-        }
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[a][q][0] = acc[a][q][0] + z[a][q][0];
+        acc[a][q][1] = acc[a][q][1] + z[a][q][1];
       }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      acc[q][0] = acc[q][0] + z[q][0];
-      acc[q][1] = acc[q][1] + z[q][1];
-    }
   }
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int t = warp + q * 8;
-    if (t < ntt) {
-      const int tm = t / nt, tn = t - tm * nt;
-      const int i = tm * 8 + gi, j = tn * 8 + ti * 2;
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = r0 + a * 8 + gi, j = c0 + q * 8 + ti * 2;
       if (i < s) {
-        if (j < s) Lc[(long long)i * bw + j] = acc[q][0];
-        if (j + 1 < s) Lc[(long long)i * bw + j + 1] = acc[q][1];
+        if (j < s) Lc[(long long)i * bw + j] = acc[a][q][0];
+        if (j + 1 < s) Lc[(long long)i * bw + j + 1] = acc[a][q][1];
       }
     }
-  }
 }
 
 cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
