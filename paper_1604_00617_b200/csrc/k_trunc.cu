@@ -457,7 +457,7 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   // small cores: one warp, warp-level syncs per rotation step (a CTA barrier
   // per step costs more than the step); large cores: the whole CTA
   int sweeps;
-  if (pc <= 32 && pr <= 128) {
+  if (pc <= 64 && pr <= 128) {
     __shared__ int s_sw;
     if (tid < 32) {
       const int sw = warp_jacobi(Bm, pr, pc, Jm, tid);
