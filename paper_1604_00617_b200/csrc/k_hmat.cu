@@ -76,6 +76,63 @@ __global__ void __launch_bounds__(HT) k_hmatA(TreeDev T, MMJobs2 JJ) {
   }
 }
 
+// Fallback phase B (trees deeper than 16; k_hmatB_sm below is the main path).
+// Register tile of phase B: one thread = one leaf row i x HB_CB columns of
+// one subtree root.  The leaf row and every ancestor U (V) row element are
+// loaded once per HB_CB columns; X is row-major [j][cp] in shared memory with
+// its columns zero-padded to a multiple of HB_CB (double2 broadcast loads).
+// Every output keeps the scalar summation order (leaf terms j = 0..s-1, then
+// y = y + z per ancestor, deepest first), so results are unchanged bitwise.
+static constexpr int HB_CB = 8;   // padding unit (largest tile)
+
+template <int CB>
+__device__ __forceinline__ void hmatB_tile(const TreeDev& T, const MMJob& J, const HB& h,
+                                           int g, int mu, int lam, int lo, int s, int ld,
+                                           const double* L, const double* Xr, int cp,
+                                           int i, int b0, int nb, int eA0, int slot) {
+  const int n = T.n;
+  double y[CB];
+#pragma unroll
+  for (int u = 0; u < CB; ++u) y[u] = 0.0;
+  for (int j = 0; j < s; ++j) {
+    const double l = J.trans ? L[j * ld + i] : L[i * ld + j];
+    const double2* x = reinterpret_cast<const double2*>(Xr + j * cp + b0);
+#pragma unroll
+    for (int u = 0; u < CB / 2; ++u) {
+      const double2 xv = x[u];
+      y[2 * u] += l * xv.x;
+      y[2 * u + 1] += l * xv.y;
+    }
+  }
+  for (int be = lam; be != mu;) {
+    be = T.parent[be];
+    const int bmid = T.mid[be];
+    const bool top = lo < bmid;
+    const int sd = J.trans ? (top ? 1 : 0) : (top ? 0 : 1);
+    const int r = h.rk[be * 2 + sd];
+    if (!r) continue;
+    const int e = T.startA[mu] + 2 * T.posA[mu * T.nnodes + be] + sd - eA0;
+    const double* t = J.tbuf + ((long long)g * J.nA + e) * J.RT * J.CT + b0;
+    const double* F = (J.trans ? h.V : h.U) + (long long)T.depth[be] * h.R * n + lo + i;
+    double z[CB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u) z[u] = 0.0;
+    for (int a = 0; a < r; ++a) {
+      const double f = F[(long long)a * n];
+      const double* ta = t + a * J.CT;
+#pragma unroll
+      for (int u = 0; u < CB; ++u)
+        if (u < nb) z[u] += f * __ldg(ta + u);
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u) y[u] = y[u] + z[u];
+  }
+#pragma unroll
+  for (int u = 0; u < CB; ++u)
+    if (u < nb) src_col(J.Y, n, g, slot, b0 + u)[lo + i] = J.alpha * y[u];
+}
+
+template <int CB>
 __global__ void __launch_bounds__(HT) k_hmatB(TreeDev T, MMJobs2 JJ, int nBmax) {
   extern __shared__ double sm[];
   const MMJob& J = JJ.j[blockIdx.z];
@@ -89,47 +146,32 @@ __global__ void __launch_bounds__(HT) k_hmatB(TreeDev T, MMJobs2 JJ, int nBmax) 
   const int lo = T.lo[lam], s = T.hi[lam] - lo;
   const int slot = mm_slot(T, mu);
   const int ld = s + 1;            // padded: conflict-free column reads
+  const int cp = (c + HB_CB - 1) / HB_CB * HB_CB;
   double* L = sm;                 // s x ld
-  double* X = L + s * ld;         // c x s (column-major panel)
+  double* X = L + ((s * ld + 1) & ~1);   // s x cp, row-major, 16-byte aligned
   const double* Lg = h.leaf + (long long)lo * bw;
   for (int idx = threadIdx.x; idx < s * s; idx += HT) {
     int i = idx / s, j = idx - i * s;
     L[i * ld + j] = Lg[(long long)i * bw + j];
   }
-  for (int idx = threadIdx.x; idx < s * c; idx += HT) {
+  for (int idx = threadIdx.x; idx < s * cp; idx += HT) {
     int b = idx / s, i = idx - b * s;
-    X[idx] = src_col(J.X, n, g, slot, b)[lo + i];
+    X[i * cp + b] = b < c ? src_col(J.X, n, g, slot, b)[lo + i] : 0.0;
   }
   __syncthreads();
   const int eA0 = T.startA[J.mu0];
-  for (int idx = threadIdx.x; idx < s * c; idx += HT) {
-    int b = idx / s, i = idx - b * s;
-    double y = 0.0;
-    if (!J.trans)
-      for (int j = 0; j < s; ++j) y += L[i * ld + j] * X[b * s + j];
-    else
-      for (int j = 0; j < s; ++j) y += L[j * ld + i] * X[b * s + j];
-    for (int be = lam; be != mu;) {
-      be = T.parent[be];
-      int bmid = T.mid[be];
-      bool top = lo < bmid;
-      int sd = J.trans ? (top ? 1 : 0) : (top ? 0 : 1);
-      int r = h.rk[be * 2 + sd];
-      if (!r) continue;
-      int e = T.startA[mu] + 2 * T.posA[mu * T.nnodes + be] + sd - eA0;
-      const double* t = J.tbuf + ((long long)g * J.nA + e) * J.RT * J.CT;
-      const double* F = (J.trans ? h.V : h.U) + (long long)T.depth[be] * h.R * n + lo + i;
-      double z = 0.0;
-      for (int a = 0; a < r; ++a) z += F[(long long)a * n] * t[a * J.CT + b];
-      y = y + z;
-    }
-    src_col(J.Y, n, g, slot, b)[lo + i] = J.alpha * y;
+  const int nch = (c + CB - 1) / CB;
+  for (int idx = threadIdx.x; idx < s * nch; idx += HT) {
+    const int q = idx / s, i = idx - q * s;
+    const int bb = q * CB, nb = c - bb < CB ? c - bb : CB;
+    hmatB_tile<CB>(T, J, h, g, mu, lam, lo, s, ld, L, X, cp, i, bb, nb, eA0, slot);
   }
 }
 
 // Phase B for jobs whose subtree roots are every non-root node (multiply M1):
 // one CTA per (leaf, element, job) serves all roots mu on the leaf's path, so
 // the leaf block is read once instead of once per ancestor.
+template <int CB>
 __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
   extern __shared__ double sm[];
   const MMJob& J = JJ.j[blockIdx.z];
@@ -140,22 +182,23 @@ __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
   const int* an = T.anc + lam * (T.maxdepth + 1);
   const int dl = T.depth[lam];
   const int ld = s + 1;            // padded: conflict-free column reads
-  double* L = sm;
-  double* X = L + s * ld;
-  // columns of each root on the path (t = 0: lam itself ... dl-1)
+  // columns of each root on the path, each padded to a multiple of HB_CB
   int cnt = 0;
   int off[16], cols[16], mus[16];
   for (int t = 0; t < dl && t < 16; ++t) {
     const int mu = an[t];
     if (mu < J.mu0 || mu >= J.mu1) continue;
     const int c = mm_cols(J, T, g, mu);
+    if (!c) continue;
     mus[cnt] = mu;
     cols[cnt] = c;
-    off[cnt] = cnt == 0 ? 0 : off[cnt - 1] + cols[cnt - 1];
+    off[cnt] = cnt == 0 ? 0 : off[cnt - 1] + (cols[cnt - 1] + HB_CB - 1) / HB_CB * HB_CB;
     ++cnt;
   }
-  const int ctot = cnt ? off[cnt - 1] + cols[cnt - 1] : 0;
-  if (!ctot) return;
+  if (!cnt) return;
+  const int cp = off[cnt - 1] + (cols[cnt - 1] + HB_CB - 1) / HB_CB * HB_CB;
+  double* L = sm;
+  double* X = L + ((s * ld + 1) & ~1);
   const double* Lg = h.leaf + (long long)lo * bw;
   for (int idx = threadIdx.x; idx < s * s; idx += HT) {
     int i = idx / s, j = idx - i * s;
@@ -163,39 +206,198 @@ __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
   }
   for (int q = 0; q < cnt; ++q) {
     const int slot = mm_slot(T, mus[q]);
-    for (int idx = threadIdx.x; idx < s * cols[q]; idx += HT) {
+    const int w = (cols[q] + HB_CB - 1) / HB_CB * HB_CB;
+    for (int idx = threadIdx.x; idx < s * w; idx += HT) {
       int b = idx / s, i = idx - b * s;
-      X[(off[q] + b) * s + i] = src_col(J.X, n, g, slot, b)[lo + i];
+      X[i * cp + off[q] + b] = b < cols[q] ? src_col(J.X, n, g, slot, b)[lo + i] : 0.0;
     }
   }
   __syncthreads();
   const int eA0 = T.startA[J.mu0];
-  for (int idx = threadIdx.x; idx < s * ctot; idx += HT) {
-    const int bb = idx / s, i = idx - bb * s;
+  const int nch = cp / CB;
+  for (int idx = threadIdx.x; idx < s * nch; idx += HT) {
+    const int ch = idx / s, i = idx - ch * s;
+    const int pos = ch * CB;
     int q = 0;
-    while (q + 1 < cnt && off[q + 1] <= bb) ++q;
-    const int mu = mus[q], b = bb - off[q];
-    double y = 0.0;
-    const double* xb = X + bb * s;
-    if (!J.trans)
-      for (int j = 0; j < s; ++j) y += L[i * ld + j] * xb[j];
-    else
-      for (int j = 0; j < s; ++j) y += L[j * ld + i] * xb[j];
-    for (int be = lam; be != mu;) {
-      be = T.parent[be];
-      const int bmid = T.mid[be];
-      const bool top = lo < bmid;
-      const int sd = J.trans ? (top ? 1 : 0) : (top ? 0 : 1);
-      const int r = h.rk[be * 2 + sd];
-      if (!r) continue;
-      const int e = T.startA[mu] + 2 * T.posA[mu * T.nnodes + be] + sd - eA0;
-      const double* t = J.tbuf + ((long long)g * J.nA + e) * J.RT * J.CT;
-      const double* F = (J.trans ? h.V : h.U) + (long long)T.depth[be] * h.R * n + lo + i;
-      double z = 0.0;
-      for (int a = 0; a < r; ++a) z += F[(long long)a * n] * t[a * J.CT + b];
-      y = y + z;
+    while (q + 1 < cnt && off[q + 1] <= pos) ++q;
+    const int bb = pos - off[q], nb = cols[q] - bb < CB ? cols[q] - bb : CB;
+    if (nb <= 0) continue;   // padding chunk of a root
+    hmatB_tile<CB>(T, J, h, g, mus[q], lam, lo, s, ld, L, X + off[q], cp, i, bb, nb, eA0,
+               mm_slot(T, mus[q]));
+  }
+}
+
+// Phase B, column-pair tiles.  A CTA serves one leaf lam and either the single
+// listB root (plain jobs) or every root on the leaf's path (M1).  Each thread
+// computes two adjacent columns of one root for one leaf row; X is staged
+// row-major [j][cp] (pairs 16-byte aligned, odd widths zero-padded) so one
+// double2 broadcast load feeds two FMAs.  Summation order per output is the
+// scalar one: leaf terms j = 0..s-1, then y = y + z per ancestor deepest
+// first (z = sum over a in order) -- equal bitwise to k_hmatB.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
+struct HBRoots {
+  int lam, cnt, cp;
+  int off[16], cols[16], mus[16];
+  int steps[16];              // mu = anc(lam, steps)
+};
+
+__device__ __forceinline__ bool hb_roots(const TreeDev& T, const MMJob& J, int g, int path,
+                                         HBRoots& R) {
+  R.cnt = 0;
+  if (path) {
+    R.lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
+    const int* an = T.anc + R.lam * (T.maxdepth + 1);
+    const int dl = T.depth[R.lam];
+    for (int t = 0; t < dl && t < 16; ++t) {
+      const int mu = an[t];
+      if (mu < J.mu0 || mu >= J.mu1) continue;
+      const int c = mm_cols(J, T, g, mu);
+      if (!c) continue;
+      R.mus[R.cnt] = mu;
+      R.cols[R.cnt] = c;
+      R.steps[R.cnt] = t;
+      R.off[R.cnt] = R.cnt == 0 ? 0 : R.off[R.cnt - 1] + ((R.cols[R.cnt - 1] + 1) & ~1);
+      ++R.cnt;
     }
-    src_col(J.Y, n, g, mm_slot(T, mu), b)[lo + i] = J.alpha * y;
+  } else {
+    const int b0 = T.startB[J.mu0], nB = T.startB[J.mu1] - b0;
+    if ((int)blockIdx.x >= nB) return false;
+    const int mu = T.listB[(b0 + blockIdx.x) * 2];
+    R.lam = T.listB[(b0 + blockIdx.x) * 2 + 1];
+    const int c = mm_cols(J, T, g, mu);
+    if (c) {
+      R.mus[0] = mu;
+      R.cols[0] = c;
+      R.off[0] = 0;
+      R.steps[0] = T.depth[R.lam] - T.depth[mu];
+      R.cnt = 1;
+    }
+  }
+  if (!R.cnt) return false;
+  R.cp = R.off[R.cnt - 1] + ((R.cols[R.cnt - 1] + 1) & ~1);
+  return true;
+}
+
+// ancestor walk of every root, tabulated once per CTA (k = steps above lam)
+struct HBAnc {
+  int r[17];
+  long long F[17];
+  const double* t[16][17];
+};
+
+__device__ __forceinline__ void hb_anc_tables(const TreeDev& T, const MMJob& J, const HB& h,
+                                              int g, const HBRoots& R, int lo, HBAnc& A) {
+  const int* an = T.anc + R.lam * (T.maxdepth + 1);
+  const int dl = T.depth[R.lam];
+  const int eA0 = T.startA[J.mu0];
+  for (int p = threadIdx.x; p < 17 * (R.cnt + 1); p += HT) {
+    const int q = p / 17 - 1, k = p % 17;
+    if (k < 1 || k > dl) continue;
+    const int be = an[k];
+    const bool top = lo < T.mid[be];
+    const int sd = J.trans ? (top ? 1 : 0) : (top ? 0 : 1);
+    if (q < 0) {
+      A.r[k] = h.rk[be * 2 + sd];
+      A.F[k] = (long long)T.depth[be] * h.R * T.n + lo;
+    } else if (k <= R.steps[q]) {
+      const int mu = R.mus[q];
+      const int e = T.startA[mu] + 2 * T.posA[mu * T.nnodes + be] + sd - eA0;
+      A.t[q][k] = J.tbuf + ((long long)g * J.nA + e) * J.RT * J.CT;
+    }
+  }
+}
+
+__device__ __forceinline__ void hb_finish_tab(const TreeDev& T, const MMJob& J, const HB& h,
+                                              int g, int q, const HBRoots& R, const HBAnc& A,
+                                              int lo, int i, int b0, int nb, double y0,
+                                              double y1) {
+  const int n = T.n;
+  const double* base = (J.trans ? h.V : h.U) + i;
+  const int nst = R.steps[q];
+  for (int k = 1; k <= nst; ++k) {
+    const int r = A.r[k];
+    if (!r) continue;
+    const double* t = A.t[q][k] + b0;
+    const double* F = base + A.F[k];
+    double z0 = 0.0, z1 = 0.0;
+#pragma unroll 4
+    for (int a = 0; a < r; ++a) {
+      const double f = F[(long long)a * n];
+      z0 += f * __ldg(t + a * J.CT);
+      if (nb > 1) z1 += f * __ldg(t + a * J.CT + 1);
+    }
+    y0 = y0 + z0;
+    y1 = y1 + z1;
+  }
+  const int slot = mm_slot(T, R.mus[q]);
+  src_col(J.Y, n, g, slot, b0)[lo + i] = J.alpha * y0;
+  if (nb > 1) src_col(J.Y, n, g, slot, b0 + 1)[lo + i] = J.alpha * y1;
+}
+
+// Leaf in padded shared memory (few registers, high occupancy);
+// X staged in windows of at most xc columns (bounded shared memory)
+__global__ void __launch_bounds__(HT) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path, int xc) {
+  extern __shared__ double sm[];
+  const MMJob& J = JJ.j[blockIdx.z];
+  const int g = blockIdx.y, bw = T.bw;
+  HBRoots R;
+  if (!hb_roots(T, J, g, path, R)) return;
+  const HB h = J.H[g];
+  const int lam = R.lam, lo = T.lo[lam], s = T.hi[lam] - lo, cp = R.cp;
+  const int ld = s + 1;
+  double* L = sm;                               // s x ld
+  double* X = L + ((s * ld + 1) & ~1);          // s x (window width), pairs aligned
+  const double* Lg = h.leaf + (long long)lo * bw;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // asynchronous staging: warp per row, lanes along the row (no divisions)
+  for (int ii = warp; ii < s; ii += HT / 32)
+    for (int j = lane; j < s; j += 32) cp_async8(L + ii * ld + j, Lg + (long long)ii * bw + j, true);
+  __shared__ HBAnc A;
+  hb_anc_tables(T, J, h, g, R, lo, A);
+  for (int w0 = 0; w0 < cp; w0 += xc) {
+    const int wc = cp - w0 < xc ? cp - w0 : xc;
+    for (int q = 0; q < R.cnt; ++q) {
+      const int slot = mm_slot(T, R.mus[q]);
+      const int q0 = R.off[q], q1 = q0 + ((R.cols[q] + 1) & ~1);
+      const int c0 = q0 > w0 ? q0 : w0, c1 = q1 < w0 + wc ? q1 : w0 + wc;
+      for (int pos = c0 + warp; pos < c1; pos += HT / 32) {
+        const int b = pos - q0;
+        const bool ok = b < R.cols[q];
+        const double* src = src_col(J.X, T.n, g, slot, ok ? b : 0) + lo;
+        for (int ii = lane; ii < s; ii += 32) cp_async8(X + ii * wc + (pos - w0), src + ii, ok);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int npairs = wc >> 1;
+    for (int idx = threadIdx.x; idx < s * npairs; idx += HT) {
+      const int pr = idx / s, i = idx - pr * s;
+      const int pos = w0 + pr * 2;
+      int q = 0;
+      while (q + 1 < R.cnt && R.off[q + 1] <= pos) ++q;
+      const int b0 = pos - R.off[q];
+      const int nb = R.cols[q] - b0 < 2 ? R.cols[q] - b0 : 2;
+      if (nb <= 0) continue;
+      double y0 = 0.0, y1 = 0.0;
+      const double2* x = reinterpret_cast<const double2*>(X + pr * 2);
+      const int li = J.trans ? i : i * ld, lj = J.trans ? ld : 1;
+      for (int j = 0; j < s; ++j) {
+        const double l = L[li + j * lj];
+        const double2 xv = x[j * npairs];
+        y0 += l * xv.x;
+        y1 += l * xv.y;
+      }
+      hb_finish_tab(T, J, h, g, q, R, A, lo, i, b0, nb, y0, y1);
+    }
+    __syncthreads();
   }
 }
 
@@ -217,23 +419,42 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  // wide column tiles only when the grid fills the GPU several times over;
+  // small (top-level) grids keep per-thread chains short
+  auto big = [](dim3 g) { return (long long)g.x * g.y * g.z >= 148LL * 8; };
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_hmatB, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_hmatB<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_path<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    cudaFuncSetAttribute(k_hmatB_path, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_hmatB_path<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr = true;
   }
-  if (jobs[0].mu0 == 1 && jobs[0].mu1 == T.nnodes && T.maxdepth <= 16) {
-    size_t smem = ((size_t)T.bw * (T.bw + 1) + (size_t)T.bw * cmax * T.maxdepth) * 8;
-    dim3 g(T.nleaves, nelem, njobs);
-    k_hmatB_path<<<g, HT, smem, st>>>(T, JJ);
+  const bool path = jobs[0].mu0 == 1 && jobs[0].mu1 == T.nnodes && T.maxdepth <= 16;
+  if (T.maxdepth <= 16) {
+    size_t cp = (size_t)((cmax + 1) & ~1) * (path ? T.maxdepth : 1);
+    if (cp > 64) cp = 64;
+    const size_t smem = ((size_t)T.bw * cp + (size_t)T.bw * (T.bw + 1) + 1) * 8;
+    dim3 g(path ? T.nleaves : nB, nelem, njobs);
+    k_hmatB_sm<<<g, HT, smem, st>>>(T, JJ, path, (int)cp);
     return cudaGetLastError();
   }
-  size_t smem = ((size_t)T.bw * (T.bw + 1) + (size_t)T.bw * cmax) * 8;
+  if (path) {
+    const size_t cpad = (size_t)(cmax + HB_CB - 1) / HB_CB * HB_CB;
+    size_t smem = ((size_t)T.bw * (T.bw + 1) + 1 + (size_t)T.bw * cpad * T.maxdepth) * 8;
+    dim3 g(T.nleaves, nelem, njobs);
+    if (big(g)) k_hmatB_path<8><<<g, HT, smem, st>>>(T, JJ);
+    else k_hmatB_path<2><<<g, HT, smem, st>>>(T, JJ);
+    return cudaGetLastError();
+  }
+  const size_t cpad = (size_t)(cmax + HB_CB - 1) / HB_CB * HB_CB;
+  size_t smem = ((size_t)T.bw * (T.bw + 1) + 1 + (size_t)T.bw * cpad) * 8;
   dim3 g(nB, nelem, njobs);
-  k_hmatB<<<g, HT, smem, st>>>(T, JJ, nB);
+  if (big(g)) k_hmatB<8><<<g, HT, smem, st>>>(T, JJ, nB);
+  else k_hmatB<2><<<g, HT, smem, st>>>(T, JJ, nB);
   return cudaGetLastError();
 }
 
