@@ -120,18 +120,42 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
 
 // Register-tiled Gauss-Jordan for leaves of size <= S (S in {16, 32, 64}):
 // (S/4)^2 threads, each owning a 4x4 tile in registers, plus a double-buffered
-// shared copy of the matrix.  Every warp computes the pivot (first index of the
-// largest |a_ik|, getrf's rule) redundantly from the shared copy, so one
-// barrier per pivot step suffices.  Singular / non-finite detection as the
-// reference's LAPACK call (algebra.py:199-207).
+// shared copy of the matrix.  Thread tid owns column group tid / TG and row
+// group tid % TG, so a column group lives in TG consecutive lanes: right after
+// the update of step k the group owning column k+1 finds the next pivot
+// (first index of the largest |a_ik|, getrf's rule) while the other warps
+// still update, and publishes it with the step's single barrier.  Singular /
+// non-finite detection as the reference's LAPACK call (algebra.py:199-207).
+template <int TG>
+__device__ __forceinline__ void gj_pivot(const double* m, int LD, int col, int k0, int s,
+                                         int ty, bool owner, int* out) {
+  double best = -1.0;
+  int p = k0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = ty * 4 + a;
+    if (i >= k0 && i < s) {
+      const double v = fabs(m[i * LD + col]);
+      if (v > best) { best = v; p = i; }
+    }
+  }
+#pragma unroll
+  for (int o = TG / 2; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, p, o);
+    if (ov > best || (ov == best && oi < p)) { best = ov; p = oi; }
+  }
+  if (owner && ty == 0) *out = p;
+}
+
 template <int S>
 __global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, const HB* H,
                                                                   int leaf, int* sing) {
   constexpr int TG = S / 4, LD = S + 1;
   extern __shared__ double buf[];              // [2][S][LD]
-  __shared__ int piv[S], inv_[S];
-  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-  const int ty = tid / TG, tx = tid - ty * TG;
+  __shared__ int piv[S + 1], inv_[S];
+  const int g = blockIdx.x, tid = threadIdx.x;
+  const int tx = tid / TG, ty = tid - tx * TG;   // column group, row group
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
   double* L = H[g].leaf + (long long)lo * bw;
   double x[4][4];
@@ -143,26 +167,17 @@ __global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, co
       x[a][b] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
       buf[r * LD + c] = x[a][b];
     }
+  // the whole warp holding column group 0 joins the shuffles (groups of TG lanes)
+  __syncwarp();
+  if (tid < 32) gj_pivot<TG>(buf, LD, 0, 0, s, ty, tx == 0, &piv[0]);
   bool bad = false;
   for (int k = 0; k < s; ++k) {
     const double* cur = buf + (k & 1) * S * LD;
     double* nxt = buf + ((k + 1) & 1) * S * LD;
     __syncthreads();
-    double best = -1.0;
-    int p = k;
-    for (int i = k + lane; i < s; i += 32) {
-      double v = fabs(cur[i * LD + k]);
-      if (v > best) { best = v; p = i; }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, p, o);
-      if (ov > best || (ov == best && oi < p)) { best = ov; p = oi; }
-    }
+    const int p = piv[k];
     const double pv = cur[p * LD + k];
-    if (pv == 0.0) { bad = true; break; }     // uniform: every warp sees the same
-    if (tid == 0) piv[k] = p;
+    if (pv == 0.0) { bad = true; break; }     // uniform: every thread sees the same
     const double inv = 1.0 / pv;
     double rk[4], ok[4];
 #pragma unroll
@@ -190,6 +205,10 @@ __global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, co
       }
 #pragma unroll
       for (int b = 0; b < 4; ++b) nxt[r * LD + tx * 4 + b] = x[a][b];
+    }
+    if (k + 1 < s && (tid >> 5) == (((k + 1) >> 2) * TG) >> 5) {
+      __syncwarp();
+      gj_pivot<TG>(nxt, LD, k + 1, k + 1, s, ty, tx == (k + 1) >> 2, &piv[k + 1]);
     }
   }
   if (bad) {
