@@ -308,6 +308,29 @@ def run_ours(args):
         "share_of_factor": tr["ms"] / max(inst_factor_ms, 1e-9),
         "kernel_classes": stats,
     }
+    # FP64 view of the same classes against the FP64 peaks measured on this
+    # GPU model (scripts/fp64_peak.cu -> profiles/r01_fp64_peak.json)
+    fp64 = {}
+    try:
+        fp64 = json.load(open(os.path.join(REPO, "profiles", "r01_fp64_peak.json")))
+    except OSError:
+        pass
+    dfma = float(fp64.get("dfma_tflops", 34.16)) * 1e3
+    dmma = float(fp64.get("dmma_tflops", 37.20)) * 1e3
+
+    def _gfs(st):
+        return st["flops"] / (st["ms"] / 1e3) / 1e9 if st["ms"] > 0 else 0.0
+    roofline_fp64 = {
+        "unit": "GFLOP/s", "peak_source": "profiles/r01_fp64_peak.json (measured DFMA / DMMA)",
+        "k_trunc": {"achieved": _gfs(tr), "peak": dfma, "frac": _gfs(tr) / dfma,
+                    "pipe": "DFMA (Householder QR, Jacobi, apply-Q)"},
+        "k_leafgemm": {"achieved": _gfs(stats["k_leafgemm"]), "peak": dmma,
+                       "frac": _gfs(stats["k_leafgemm"]) / dmma,
+                       "pipe": "DMMA m8n8k4 (dense leaf products)"},
+        "k_leafinv": {"achieved": _gfs(stats["k_leafinv"]), "peak": dfma,
+                      "frac": _gfs(stats["k_leafinv"]) / dfma,
+                      "pipe": "DFMA (register-tiled Gauss-Jordan)"},
+    }
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
@@ -325,7 +348,7 @@ def run_ours(args):
                 "ms_per_step": e2e_ms, "solve_ms": solve_ms,
                 "residual_max_col": res_max, "residual_fro": res_fro},
         "gpu_launches": launches_per_factor * args.steps,
-        "roofline": roofline,
+        "roofline": roofline, "roofline_fp64": roofline_fp64,
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

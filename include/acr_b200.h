@@ -96,7 +96,11 @@ long long acr_kernel_launches(const acr_plan_t* p);
  * [2..7] block-path clock64 cycles per phase (load, QR, core, Jacobi, select,
  * output), [8] block-path full tasks, [9] warp-path full tasks, [10]/[11]
  * Jacobi sweeps (block / warp), [12..15] warp-path cycles (load, QR, core,
- * Jacobi+rest). */
+ * Jacobi).  Classes 1 and 2: counters[0] = dense-leaf FLOPs (2 s^3 per leaf
+ * inverse / product, 2 s^2 on the exact diagonal path).  cls 100: the raw
+ * 160 device counters ([16..65] warp-path histogram, [66]/[67] warp-path
+ * select / output cycles, [72..146] block-path histogram: counts, cycles,
+ * Jacobi cycles by rank x rows bucket). */
 int acr_kernel_stats(const acr_plan_t* p, int cls, long long* launches,
                      double* ms, unsigned long long* counters);
 int acr_last_error(const acr_plan_t* p, char* buf, int len);

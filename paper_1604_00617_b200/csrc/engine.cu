@@ -463,7 +463,8 @@ struct Plan {
   std::vector<std::pair<int, size_t>> evmarks;   // (class, index of start event)
   double kms[NCLS] = {0};
   long long kcnt[NCLS] = {0};
-  unsigned long long kctr[72] = {0};
+  unsigned long long kctr[160] = {0};
+  double hflops[NCLS] = {0};   // host-side FLOP counts (leaf classes), per factor
   Dev dctr;
   // scratch pool
   std::vector<Dev> scr;
@@ -575,11 +576,11 @@ struct Plan {
   void prof_reset() {
     evused = 0;
     evmarks.clear();
-    for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; }
+    for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; hflops[i] = 0; }
     for (auto& c : kctr) c = 0;
     if (prof_on) {
-      if (!dctr.p) dctr.alloc(72 * sizeof(unsigned long long), st);
-      CK(cudaMemsetAsync(dctr.p, 0, 72 * sizeof(unsigned long long), st));
+      if (!dctr.p) dctr.alloc(160 * sizeof(unsigned long long), st);
+      CK(cudaMemsetAsync(dctr.p, 0, 160 * sizeof(unsigned long long), st));
     }
   }
   void prof_collect() {   // after a stream sync
@@ -642,7 +643,7 @@ struct Plan {
     const bool may_big = !direct && wworst > trunc_warp_pool_doubles();
     int* q = nullptr;
     int* qc = nullptr;
-    const long long SMD = 24576;                 // 192 KB of doubles
+    const long long SMD = 28416;                 // 222 KB of doubles
     a.smem_doubles = (int)std::min(bworst, SMD);
     a.gscr = nullptr;
     a.gscr_stride = 0;
@@ -730,6 +731,12 @@ struct Plan {
     const cudaStream_t s2 = side();
     fork(s2);
     kbegin(2);
+    if (prof_on)   // dense leaf products: 2 s^3 each (2 s^2 on the exact diagonal path)
+      for (int v = 0; v < nn; ++v)
+        if (ht.isleaf[v]) {
+          const double sz = ht.hi[v] - ht.lo[v];
+          hflops[2] += (double)G * 2.0 * sz * sz * (diag ? 1.0 : sz);
+        }
     CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), diag,
                        s2));
     kend();
@@ -902,6 +909,10 @@ struct Plan {
   void inv_node(InvCtx& c, int nu) {
     if (ht.isleaf[nu]) {
       kbegin(1);
+      if (prof_on) {   // Gauss-Jordan inverse: 2 s^3
+        const double sz = ht.hi[nu] - ht.lo[nu];
+        hflops[1] += (double)c.G * 2.0 * sz * sz * sz;
+      }
       CK(launch_leafinv(dt.T, c.H, c.G, nu, c.sing, st));
       kend();
       ++launches;
@@ -1803,8 +1814,10 @@ int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
   *ms = cls == 100 ? 0.0 : P.kms[cls];
   if (counters)
     for (int i = 0; i < 16; ++i) counters[i] = cls == 0 ? P.kctr[i] : 0;
+  if (counters && cls > 0 && cls < Plan::NCLS)
+    counters[0] = (unsigned long long)P.hflops[cls];
   if (counters && cls == 100)
-    for (int i = 0; i < 72; ++i) counters[i] = P.kctr[i];
+    for (int i = 0; i < 160; ++i) counters[i] = P.kctr[i];
   return ACR_OK;
 }
 

@@ -151,6 +151,31 @@ __device__ void group_apply_q(const double* W, int mr, int p, const double* tau,
   }
 }
 
+// Explicit Q (mr x p) formed in place over the reflectors (LAPACK dorg2r
+// order: last reflector first); the R factor in the upper triangle is
+// overwritten, so the core product must be formed before.
+__device__ void group_form_q(double* W, int mr, int p, const double* tau, const Grp& g) {
+  for (int j = p - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    const double* v = W + (long long)j * mr;
+    if (tj != 0.0) {
+      for (int c = j + 1 + g.w; c < p; c += g.nw) {
+        double* xc = W + (long long)c * mr;
+        double w = 0.0;
+        for (int i = j + 1 + g.lane; i < mr; i += 32) w += v[i] * xc[i];
+        w = (warp_sum(w) + xc[j]) * tj;
+        for (int i = j + 1 + g.lane; i < mr; i += 32) xc[i] -= w * v[i];
+        if (g.lane == 0) xc[j] -= w;
+      }
+    }
+    gbar(g);
+    double* cj = W + (long long)j * mr;
+    for (int i = g.t; i < mr; i += g.nt)
+      cj[i] = i > j ? -tj * cj[i] : (i == j ? 1.0 - tj : 0.0);
+    gbar(g);
+  }
+}
+
 // Householder QR of W (mr x R, column-major, ld = mr), in place.  On exit
 // the upper trapezoid holds R, below-diagonal the reflector tails, tau[j].
 __device__ void block_qr(double* W, int mr, int R, double* tau, double* red,
@@ -368,7 +393,7 @@ __device__ __forceinline__ bool task_is_full(const TruncArgs& A, const TaskCtx& 
 }
 
 __host__ __device__ long long trunc_need_doubles(int um, int vm, int R) {
-  return 2LL * (um + vm) * R + 2LL * R * R + 4LL * R + 8;
+  return (long long)(um + vm) * R + 4LL * R * R + 4LL * R + 8;
 }
 
 __host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
@@ -393,11 +418,11 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   const int pu = um < R ? um : R, pv = vm < R ? vm : R;
   double* Uw = wk;
   double* Vw = Uw + (long long)um * R;
-  double* Ou = Vw + (long long)vm * R;
-  double* Ov = Ou + (long long)um * R;
-  double* Bm = Ov + (long long)vm * R;
+  double* Bm = Vw + (long long)vm * R;
   double* Jm = Bm + (long long)R * R;
-  double* tauU = Jm + (long long)R * R;
+  double* Cu = Jm + (long long)R * R;          // pu x keep coefficients
+  double* Cv = Cu + (long long)R * R;          // pv x keep
+  double* tauU = Cv + (long long)R * R;
   double* tauV = tauU + R;
   double* sig = tauV + R;
   int* ord = reinterpret_cast<int*>(sig + R);
@@ -513,43 +538,57 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
       for (int i = 0; i < 5; ++i) atomicAdd(A.ctr + 2 + i, (unsigned long long)ph[i]);
     return;
   }
-  // left/right factors padded with zeros, then Q applied
-  for (int idx = tid; idx < um * keep; idx += TT) {
-    int c = idx / um, i = idx - c * um;
-    int j = ord[c];
-    double v = 0.0;
-    if (i < pu) v = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
-    Ou[idx] = v;
+  // coefficients of the kept singular pairs, then explicit Q (in place over
+  // the reflectors, half-CTA per side) and U' = Q_u C_u, V' = Q_v C_v written
+  // straight to the output columns
+  for (int idx = tid; idx < pu * keep; idx += TT) {
+    const int c = idx / pu, i = idx - c * pu;
+    const int j = ord[c];
+    Cu[idx] = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
   }
-  for (int idx = tid; idx < vm * keep; idx += TT) {
-    int c = idx / vm, i = idx - c * vm;
-    int j = ord[c];
-    double v = 0.0;
-    if (i < pv) v = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
-    Ov[idx] = v;
+  for (int idx = tid; idx < pv * keep; idx += TT) {
+    const int c = idx / pv, i = idx - c * pv;
+    const int j = ord[c];
+    Cv[idx] = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
   }
-  __syncthreads();
   {
     const int half = tid >= TT / 2 ? 1 : 0;
     const int t = tid - half * (TT / 2);
     Grp g{1 + half, TT / 2, t, NWB / 2, t >> 5, tid & 31, red + half * (NWB / 2),
           nullptr};
-    if (!half) group_apply_q(Uw, um, pu, tauU, Ou, keep, g);
-    else group_apply_q(Vw, vm, pv, tauV, Ov, keep, g);
+    if (!half) group_form_q(Uw, um, pu, tauU, g);
+    else group_form_q(Vw, vm, pv, tauV, g);
   }
   __syncthreads();
   for (int idx = tid; idx < um * keep; idx += TT) {
-    int c = idx / um, i = idx - c * um;
-    Uo[(long long)c * n + i] = Ou[idx];
+    const int c = idx / um, i = idx - c * um;
+    const double* cc = Cu + (long long)c * pu;
+    double y = 0.0;
+    for (int l = 0; l < pu; ++l) y += Uw[(long long)l * um + i] * cc[l];
+    Uo[(long long)c * n + i] = y;
   }
   for (int idx = tid; idx < vm * keep; idx += TT) {
-    int c = idx / vm, i = idx - c * vm;
-    Vo[(long long)c * n + i] = Ov[idx];
+    const int c = idx / vm, i = idx - c * vm;
+    const double* cc = Cv + (long long)c * pv;
+    double y = 0.0;
+    for (int l = 0; l < pv; ++l) y += Vw[(long long)l * vm + i] * cc[l];
+    Vo[(long long)c * n + i] = y;
   }
   if (tid == 0) *ro = keep;
   ACR_PH(5);
-  if (A.ctr && tid == 0)
+  if (A.ctr && tid == 0) {
     for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 2 + i, (unsigned long long)ph[i]);
+    // histogram: R bucket (<=8, <=16, <=32, <=64, >64) x m bucket (<=128, 256,
+    // 512, 1024, >1024): count, total cycles, Jacobi cycles
+    const int rb = R <= 8 ? 0 : R <= 16 ? 1 : R <= 32 ? 2 : R <= 64 ? 3 : 4;
+    const int mm = um > vm ? um : vm;
+    const int mb = mm <= 128 ? 0 : mm <= 256 ? 1 : mm <= 512 ? 2 : mm <= 1024 ? 3 : 4;
+    long long tot = 0;
+    for (int i = 0; i < 6; ++i) tot += ph[i];
+    atomicAdd(A.ctr + 72 + rb * 5 + mb, 1ull);
+    atomicAdd(A.ctr + 97 + rb * 5 + mb, (unsigned long long)tot);
+    atomicAdd(A.ctr + 122 + rb * 5 + mb, (unsigned long long)ph[3]);
+  }
 }
 
 
@@ -979,7 +1018,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   if (lane == 0) *tc.ro = keep;
   ACR_PH(5);
   if (A.ctr && lane == 0) {
-    for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 12 + (i < 4 ? i : 3), (unsigned long long)ph[i]);
+    for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + (i < 4 ? 12 + i : 62 + i), (unsigned long long)ph[i]);
     // histogram: R bucket (<=4, <=8, <=16, <=32, >32) x m bucket (<=32, 64, 128, 256, >256)
     const int rb = R <= 4 ? 0 : R <= 8 ? 1 : R <= 16 ? 2 : R <= 32 ? 3 : 4;
     const int mm = um > vm ? um : vm;
@@ -1069,7 +1108,7 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
     cudaFuncSetAttribute(k_trunc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          NSLOT * SLOT * 8);
     cudaFuncSetAttribute(k_trunc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+                         28416 * 8 + 64);   // engine caps smem_doubles at 28416
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -40,10 +40,16 @@ for name in cfgs:
             if cls == 0:
                 st["trunc_ctr"] = list(ctr)
         print(json.dumps(dict(cfg=name, instrumented_factor_ms=round(sol.factor_ms, 1), classes=st)), flush=True)
-        nl = C.c_longlong(); ms = C.c_double(); ctr = (C.c_ulonglong * 72)()
+        nl = C.c_longlong(); ms = C.c_double(); ctr = (C.c_ulonglong * 160)()
         sol.lib.acr_kernel_stats(sol.plan, 100, C.byref(nl), C.byref(ms), ctr)
         cnt = list(ctr)[16:41]; cyc = list(ctr)[41:66]
         tot = sum(cyc) or 1
         print("warp-path histogram (rows R<=4,8,16,32,>32; cols m<=32,64,128,256,>256): count / %cycles / kcyc-per-task")
         for rb in range(5):
             print("  ", " | ".join(f"{cnt[rb*5+mb]:8d} {100*cyc[rb*5+mb]/tot:5.1f}% {cyc[rb*5+mb]/max(cnt[rb*5+mb],1)/1e3:6.1f}" for mb in range(5)))
+        print("warp phases G (load, qr, core, jacobi, select, output):", [round(ctr[i] / 1e9, 2) for i in (12, 13, 14, 15, 66, 67)])
+        print("block phases G (load, qr, core, jacobi, select, output):", [round(ctr[i] / 1e9, 2) for i in range(2, 8)])
+        bc = list(ctr)[72:97]; by = list(ctr)[97:122]; bj = list(ctr)[122:147]
+        print("block-path histogram (R<=8,16,32,64,>64; m<=128,256,512,1024,>1024): count / kcyc-per-task / jacobi%")
+        for rb in range(5):
+            print("  ", " | ".join(f"{bc[rb*5+mb]:7d} {by[rb*5+mb]/max(bc[rb*5+mb],1)/1e3:7.1f} {100*bj[rb*5+mb]/max(by[rb*5+mb],1):4.0f}%" for mb in range(5)))
