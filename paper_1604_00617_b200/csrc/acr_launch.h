@@ -16,6 +16,10 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
                          int* bigq, int* bigcount, cudaStream_t st);
 int trunc_direct_max();
 long long warp_need_doubles(int um, int vm, int R);
+// CTA-pair (cluster of 2) recompression for direct launches of large tasks
+cudaError_t launch_trunc_pair(const TruncArgs& a, int nelem, long long smem_doubles,
+                              cudaStream_t st);
+long long pair_need_doubles(int m, int R);
 
 // leaf kernels (k_leaf.cu)
 cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,

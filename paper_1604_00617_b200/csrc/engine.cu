@@ -631,19 +631,30 @@ struct Plan {
     a.ntasks = t1 - t0;
     a.ctr = prof_on ? dctr.as<unsigned long long>() : nullptr;
     const int Rw = (a.mode == TM_TRUNCATE) ? Ra : Ra + Rb;
-    long long wworst = 0, bworst = 0;
+    long long wworst = 0, bworst = 0, pworst = 0;
     for (int i = t0; i < t1; ++i) {
       int bb = ht.listA[i * 3 + 1];
       int um = ht.mid[bb] - ht.lo[bb], vm = ht.hi[bb] - ht.mid[bb];
       wworst = std::max(wworst, warp_need_doubles(um, vm, Rw));
       bworst = std::max(bworst, trunc_need_doubles(um, vm, Rw));
+      pworst = std::max(pworst, pair_need_doubles(std::max(um, vm), Rw));
     }
     const int nitems = a.ntasks * nelem;
     const bool direct = nitems <= trunc_direct_max();
+    const long long SMD = 28416;                 // 222 KB of doubles
+    // latency-bound launches whose panels do not fit one CTA's shared memory:
+    // one CTA per side (cluster pair) instead of the global-memory scratch
+    if (direct && bworst > SMD && pworst <= SMD) {
+      fork(s);
+      kbegin(0);
+      CK(launch_trunc_pair(a, nelem, pworst, s));
+      kend();
+      launches += 1;
+      return;
+    }
     const bool may_big = !direct && wworst > trunc_warp_pool_doubles();
     int* q = nullptr;
     int* qc = nullptr;
-    const long long SMD = 28416;                 // 222 KB of doubles
     a.smem_doubles = (int)std::min(bworst, SMD);
     a.gscr = nullptr;
     a.gscr_stride = 0;

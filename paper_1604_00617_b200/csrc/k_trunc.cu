@@ -12,6 +12,8 @@
 //                  optional cap, U' = Qu (W s), V' = Qv Z.
 // All reductions are fixed-order (warp shuffles + 4-way smem) so results are
 // bitwise reproducible run to run and independent of elimination order.
+#include <cooperative_groups.h>
+
 #include "acr_types.cuh"
 #include "acr_launch.h"
 
@@ -661,6 +663,218 @@ __global__ void __launch_bounds__(TT) k_trunc_big(TruncArgs A, const int* q,
     trunc_block_full(A, c, wk, red, iflag);
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair path (thread-block cluster of 2) for latency-bound launches of
+// large tasks: CTA 0 owns U, CTA 1 owns V, each with all TT threads and its
+// panel in its own shared memory.  R_v and |R_v|_F reach CTA 0 through
+// distributed shared memory; CTA 0 forms the core, runs the Jacobi SVD and
+// the rank decision and writes the coefficients of both sides (C_v into CTA
+// 1's shared memory); then each CTA forms its explicit Q in place and writes
+// its output factor.  Same arithmetic as trunc_block_full.
+// ---------------------------------------------------------------------------
+__host__ __device__ long long pair_need_doubles(int m, int R) {
+  return (long long)m * R + 4LL * R * R + 3LL * R + 8;
+}
+
+__device__ __forceinline__ bool task_trivial(const TruncArgs& A, const TaskCtx& c) {
+  if (A.mode != TM_TRUNCATE) return c.a.r == 0 || c.b.r == 0;
+  return c.a.r < 2;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
+    k_trunc_pair(TruncArgs A, int nitems) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  __shared__ double red[NWB + 4];
+  __shared__ int iflag[2];
+  const int side = (int)cl.block_rank();
+  const int tid = threadIdx.x, n = A.T.n;
+  for (int item = blockIdx.x / 2; item < nitems; item += gridDim.x / 2) {
+    const int task = item % A.ntasks, g = item / A.ntasks;
+    TaskCtx c = resolve_task(A, task, g);
+    __syncthreads();
+    if (task_trivial(A, c)) {                 // both CTAs agree; CTA 0 writes
+      if (side == 0) block_trivial(A, c, red);
+      __syncthreads();
+      continue;
+    }
+    const OpRes& a = c.a;
+    const OpRes& b = c.b;
+    const int R = a.r + b.r;
+    const int m = side ? c.vm : c.um;
+    const int p = m < R ? m : R;
+    double* W = sm;
+    double* Rs = W + (long long)m * R;        // own R factor, [l][i] = Rs[l * R + i]
+    double* Bm = Rs + (long long)R * R;
+    double* Jm = Bm + (long long)R * R;
+    double* Cs = Jm + (long long)R * R;       // own coefficients p x keep
+    double* tau = Cs + (long long)R * R;
+    double* sig = tau + R;
+    int* ord = reinterpret_cast<int*>(sig + R);
+    double* misc = sig + 2 * R;               // [0] |R|_F^2, [1] keep
+    long long ph[6] = {0, 0, 0, 0, 0, 0};
+    long long t_ph = clock64();
+    for (int idx = tid; idx < m * R; idx += TT) {
+      const int cc = idx / m, i = idx - cc * m;
+      double v;
+      if (side == 0)
+        v = cc < a.r ? a.sc * a.U[(long long)cc * n + i]
+                     : b.sc * b.U[(long long)(cc - a.r) * n + i];
+      else
+        v = cc < a.r ? a.V[(long long)cc * n + i] : b.V[(long long)(cc - a.r) * n + i];
+      W[idx] = v;
+    }
+    __syncthreads();
+    ACR_PH(0);
+    const Grp gf{1, TT, tid, NWB, tid >> 5, tid & 31, red, nullptr};
+    group_qr(W, m, R, tau, gf);
+    __syncthreads();
+    ACR_PH(1);
+    double nr2 = 0.0;
+    for (int idx = tid; idx < R * R; idx += TT) {
+      const int l = idx / R, i = idx - l * R;
+      const double x = (i < p && l >= i) ? W[(long long)l * m + i] : 0.0;
+      Rs[idx] = x;
+      nr2 += x * x;
+    }
+    nr2 = block_sum(nr2, red);
+    if (tid == 0) misc[0] = nr2;
+    cl.sync();                                 // both R factors published
+    if (side == 0) {
+      const double* Rv = cl.map_shared_rank(Rs, 1);
+      const double* mv = cl.map_shared_rank(misc, 1);
+      double* Cv = cl.map_shared_rank(Cs, 1);
+      double* mv_w = cl.map_shared_rank(misc, 1);
+      const double nu2 = nr2, nv2 = mv[0];
+      const int pu = p, pv = c.vm < R ? c.vm : R;
+      const bool tr = pu < pv;
+      const int pr = tr ? pv : pu, pc = tr ? pu : pv;
+      for (int idx = tid; idx < pu * pv; idx += TT) {
+        const int i = idx / pv, j = idx - i * pv;
+        const int l0 = i > j ? i : j;
+        double sacc = 0.0;
+        for (int l = l0; l < R; ++l) sacc += Rs[l * R + i] * Rv[l * R + j];
+        if (!tr) Bm[(long long)j * pr + i] = sacc;
+        else Bm[(long long)i * pr + j] = sacc;
+      }
+      __syncthreads();
+      ACR_PH(2);
+      int sweeps;
+      if (pc <= 64 && pr <= 128) {
+        __shared__ int s_sw;
+        if (tid < 32) {
+          const int sw = warp_jacobi(Bm, pr, pc, Jm, tid);
+          if (tid == 0) s_sw = sw;
+        }
+        __syncthreads();
+        sweeps = s_sw;
+      } else {
+        sweeps = block_jacobi(Bm, pr, pc, Jm, iflag);
+      }
+      ACR_PH(3);
+      for (int j = tid; j < pc; j += TT) {
+        double sacc = 0.0;
+        const double* bj = Bm + (long long)j * pr;
+        for (int r = 0; r < pr; ++r) sacc += bj[r] * bj[r];
+        sig[j] = sqrt(sacc);
+      }
+      __syncthreads();
+      for (int j = tid; j < pc; j += TT) {
+        const double sj = sig[j];
+        int rnk = 0;
+        for (int i = 0; i < pc; ++i) {
+          const double si = sig[i];
+          rnk += (si > sj) || (si == sj && i < j);
+        }
+        ord[rnk] = j;
+      }
+      __syncthreads();
+      const double s1 = sig[ord[0]];
+      const double guard = (double)R * 2.220446049250313e-16 * sqrt(nu2) * sqrt(nv2);
+      int keep = 0;
+      if (s1 > guard) {
+        const double thr = A.eps * s1;
+        for (int i = 0; i < pc; ++i) keep += sig[i] >= thr;
+        if (A.cap > 0 && keep > A.cap) keep = A.cap;
+      }
+      if (keep > c.Rout) {
+        if (tid == 0) atomicMax(A.overflow, keep);
+        keep = 0;
+      }
+      for (int idx = tid; idx < pu * keep; idx += TT) {
+        const int cc = idx / pu, i = idx - cc * pu;
+        const int j = ord[cc];
+        Cs[idx] = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
+      }
+      for (int idx = tid; idx < pv * keep; idx += TT) {
+        const int cc = idx / pv, i = idx - cc * pv;
+        const int j = ord[cc];
+        Cv[idx] = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
+      }
+      if (tid == 0) {
+        misc[1] = keep;
+        mv_w[1] = keep;
+      }
+      ACR_PH(4);
+      if (A.ctr && tid == 0) {   // census formulas of SURVEY.md Appendix C
+        const unsigned long long um = c.um, vm = c.vm;
+        unsigned long long fl = 4ull * um * R * R + 4ull * vm * R * R + 24ull * R * R * R +
+                                2ull * (um + vm) * R * keep;
+        atomicAdd(A.ctr, fl);
+        atomicAdd(A.ctr + 1, 8ull * (um * R + vm * R + um * keep + vm * keep));
+        atomicAdd(A.ctr + 8, 1ull);
+        atomicAdd(A.ctr + 10, (unsigned long long)sweeps);
+      }
+    }
+    cl.sync();                                 // coefficients and keep published
+    const int keep = (int)misc[1];
+    if (keep > 0) {
+      group_form_q(W, m, p, tau, gf);
+      __syncthreads();
+      double* O = side ? c.Vo : c.Uo;
+      for (int idx = tid; idx < m * keep; idx += TT) {
+        const int cc = idx / m, i = idx - cc * m;
+        const double* co = Cs + (long long)cc * p;
+        double y = 0.0;
+        for (int l = 0; l < p; ++l) y += W[(long long)l * m + i] * co[l];
+        O[(long long)cc * n + i] = y;
+      }
+    }
+    if (side == 0 && tid == 0) *c.ro = keep;
+    ACR_PH(5);
+    if (A.ctr && side == 0 && tid == 0) {
+      for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 2 + i, (unsigned long long)ph[i]);
+      const int rb = R <= 8 ? 0 : R <= 16 ? 1 : R <= 32 ? 2 : R <= 64 ? 3 : 4;
+      const int mm = c.um > c.vm ? c.um : c.vm;
+      const int mb = mm <= 128 ? 0 : mm <= 256 ? 1 : mm <= 512 ? 2 : mm <= 1024 ? 3 : 4;
+      long long tot = 0;
+      for (int i = 0; i < 6; ++i) tot += ph[i];
+      atomicAdd(A.ctr + 72 + rb * 5 + mb, 1ull);
+      atomicAdd(A.ctr + 97 + rb * 5 + mb, (unsigned long long)tot);
+      atomicAdd(A.ctr + 122 + rb * 5 + mb, (unsigned long long)ph[3]);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_trunc_pair(const TruncArgs& a, int nelem, long long smem_doubles,
+                              cudaStream_t st) {
+  if (a.ntasks == 0 || nelem == 0) return cudaSuccess;
+  const size_t bytes = (size_t)smem_doubles * 8 + 64;
+  static size_t attr = 0;
+  if (bytes > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_trunc_pair,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e != cudaSuccess) return e;
+    attr = bytes;
+  }
+  const int nitems = a.ntasks * nelem;
+  k_trunc_pair<<<2 * nitems, TT, bytes, st>>>(a, nitems);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
