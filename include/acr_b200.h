@@ -58,7 +58,9 @@ int acr_loopback_solve(int nranks, const int* bnd0, int m, int n, int leaf_size,
 
 /* option 1: keep every level's D blocks for export (tests); value 0/1
  * option 2: per-kernel-class instrumentation (CUDA events around every
- *           launch of a class + algorithmic FLOP/byte counters); 0/1 */
+ *           launch of a class + algorithmic FLOP/byte counters); 0/1
+ * option 3: route every latency-bound (direct) recompression launch that
+ *           fits through the CTA-pair cluster kernel (tests); 0/1 */
 int acr_plan_set_option(acr_plan_t* p, int option, long long value);
 
 /* Factor phase (reference lift_system reduction.py:156-166 + reduce_level

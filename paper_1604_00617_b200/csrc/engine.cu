@@ -434,6 +434,7 @@ struct Plan {
   int m, n, leaf, cutoff, cap;
   double eps;
   bool keep_levels = false;
+  bool force_pair = false;    // option 3: CTA-pair recompression for every direct launch that fits
   HostTree ht;
   DeviceTree dt;
   cudaStream_t st = 0;
@@ -644,7 +645,7 @@ struct Plan {
     const long long SMD = 28416;                 // 222 KB of doubles
     // latency-bound launches whose panels do not fit one CTA's shared memory:
     // one CTA per side (cluster pair) instead of the global-memory scratch
-    if (direct && bworst > SMD && pworst <= SMD) {
+    if (direct && pworst <= SMD && (bworst > SMD || force_pair)) {
       fork(s);
       kbegin(0);
       CK(launch_trunc_pair(a, nelem, pworst, s));
@@ -1761,6 +1762,10 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
   }
   if (option == 2) {
     h->p->prof_on = value != 0;
+    return ACR_OK;
+  }
+  if (option == 3) {
+    h->p->force_pair = value != 0;
     return ACR_OK;
   }
   return set_err(h, ACR_EARG, "unknown option");

@@ -258,3 +258,23 @@ def test_config5_column0_against_reference(solver_mod):
     stride = int(z["u_stride"])
     _check_against_golden(rep, u, z, "", c["eps"], stride=stride,
                           shape=(c["n"], c["n"], c["leaf"]))
+
+
+def test_cta_pair_recompression_path(solver_mod):
+    """Option 3 routes every direct recompression launch through the cluster
+    (CTA-pair) kernel that config 5's root panels need; same schedule, so the
+    solution matches the default path to roundoff and the reference's residual."""
+    c = P.CONFIGS["cfg2"]
+    s = P.make_config("cfg2")
+    tol = Tolerance(c["eps"])
+    out = []
+    for force in (0, 1):
+        sol = solver_mod.AcrSolver(s.n_blocks, s.block_dim, tol, 1, c["leaf"])
+        assert sol.lib.acr_plan_set_option(sol.plan, 3, force) == 0
+        sol.factor(sol.device_bands(s))
+        f = torch.as_tensor(s.rhs, device="cuda")
+        out.append(sol.solve(f).cpu().numpy())
+    assert _rel(out[1], out[0]) <= 1e-9
+    z = load_npz("cfg2.npz")
+    res = O.relative_residual(s, out[1])
+    assert res <= 2 * float(z["residual"]) + 1e-15
