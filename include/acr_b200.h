@@ -123,6 +123,24 @@ int acr_residual(int m, int n, int k, const double* D_sub, const double* D_diag,
                  const double* u, const double* f, double* out_r,
                  double* out_f, void* stream);
 
+/* Problem generators on the device (formulas of 8(d),
+ * the reference's BlockTridiagSystem layout, problems.py:88-133).
+ * acr_gen_constant: every band constant; values5 = {sub, diag, sup, E, F}
+ *   (configs 1, 3, 4).
+ * acr_gen_varcoef: configs 2 and 5, a = exp(sum_k c_k cos(2 pi (p_k x +
+ *   q_k y) + phi_k)) on the (n+2)^2 nodes (work: (n+2)^2 doubles),
+ *   harmonic-mean faces; parameters drawn on the host (numpy draw order).
+ * acr_gen_uniform: N x k row-major Uniform[low, high) = the transposed
+ *   (k, N) sample of numpy's default_rng continuing from the PCG64 state
+ *   pcg_state4 = {state_hi, state_lo, inc_hi, inc_lo}; bitwise numpy's. */
+int acr_gen_constant(int m, int n, const double* values5, double* D_sub, double* D_diag,
+                     double* D_sup, double* E, double* F, void* stream);
+int acr_gen_varcoef(int n, const double* c8, const long long* p8, const long long* q8,
+                    const double* phi8, double* work, double* D_sub, double* D_diag,
+                    double* D_sup, double* E, double* F, void* stream);
+int acr_gen_uniform(const unsigned long long* pcg_state4, long long N, int k, double low,
+                    double high, double* out, void* stream);
+
 /* Kernel-level entry points (parity tests against hodlr.py:176-200 and
  * algebra.py:199-207 on captured operands).  U (m x R) and V (k x R) are
  * column-major; Uo (m x R), Vo (k x R) receive the truncated factor. */

@@ -46,6 +46,13 @@ _SIGS = [
                                      C.c_void_p, C.c_void_p]),
     ("acr_residual", C.c_int, [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 7 +
      [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p]),
+    ("acr_gen_constant", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)] +
+     [C.c_void_p] * 6),
+    ("acr_gen_varcoef", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_longlong),
+                                  C.POINTER(C.c_longlong), C.POINTER(C.c_double)] +
+     [C.c_void_p] * 7),
+    ("acr_gen_uniform", C.c_int, [C.POINTER(C.c_ulonglong), C.c_longlong, C.c_int,
+                                  C.c_double, C.c_double, C.c_void_p, C.c_void_p]),
     ("acr_truncate_factor", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p,
                                       C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                       C.c_void_p, C.POINTER(C.c_int), C.c_void_p]),

@@ -76,4 +76,18 @@ cudaError_t launch_residual(int m, int n, int k, const double* sub,
                             const double* f, double* partial, int nparts,
                             cudaStream_t st);
 
+// problem generators (k_gen.cu)
+struct GenField {
+  double c[8];
+  long long p[8], q[8];
+  double phi[8];
+};
+cudaError_t launch_gen_const(int m, int n, const double* v, double* D_sub, double* D_diag,
+                             double* D_sup, double* E, double* F, cudaStream_t st);
+cudaError_t launch_gen_varcoef(int n, const GenField& P, double* work, double* D_sub,
+                               double* D_diag, double* D_sup, double* E, double* F,
+                               cudaStream_t st);
+cudaError_t launch_gen_uniform(const unsigned long long* state, long long N, int k,
+                               double low, double high, double* out, cudaStream_t st);
+
 }  // namespace acr

@@ -1915,6 +1915,43 @@ int acr_residual(int m, int n, int k, const double* D_sub, const double* D_diag,
   return ACR_OK;
 }
 
+int acr_gen_constant(int m, int n, const double* values5, double* D_sub, double* D_diag,
+                     double* D_sup, double* E, double* F, void* stream) {
+  if (m < 1 || n < 1 || !values5) return set_err(nullptr, ACR_EARG, "bad shape");
+  ACR_GUARD(nullptr, {
+    CK(acr::launch_gen_const(m, n, values5, D_sub, D_diag, D_sup, E, F,
+                             (cudaStream_t)stream));
+  });
+  return ACR_OK;
+}
+
+int acr_gen_varcoef(int n, const double* c8, const long long* p8, const long long* q8,
+                    const double* phi8, double* work, double* D_sub, double* D_diag,
+                    double* D_sup, double* E, double* F, void* stream) {
+  if (n < 1 || !c8 || !p8 || !q8 || !phi8 || !work)
+    return set_err(nullptr, ACR_EARG, "bad arguments");
+  ACR_GUARD(nullptr, {
+    acr::GenField P;
+    for (int t = 0; t < 8; ++t) {
+      P.c[t] = c8[t];
+      P.p[t] = p8[t];
+      P.q[t] = q8[t];
+      P.phi[t] = phi8[t];
+    }
+    CK(acr::launch_gen_varcoef(n, P, work, D_sub, D_diag, D_sup, E, F, (cudaStream_t)stream));
+  });
+  return ACR_OK;
+}
+
+int acr_gen_uniform(const unsigned long long* pcg_state4, long long N, int k, double low,
+                    double high, double* out, void* stream) {
+  if (N < 0 || k < 1 || !pcg_state4) return set_err(nullptr, ACR_EARG, "bad arguments");
+  ACR_GUARD(nullptr, {
+    CK(acr::launch_gen_uniform(pcg_state4, N, k, low, high, out, (cudaStream_t)stream));
+  });
+  return ACR_OK;
+}
+
 int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
                         double eps, int max_rank_cap, double* Uo, double* Vo,
                         int* rank_out, void* stream) {

@@ -125,3 +125,34 @@ def test_block_partition_rules():
     assert distributed_levels(2048, 2) == 10
     assert level_bounds(block_partition(2048, 8), 2048, 3) == [32 * r for r in range(8)] + [256]
     assert not distributed_ok(block_partition(2048, 8), 2048, 8)
+
+
+def _pcg64_uniform(state, inc, count, low=-1.0, high=1.0):
+    """Pure-Python PCG64 (XSL-RR 128/64) + next_double, the algorithm the
+    device generator acr_gen_uniform implements."""
+    M = 0x2360ED051FC65DA44385DF649FCCF645
+    MASK = (1 << 128) - 1
+    out = []
+    for _ in range(count):
+        state = (state * M + inc) & MASK
+        x = ((state >> 64) ^ state) & 0xFFFFFFFFFFFFFFFF
+        r = state >> 122
+        x = ((x >> r) | (x << (64 - r))) & 0xFFFFFFFFFFFFFFFF
+        out.append(low + (high - low) * ((x >> 11) * (1.0 / 9007199254740992.0)))
+    return out
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_device_generator_rng_handoff(name):
+    """The host draws of device_config leave numpy's PCG64 at the state whose
+    continuation is make_config's right-hand side (pins the hand-off and the
+    generator algorithm against numpy itself)."""
+    import numpy as np
+    from paper_1604_00617_b200 import problems as PR
+    rng = np.random.default_rng(0)
+    if PR.CONFIGS[name]["kind"] == "varcoef":
+        PR._varcoef_params(rng)
+    st = rng.bit_generator.state["state"]
+    got = _pcg64_uniform(st["state"], st["inc"], 64)
+    ref = PR.make_config(name).rhs[:64]
+    assert np.array_equal(np.array(got), ref)
