@@ -63,7 +63,8 @@ cudaError_t launch_rhs_combine(const double* f, long long fs, const double* a,
 cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
                            const int* rowblk, const int* colblk, double* A,
                            int ld, cudaStream_t st);
-cudaError_t lu_factor(double* A, int N, int* piv, int* info, cudaStream_t st);
+// work: unused (reserved), pass null
+cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work, cudaStream_t st);
 cudaError_t lu_solve(const double* A, int N, const int* piv, double* B,
                      int nrhs, cudaStream_t st);
 cudaError_t launch_rhs_in(const double* rhs, int N, int k, int n, double* P,

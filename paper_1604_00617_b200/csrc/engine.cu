@@ -1348,8 +1348,8 @@ struct Plan {
       CK(cudaMemsetAsync(lu.p, 0, sizeof(double) * (size_t)Nc * Nc, st));
       CK(launch_todense(dt.T, tab.as<HB>(), cntb, drc.as<int>(), drc.as<int>() + cntb,
                         lu.as<double>(), Nc, st));
-      CK(lu_factor(lu.as<double>(), Nc, piv.as<int>(), info.as<int>(), st));
-      launches += 1 + 3 * ((Nc + 31) / 32);
+      CK(lu_factor(lu.as<double>(), Nc, piv.as<int>(), info.as<int>(), nullptr, st));
+      launches += 1 + 4 * ((Nc + 31) / 32);
       int hinfo = 0;
       CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(ev1, st));

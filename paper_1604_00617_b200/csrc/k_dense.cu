@@ -115,15 +115,15 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel(double* A, int N, int j0,
       const double ajc = A[(long long)j * N + c];
       constexpr int ST = LU_PT / 32;
       int i = j + 1 + warp;
-      for (; i + 3 * ST < N; i += 4 * ST) {      // 4 independent rows in flight
-        double l0 = A[(long long)i * N + j], l1 = A[(long long)(i + ST) * N + j];
-        double l2 = A[(long long)(i + 2 * ST) * N + j], l3 = A[(long long)(i + 3 * ST) * N + j];
-        double a0 = A[(long long)i * N + c], a1 = A[(long long)(i + ST) * N + c];
-        double a2 = A[(long long)(i + 2 * ST) * N + c], a3 = A[(long long)(i + 3 * ST) * N + c];
-        A[(long long)i * N + c] = a0 - l0 * ajc;
-        A[(long long)(i + ST) * N + c] = a1 - l1 * ajc;
-        A[(long long)(i + 2 * ST) * N + c] = a2 - l2 * ajc;
-        A[(long long)(i + 3 * ST) * N + c] = a3 - l3 * ajc;
+      for (; i + 7 * ST < N; i += 8 * ST) {      // 8 independent rows in flight
+        double l[8], a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          l[u] = A[(long long)(i + u * ST) * N + j];
+          a[u] = A[(long long)(i + u * ST) * N + c];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) A[(long long)(i + u * ST) * N + c] = a[u] - l[u] * ajc;
       }
       for (; i < N; i += ST) A[(long long)i * N + c] -= A[(long long)i * N + j] * ajc;
     }
@@ -200,11 +200,244 @@ __global__ void __launch_bounds__(256) k_lu_gemm(double* A, int N, int j0, int j
     }
 }
 
-cudaError_t lu_factor(double* A, int N, int* piv, int* info, cudaStream_t st) {
+// Panel j0 (rows j0..N-1, jb columns) factored in sub-panels of LU_SB columns
+// held in shared memory (column-major, ld = rows), right-looking inside the
+// panel: getf2 on the sub-panel (pivot = first index of the largest |a|,
+// whole panel row swapped, scale by 1/pivot, rank-1 updates), then the
+// sub-panel's U row block (unit-lower solve) and the rank-LU_SB update of the
+// panel columns to its right.  piv is absolute; columns outside the panel
+// are swapped afterwards by k_lu_laswp.
+static constexpr int LU_SB = 8;
+
+__device__ __forceinline__ void lu_argmax(double best, int bidx, double* bv, int* bi, int* out,
+                                          int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+  }
+  if (lane == 0) { bv[warp] = best; bi[warp] = bidx; }
+  __syncthreads();
+  if (warp == 0) {
+    best = lane < LU_PT / 32 ? bv[lane] : -2.0;
+    bidx = lane < LU_PT / 32 ? bi[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if (lane == 0) *out = bidx;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(LU_PT) k_lu_panel_blk(double* A, int N, int j0, int jb,
+                                                       int* piv, int* info) {
+  extern __shared__ double S[];                 // LU_SB x Ms, column-major
+  __shared__ double bv[LU_PT / 32];
+  __shared__ int bi[LU_PT / 32];
+  __shared__ int sp;
+  const int tid = threadIdx.x;
+  for (int s0 = 0; s0 < jb; s0 += LU_SB) {
+    const int sb = jb - s0 < LU_SB ? jb - s0 : LU_SB;
+    const int js = j0 + s0, Ms = N - js;
+    for (int idx = tid; idx < Ms * sb; idx += LU_PT) {
+      const int r = idx / sb, c = idx - r * sb;
+      S[c * Ms + r] = A[(long long)(js + r) * N + js + c];
+    }
+    __syncthreads();
+    for (int jj = 0; jj < sb; ++jj) {
+      const double* cj = S + jj * Ms;
+      double best = -1.0;
+      int bidx = jj;
+      for (int i = jj + tid; i < Ms; i += LU_PT) {
+        const double v = fabs(cj[i]);
+        if (v > best) { best = v; bidx = i; }
+      }
+      lu_argmax(best, bidx, bv, bi, &sp, tid);
+      const int p = sp;
+      const double pv = cj[p];
+      if (tid == 0) {
+        piv[js + jj] = js + p;
+        if (pv == 0.0 && *info == 0) *info = js + jj + 1;
+      }
+      __syncthreads();                            // everyone has read the pivot
+      if (p != jj && tid < sb) {                  // sub-panel rows in smem
+        double* cc = S + tid * Ms;
+        const double t = cc[jj];
+        cc[jj] = cc[p];
+        cc[p] = t;
+      }
+      __syncthreads();
+      // scale and rank-1 update fused per row (the row's own multiplier)
+      const double rinv = pv != 0.0 ? 1.0 / pv : 0.0;
+      for (int i = jj + 1 + tid; i < Ms; i += LU_PT) {
+        double* cw = S + jj * Ms;
+        const double l = pv != 0.0 ? cw[i] * rinv : cw[i];
+        cw[i] = l;
+        for (int c = jj + 1; c < sb; ++c) {
+          double* cc = S + c * Ms;
+          cc[i] = cc[i] - l * cc[jj];
+        }
+      }
+      __syncthreads();
+    }
+    // the sub-panel's row interchanges on the other panel columns: touched
+    // rows (<= 2 LU_SB) staged in shared memory, swaps replayed, written back
+    {
+      __shared__ int rws[2 * LU_SB], sa[LU_SB], sbb[LU_SB], nrw;
+      __shared__ double tile[2 * LU_SB][LU_NB];
+      if (tid == 0) {
+        int cnt = 0;
+        for (int k = 0; k < sb; ++k) {
+          const int r1 = js + k, r2 = piv[js + k];
+          int q1 = -1, q2 = -1;
+          for (int q = 0; q < cnt; ++q) {
+            if (rws[q] == r1) q1 = q;
+            if (rws[q] == r2) q2 = q;
+          }
+          if (q1 < 0) { rws[cnt] = r1; q1 = cnt++; }
+          if (q2 < 0) { if (r2 == r1) q2 = q1; else { rws[cnt] = r2; q2 = cnt++; } }
+          sa[k] = q1;
+          sbb[k] = q2;
+        }
+        nrw = cnt;
+      }
+      __syncthreads();
+      const int ncol = jb - sb;                   // panel columns outside the sub-panel
+      for (int idx = tid; idx < nrw * ncol; idx += LU_PT) {
+        const int q = idx / ncol, k = idx - q * ncol;
+        const int c = j0 + (k < s0 ? k : k + sb);
+        tile[q][k] = A[(long long)rws[q] * N + c];
+      }
+      __syncthreads();
+      if (tid < ncol)
+        for (int k = 0; k < sb; ++k) {
+          const double t = tile[sa[k]][tid];
+          tile[sa[k]][tid] = tile[sbb[k]][tid];
+          tile[sbb[k]][tid] = t;
+        }
+      __syncthreads();
+      for (int idx = tid; idx < nrw * ncol; idx += LU_PT) {
+        const int q = idx / ncol, k = idx - q * ncol;
+        const int c = j0 + (k < s0 ? k : k + sb);
+        A[(long long)rws[q] * N + c] = tile[q][k];
+      }
+    }
+    for (int idx = tid; idx < Ms * sb; idx += LU_PT) {
+      const int r = idx / sb, c = idx - r * sb;
+      A[(long long)(js + r) * N + js + c] = S[c * Ms + r];
+    }
+    const int c0 = js + sb, nr = j0 + jb - c0;   // panel columns to the right
+    if (nr > 0) {
+      // U12 = L11^{-1} A12 (unit lower), one thread per column
+      if (tid < nr) {
+        const int c = c0 + tid;
+        double x[LU_SB];
+#pragma unroll
+        for (int k = 0; k < LU_SB; ++k) {
+          if (k < sb) {
+            double v = A[(long long)(js + k) * N + c];
+            for (int q = 0; q < k; ++q) v -= S[q * Ms + k] * x[q];
+            x[k] = v;
+            A[(long long)(js + k) * N + c] = v;
+          }
+        }
+      }
+      __syncthreads();
+      // A22 -= L21 U12 for the panel columns to the right
+      for (int idx = tid; idx < (Ms - sb) * nr; idx += LU_PT) {
+        const int r = sb + idx / nr, c = c0 + idx % nr;
+        double v = A[(long long)(js + r) * N + c];
+        for (int k = 0; k < sb; ++k) v -= S[k * Ms + r] * A[(long long)(js + k) * N + c];
+        A[(long long)(js + r) * N + c] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Row interchanges of panel j0 applied to every column outside it (laswp):
+// a CTA stages the <= 2 jb touched rows of its 32 columns in shared memory,
+// replays the swaps there (thread per column) and writes the rows back.
+__global__ void k_lu_laswp(double* A, int N, int j0, int jb, const int* piv) {
+  __shared__ double t[2 * LU_NB][33];
+  __shared__ int rows[2 * LU_NB], sa[LU_NB], sb[LU_NB], nrows;
+  // slots 0..jb-1: rows j0..j0+jb-1; pivot rows below the panel get extra
+  // slots in first-occurrence order (parallel over k)
+  __shared__ int extra[LU_NB];
+  const int tl = threadIdx.y * 32 + threadIdx.x;
+  if (tl < jb) {
+    const int pr = piv[j0 + tl];
+    int first = 1;
+    if (pr >= j0 + jb)
+      for (int q = 0; q < tl; ++q)
+        if (piv[j0 + q] == pr) { first = 0; break; }
+    extra[tl] = (pr >= j0 + jb && first) ? 1 : 0;
+    rows[tl] = j0 + tl;
+  }
+  __syncthreads();
+  if (tl < jb) {
+    const int pr = piv[j0 + tl];
+    sa[tl] = tl;
+    if (pr < j0 + jb) {
+      sb[tl] = pr - j0;
+    } else {
+      int q0 = tl;                                // first occurrence of pr
+      for (int q = 0; q < tl; ++q)
+        if (piv[j0 + q] == pr) { q0 = q; break; }
+      int pos = jb;
+      for (int q = 0; q < q0; ++q) pos += extra[q];
+      sb[tl] = pos;
+      if (q0 == tl) rows[pos] = pr;
+    }
+  }
+  if (tl == 0) {
+    int cnt = jb;
+    for (int q = 0; q < jb; ++q) cnt += extra[q];
+    nrows = cnt;
+  }
+  __syncthreads();
+  // columns of this CTA: [0, j0) and [j0 + jb, N) enumerated contiguously
+  int c = blockIdx.x * 32 + threadIdx.x;
+  if (c >= j0) c += jb;
+  const bool okc = c < N;
+  for (int q = threadIdx.y; q < nrows; q += blockDim.y)
+    t[q][threadIdx.x] = okc ? A[(long long)rows[q] * N + c] : 0.0;
+  __syncthreads();
+  if (threadIdx.y == 0 && okc)
+    for (int k = 0; k < jb; ++k) {
+      const double x = t[sa[k]][threadIdx.x];
+      t[sa[k]][threadIdx.x] = t[sb[k]][threadIdx.x];
+      t[sb[k]][threadIdx.x] = x;
+    }
+  __syncthreads();
+  for (int q = threadIdx.y; q < nrows; q += blockDim.y)
+    if (okc) A[(long long)rows[q] * N + c] = t[q][threadIdx.x];
+}
+
+cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work,
+                      cudaStream_t st) {
+  (void)work;
   cudaMemsetAsync(info, 0, sizeof(int), st);
   for (int j0 = 0; j0 < N; j0 += LU_NB) {
     int jb = N - j0 < LU_NB ? N - j0 : LU_NB;
-    k_lu_panel<<<1, LU_PT, 0, st>>>(A, N, j0, jb, piv, info);
+    const size_t sbytes = (size_t)LU_SB * (N - j0) * sizeof(double);
+    if (sbytes <= 200 * 1024) {   // sub-panels in shared memory
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_lu_panel_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+      }
+      k_lu_panel_blk<<<1, LU_PT, sbytes, st>>>(A, N, j0, jb, piv, info);
+      if (N - jb > 0) k_lu_laswp<<<(N - jb + 31) / 32, dim3(32, 8), 0, st>>>(A, N, j0, jb, piv);
+    } else {
+      k_lu_panel<<<1, LU_PT, 0, st>>>(A, N, j0, jb, piv, info);
+    }
     int rest = N - j0 - jb;
     if (rest > 0) {
       k_lu_trsm<<<(rest + 63) / 64, 64, 0, st>>>(A, N, j0, jb);
