@@ -243,11 +243,19 @@ def run_ours(args):
     d2h = u_h.numel() * 8
     e2e_steps = max(1, min(args.steps, 3))
 
+    copy_stream = torch.cuda.Stream()
+
     def e2e_step():
         for d, h in zip(dev, host):
             d.copy_(h, non_blocking=True)
-        rhs_d.copy_(rhs_h, non_blocking=True)
+        # the right-hand sides are only read by the solve: their upload runs on
+        # a copy stream concurrently with the factorisation (after the
+        # previous step's solve has consumed rhs_d)
+        copy_stream.wait_stream(stream)
+        with torch.cuda.stream(copy_stream):
+            rhs_d.copy_(rhs_h, non_blocking=True)
         solver.factor(dev)
+        stream.wait_stream(copy_stream)
         uu = solver.solve(rhs_d) if ws == 1 else solver.solve(rhs_d, u_d)
         u_h.copy_(uu, non_blocking=True)
         return uu
