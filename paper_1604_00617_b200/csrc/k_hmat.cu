@@ -465,7 +465,9 @@ struct GPJobs2 {
   GPJob j[2];
 };
 
-__global__ void __launch_bounds__(HT) k_gp(TreeDev T, GPJobs2 JJ, const int* nodes) {
+// GT threads: 256 for small (latency-bound) grids, 128 for large ones
+template <int GT>
+__global__ void __launch_bounds__(GT) k_gp(TreeDev T, GPJobs2 JJ, const int* nodes) {
   extern __shared__ double K[];
   const GPJob& J = JJ.j[blockIdx.z];
   const int g = blockIdx.y, n = T.n;
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(HT) k_gp(TreeDev T, GPJobs2 JJ, const int* nod
   const int r1 = J.hx ? mid : lo, l1 = J.hx ? hi - mid : mid - lo;
   const int r2 = J.hw ? mid : lo, l2 = J.hw ? hi - mid : mid - lo;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int p = warp; p < rx * ry; p += HT / 32) {
+  for (int p = warp; p < rx * ry; p += GT / 32) {
     int a = p / ry, b = p - a * ry;
     const double* xa = src_col(J.X, n, g, slot, a) + r1;
     const double* yb = src_col(J.Y, n, g, slot, b) + r1;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(HT) k_gp(TreeDev T, GPJobs2 JJ, const int* nod
   }
   __syncthreads();
   // thread per output row: W[i][:] loaded once, all ry outputs of the row
-  for (int i = threadIdx.x; i < l2; i += HT) {
+  for (int i = threadIdx.x; i < l2; i += GT) {
     double w[32];
     for (int a0 = 0; a0 < rx; a0 += 32) {
       const int na = rx - a0 < 32 ? rx - a0 : 32;
@@ -522,12 +524,15 @@ cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
   size_t smem = (size_t)kcap * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_gp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(k_gp<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr = true;
   }
   dim3 g(nnodes, nelem, njobs);
-  k_gp<<<g, HT, smem, st>>>(T, JJ, nodes);
+  if ((long long)nnodes * nelem * njobs < 148LL * 4) k_gp<256><<<g, 256, smem, st>>>(T, JJ, nodes);
+  else k_gp<128><<<g, 128, smem, st>>>(T, JJ, nodes);
   return cudaGetLastError();
 }
 

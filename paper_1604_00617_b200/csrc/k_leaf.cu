@@ -14,7 +14,7 @@
 
 namespace acr {
 
-static constexpr int LT = 128;
+static constexpr int LT = 256;
 
 // ---------------------------------------------------------------------------
 // leaf inverse: in-place Gauss-Jordan with row partial pivoting (the pivot
@@ -492,21 +492,46 @@ __global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
   const int slot = T.depth[node];
   const double* U = src_col(Us, n, g, slot, 0) + lo;
   const double* V = src_col(Vs, n, g, slot, 0) + lo;
-  // stage the leaf rows of U and V (r columns) once: u[c][i], v[c][j]
+  // stage the leaf rows of U and V (r columns) once: u[c][i], v[c][j];
+  // loads issued in batches of 4 before their shared-memory stores
   double* u = sm;
   double* v = u + r * s;
-  for (int idx = tid; idx < r * s; idx += LT) {
-    const int c = idx / s, i = idx - c * s;
-    u[idx] = U[(long long)c * n + i];
-    v[idx] = V[(long long)c * n + i];
+  for (int base = tid; base < r * s; base += 4 * LT) {
+    double a[4], b[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = base + q * LT;
+      const int c = idx / s, i = idx - c * s;
+      a[q] = idx < r * s ? U[(long long)c * n + i] : 0.0;
+      b[q] = idx < r * s ? V[(long long)c * n + i] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = base + q * LT;
+      if (idx < r * s) { u[idx] = a[q]; v[idx] = b[q]; }
+    }
   }
   __syncthreads();
+  // leaf += u v^T: 8 leaf entries per thread in flight (same sum order)
   double* L = H[g].leaf + (long long)lo * bw;
-  for (int idx = tid; idx < s * s; idx += LT) {
-    int i = idx / s, j = idx - i * s;
-    double z = 0.0;
-    for (int c = 0; c < r; ++c) z += u[c * s + i] * v[c * s + j];
-    L[(long long)i * bw + j] = L[(long long)i * bw + j] + z;
+  for (int base = tid; base < s * s; base += 8 * LT) {
+    double lv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = base + q * LT;
+      const int i = idx / s, j = idx - i * s;
+      lv[q] = idx < s * s ? L[(long long)i * bw + j] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = base + q * LT;
+      if (idx < s * s) {
+        const int i = idx / s, j = idx - i * s;
+        double z = 0.0;
+        for (int c = 0; c < r; ++c) z += u[c * s + i] * v[c * s + j];
+        L[(long long)i * bw + j] = lv[q] + z;
+      }
+    }
   }
 }
 
