@@ -126,14 +126,14 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
 // (first index of the largest |a_ik|, getrf's rule) while the other warps
 // still update, and publishes it with the step's single barrier.  Singular /
 // non-finite detection as the reference's LAPACK call (algebra.py:199-207).
-template <int TG>
+template <int TG, int TL, unsigned MASK>
 __device__ __forceinline__ void gj_pivot(const double* m, int LD, int col, int k0, int s,
                                          int ty, bool owner, int* out) {
   double best = -1.0;
   int p = k0;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int i = ty * 4 + a;
+  for (int a = 0; a < TL; ++a) {
+    const int i = ty * TL + a;
     if (i >= k0 && i < s) {
       const double v = fabs(m[i * LD + col]);
       if (v > best) { best = v; p = i; }
@@ -141,35 +141,38 @@ __device__ __forceinline__ void gj_pivot(const double* m, int LD, int col, int k
   }
 #pragma unroll
   for (int o = TG / 2; o; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, p, o);
+    const double ov = __shfl_xor_sync(MASK, best, o);
+    const int oi = __shfl_xor_sync(MASK, p, o);
     if (ov > best || (ov == best && oi < p)) { best = ov; p = oi; }
   }
   if (owner && ty == 0) *out = p;
 }
 
-template <int S>
-__global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, const HB* H,
-                                                                  int leaf, int* sing) {
-  constexpr int TG = S / 4, LD = S + 1;
+// TL x TL register tiles (the arithmetic per element does not depend on TL).
+template <int S, int TL>
+__global__ void __launch_bounds__((S / TL) * (S / TL)) k_leafinv_reg(TreeDev T, const HB* H,
+                                                                    int leaf, int* sing) {
+  constexpr int TG = S / TL, LD = S + 1;
+  constexpr int NT = TG * TG;
+  constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : (1u << NT) - 1u;
   extern __shared__ double buf[];              // [2][S][LD]
   __shared__ int piv[S + 1], inv_[S];
   const int g = blockIdx.x, tid = threadIdx.x;
   const int tx = tid / TG, ty = tid - tx * TG;   // column group, row group
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
   double* L = H[g].leaf + (long long)lo * bw;
-  double x[4][4];
+  double x[TL][TL];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < TL; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int r = ty * 4 + a, c = tx * 4 + b;
+    for (int b = 0; b < TL; ++b) {
+      const int r = ty * TL + a, c = tx * TL + b;
       x[a][b] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
       buf[r * LD + c] = x[a][b];
     }
   // the whole warp holding column group 0 joins the shuffles (groups of TG lanes)
-  __syncwarp();
-  if (tid < 32) gj_pivot<TG>(buf, LD, 0, 0, s, ty, tx == 0, &piv[0]);
+  __syncwarp(MASK);
+  if (tid < 32) gj_pivot<TG, TL, MASK>(buf, LD, 0, 0, s, ty, tx == 0, &piv[0]);
   bool bad = false;
   for (int k = 0; k < s; ++k) {
     const double* cur = buf + (k & 1) * S * LD;
@@ -179,36 +182,36 @@ __global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, co
     const double pv = cur[p * LD + k];
     if (pv == 0.0) { bad = true; break; }     // uniform: every thread sees the same
     const double inv = 1.0 / pv;
-    double rk[4], ok[4];
+    double rk[TL], ok[TL];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int c = tx * 4 + b;
+    for (int b = 0; b < TL; ++b) {
+      const int c = tx * TL + b;
       rk[b] = (c == k) ? inv : cur[p * LD + c] * inv;   // new row k = old row p / pv
       ok[b] = cur[k * LD + c];                           // old row k -> row p
     }
     const double fk = cur[k * LD + k];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = ty * 4 + a;
+    for (int a = 0; a < TL; ++a) {
+      const int r = ty * TL + a;
       if (r == k) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) x[a][b] = rk[b];
+        for (int b = 0; b < TL; ++b) x[a][b] = rk[b];
       } else {
         const bool isp = (r == p);
         const double f = isp ? fk : cur[r * LD + k];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int c = tx * 4 + b;
+        for (int b = 0; b < TL; ++b) {
+          const int c = tx * TL + b;
           const double src = isp ? ok[b] : x[a][b];
           x[a][b] = (c == k) ? -f * inv : src - f * rk[b];
         }
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) nxt[r * LD + tx * 4 + b] = x[a][b];
+      for (int b = 0; b < TL; ++b) nxt[r * LD + tx * TL + b] = x[a][b];
     }
-    if (k + 1 < s && (tid >> 5) == (((k + 1) >> 2) * TG) >> 5) {
-      __syncwarp();
-      gj_pivot<TG>(nxt, LD, k + 1, k + 1, s, ty, tx == (k + 1) >> 2, &piv[k + 1]);
+    if (k + 1 < s && (tid >> 5) == (((k + 1) / TL) * TG) >> 5) {
+      __syncwarp(MASK);
+      gj_pivot<TG, TL, MASK>(nxt, LD, k + 1, k + 1, s, ty, tx == (k + 1) / TL, &piv[k + 1]);
     }
   }
   if (bad) {
@@ -235,10 +238,10 @@ __global__ void __launch_bounds__((S / 4) * (S / 4)) k_leafinv_reg(TreeDev T, co
   __syncthreads();
   int nf = 0;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < TL; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int r = ty * 4 + a, c = tx * 4 + b;
+    for (int b = 0; b < TL; ++b) {
+      const int r = ty * TL + a, c = tx * TL + b;
       if (r < s && c < s) {
         if (!isfinite(x[a][b])) nf = 1;
         L[(long long)r * bw + inv_[c]] = x[a][b];
@@ -258,11 +261,13 @@ static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int lea
   const size_t smem = 2ull * S * (S + 1) * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_leafinv_reg<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_leafinv_reg<S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  k_leafinv_reg<S><<<nelem, (S / 4) * (S / 4), smem, st>>>(T, H, leaf, sing);
+  // TL = 2 (4x the threads per matrix) measured no faster for single-matrix
+  // launches: a pivot step is bound by its dependency chain, not by issue
+  k_leafinv_reg<S, 4><<<nelem, (S / 4) * (S / 4), smem, st>>>(T, H, leaf, sing);
   return cudaGetLastError();
 }
 
