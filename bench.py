@@ -303,12 +303,22 @@ def run_ours(args):
     avg_ms = tr["ms"] / max(tr["launches"], 1)
     per_launch_bytes = tr["bytes"] / max(tr["launches"], 1)
     achieved = per_launch_bytes / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
+    traffic = None
+    try:
+        dr = json.load(open(os.path.join(REPO, "profiles", "r01_trunc_dram.json")))
+        if cfg == "cfg5" and ws == 1:
+            traffic = dr["dram_bytes_total"] / max(tr["launches"], 1)
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {
         "kernel": "k_trunc (batched QR+Jacobi-SVD recompression)",
         "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
         "frac": achieved / hbm_peak,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": "profiles/r01_trunc_dram.json (ncu dram__bytes_read+write over every "
+                          "k_trunc launch of one config-5 factor, per instrumented launch)"
+        if traffic is not None else None,
         "algorithmic_bytes_per_launch": per_launch_bytes,
         "avg_launch_ms": avg_ms,
         "fp64_gflops_achieved": (tr["flops"] / max(tr["launches"], 1)) / (avg_ms / 1e3) / 1e9
