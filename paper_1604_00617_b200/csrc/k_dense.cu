@@ -473,10 +473,112 @@ __global__ void __launch_bounds__(1024) k_lu_solve(const double* A, int N,
   }
 }
 
+// Blocked substitution for one right-hand side per CTA, the column in shared
+// memory: row interchanges replayed in shared memory, then 32-row blocks --
+// warp 0 solves the diagonal block from a staged tile, all threads apply the
+// block to the remaining rows.  Every row subtracts its terms in the same
+// order as k_lu_solve (ascending j forward, descending j backward), so the
+// result is identical.
+static constexpr int LS_T = 1024;
+
+__global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, int N, const int* piv,
+                                                      double* B) {
+  extern __shared__ double y[];                 // N doubles, then N ints
+  int* pv = reinterpret_cast<int*>(y + N);
+  __shared__ double T[32][33];
+  double* b = B + (long long)blockIdx.x * N;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < N; i += LS_T) { y[i] = b[i]; pv[i] = piv[i]; }
+  __syncthreads();
+  if (tid == 0)
+    for (int j = 0; j < N; ++j) {
+      const int p = pv[j];
+      if (p != j) { const double t = y[j]; y[j] = y[p]; y[p] = t; }
+    }
+  __syncthreads();
+  // forward: unit lower L
+  for (int b0 = 0; b0 < N; b0 += 32) {
+    const int bs = N - b0 < 32 ? N - b0 : 32;
+    for (int idx = tid; idx < bs * bs; idx += LS_T) {
+      const int r = idx / bs, c = idx - r * bs;
+      T[r][c] = A[(long long)(b0 + r) * N + b0 + c];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double v = lane < bs ? y[b0 + lane] : 0.0;
+      for (int k = 0; k < bs; ++k) {
+        const double yk = __shfl_sync(0xffffffffu, v, k);
+        if (lane > k && lane < bs) v -= T[lane][k] * yk;
+      }
+      if (lane < bs) y[b0 + lane] = v;
+    }
+    __syncthreads();
+    for (int i = b0 + bs + tid; i < N; i += LS_T) {
+      const double* ar = A + (long long)i * N + b0;
+      double v = y[i];
+      for (int kb = 0; kb < bs; kb += 8) {       // 8 loads in flight, order kept
+        double a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = kb + u < bs ? ar[kb + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (kb + u < bs) v -= a[u] * y[b0 + kb + u];
+      }
+      y[i] = v;
+    }
+    __syncthreads();
+  }
+  // backward: upper U (non-unit diagonal), blocks from the bottom
+  for (int b0 = ((N - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
+    const int bs = N - b0 < 32 ? N - b0 : 32;
+    for (int idx = tid; idx < bs * bs; idx += LS_T) {
+      const int r = idx / bs, c = idx - r * bs;
+      T[r][c] = A[(long long)(b0 + r) * N + b0 + c];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double v = lane < bs ? y[b0 + lane] : 0.0;
+      for (int k = bs - 1; k >= 0; --k) {
+        if (lane == k) v = v / T[k][k];
+        const double yk = __shfl_sync(0xffffffffu, v, k);
+        if (lane < k) v -= T[lane][k] * yk;
+      }
+      if (lane < bs) y[b0 + lane] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < b0; i += LS_T) {
+      const double* ar = A + (long long)i * N + b0;
+      double v = y[i];
+      for (int kb = bs - 1; kb >= 0; kb -= 8) {  // descending, 8 loads in flight
+        double a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = kb - u >= 0 ? ar[kb - u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (kb - u >= 0) v -= a[u] * y[b0 + kb - u];
+      }
+      y[i] = v;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < N; i += LS_T) b[i] = y[i];
+}
+
 cudaError_t lu_solve(const double* A, int N, const int* piv, double* B,
                      int nrhs, cudaStream_t st) {
   if (!nrhs) return cudaSuccess;
-  k_lu_solve<<<nrhs, 1024, 0, st>>>(A, N, piv, B);
+  const size_t smem = (size_t)N * (sizeof(double) + sizeof(int));
+  if (smem <= 160 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_lu_solve_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
+      attr = true;
+    }
+    k_lu_solve_blk<<<nrhs, LS_T, smem, st>>>(A, N, piv, B);
+  } else {
+    k_lu_solve<<<nrhs, 1024, 0, st>>>(A, N, piv, B);
+  }
   return cudaGetLastError();
 }
 
