@@ -841,6 +841,7 @@ struct Plan {
     double *P1, *P2, *P3, *tb;
     long long ps;
     int* sing;
+    bool pend = false;   // S's off-diagonal recompressions still running on the side stream
   };
 
   void invert(const HB* H, int G, int R, int* sing) {
@@ -858,6 +859,16 @@ struct Plan {
     c.tb = scratch<double>(9, (size_t)G * maxA * R * R);
     c.sing = sing;
     inv_node(c, 0);
+    settle(c);
+  }
+
+  // the side-stream recompressions of a Schur complement must finish before
+  // anything reads its off-diagonal factors (only leaf inverses may overlap)
+  void settle(InvCtx& c) {
+    if (c.pend) {
+      join(side());
+      c.pend = false;
+    }
   }
 
   void inv_hmat(InvCtx& c, int mu, bool second) {
@@ -935,6 +946,7 @@ struct Plan {
     const Src P2 = s_pan(c.P2, c.ps * c.R, c.R);
     const Src P3 = s_pan(c.P3, c.ps * c.R, c.R);
     inv_node(c, a0);                                   // x11
+    settle(c);
     inv_hmat(c, a0, false);                            // T, Hh
     {
       GPJob j;                                          // W = -U21 (V21^T T)
@@ -948,9 +960,29 @@ struct Plan {
       ++launches;
     }
     const cudaStream_t s2 = side();
-    inv_lowrank(c, nu, a1, P3, s_hbV(c.H), 0, s2);     // S = H22 + W V12^T
-    join(s2);
+    {                                                  // S = H22 + W V12^T
+      // leaves on the main stream, off-diagonal combines on the side stream:
+      // the first leaf inverse of sinv below overlaps the recompressions
+      CK(launch_leaflr_n(dt.T, c.H, c.G, a1, ht.nleaves_under(a1), P3, s_hbV(c.H),
+                         r_hb(c.H), nu, 0, st));
+      ++launches;
+      const int t0 = ht.startA[a1], t1 = ht.startA[a1 + 1];
+      if (t1 > t0) {
+        fork(s2);
+        TruncArgs a;
+        memset(&a, 0, sizeof(a));
+        a.mode = TM_COMBINE;
+        a.a = op_own(s_hbU(c.H), s_hbV(c.H), r_hb(c.H));
+        a.b = op_own(P3, s_hbV(c.H), r_hb(c.H));
+        a.b.sel = SEL_FIXED;
+        a.b.node = nu;
+        a.b.fside = 0;
+        run_trunc(a, t0, t1, c.H, c.G, c.R, c.R, s2);
+        c.pend = s2 != st;
+      }
+    }
     inv_node(c, a1);                                   // sinv
+    settle(c);
     inv_hmat(c, a1, true);                             // Z, S2
     {
       GPJob j;                                          // G = T (V12^T Z)
