@@ -278,3 +278,45 @@ def test_cta_pair_recompression_path(solver_mod):
     z = load_npz("cfg2.npz")
     res = O.relative_residual(s, out[1])
     assert res <= 2 * float(z["residual"]) + 1e-15
+
+
+def test_config2_reversed_bitwise(solver_mod):
+    """inversion_order only permutes independent block inversions
+    (reduction.py:193-201): bitwise identical at config-2 scale too."""
+    c = P.CONFIGS["cfg2"]
+    s = P.make_config("cfg2")
+    a, _ = solver_mod.acr_solve(s, Tolerance(c["eps"]), leaf_size=c["leaf"],
+                                inversion_order="forward")
+    b, _ = solver_mod.acr_solve(s, Tolerance(c["eps"]), leaf_size=c["leaf"],
+                                inversion_order="reversed")
+    np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("cutoff,cap", [(4, None), (1, 3), (3, 5)])
+def test_cutoff_and_rank_cap_against_oracle(solver_mod, cutoff, cap):
+    """Dense cutoff of several blocks (reduction.py:305-310) and the rank cap
+    (hodlr.py:196-197) on a variable-coefficient problem, against the oracle."""
+    s = P.varcoef_diffusion(48, seed=7)
+    tol = Tolerance(1e-8, max_rank_cap=cap)
+    u, rep = solver_mod.acr_solve(s, tol, cutoff_blocks=cutoff, leaf_size=8)
+    uo, ro = O.acr_solve(s, tol, cutoff_blocks=cutoff, leaf_size=8)
+    assert rep.levels == ro.levels and rep.cutoff_blocks == ro.cutoff_blocks
+    assert rep.max_rank == ro.max_rank
+    if cap is not None:
+        assert rep.max_rank <= cap
+    assert _rel(u, uo) <= 1e-9
+    assert rep.residual <= 2 * O.relative_residual(s, uo) + 1e-15
+
+
+def test_multi_rhs_columns_match_single_solves(solver_mod):
+    """A k-column solve equals k single-column solves against the same
+    factorisation (the solve is column-independent)."""
+    c = P.CONFIGS["cfg2"]
+    s = P.make_config("cfg2", nrhs=3)
+    sol = solver_mod.AcrSolver(s.n_blocks, s.block_dim, Tolerance(c["eps"]), 1, c["leaf"])
+    sol.factor(sol.device_bands(s))
+    f = torch.as_tensor(s.rhs, device="cuda")
+    u3 = sol.solve(f).cpu().numpy()
+    for j in range(3):
+        uj = sol.solve(f[:, j].contiguous()).cpu().numpy()
+        assert _rel(u3[:, j], uj) <= 1e-13
