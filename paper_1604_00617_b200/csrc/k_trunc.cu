@@ -28,6 +28,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   __syncthreads();
@@ -35,7 +36,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < NWB; ++w) s += red[w];   // fixed order
+  for (int w = 0; w < (NT / 32); ++w) s += red[w];   // fixed order
   return s;
 }
 
@@ -178,72 +179,6 @@ __device__ void group_form_q(double* W, int mr, int p, const double* tau, const 
   }
 }
 
-// Householder QR of W (mr x R, column-major, ld = mr), in place.  On exit
-// the upper trapezoid holds R, below-diagonal the reflector tails, tau[j].
-__device__ void block_qr(double* W, int mr, int R, double* tau, double* red,
-                         double* bc) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int p = mr < R ? mr : R;
-  for (int j = 0; j < p; ++j) {
-    double* cj = W + (long long)j * mr;
-    double ss = 0.0;
-    for (int i = j + 1 + tid; i < mr; i += TT) ss += cj[i] * cj[i];
-    ss = block_sum(ss, red);
-    if (tid == 0) {
-      double alpha = cj[j];
-      double tj = 0.0, scal = 0.0;
-      if (ss != 0.0) {
-        double xnorm = sqrt(ss);
-        double beta = -copysign(hypot(alpha, xnorm), alpha);
-        tj = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-        cj[j] = beta;
-      }
-      tau[j] = tj;
-      bc[0] = scal;
-    }
-    __syncthreads();
-    const double tj = tau[j];
-    if (tj != 0.0) {
-      const double scal = bc[0];
-      for (int i = j + 1 + tid; i < mr; i += TT) cj[i] *= scal;
-      __syncthreads();
-      for (int c = j + 1 + warp; c < R; c += TT / 32) {
-        double* cc = W + (long long)c * mr;
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < mr; i += 32) w += cj[i] * cc[i];
-        w = warp_sum(w) + cc[j];
-        w *= tj;
-        if (lane == 0) cc[j] -= w;
-        for (int i = j + 1 + lane; i < mr; i += 32) cc[i] -= w * cj[i];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// X (mr x nc, ld mr) := Q X where Q = H_0 ... H_{p-1} from block_qr.
-__device__ void block_apply_q(const double* W, int mr, int p, const double* tau,
-                              double* X, int nc) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = p - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj != 0.0) {
-      const double* v = W + (long long)j * mr;
-      for (int c = warp; c < nc; c += TT / 32) {
-        double* xc = X + (long long)c * mr;
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < mr; i += 32) w += v[i] * xc[i];
-        w = (warp_sum(w) + xc[j]) * tj;
-        if (lane == 0) xc[j] -= w;
-        for (int i = j + 1 + lane; i < mr; i += 32) xc[i] -= w * v[i];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Round-robin (circle method) pairing of np players (np even).
 __device__ __forceinline__ int rr_player(int step, int x, int np) {
   if (x == 0) return 0;
   int t = x - 1 + step;              // < 2 (np - 1): one conditional wrap
@@ -254,27 +189,28 @@ __device__ __forceinline__ int rr_player(int step, int x, int np) {
 // One-sided Jacobi on B (pr x pc, column-major ld pr) accumulating J (pc x pc).
 // The disjoint pairs of one round-robin step are spread over lane groups of
 // size gs (power of two) across the whole CTA.
+template <int NT>
 __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
   const int tid = threadIdx.x;
-  for (int i = tid; i < pc * pc; i += TT) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
+  for (int i = tid; i < pc * pc; i += NT) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
   __syncthreads();
   if (pc < 2) return 0;
   const int np = pc + (pc & 1), npairs = np / 2;
   int gs = 32;
-  while (gs > 1 && gs * npairs > TT) gs >>= 1;
-  const int per = TT / gs;
+  while (gs > 1 && gs * npairs > NT) gs >>= 1;
+  const int per = NT / gs;
   const int sub = tid & (gs - 1), grp = tid / gs;
   const double tol = sqrt((double)pr) * 2.220446049250313e-16;
   // columns below eps64 * |B|_F cannot move any singular value that a
   // relative threshold >= 1e-14 keeps: rotations involving them are skipped
   double nb = 0.0;
-  for (int i = tid; i < pr * pc; i += TT) nb += B[i] * B[i];
-  __shared__ double s_nb[NWB];
+  for (int i = tid; i < pr * pc; i += NT) nb += B[i] * B[i];
+  __shared__ double s_nb[(NT / 32)];
   nb = warp_sum(nb);
   if ((tid & 31) == 0) s_nb[tid >> 5] = nb;
   __syncthreads();
   nb = 0.0;
-  for (int w = 0; w < NWB; ++w) nb += s_nb[w];
+  for (int w = 0; w < (NT / 32); ++w) nb += s_nb[w];
   const double tiny = nb * 4.930380657631324e-32;   // (eps64 |B|_F)^2
   (void)flag;
   for (int sweep = 0; sweep < 40; ++sweep) {
@@ -334,14 +270,15 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
   return 40;
 }
 
+template <int NT>
 __device__ void copy_factor(const OpRes& s, double* Uo, double* Vo, int um,
                             int vm, int n, int r) {
   if (s.U == Uo && s.V == Vo && s.sc == 1.0) return;
-  for (int idx = threadIdx.x; idx < um * r; idx += TT) {
+  for (int idx = threadIdx.x; idx < um * r; idx += NT) {
     int c = idx / um, i = idx - c * um;
     Uo[(long long)c * n + i] = s.sc * s.U[(long long)c * n + i];
   }
-  for (int idx = threadIdx.x; idx < vm * r; idx += TT) {
+  for (int idx = threadIdx.x; idx < vm * r; idx += NT) {
     int c = idx / vm, i = idx - c * vm;
     Vo[(long long)c * n + i] = s.V[(long long)c * n + i];
   }
@@ -407,6 +344,7 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane);
 // ---------------------------------------------------------------------------
 // block path (one CTA per queued task; used for tasks too large for a warp)
 // ---------------------------------------------------------------------------
+template <int NT>
 __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
                                  double* red, int* iflag) {
   const int tid = threadIdx.x, n = A.T.n;
@@ -432,21 +370,21 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   long long ph[6] = {0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
 #define ACR_PH(i) do { if (A.ctr) { long long t_ = clock64(); ph[i] += t_ - t_ph; t_ph = t_; } } while (0)
-  for (int idx = tid; idx < um * R; idx += TT) {
+  for (int idx = tid; idx < um * R; idx += NT) {
     int c = idx / um, i = idx - c * um;
     Uw[idx] = c < a.r ? a.sc * a.U[(long long)c * n + i]
                       : b.sc * b.U[(long long)(c - a.r) * n + i];
   }
-  for (int idx = tid; idx < vm * R; idx += TT) {
+  for (int idx = tid; idx < vm * R; idx += NT) {
     int c = idx / vm, i = idx - c * vm;
     Vw[idx] = c < a.r ? a.V[(long long)c * n + i] : b.V[(long long)(c - a.r) * n + i];
   }
   __syncthreads();
   ACR_PH(0);
   {
-    const int half = tid >= TT / 2 ? 1 : 0;
-    const int t = tid - half * (TT / 2);
-    Grp g{1 + half, TT / 2, t, NWB / 2, t >> 5, tid & 31, red + half * (NWB / 2),
+    const int half = tid >= NT / 2 ? 1 : 0;
+    const int t = tid - half * (NT / 2);
+    Grp g{1 + half, NT / 2, t, (NT / 32) / 2, t >> 5, tid & 31, red + half * ((NT / 32) / 2),
           nullptr};
     if (!half) group_qr(Uw, um, R, tauU, g);
     else group_qr(Vw, vm, R, tauV, g);
@@ -456,21 +394,21 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
 
   // Frobenius norms of the triangular factors (hodlr.py:191-192)
   double nu2 = 0.0, nv2 = 0.0;
-  for (int idx = tid; idx < pu * R; idx += TT) {
+  for (int idx = tid; idx < pu * R; idx += NT) {
     int l = idx / pu, i = idx - l * pu;
     if (l >= i) { double x = Uw[(long long)l * um + i]; nu2 += x * x; }
   }
-  for (int idx = tid; idx < pv * R; idx += TT) {
+  for (int idx = tid; idx < pv * R; idx += NT) {
     int l = idx / pv, i = idx - l * pv;
     if (l >= i) { double x = Vw[(long long)l * vm + i]; nv2 += x * x; }
   }
-  nu2 = block_sum(nu2, red);
-  nv2 = block_sum(nv2, red);
+  nu2 = block_sum<NT>(nu2, red);
+  nv2 = block_sum<NT>(nv2, red);
 
   // core M = Ru Rv^T (pu x pv); B = M (pu >= pv) or M^T
   const bool tr = pu < pv;
   const int pr = tr ? pv : pu, pc = tr ? pu : pv;
-  for (int idx = tid; idx < pu * pv; idx += TT) {
+  for (int idx = tid; idx < pu * pv; idx += NT) {
     int i = idx / pv, j = idx - i * pv;
     int l0 = i > j ? i : j;
     double s = 0.0;
@@ -493,17 +431,17 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     __syncthreads();
     sweeps = s_sw;
   } else {
-    sweeps = block_jacobi(Bm, pr, pc, Jm, iflag);
+    sweeps = block_jacobi<NT>(Bm, pr, pc, Jm, iflag);
   }
   ACR_PH(3);
-  for (int j = tid; j < pc; j += TT) {
+  for (int j = tid; j < pc; j += NT) {
     double s = 0.0;
     const double* bj = Bm + (long long)j * pr;
     for (int r = 0; r < pr; ++r) s += bj[r] * bj[r];
     sig[j] = sqrt(s);
   }
   __syncthreads();
-  for (int j = tid; j < pc; j += TT) {
+  for (int j = tid; j < pc; j += NT) {
     double sj = sig[j];
     int rnk = 0;
     for (int i = 0; i < pc; ++i) {
@@ -543,33 +481,33 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   // coefficients of the kept singular pairs, then explicit Q (in place over
   // the reflectors, half-CTA per side) and U' = Q_u C_u, V' = Q_v C_v written
   // straight to the output columns
-  for (int idx = tid; idx < pu * keep; idx += TT) {
+  for (int idx = tid; idx < pu * keep; idx += NT) {
     const int c = idx / pu, i = idx - c * pu;
     const int j = ord[c];
     Cu[idx] = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
   }
-  for (int idx = tid; idx < pv * keep; idx += TT) {
+  for (int idx = tid; idx < pv * keep; idx += NT) {
     const int c = idx / pv, i = idx - c * pv;
     const int j = ord[c];
     Cv[idx] = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
   }
   {
-    const int half = tid >= TT / 2 ? 1 : 0;
-    const int t = tid - half * (TT / 2);
-    Grp g{1 + half, TT / 2, t, NWB / 2, t >> 5, tid & 31, red + half * (NWB / 2),
+    const int half = tid >= NT / 2 ? 1 : 0;
+    const int t = tid - half * (NT / 2);
+    Grp g{1 + half, NT / 2, t, (NT / 32) / 2, t >> 5, tid & 31, red + half * ((NT / 32) / 2),
           nullptr};
     if (!half) group_form_q(Uw, um, pu, tauU, g);
     else group_form_q(Vw, vm, pv, tauV, g);
   }
   __syncthreads();
-  for (int idx = tid; idx < um * keep; idx += TT) {
+  for (int idx = tid; idx < um * keep; idx += NT) {
     const int c = idx / um, i = idx - c * um;
     const double* cc = Cu + (long long)c * pu;
     double y = 0.0;
     for (int l = 0; l < pu; ++l) y += Uw[(long long)l * um + i] * cc[l];
     Uo[(long long)c * n + i] = y;
   }
-  for (int idx = tid; idx < vm * keep; idx += TT) {
+  for (int idx = tid; idx < vm * keep; idx += NT) {
     const int c = idx / vm, i = idx - c * vm;
     const double* cc = Cv + (long long)c * pv;
     double y = 0.0;
@@ -595,6 +533,7 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
 
 
 // rank-0 / passthrough / rank-1 shortcut cases, whole CTA (uniform branch)
+template <int NT>
 __device__ bool block_trivial(const TruncArgs& A, const TaskCtx& c, double* red) {
   const int tid = threadIdx.x, n = A.T.n;
   if (A.mode != TM_TRUNCATE && (c.a.r == 0 || c.b.r == 0)) {   // algebra.py:93-96
@@ -604,7 +543,7 @@ __device__ bool block_trivial(const TruncArgs& A, const TaskCtx& c, double* red)
       if (tid == 0) atomicMax(A.overflow, r);
       r = c.Rout;
     }
-    if (r) copy_factor(s, c.Uo, c.Vo, c.um, c.vm, n, r);
+    if (r) copy_factor<NT>(s, c.Uo, c.Vo, c.um, c.vm, n, r);
     if (tid == 0) {
       *c.ro = r;
       if (A.ctr && r && !(s.U == c.Uo && s.V == c.Vo && s.sc == 1.0))
@@ -616,16 +555,16 @@ __device__ bool block_trivial(const TruncArgs& A, const TaskCtx& c, double* red)
     int r = 0;
     if (c.a.r == 1) {                                           // hodlr.py:181-185
       double nzu = 0.0, nzv = 0.0;
-      for (int i = tid; i < c.um; i += TT) nzu += (c.a.U[i] != 0.0) ? 1.0 : 0.0;
-      for (int i = tid; i < c.vm; i += TT) nzv += (c.a.V[i] != 0.0) ? 1.0 : 0.0;
-      nzu = block_sum(nzu, red);
-      nzv = block_sum(nzv, red);
+      for (int i = tid; i < c.um; i += NT) nzu += (c.a.U[i] != 0.0) ? 1.0 : 0.0;
+      for (int i = tid; i < c.vm; i += NT) nzv += (c.a.V[i] != 0.0) ? 1.0 : 0.0;
+      nzu = block_sum<NT>(nzu, red);
+      nzv = block_sum<NT>(nzv, red);
       r = (nzu > 0.0 && nzv > 0.0) ? 1 : 0;
       if (r > c.Rout) {
         if (tid == 0) atomicMax(A.overflow, r);
         r = 0;
       }
-      if (r) copy_factor(c.a, c.Uo, c.Vo, c.um, c.vm, n, 1);
+      if (r) copy_factor<NT>(c.a, c.Uo, c.Vo, c.um, c.vm, n, 1);
     }
     if (tid == 0) *c.ro = r;
     return true;
@@ -635,10 +574,11 @@ __device__ bool block_trivial(const TruncArgs& A, const TaskCtx& c, double* red)
 
 // q == nullptr: direct mode, one CTA per item (small launches, latency bound)
 // otherwise: persistent CTAs over the queue of tasks the warp path rejected
-__global__ void __launch_bounds__(TT) k_trunc_big(TruncArgs A, const int* q,
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_trunc_big(TruncArgs A, const int* q,
                                                   const int* qcount, int nitems) {
   extern __shared__ double sm[];
-  __shared__ double red[NWB + 4];
+  __shared__ double red[(NT / 32) + 4];
   __shared__ int iflag[2];
   const int cnt = q ? *qcount : nitems;
   for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
@@ -646,7 +586,7 @@ __global__ void __launch_bounds__(TT) k_trunc_big(TruncArgs A, const int* q,
     const int task = item % A.ntasks, g = item / A.ntasks;
     TaskCtx c = resolve_task(A, task, g);
     __syncthreads();
-    if (!q && block_trivial(A, c, red)) {
+    if (!q && block_trivial<NT>(A, c, red)) {
       __syncthreads();
       continue;
     }
@@ -660,7 +600,7 @@ __global__ void __launch_bounds__(TT) k_trunc_big(TruncArgs A, const int* q,
       }
       wk = A.gscr + (long long)blockIdx.x * A.gscr_stride;
     }
-    trunc_block_full(A, c, wk, red, iflag);
+    trunc_block_full<NT>(A, c, wk, red, iflag);
     __syncthreads();
   }
 }
@@ -697,7 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     TaskCtx c = resolve_task(A, task, g);
     __syncthreads();
     if (task_trivial(A, c)) {                 // both CTAs agree; CTA 0 writes
-      if (side == 0) block_trivial(A, c, red);
+      if (side == 0) block_trivial<TT>(A, c, red);
       __syncthreads();
       continue;
     }
@@ -740,7 +680,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
       Rs[idx] = x;
       nr2 += x * x;
     }
-    nr2 = block_sum(nr2, red);
+    nr2 = block_sum<TT>(nr2, red);
     if (tid == 0) misc[0] = nr2;
     cl.sync();                                 // both R factors published
     if (side == 0) {
@@ -772,7 +712,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
         __syncthreads();
         sweeps = s_sw;
       } else {
-        sweeps = block_jacobi(Bm, pr, pc, Jm, iflag);
+        sweeps = block_jacobi<TT>(Bm, pr, pc, Jm, iflag);
       }
       ACR_PH(3);
       for (int j = tid; j < pc; j += TT) {
@@ -884,6 +824,7 @@ static constexpr int TW = 16;          // warps per CTA
 static constexpr int SLOT = 384;       // doubles per slot (3 KB)
 static constexpr int NSLOT = 64;       // 192 KB pool, one 64-bit occupancy mask
 static constexpr unsigned FULL = 0xffffffffu;
+static constexpr int QHALF = 112 * 1024;   // queue CTAs: two per SM below this work area
 
 __device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns) {
   const unsigned long long want = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
@@ -1321,8 +1262,10 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   if (!attr) {
     cudaFuncSetAttribute(k_trunc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          NSLOT * SLOT * 8);
-    cudaFuncSetAttribute(k_trunc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_trunc_big<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          28416 * 8 + 64);   // engine caps smem_doubles at 28416
+    cudaFuncSetAttribute(k_trunc_big<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         QHALF);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1331,7 +1274,7 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   const int nitems = a.ntasks * nelem;
   const size_t bsm = (size_t)a.smem_doubles * 8 + 64;
   if (direct) {
-    k_trunc_big<<<nitems, TT, bsm, st>>>(a, nullptr, nullptr, nitems);
+    k_trunc_big<512><<<nitems, 512, bsm, st>>>(a, nullptr, nullptr, nitems);
     return cudaGetLastError();
   }
   if (may_big) {
@@ -1343,8 +1286,15 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   k_trunc_warp<<<blocks, TW * 32, NSLOT * SLOT * 8, st>>>(a, nitems, bigq, bigcount);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !may_big) return e;
-  int bb = nitems < nsm ? nitems : nsm;
-  k_trunc_big<<<bb, TT, bsm, st>>>(a, bigq, bigcount, nitems);
+  // queue of oversized tasks: two 256-thread CTAs per SM when their work areas
+  // fit, so one task's single-warp Jacobi overlaps the other's QR / output
+  if (bsm <= QHALF) {
+    const int bb = nitems < 2 * nsm ? nitems : 2 * nsm;
+    k_trunc_big<256><<<bb, 256, bsm, st>>>(a, bigq, bigcount, nitems);
+  } else {
+    const int bb = nitems < nsm ? nitems : nsm;
+    k_trunc_big<512><<<bb, 512, bsm, st>>>(a, bigq, bigcount, nitems);
+  }
   return cudaGetLastError();
 }
 
