@@ -157,20 +157,6 @@ def run_reference(args):
               f"({sub.n_unknowns} unknowns, n={sub.block_dim}); "
               "reduce phase of oracle/acr_oracle.py (reference algorithm, "
               "numpy/LAPACK), per step")
-    # end-to-end roofline of the whole factor: T_roof =
-    # max(census FLOPs / FP64 peak, compulsory bytes / HBM peak) over the
-    # measured factor time; census per unknown from SURVEY.md Appendix C
-    census = {"cfg1": (20.3e3, 2128), "cfg2": (45.0e3, 4009), "cfg3": (59.7e3, 4366),
-              "cfg4": (185.5e3, 5105), "cfg5": (146.8e3, 7812)}
-    f_un, b_un = census[cfg]
-    t_flop = f_un * N / (dfma * 1e9) * 1e3
-    t_byte = b_un * N / (hbm_peak * 1e9) * 1e3
-    roofline_e2e = {"t_roof_ms": max(t_flop, t_byte), "t_fp64_ms": t_flop,
-                    "t_hbm_ms": t_byte, "t_factor_ms": ms,
-                    "frac": max(t_flop, t_byte) / ms,
-                    "census": "SURVEY.md 8(d) / Appendix C: %.1f kFLOP and %d compulsory "
-                              "bytes per unknown (%s)" % (f_un / 1e3, b_un, cfg)}
-
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup,
