@@ -9,6 +9,7 @@
 //   k_negate    scale(H, -1) (algebra.py:115-125)
 //   k_lift*     exact lift of the bands (hodlr.py:242-314)
 #include <climits>
+#include <cstdlib>
 #include "acr_types.cuh"
 #include "acr_launch.h"
 
@@ -119,43 +120,21 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
 }
 
 // Register-tiled Gauss-Jordan for leaves of size <= S (S in {16, 32, 64}):
-// (S/4)^2 threads, each owning a 4x4 tile in registers, plus a double-buffered
-// shared copy of the matrix.  Thread tid owns column group tid / TG and row
-// group tid % TG, so a column group lives in TG consecutive lanes: right after
-// the update of step k the group owning column k+1 finds the next pivot
-// (first index of the largest |a_ik|, getrf's rule) while the other warps
-// still update, and publishes it with the step's single barrier.  Singular /
-// non-finite detection as the reference's LAPACK call (algebra.py:199-207).
-template <int TG, int TL, unsigned MASK>
-__device__ __forceinline__ void gj_pivot(const double* m, int LD, int col, int k0, int s,
-                                         int ty, bool owner, int* out) {
-  double best = -1.0;
-  int p = k0;
-#pragma unroll
-  for (int a = 0; a < TL; ++a) {
-    const int i = ty * TL + a;
-    if (i >= k0 && i < s) {
-      const double v = fabs(m[i * LD + col]);
-      if (v > best) { best = v; p = i; }
-    }
-  }
-#pragma unroll
-  for (int o = TG / 2; o; o >>= 1) {
-    const double ov = __shfl_xor_sync(MASK, best, o);
-    const int oi = __shfl_xor_sync(MASK, p, o);
-    if (ov > best || (ov == best && oi < p)) { best = ov; p = oi; }
-  }
-  if (owner && ty == 0) *out = p;
-}
-
-// TL x TL register tiles (the arithmetic per element does not depend on TL).
-template <int S, int TL>
-__global__ void __launch_bounds__((S / TL) * (S / TL)) k_leafinv_reg(TreeDev T, const HB* H,
-                                                                    int leaf, int* sing) {
-  constexpr int TG = S / TL, LD = S + 1;
-  constexpr int NT = TG * TG;
+// (S/4)^2 threads, each owning a 4x4 tile in registers; the pivot sequence
+// equals getrf's (first index of the largest |a_ik| among the remaining
+// rows), rows k and p are exchanged implicitly.  The special cases are off the
+// common path: every element does one FMA x -= a_rk * (row_p / pivot); the
+// owner of column k zeroes it first (x_rk := -a_rk / pivot), and only the
+// threads holding rows k and p fix those rows.  Shared memory carries just
+// the pivot column (published with the pivot search by its owner group) and
+// rows p and k (published after the pivot is known): two barriers per step,
+// no full-matrix copy.
+template <int S>
+__global__ void __launch_bounds__((S / 4) * (S / 4), 3) k_leafinv_v2(TreeDev T, const HB* H,
+                                                                 int leaf, int* sing) {
+  constexpr int TL = 4, TG = S / TL, NT = TG * TG;
   constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : (1u << NT) - 1u;
-  extern __shared__ double buf[];              // [2][S][LD]
+  __shared__ double colbuf[2][S], rowP[S], rowK[S];
   __shared__ int piv[S + 1], inv_[S];
   const int g = blockIdx.x, tid = threadIdx.x;
   const int tx = tid / TG, ty = tid - tx * TG;   // column group, row group
@@ -168,50 +147,108 @@ __global__ void __launch_bounds__((S / TL) * (S / TL)) k_leafinv_reg(TreeDev T, 
     for (int b = 0; b < TL; ++b) {
       const int r = ty * TL + a, c = tx * TL + b;
       x[a][b] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
-      buf[r * LD + c] = x[a][b];
     }
-  // the whole warp holding column group 0 joins the shuffles (groups of TG lanes)
-  __syncwarp(MASK);
-  if (tid < 32) gj_pivot<TG, TL, MASK>(buf, LD, 0, 0, s, ty, tx == 0, &piv[0]);
-  bool bad = false;
-  for (int k = 0; k < s; ++k) {
-    const double* cur = buf + (k & 1) * S * LD;
-    double* nxt = buf + ((k + 1) & 1) * S * LD;
-    __syncthreads();
-    const int p = piv[k];
-    const double pv = cur[p * LD + k];
-    if (pv == 0.0) { bad = true; break; }     // uniform: every thread sees the same
-    const double inv = 1.0 / pv;
-    double rk[TL], ok[TL];
-#pragma unroll
-    for (int b = 0; b < TL; ++b) {
-      const int c = tx * TL + b;
-      rk[b] = (c == k) ? inv : cur[p * LD + c] * inv;   // new row k = old row p / pv
-      ok[b] = cur[k * LD + c];                           // old row k -> row p
-    }
-    const double fk = cur[k * LD + k];
+  // column 0 and its pivot: the warp holding column group 0
+  if (tid < 32) {
+    double best = -1.0;
+    int pb = 0;
 #pragma unroll
     for (int a = 0; a < TL; ++a) {
       const int r = ty * TL + a;
-      if (r == k) {
+      if (tx == 0) colbuf[0][r] = x[a][0];
+      const double v = fabs(x[a][0]);
+      if (r < s && v > best) { best = v; pb = r; }
+    }
 #pragma unroll
-        for (int b = 0; b < TL; ++b) x[a][b] = rk[b];
-      } else {
-        const bool isp = (r == p);
-        const double f = isp ? fk : cur[r * LD + k];
+    for (int o = TG / 2; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(MASK, best, o);
+      const int oi = __shfl_xor_sync(MASK, pb, o);
+      if (ov > best || (ov == best && oi < pb)) { best = ov; pb = oi; }
+    }
+    if (tx == 0 && ty == 0) piv[0] = pb;
+  }
+  bool bad = false;
+  for (int k = 0; k < s; ++k) {
+    __syncthreads();                            // colbuf[k & 1], piv[k]
+    const int p = piv[k];
+    const double* cb = colbuf[k & 1];
+    const double pv = cb[p];
+    if (pv == 0.0) { bad = true; break; }       // uniform
+    if (ty == (p >> 2)) {                       // old row p (select chain: x stays in registers)
+      const int ap = p & 3;
 #pragma unroll
-        for (int b = 0; b < TL; ++b) {
-          const int c = tx * TL + b;
-          const double src = isp ? ok[b] : x[a][b];
-          x[a][b] = (c == k) ? -f * inv : src - f * rk[b];
+      for (int b = 0; b < TL; ++b)
+        rowP[tx * TL + b] = ap == 0 ? x[0][b] : ap == 1 ? x[1][b] : ap == 2 ? x[2][b] : x[3][b];
+    }
+    if (ty == (k >> 2)) {                       // old row k
+      const int ak = k & 3;
+#pragma unroll
+      for (int b = 0; b < TL; ++b)
+        rowK[tx * TL + b] = ak == 0 ? x[0][b] : ak == 1 ? x[1][b] : ak == 2 ? x[2][b] : x[3][b];
+    }
+    __syncthreads();
+    const double inv = 1.0 / pv;
+    double rk[TL];
+#pragma unroll
+    for (int b = 0; b < TL; ++b) {
+      const int c = tx * TL + b;
+      rk[b] = (c == k) ? inv : rowP[c] * inv;   // new row k = old row p / pv
+    }
+    if (tx == (k >> 2)) {                       // column k acts as zero
+      const int bk = k & 3;
+#pragma unroll
+      for (int a = 0; a < TL; ++a) {
+        x[a][0] = bk == 0 ? 0.0 : x[a][0];
+        x[a][1] = bk == 1 ? 0.0 : x[a][1];
+        x[a][2] = bk == 2 ? 0.0 : x[a][2];
+        x[a][3] = bk == 3 ? 0.0 : x[a][3];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < TL; ++a) {
+      const double f = cb[ty * TL + a];
+#pragma unroll
+      for (int b = 0; b < TL; ++b) x[a][b] -= f * rk[b];
+    }
+    if (ty == (k >> 2) || ty == (p >> 2)) {
+      const double fk = cb[k];                  // old a_kk: row k moves to p
+#pragma unroll
+      for (int a = 0; a < TL; ++a) {
+        const int r = ty * TL + a;
+        if (r == p && p != k) {
+#pragma unroll
+          for (int b = 0; b < TL; ++b) {
+            const int c = tx * TL + b;
+            const double ok = (c == k) ? 0.0 : rowK[c];
+            x[a][b] = ok - fk * rk[b];
+          }
+        }
+        if (r == k) {
+#pragma unroll
+          for (int b = 0; b < TL; ++b) x[a][b] = rk[b];
         }
       }
-#pragma unroll
-      for (int b = 0; b < TL; ++b) nxt[r * LD + tx * TL + b] = x[a][b];
     }
-    if (k + 1 < s && (tid >> 5) == (((k + 1) / TL) * TG) >> 5) {
-      __syncwarp(MASK);
-      gj_pivot<TG, TL, MASK>(nxt, LD, k + 1, k + 1, s, ty, tx == (k + 1) / TL, &piv[k + 1]);
+    const int kn = k + 1;                       // next pivot by column kn's owners
+    if (kn < s && (tid >> 5) == ((kn / TL) * TG) >> 5) {
+      const bool own = tx == kn / TL;
+      const int bn = kn % TL;
+      double best = -1.0;
+      int pb = kn;
+#pragma unroll
+      for (int a = 0; a < TL; ++a) {
+        const double v = bn == 0 ? x[a][0] : bn == 1 ? x[a][1] : bn == 2 ? x[a][2] : x[a][3];
+        const int r = ty * TL + a;
+        if (own) colbuf[kn & 1][r] = v;
+        if (r >= kn && r < s && fabs(v) > best) { best = fabs(v); pb = r; }
+      }
+#pragma unroll
+      for (int o = TG / 2; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(MASK, best, o);
+        const int oi = __shfl_xor_sync(MASK, pb, o);
+        if (ov > best || (ov == best && oi < pb)) { best = ov; pb = oi; }
+      }
+      if (own && ty == 0) piv[kn] = pb;
     }
   }
   if (bad) {
@@ -226,10 +263,10 @@ __global__ void __launch_bounds__((S / TL) * (S / TL)) k_leafinv_reg(TreeDev T, 
   __syncthreads();
   // A^{-1} = X P: undo the column swaps in reverse order
   if (tid == 0) {
-    int* pos = reinterpret_cast<int*>(buf);
+    int* pos = reinterpret_cast<int*>(rowP);   // S ints fit in S doubles
     for (int j = 0; j < s; ++j) pos[j] = j;
     for (int k = s - 1; k >= 0; --k) {
-      int t = pos[k];
+      const int t = pos[k];
       pos[k] = pos[piv[k]];
       pos[piv[k]] = t;
     }
@@ -258,16 +295,7 @@ __global__ void __launch_bounds__((S / TL) * (S / TL)) k_leafinv_reg(TreeDev T, 
 template <int S>
 static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int leaf,
                                int* sing, cudaStream_t st) {
-  const size_t smem = 2ull * S * (S + 1) * 8;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_leafinv_reg<S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
-  // TL = 2 (4x the threads per matrix) measured no faster for single-matrix
-  // launches: a pivot step is bound by its dependency chain, not by issue
-  k_leafinv_reg<S, 4><<<nelem, (S / 4) * (S / 4), smem, st>>>(T, H, leaf, sing);
+  k_leafinv_v2<S><<<nelem, (S / 4) * (S / 4), 0, st>>>(T, H, leaf, sing);
   return cudaGetLastError();
 }
 
