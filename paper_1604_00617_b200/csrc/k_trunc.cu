@@ -1274,7 +1274,11 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   const int nitems = a.ntasks * nelem;
   const size_t bsm = (size_t)a.smem_doubles * 8 + 64;
   if (direct) {
-    k_trunc_big<512><<<nitems, 512, bsm, st>>>(a, nullptr, nullptr, nitems);
+    // more tasks than SMs: 256-thread CTAs, two per SM, when the work areas fit
+    if (nitems > nsm && bsm <= QHALF)
+      k_trunc_big<256><<<nitems, 256, bsm, st>>>(a, nullptr, nullptr, nitems);
+    else
+      k_trunc_big<512><<<nitems, 512, bsm, st>>>(a, nullptr, nullptr, nitems);
     return cudaGetLastError();
   }
   if (may_big) {
