@@ -9,6 +9,7 @@
 //   subtree, deepest first -- the reference's recursion order)
 #include "acr_types.cuh"
 #include "acr_launch.h"
+#include <cstdlib>
 
 namespace acr {
 
@@ -298,7 +299,7 @@ __device__ __forceinline__ void hb_anc_tables(const TreeDev& T, const MMJob& J, 
   const int* an = T.anc + R.lam * (T.maxdepth + 1);
   const int dl = T.depth[R.lam];
   const int eA0 = T.startA[J.mu0];
-  for (int p = threadIdx.x; p < 17 * (R.cnt + 1); p += HT) {
+  for (int p = threadIdx.x; p < 17 * (R.cnt + 1); p += blockDim.x) {
     const int q = p / 17 - 1, k = p % 17;
     if (k < 1 || k > dl) continue;
     const int be = an[k];
@@ -344,7 +345,8 @@ __device__ __forceinline__ void hb_finish_tab(const TreeDev& T, const MMJob& J, 
 
 // Leaf in padded shared memory (few registers, high occupancy);
 // X staged in windows of at most xc columns (bounded shared memory)
-__global__ void __launch_bounds__(HT) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path, int xc) {
+template <int NTB>
+__global__ void __launch_bounds__(NTB) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path, int xc) {
   extern __shared__ double sm[];
   const MMJob& J = JJ.j[blockIdx.z];
   const int g = blockIdx.y, bw = T.bw;
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(HT) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path
   const double* Lg = h.leaf + (long long)lo * bw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // asynchronous staging: warp per row, lanes along the row (no divisions)
-  for (int ii = warp; ii < s; ii += HT / 32)
+  for (int ii = warp; ii < s; ii += NTB / 32)
     for (int j = lane; j < s; j += 32) cp_async8(L + ii * ld + j, Lg + (long long)ii * bw + j, true);
   __shared__ HBAnc A;
   hb_anc_tables(T, J, h, g, R, lo, A);
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(HT) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path
       const int slot = mm_slot(T, R.mus[q]);
       const int q0 = R.off[q], q1 = q0 + ((R.cols[q] + 1) & ~1);
       const int c0 = q0 > w0 ? q0 : w0, c1 = q1 < w0 + wc ? q1 : w0 + wc;
-      for (int pos = c0 + warp; pos < c1; pos += HT / 32) {
+      for (int pos = c0 + warp; pos < c1; pos += NTB / 32) {
         const int b = pos - q0;
         const bool ok = b < R.cols[q];
         const double* src = src_col(J.X, T.n, g, slot, ok ? b : 0) + lo;
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(HT) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path
     cp_async_wait_all();
     __syncthreads();
     const int npairs = wc >> 1;
-    for (int idx = threadIdx.x; idx < s * npairs; idx += HT) {
+    for (int idx = threadIdx.x; idx < s * npairs; idx += NTB) {
       const int pr = idx / s, i = idx - pr * s;
       const int pos = w0 + pr * 2;
       int q = 0;
@@ -425,7 +427,7 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_hmatB<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_hmatB_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_sm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hmatB<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hmatB_path<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
@@ -439,7 +441,8 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     if (cp > 64) cp = 64;
     const size_t smem = ((size_t)T.bw * cp + (size_t)T.bw * (T.bw + 1) + 1) * 8;
     dim3 g(path ? T.nleaves : nB, nelem, njobs);
-    k_hmatB_sm<<<g, HT, smem, st>>>(T, JJ, path, (int)cp);
+    // 256 threads per leaf CTA (measured: 128 and 512 are slower)
+    k_hmatB_sm<256><<<g, 256, smem, st>>>(T, JJ, path, (int)cp);
     return cudaGetLastError();
   }
   if (path) {
