@@ -820,9 +820,9 @@ cudaError_t launch_trunc_pair(const TruncArgs& a, int nelem, long long smem_doub
 // ---------------------------------------------------------------------------
 // warp path: one warp per task, work area carved from a per-CTA smem pool
 // ---------------------------------------------------------------------------
-static constexpr int TW = 16;          // warps per CTA
-static constexpr int SLOT = 384;       // doubles per slot (3 KB)
-static constexpr int NSLOT = 64;       // 192 KB pool, one 64-bit occupancy mask
+static constexpr int TW = 20;          // warps per CTA (96 registers, no spills)
+static constexpr int SLOT = 448;       // doubles per slot (3.5 KB)
+static constexpr int NSLOT = 64;       // 224 KB pool, one 64-bit occupancy mask
 static constexpr unsigned FULL = 0xffffffffu;
 static constexpr int QHALF = 112 * 1024;   // queue CTAs: two per SM below this work area
 
