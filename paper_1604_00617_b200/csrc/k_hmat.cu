@@ -235,15 +235,6 @@ __global__ void __launch_bounds__(HT) k_hmatB_path(TreeDev T, MMJobs2 JJ) {
 // double2 broadcast load feeds two FMAs.  Summation order per output is the
 // scalar one: leaf terms j = 0..s-1, then y = y + z per ancestor deepest
 // first (z = sum over a in order) -- equal bitwise to k_hmatB.
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
-               "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
-}
-
 struct HBRoots {
   int lam, cnt, cp;
   int off[16], cols[16], mus[16];

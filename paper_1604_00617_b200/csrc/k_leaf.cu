@@ -418,12 +418,13 @@ __global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, c
     }
     return;                        // level-0 couplings have rank-0 factors
   }
-  for (int idx = tid; idx < 64 * 64; idx += GT) {
+  for (int idx = tid; idx < 64 * 64; idx += GT) {   // asynchronous staging
     const int i = idx >> 6, j = idx & 63;
     const bool in = i < s && j < s;
-    sa[i * GLD + j] = in ? La[(long long)i * bw + j] : 0.0;
-    sb[i * GLD + j] = in ? Lb[(long long)i * bw + j] : 0.0;
+    cp_async8(sa + i * GLD + j, in ? La + (long long)i * bw + j : La, in);
+    cp_async8(sb + i * GLD + j, in ? Lb + (long long)i * bw + j : Lb, in);
   }
+  cp_async_wait_all();
   __syncthreads();
   const int gi = lane >> 2, ti = lane & 3;
   const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;   // 4 x 2 warp grid
@@ -455,9 +456,10 @@ __global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, c
       for (int idx = tid; idx < 64 * rp; idx += GT) {
         const int c = idx / 64, i = idx - c * 64;             // coalesced in i
         const bool in = i < s && c < kr;
-        sa[i * GLD + c] = in ? P[(long long)(k0 + c) * n + i] : 0.0;   // P[i][c]
-        sb[c * GLD + i] = in ? Q[(long long)(k0 + c) * n + i] : 0.0;   // Q^T[c][i]
+        cp_async8(sa + i * GLD + c, in ? P + (long long)(k0 + c) * n + i : P, in);   // P[i][c]
+        cp_async8(sb + c * GLD + i, in ? Q + (long long)(k0 + c) * n + i : Q, in);   // Q^T[c][i]
       }
+      cp_async_wait_all();
       __syncthreads();
       dmma_block(z, sa, sb, r0, c0, rp, gi, ti);
     }
