@@ -147,6 +147,9 @@ int acr_gen_uniform(const unsigned long long* pcg_state4, long long N, int k, do
 int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
                         double eps, int max_rank_cap, double* Uo, double* Vo,
                         int* rank_out, void* stream);
+/* Test hook: recompression path used by acr_truncate_factor (0 = one CTA per
+ * task (default), 1 = warp-per-task kernel, 2 = CTA pair).  Process-wide. */
+int acr_set_truncate_path(int path);
 /* A: s x s row-major; X: inverse; *singular set to 1 on a zero pivot or a
  * non-finite result. */
 int acr_leaf_inverse(int s, const double* A, double* X, int* singular,

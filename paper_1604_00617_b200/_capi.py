@@ -56,6 +56,7 @@ _SIGS = [
     ("acr_truncate_factor", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p,
                                       C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                       C.c_void_p, C.POINTER(C.c_int), C.c_void_p]),
+    ("acr_set_truncate_path", C.c_int, [C.c_int]),
     ("acr_leaf_inverse", C.c_int, [C.c_int, C.c_void_p, C.c_void_p,
                                    C.POINTER(C.c_int), C.c_void_p]),
 ]
@@ -74,8 +75,8 @@ def load(build_if_missing: bool = True):
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.LIB
-    if build_if_missing and (not os.path.exists(path) or _build.needs_build()) \
+    path = os.environ.get("ACR_LIB_OVERRIDE") or _build.LIB   # A/B development aid
+    if path == _build.LIB and build_if_missing and (not os.path.exists(path) or _build.needs_build()) \
             and os.path.exists(_build.NVCC):
         _build.build()
     if not os.path.exists(path):
@@ -84,6 +85,8 @@ def load(build_if_missing: bool = True):
             "`python -m paper_1604_00617_b200.build` (no CPU fallback exists)")
     lib = C.CDLL(path)
     for name, res, args in _SIGS:
+        if path != _build.LIB and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

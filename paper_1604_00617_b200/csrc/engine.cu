@@ -434,6 +434,7 @@ struct Plan {
   int m, n, leaf, cutoff, cap;
   double eps;
   bool keep_levels = false;
+  bool no_side = false;       // option 4: every launch on the plan's stream
   bool force_pair = false;    // option 3: CTA-pair recompression for every direct launch that fits
   HostTree ht;
   DeviceTree dt;
@@ -495,7 +496,7 @@ struct Plan {
   cudaStream_t st2 = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   cudaStream_t side() {
-    if (prof_on) return st;
+    if (prof_on || no_side) return st;
     if (!st2) {
       CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
@@ -674,6 +675,57 @@ struct Plan {
     CK(launch_trunc(a, nelem, direct, may_big, q, qc, s));
     kend();
     launches += may_big ? 2 : 1;
+    if (getenv("ACR_TDUMP")) tdump(a, t0, t1, out, nelem, direct, may_big);
+  }
+
+  // development aid: per-launch checksum of the recompression outputs
+  void tdump(const TruncArgs& a, int t0, int t1, const HB* out, int nelem, bool direct,
+             bool may_big) {
+    static long long idx = 0;
+    CK(cudaDeviceSynchronize());
+    std::vector<HB> hb(nelem);
+    CK(cudaMemcpy(hb.data(), out, sizeof(HB) * nelem, cudaMemcpyDeviceToHost));
+    long long rs = 0;
+    double ss = 0.0;
+    int maxR = 0;
+    for (int g = 0; g < nelem; ++g) {
+      const int nn = (int)ht.lo.size();
+      std::vector<int> rk(2 * nn);
+      CK(cudaMemcpy(rk.data(), hb[g].rk, sizeof(int) * 2 * nn, cudaMemcpyDeviceToHost));
+      for (int i = t0; i < t1; ++i) {
+        const int beta = ht.listA[i * 3 + 1], side = ht.listA[i * 3 + 2];
+        const int r = rk[beta * 2 + side];
+        rs += r;
+        maxR = std::max(maxR, r);
+        const int lo = ht.lo[beta], mid = ht.mid[beta], hi = ht.hi[beta];
+        const int urow = side ? mid : lo, vrow = side ? lo : mid;
+        const int um = side ? hi - mid : mid - lo, vm = side ? mid - lo : hi - mid;
+        const long long slot = (long long)ht.depth[beta] * hb[g].R * n;
+        std::vector<double> col(std::max(um, vm));
+        std::vector<double> dense((size_t)um * vm, 0.0), uc((size_t)um * r), vc((size_t)vm * r);
+        for (int c = 0; c < r; ++c) {
+          CK(cudaMemcpy(col.data(), hb[g].U + slot + (long long)c * n + urow, 8 * um, cudaMemcpyDeviceToHost));
+          for (int k = 0; k < um; ++k) { ss += col[k] * col[k]; uc[(size_t)c * um + k] = col[k]; }
+          CK(cudaMemcpy(col.data(), hb[g].V + slot + (long long)c * n + vrow, 8 * vm, cudaMemcpyDeviceToHost));
+          for (int k = 0; k < vm; ++k) { ss += col[k] * col[k] * 1.7; vc[(size_t)c * vm + k] = col[k]; }
+        }
+        static FILE* fdump = getenv("ACR_TDUMP_FILE") ? fopen(getenv("ACR_TDUMP_FILE"), "wb") : nullptr;
+        if (fdump && idx == atoll(getenv("ACR_TDUMP_IDX") ? getenv("ACR_TDUMP_IDX") : "-1")) {
+          for (int x = 0; x < um; ++x)
+            for (int y = 0; y < vm; ++y) {
+              double acc = 0.0;
+              for (int c = 0; c < r; ++c) acc += uc[(size_t)c * um + x] * vc[(size_t)c * vm + y];
+              dense[(size_t)x * vm + y] = acc;
+            }
+          int hdr[6] = {g, i, beta, side, r, um * 1000 + vm};
+          fwrite(hdr, sizeof(int), 6, fdump);
+          fwrite(dense.data(), 8, dense.size(), fdump);
+          fflush(fdump);
+        }
+      }
+    }
+    fprintf(stderr, "TDUMP %lld mode %d tasks %d nelem %d direct %d big %d ranksum %lld maxr %d ss %.17g\n",
+            idx++, a.mode, t1 - t0, nelem, (int)direct, (int)may_big, rs, maxR, ss);
   }
 
   static void offset_src(Src& s, int e0) {
@@ -1800,6 +1852,10 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
     h->p->force_pair = value != 0;
     return ACR_OK;
   }
+  if (option == 4) {
+    h->p->no_side = value != 0;
+    return ACR_OK;
+  }
   return set_err(h, ACR_EARG, "unknown option");
 }
 
@@ -1984,6 +2040,14 @@ int acr_gen_uniform(const unsigned long long* pcg_state4, long long N, int k, do
   return ACR_OK;
 }
 
+static int g_trunc_path = 0;
+
+int acr_set_truncate_path(int path) {
+  if (path < 0 || path > 2) return set_err(nullptr, ACR_EARG, "path must be 0, 1 or 2");
+  g_trunc_path = path;
+  return ACR_OK;
+}
+
 int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
                         double eps, int max_rank_cap, double* Uo, double* Vo,
                         int* rank_out, void* stream) {
@@ -2056,7 +2120,11 @@ int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
     a.gscr = g.as<double>();
     a.gscr_stride = need;
     a.smem_doubles = (int)std::min<long long>(need, 24576);
-    CK(acr::launch_trunc(a, 1, true, false, q.as<int>(), qc.as<int>(), st));
+    if (g_trunc_path == 2 && acr::pair_need_doubles(std::max(m, k), Rc) <= 28416)
+      CK(acr::launch_trunc_pair(a, 1, acr::pair_need_doubles(std::max(m, k), Rc), st));
+    else
+      CK(acr::launch_trunc(a, 1, g_trunc_path != 1, g_trunc_path == 1, q.as<int>(),
+                           qc.as<int>(), st));
     int hr2[6];
     CK(cudaMemcpyAsync(hr2, rk.p, sizeof(hr2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -826,19 +826,22 @@ static constexpr int NSLOT = 64;       // 224 KB pool, one 64-bit occupancy mask
 static constexpr unsigned FULL = 0xffffffffu;
 static constexpr int QHALF = 112 * 1024;   // queue CTAs: two per SM below this work area
 
-__device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns) {
+// Reserve ns contiguous slots of the per-CTA pool.  The whole warp runs the
+// loop (lane 0 does the atomics, the outcome is broadcast every iteration),
+// so no lane ever waits in a shuffle while lane 0 spins alone.
+__device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns, int lane) {
   const unsigned long long want = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
   while (true) {
-    unsigned long long m = atomicAdd(mask, 0ull);
     int s = -1;
-    for (int k = 0; k + ns <= NSLOT; ++k)
-      if (((m >> k) & want) == 0ull) { s = k; break; }
-    if (s >= 0) {
-      unsigned long long w = want << s;
-      if (atomicCAS(mask, m, m | w) == m) return s;
-      continue;
+    if (lane == 0) {
+      const unsigned long long m = atomicAdd(mask, 0ull);
+      for (int k = 0; k + ns <= NSLOT; ++k)
+        if (((m >> k) & want) == 0ull) { s = k; break; }
+      if (s >= 0 && atomicCAS(mask, m, m | (want << s)) != m) s = -2;
     }
-    __nanosleep(128);
+    s = __shfl_sync(FULL, s, 0);
+    if (s >= 0) return s;
+    if (s == -1) __nanosleep(128);
   }
 }
 
@@ -963,6 +966,8 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
   }
 }
 
+
+
 // one-sided Jacobi on B (pr x pc col-major), J (pc x pc); pairs of a
 // round-robin step are spread over lane groups of size gs
 __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
@@ -1035,29 +1040,27 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
   return 40;
 }
 
-// W[c*m + i] = [sa*A | sb*B] columns, global -> smem, 4 loads in flight
-__device__ __forceinline__ void warp_load_cols(double* __restrict__ W, int m,
-                                               const double* __restrict__ A, int ra,
-                                               double sa, const double* __restrict__ B,
-                                               int rb, double sb, int n, int lane) {
-  const int R = ra + rb;
-  for (int i = lane; i < m; i += 32) {
-    int c = 0;
-    for (; c + 4 <= R; c += 4) {
-      double v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int cc = c + u;
-        v[u] = cc < ra ? sa * __ldg(A + (long long)cc * n + i)
-                       : sb * __ldg(B + (long long)(cc - ra) * n + i);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) W[(long long)(c + u) * m + i] = v[u];
-    }
-    for (; c < R; ++c)
-      W[(long long)c * m + i] = c < ra ? sa * __ldg(A + (long long)c * n + i)
-                                       : sb * __ldg(B + (long long)(c - ra) * n + i);
-  }
+
+// W[c*m + i] = [A | B] columns, every element an asynchronous 8-byte copy (all
+// of a lane's loads in flight at once); the exact sign scales are applied
+// after the wait (warp_scale_cols)
+__device__ __forceinline__ void warp_issue_cols(double* __restrict__ W, int m,
+                                                const double* __restrict__ A, int ra,
+                                                const double* __restrict__ B, int rb, int n,
+                                                int lane) {
+  for (int c = 0; c < ra; ++c)
+    for (int i = lane; i < m; i += 32) cp_async8(W + (long long)c * m + i, A + (long long)c * n + i, true);
+  for (int c = 0; c < rb; ++c)
+    for (int i = lane; i < m; i += 32)
+      cp_async8(W + (long long)(ra + c) * m + i, B + (long long)c * n + i, true);
+}
+
+__device__ __forceinline__ void warp_scale_cols(double* W, int m, int ra, double sa, int rb,
+                                                double sb, int lane) {
+  if (sa != 1.0)
+    for (int idx = lane; idx < ra * m; idx += 32) W[idx] *= sa;
+  if (sb != 1.0)
+    for (int idx = lane; idx < rb * m; idx += 32) W[ra * m + idx] *= sb;
 }
 
 __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
@@ -1076,13 +1079,17 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   double* tauV = tauU + R;
   double* sig = tauV + R;
   int* ord = reinterpret_cast<int*>(sig + R);
-  double* ob = sig + 2 * R;
   // operand load: all global reads of a lane issued before its smem stores
   long long ph[6] = {0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
-  warp_load_cols(Uw, um, a.U, a.r, a.sc, b.U, b.r, b.sc, n, lane);
-  warp_load_cols(Vw, vm, a.V, a.r, 1.0, b.V, b.r, 1.0, n, lane);
+  warp_issue_cols(Uw, um, a.U, a.r, b.U, b.r, n, lane);
+  warp_issue_cols(Vw, vm, a.V, a.r, b.V, b.r, n, lane);
+  cp_async_wait_all();
   __syncwarp();
+  if (a.sc != 1.0 || b.sc != 1.0) {
+    warp_scale_cols(Uw, um, a.r, a.sc, b.r, b.sc, lane);
+    __syncwarp();
+  }
   ACR_PH(0);
   warp_qr2(Uw, um, tauU, Vw, vm, tauV, R, lane);
   ACR_PH(1);
@@ -1149,6 +1156,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     atomicAdd(A.ctr + 9, 1ull);
     atomicAdd(A.ctr + 11, (unsigned long long)sweeps);
   }
+  double* ob = sig + 2 * R;          // one output column per side (um + vm)
   double* ob2 = ob + um;
   for (int c = 0; c < keep; ++c) {
     const int j = ord[c];
@@ -1239,9 +1247,11 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
       continue;
     }
     const int ns = (int)((need + SLOT - 1) / SLOT);
-    int s0 = 0;
-    if (lane == 0) s0 = acquire_slots(&mask, ns);
-    s0 = __shfl_sync(FULL, s0, 0);
+    const int s0 = acquire_slots(&mask, ns, lane);
+    // order this warp's accesses to the slots after the previous owner's
+    // (without this fence the hand-over raced once the tasks got shorter)
+    __syncwarp();
+    __threadfence_block();
     trunc_warp_full(A, tc, pool + (long long)s0 * SLOT, lane);
     __syncwarp();
     __threadfence_block();

@@ -76,10 +76,23 @@ def _check_against_golden(rep, u, z, prefix, eps, u_ref=None, stride=1,
     assert abs(rep.storage_bytes - sb) <= 1e-4 * sb
 
 
-def test_truncate_kernel_vectors(solver_mod):
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_truncate_kernel_vectors(solver_mod, path):
+    """Captured truncate_factor operands (hodlr.py:176-200) through each
+    recompression path: one CTA per task, warp per task, CTA pair."""
     from paper_1604_00617_b200 import _capi
     import ctypes as C
     lib = _capi.load()
+    assert lib.acr_set_truncate_path(path) == 0
+    try:
+        _truncate_vectors(lib)
+    finally:
+        lib.acr_set_truncate_path(0)
+
+
+def _truncate_vectors(lib):
+    from paper_1604_00617_b200 import _capi
+    import ctypes as C
     z = load_npz("kernels_cfg1.npz")
     for i in range(int(z["n_trunc"])):
         U, V = z[f"t{i}/U"], z[f"t{i}/V"]
