@@ -662,7 +662,7 @@ struct Plan {
     a.gscr_stride = 0;
     a.gscr_ntasks = 0;
     if (may_big) {
-      q = scratch<int>(alt ? 16 : 13, (size_t)nitems + 1);
+      q = scratch<int>(alt ? 16 : 13, 2 * (size_t)nitems + 2);
       qc = scratch<int>(alt ? 17 : 14, 4);
     }
     if ((direct || may_big) && bworst > SMD) {
@@ -674,7 +674,7 @@ struct Plan {
     kbegin(0);
     CK(launch_trunc(a, nelem, direct, may_big, q, qc, s));
     kend();
-    launches += may_big ? 2 : 1;
+    launches += may_big ? ((long long)a.smem_doubles * 8 + 64 > 112 * 1024 ? 3 : 2) : 1;
     if (getenv("ACR_TDUMP")) tdump(a, t0, t1, out, nelem, direct, may_big);
   }
 

@@ -825,6 +825,7 @@ static constexpr int SLOT = 448;       // doubles per slot (3.5 KB)
 static constexpr int NSLOT = 64;       // 224 KB pool, one 64-bit occupancy mask
 static constexpr unsigned FULL = 0xffffffffu;
 static constexpr int QHALF = 112 * 1024;   // queue CTAs: two per SM below this work area
+static constexpr int QHALF_D = (QHALF - 64) / 8;
 
 // Reserve ns contiguous slots of the per-CTA pool.  The whole warp runs the
 // loop (lane 0 does the atomics, the outcome is broadcast every iteration),
@@ -1242,8 +1243,15 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     }
     const int R = a.r + b.r;
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
-    if (need > (long long)NSLOT * SLOT / 8) {   // large: 512-thread block path
-      if (lane == 0) bigq[atomicAdd(bigcount, 1)] = item;
+    if (need > (long long)NSLOT * SLOT / 8) {   // large: block path queues
+      // queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM);
+      // queue 1 (stored from bigq + nitems): one 512-thread CTA per SM
+      if (lane == 0) {
+        if (trunc_need_doubles(tc.um, tc.vm, R) <= QHALF_D)
+          bigq[atomicAdd(bigcount, 1)] = item;
+        else
+          bigq[nitems + atomicAdd(bigcount + 1, 1)] = item;
+      }
       continue;
     }
     const int ns = (int)((need + SLOT - 1) / SLOT);
@@ -1292,7 +1300,7 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
     return cudaGetLastError();
   }
   if (may_big) {
-    cudaError_t e = cudaMemsetAsync(bigcount, 0, sizeof(int), st);
+    cudaError_t e = cudaMemsetAsync(bigcount, 0, 2 * sizeof(int), st);
     if (e != cudaSuccess) return e;
   }
   int blocks = (nitems + TW - 1) / TW;
@@ -1300,14 +1308,21 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   k_trunc_warp<<<blocks, TW * 32, NSLOT * SLOT * 8, st>>>(a, nitems, bigq, bigcount);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !may_big) return e;
-  // queue of oversized tasks: two 256-thread CTAs per SM when their work areas
-  // fit, so one task's single-warp Jacobi overlaps the other's QR / output
-  if (bsm <= QHALF) {
+  // queues of oversized tasks, split by each task's own work area: two
+  // 256-thread CTAs per SM for those that fit half an SM's shared memory (one
+  // task's single-warp Jacobi overlaps the other's QR / output), one
+  // 512-thread CTA per SM for the rest
+  {
+    TruncArgs ah = a;
+    ah.smem_doubles = QHALF_D;
     const int bb = nitems < 2 * nsm ? nitems : 2 * nsm;
-    k_trunc_big<256><<<bb, 256, bsm, st>>>(a, bigq, bigcount, nitems);
-  } else {
+    k_trunc_big<256><<<bb, 256, QHALF, st>>>(ah, bigq, bigcount, nitems);
+  }
+  if (bsm > QHALF) {
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     const int bb = nitems < nsm ? nitems : nsm;
-    k_trunc_big<512><<<bb, 512, bsm, st>>>(a, bigq, bigcount, nitems);
+    k_trunc_big<512><<<bb, 512, bsm, st>>>(a, bigq + nitems, bigcount + 1, nitems);
   }
   return cudaGetLastError();
 }
