@@ -836,9 +836,14 @@ __device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns, i
     int s = -1;
     if (lane == 0) {
       const unsigned long long m = atomicAdd(mask, 0ull);
-      for (int k = 0; k + ns <= NSLOT; ++k)
-        if (((m >> k) & want) == 0ull) { s = k; break; }
-      if (s >= 0 && atomicCAS(mask, m, m | (want << s)) != m) s = -2;
+      // bit k of run: slots k .. k+ns-1 all free (shifts bring in used bits)
+      unsigned long long run = ~m;
+      for (int i = 1; i < ns; ++i) run &= ~m >> i;
+      if (ns > 1) run &= ~0ull >> (ns - 1);
+      if (run) {
+        s = __ffsll((long long)run) - 1;
+        if (atomicCAS(mask, m, m | (want << s)) != m) s = -2;
+      }
     }
     s = __shfl_sync(FULL, s, 0);
     if (s >= 0) return s;
