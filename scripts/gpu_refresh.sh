@@ -16,9 +16,9 @@ for name in ['k_trunc_warp','k_trunc_big']:
     ks=[(i,t(r)) for i,r in enumerate(rows[1:]) if name in r[ki]]
     j=max(range(len(ks)), key=lambda q: ks[q][1]) if ks else 0
     idx[name]=j
-open('gpurun_out/prof_idx.txt','w').write('\n'.join(f'{k} {v}' for k,v in idx.items()))
+open('gpurun_out/prof_idx.txt','w').write(''.join(f'{k} {v}\n' for k,v in idx.items()))
 PY
 while read K I; do
-  ncu --set full --clock-control none --import-source on -k regex:$K -s $I -c 1 -o gpurun_out/${V}_$K -f python scripts/factor_once.py cfg5 > gpurun_out/ncu_$K.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:$K -s $I -c 1 -o gpurun_out/${V}_$K -f python scripts/factor_once.py cfg5 > gpurun_out/ncu_$K.log 2>&1 < /dev/null
 done < gpurun_out/prof_idx.txt
 echo done > gpurun_out/refresh_done
