@@ -794,12 +794,16 @@ struct Plan {
     }
     const cudaStream_t s2 = side();
     fork(s2);
-    kbegin(2);
-    if (prof_on)   // dense leaf products: 2 s^3 each (2 s^2 on the exact diagonal path)
+    // class 2: dense leaf products on DMMA, 2 s^3 FLOP each; class 4: the exact
+    // diagonal path (level 0, E/F diagonal), HBM-bound: algorithmic bytes =
+    // read the dense leaf and the diagonal, write the product, 8 (2 s^2 + s)
+    kbegin(diag ? 4 : 2);
+    if (prof_on)
       for (int v = 0; v < nn; ++v)
         if (ht.isleaf[v]) {
           const double sz = ht.hi[v] - ht.lo[v];
-          hflops[2] += (double)G * 2.0 * sz * sz * (diag ? 1.0 : sz);
+          if (diag) hflops[4] += (double)G * 8.0 * (2.0 * sz * sz + sz);
+          else hflops[2] += (double)G * 2.0 * sz * sz * sz;
         }
     CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), diag,
                        s2));
