@@ -381,8 +381,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // A fragment: A[r][k] (row-major sa), B fragment: B[k][c] (row-major sb).
 __device__ __forceinline__ void dmma_block(double (&acc)[2][4][2], const double* sa,
                                            const double* sb, int r0, int c0, int K,
-                                           int gi, int ti) {
-  for (int k = 0; k < K; k += 4) {
+                                           int gi, int ti, int K0 = 0) {
+  for (int k = K0; k < K; k += 4) {
     double a0 = sa[(r0 + gi) * GLD + k + ti];
     double a1 = sa[(r0 + 8 + gi) * GLD + k + ti];
     double b[4];
@@ -396,7 +396,7 @@ __device__ __forceinline__ void dmma_block(double (&acc)[2][4][2], const double*
   }
 }
 
-__global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, const HB* B,
+__global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, const HB* B,
                                                       const HB* C, Src PX, RankRef xr,
                                                       int diag) {
   extern __shared__ double sm[];
@@ -410,6 +410,23 @@ __global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, c
   const double* Lb = B[g].leaf + (long long)lo * bw;
   double* Lc = C[g].leaf + (long long)lo * bw;
   if (diag) {                      // exact: C = diag(a) B or A diag(b)
+    if (s == 64 && (bw & 1) == 0) {  // 16-byte rows, shifts instead of divisions
+      for (int idx = tid; idx < 64 * 32; idx += GT) {
+        const int i = idx >> 5, j = (idx & 31) * 2;
+        double2 v;
+        if (diag == 1) {
+          const double d = La[(long long)i * bw + i];
+          const double2 b = *reinterpret_cast<const double2*>(Lb + (long long)i * bw + j);
+          v = make_double2(d * b.x, d * b.y);
+        } else {
+          const double2 a = *reinterpret_cast<const double2*>(La + (long long)i * bw + j);
+          v = make_double2(a.x * Lb[(long long)j * bw + j],
+                           a.y * Lb[(long long)(j + 1) * bw + j + 1]);
+        }
+        *reinterpret_cast<double2*>(Lc + (long long)i * bw + j) = v;
+      }
+      return;
+    }
     for (int idx = tid; idx < s * s; idx += GT) {
       const int i = idx / s, j = idx - i * s;
       Lc[(long long)i * bw + j] = diag == 1
@@ -418,11 +435,19 @@ __global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, c
     }
     return;                        // level-0 couplings have rank-0 factors
   }
-  for (int idx = tid; idx < 64 * 64; idx += GT) {   // asynchronous staging
-    const int i = idx >> 6, j = idx & 63;
-    const bool in = i < s && j < s;
-    cp_async8(sa + i * GLD + j, in ? La + (long long)i * bw + j : La, in);
-    cp_async8(sb + i * GLD + j, in ? Lb + (long long)i * bw + j : Lb, in);
+  if (s == 64 && (bw & 1) == 0) {   // asynchronous staging, 16-byte copies
+    for (int idx = tid; idx < 64 * 32; idx += GT) {
+      const int i = idx >> 5, j = (idx & 31) * 2;
+      cp_async16(sa + i * GLD + j, La + (long long)i * bw + j);
+      cp_async16(sb + i * GLD + j, Lb + (long long)i * bw + j);
+    }
+  } else {
+    for (int idx = tid; idx < 64 * 64; idx += GT) {
+      const int i = idx >> 6, j = idx & 63;
+      const bool in = i < s && j < s;
+      cp_async8(sa + i * GLD + j, in ? La + (long long)i * bw + j : La, in);
+      cp_async8(sb + i * GLD + j, in ? Lb + (long long)i * bw + j : Lb, in);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
@@ -437,8 +462,58 @@ __global__ void __launch_bounds__(GT, 3) k_leafgemm_tc(TreeDev T, const HB* A, c
   // ancestor cross terms, parent first: acc += P Q^T, one ancestor at a time
   const HB bb = B[g];
   const int* cr = rank_base(xr, g);
+  // every ancestor's P and Q^T in one staging phase when their padded ranks
+  // fit the 64 columns of sa / sb (the usual case); the products are still
+  // formed and added one ancestor at a time, parent first
+  int tot = 0;
+  {
+    int ch = lam;
+    for (int al = T.parent[lam]; al >= 0; ch = al, al = T.parent[al])
+      tot += (cr[al * 2 + (ch == T.c0[al] ? 0 : 1)] + 3) & ~3;
+  }
+  if (tot > 0 && tot <= 64) {
+    __syncthreads();                             // main product done with sa / sb
+    int off = 0, ch = lam;
+    for (int al = T.parent[lam]; al >= 0; ch = al, al = T.parent[al]) {
+      const int r = cr[al * 2 + (ch == T.c0[al] ? 0 : 1)];
+      if (!r) continue;
+      const int rp = (r + 3) & ~3, slot = T.depth[al];
+      const double* P = src_col(PX, n, g, slot, 0) + lo;
+      const double* Q = bb.V + (long long)slot * bb.R * n + lo;
+      for (int idx = tid; idx < 64 * rp; idx += GT) {
+        const int c = idx / 64, i = idx - c * 64;
+        const bool in = i < s && c < r;
+        cp_async8(sa + i * GLD + off + c, in ? P + (long long)c * n + i : P, in);
+        cp_async8(sb + (off + c) * GLD + i, in ? Q + (long long)c * n + i : Q, in);
+      }
+      off += rp;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    off = 0;
+    ch = lam;
+    for (int al = T.parent[lam]; al >= 0; ch = al, al = T.parent[al]) {
+      const int r = cr[al * 2 + (ch == T.c0[al] ? 0 : 1)];
+      if (!r) continue;
+      const int rp = (r + 3) & ~3;
+      double z[2][4][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) z[a][q][0] = z[a][q][1] = 0.0;
+      dmma_block(z, sa, sb, r0, c0, off + rp, gi, ti, off);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[a][q][0] = acc[a][q][0] + z[a][q][0];
+          acc[a][q][1] = acc[a][q][1] + z[a][q][1];
+        }
+      off += rp;
+    }
+  }
   int child = lam;
-  for (int al = T.parent[lam]; al >= 0; child = al, al = T.parent[al]) {
+  for (int al = T.parent[lam]; tot > 64 && al >= 0; child = al, al = T.parent[al]) {
     const int r = cr[al * 2 + (child == T.c0[al] ? 0 : 1)];
     if (!r) continue;
     const int slot = T.depth[al];

@@ -33,7 +33,7 @@ for name in cfgs:
         sol.factor(bands)
         sol.lib.acr_plan_set_option(sol.plan, 2, 0)
         st = {}
-        for cls, nm in enumerate(["trunc", "leafinv", "leafgemm", "hmat"]):
+        for cls, nm in enumerate(["trunc", "leafinv", "leafgemm", "hmat", "leafgemm_diag"]):
             nl = C.c_longlong(); ms = C.c_double(); ctr = (C.c_ulonglong * 16)()
             sol.lib.acr_kernel_stats(sol.plan, cls, C.byref(nl), C.byref(ms), ctr)
             st[nm] = (nl.value, round(ms.value, 1))
