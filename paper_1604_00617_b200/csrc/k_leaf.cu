@@ -129,38 +129,44 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
 // the pivot column (published with the pivot search by its owner group) and
 // rows p and k (published after the pivot is known): two barriers per step,
 // no full-matrix copy.
-template <int S>
-__global__ void __launch_bounds__((S / 4) * (S / 4), 3) k_leafinv_v2(TreeDev T, const HB* H,
-                                                                 int leaf, int* sing) {
-  constexpr int TL = 4, TG = S / TL, NT = TG * TG;
-  constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : (1u << NT) - 1u;
+// TR x TC register tiles, S/TR row groups (<= 32: one warp segment holds a
+// column group) x S/TC column groups; (4, 4) with 256 threads for batched
+// (throughput) launches, (2, 2) with 1024 threads for launches with fewer
+// leaves than SMs, where the pivot chain's latency is the cost.
+template <int S, int TR, int TC, int MINB>
+__global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDev T, const HB* H,
+                                                                       int leaf, int* sing) {
+  constexpr int TGY = S / TR, TGX = S / TC, NT = TGX * TGY;
+  static_assert(TGY <= 32, "a column group must fit one warp");
+  constexpr unsigned MASK = TGY >= 32 ? 0xffffffffu : (NT >= 32 ? 0xffffffffu : (1u << NT) - 1u);
   __shared__ double colbuf[2][S], rowP[S], rowK[S];
   __shared__ int piv[S + 1], inv_[S];
   const int g = blockIdx.x, tid = threadIdx.x;
-  const int tx = tid / TG, ty = tid - tx * TG;   // column group, row group
+  const int tx = tid / TGY, ty = tid - tx * TGY;   // column group, row group
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
   double* L = H[g].leaf + (long long)lo * bw;
-  double x[TL][TL];
+  double x[TR][TC];
 #pragma unroll
-  for (int a = 0; a < TL; ++a)
+  for (int a = 0; a < TR; ++a)
 #pragma unroll
-    for (int b = 0; b < TL; ++b) {
-      const int r = ty * TL + a, c = tx * TL + b;
+    for (int b = 0; b < TC; ++b) {
+      const int r = ty * TR + a, c = tx * TC + b;
       x[a][b] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
     }
-  // column 0 and its pivot: the warp holding column group 0
+  // column 0 and its pivot: the warp holding column group 0 (every lane takes
+  // part in the shuffles; only column group 0 publishes)
   if (tid < 32) {
     double best = -1.0;
     int pb = 0;
 #pragma unroll
-    for (int a = 0; a < TL; ++a) {
-      const int r = ty * TL + a;
+    for (int a = 0; a < TR; ++a) {
+      const int r = ty * TR + a;
       if (tx == 0) colbuf[0][r] = x[a][0];
       const double v = fabs(x[a][0]);
       if (r < s && v > best) { best = v; pb = r; }
     }
 #pragma unroll
-    for (int o = TG / 2; o; o >>= 1) {
+    for (int o = TGY / 2; o; o >>= 1) {
       const double ov = __shfl_xor_sync(MASK, best, o);
       const int oi = __shfl_xor_sync(MASK, pb, o);
       if (ov > best || (ov == best && oi < pb)) { best = ov; pb = oi; }
@@ -174,76 +180,83 @@ __global__ void __launch_bounds__((S / 4) * (S / 4), 3) k_leafinv_v2(TreeDev T, 
     const double* cb = colbuf[k & 1];
     const double pv = cb[p];
     if (pv == 0.0) { bad = true; break; }       // uniform
-    if (ty == (p >> 2)) {                       // old row p (select chain: x stays in registers)
-      const int ap = p & 3;
+    if (ty == p / TR) {                         // old row p (select chain: x stays in registers)
+      const int ap = p % TR;
 #pragma unroll
-      for (int b = 0; b < TL; ++b)
-        rowP[tx * TL + b] = ap == 0 ? x[0][b] : ap == 1 ? x[1][b] : ap == 2 ? x[2][b] : x[3][b];
+      for (int b = 0; b < TC; ++b) {
+        double v = x[0][b];
+#pragma unroll
+        for (int a = 1; a < TR; ++a) v = ap == a ? x[a][b] : v;
+        rowP[tx * TC + b] = v;
+      }
     }
-    if (ty == (k >> 2)) {                       // old row k
-      const int ak = k & 3;
+    if (ty == k / TR) {                         // old row k
+      const int ak = k % TR;
 #pragma unroll
-      for (int b = 0; b < TL; ++b)
-        rowK[tx * TL + b] = ak == 0 ? x[0][b] : ak == 1 ? x[1][b] : ak == 2 ? x[2][b] : x[3][b];
+      for (int b = 0; b < TC; ++b) {
+        double v = x[0][b];
+#pragma unroll
+        for (int a = 1; a < TR; ++a) v = ak == a ? x[a][b] : v;
+        rowK[tx * TC + b] = v;
+      }
     }
     __syncthreads();
     const double inv = 1.0 / pv;
-    double rk[TL];
+    double rk[TC];
 #pragma unroll
-    for (int b = 0; b < TL; ++b) {
-      const int c = tx * TL + b;
+    for (int b = 0; b < TC; ++b) {
+      const int c = tx * TC + b;
       rk[b] = (c == k) ? inv : rowP[c] * inv;   // new row k = old row p / pv
     }
-    if (tx == (k >> 2)) {                       // column k acts as zero
-      const int bk = k & 3;
+    if (tx == k / TC) {                         // column k acts as zero
+      const int bk = k % TC;
 #pragma unroll
-      for (int a = 0; a < TL; ++a) {
-        x[a][0] = bk == 0 ? 0.0 : x[a][0];
-        x[a][1] = bk == 1 ? 0.0 : x[a][1];
-        x[a][2] = bk == 2 ? 0.0 : x[a][2];
-        x[a][3] = bk == 3 ? 0.0 : x[a][3];
-      }
+      for (int a = 0; a < TR; ++a)
+#pragma unroll
+        for (int b = 0; b < TC; ++b) x[a][b] = bk == b ? 0.0 : x[a][b];
     }
 #pragma unroll
-    for (int a = 0; a < TL; ++a) {
-      const double f = cb[ty * TL + a];
+    for (int a = 0; a < TR; ++a) {
+      const double f = cb[ty * TR + a];
 #pragma unroll
-      for (int b = 0; b < TL; ++b) x[a][b] -= f * rk[b];
+      for (int b = 0; b < TC; ++b) x[a][b] -= f * rk[b];
     }
-    if (ty == (k >> 2) || ty == (p >> 2)) {
+    if (ty == k / TR || ty == p / TR) {
       const double fk = cb[k];                  // old a_kk: row k moves to p
 #pragma unroll
-      for (int a = 0; a < TL; ++a) {
-        const int r = ty * TL + a;
+      for (int a = 0; a < TR; ++a) {
+        const int r = ty * TR + a;
         if (r == p && p != k) {
 #pragma unroll
-          for (int b = 0; b < TL; ++b) {
-            const int c = tx * TL + b;
+          for (int b = 0; b < TC; ++b) {
+            const int c = tx * TC + b;
             const double ok = (c == k) ? 0.0 : rowK[c];
             x[a][b] = ok - fk * rk[b];
           }
         }
         if (r == k) {
 #pragma unroll
-          for (int b = 0; b < TL; ++b) x[a][b] = rk[b];
+          for (int b = 0; b < TC; ++b) x[a][b] = rk[b];
         }
       }
     }
     const int kn = k + 1;                       // next pivot by column kn's owners
-    if (kn < s && (tid >> 5) == ((kn / TL) * TG) >> 5) {
-      const bool own = tx == kn / TL;
-      const int bn = kn % TL;
+    if (kn < s && (tid >> 5) == ((kn / TC) * TGY) >> 5) {
+      const bool own = tx == kn / TC;
+      const int bn = kn % TC;
       double best = -1.0;
       int pb = kn;
 #pragma unroll
-      for (int a = 0; a < TL; ++a) {
-        const double v = bn == 0 ? x[a][0] : bn == 1 ? x[a][1] : bn == 2 ? x[a][2] : x[a][3];
-        const int r = ty * TL + a;
+      for (int a = 0; a < TR; ++a) {
+        double v = x[a][0];
+#pragma unroll
+        for (int b = 1; b < TC; ++b) v = bn == b ? x[a][b] : v;
+        const int r = ty * TR + a;
         if (own) colbuf[kn & 1][r] = v;
         if (r >= kn && r < s && fabs(v) > best) { best = fabs(v); pb = r; }
       }
 #pragma unroll
-      for (int o = TG / 2; o; o >>= 1) {
+      for (int o = TGY / 2; o; o >>= 1) {
         const double ov = __shfl_xor_sync(MASK, best, o);
         const int oi = __shfl_xor_sync(MASK, pb, o);
         if (ov > best || (ov == best && oi < pb)) { best = ov; pb = oi; }
@@ -275,10 +288,10 @@ __global__ void __launch_bounds__((S / 4) * (S / 4), 3) k_leafinv_v2(TreeDev T, 
   __syncthreads();
   int nf = 0;
 #pragma unroll
-  for (int a = 0; a < TL; ++a)
+  for (int a = 0; a < TR; ++a)
 #pragma unroll
-    for (int b = 0; b < TL; ++b) {
-      const int r = ty * TL + a, c = tx * TL + b;
+    for (int b = 0; b < TC; ++b) {
+      const int r = ty * TR + a, c = tx * TC + b;
       if (r < s && c < s) {
         if (!isfinite(x[a][b])) nf = 1;
         L[(long long)r * bw + inv_[c]] = x[a][b];
@@ -295,7 +308,13 @@ __global__ void __launch_bounds__((S / 4) * (S / 4), 3) k_leafinv_v2(TreeDev T, 
 template <int S>
 static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int leaf,
                                int* sing, cudaStream_t st) {
-  k_leafinv_v2<S><<<nelem, (S / 4) * (S / 4), 0, st>>>(T, H, leaf, sing);
+  if constexpr (S == 64) {
+    if (nelem < 148) {                // latency-bound: 1024 threads, 2 x 2 tiles
+      k_leafinv_v2<S, 2, 2, 1><<<nelem, (S / 2) * (S / 2), 0, st>>>(T, H, leaf, sing);
+      return cudaGetLastError();
+    }
+  }
+  k_leafinv_v2<S, 4, 4, 3><<<nelem, (S / 4) * (S / 4), 0, st>>>(T, H, leaf, sing);
   return cudaGetLastError();
 }
 
