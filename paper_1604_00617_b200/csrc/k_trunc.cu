@@ -866,6 +866,7 @@ __device__ __forceinline__ void warp_copy_factor(const OpRes& s, double* Uo, dou
 
 // Householder QR of U (mu x R) and V (mv x R) by one warp, interleaved: the
 // two factorisations are independent, so their reduction chains overlap.
+template <int MR>
 __device__ __forceinline__ void warp_reflector(double* cj, int j, int mr, double ss,
                                                double& tj, int lane) {
   const double alpha = cj[j];
@@ -879,11 +880,20 @@ __device__ __forceinline__ void warp_reflector(double* cj, int j, int mr, double
   }
   __syncwarp();
   if (tj != 0.0) {
-    for (int i = j + 1 + lane; i < mr; i += 32) cj[i] *= scal;
+    if constexpr (MR > 0) {
+#pragma unroll
+      for (int h = 0; h < MR; ++h)
+        if (lane + 32 * h > j) cj[lane + 32 * h] *= scal;
+    } else {
+      for (int i = j + 1 + lane; i < mr; i += 32) cj[i] *= scal;
+    }
     if (lane == 0) cj[j] = beta;
   }
 }
 
+// MR > 0: both panels have exactly 32 MR rows (lane owns rows lane + 32 h);
+// the same operations in the same per-lane order as the generic MR = 0 path.
+template <int MR>
 __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, double* tv,
                          int R, int lane) {
   const int pu = mu < R ? mu : R, pv = mv < R ? mv : R;
@@ -893,16 +903,27 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
     double* cu = Wu + (long long)j * mu;
     double* cv = Wv + (long long)j * mv;
     double su = 0.0, sv = 0.0;
-    if (du) for (int i = j + 1 + lane; i < mu; i += 32) su += cu[i] * cu[i];
-    if (dv) for (int i = j + 1 + lane; i < mv; i += 32) sv += cv[i] * cv[i];
+    if constexpr (MR > 0) {
+#pragma unroll
+      for (int h = 0; h < MR; ++h) {
+        const int i = lane + 32 * h;
+        if (i > j) {
+          if (du) su += cu[i] * cu[i];
+          if (dv) sv += cv[i] * cv[i];
+        }
+      }
+    } else {
+      if (du) for (int i = j + 1 + lane; i < mu; i += 32) su += cu[i] * cu[i];
+      if (dv) for (int i = j + 1 + lane; i < mv; i += 32) sv += cv[i] * cv[i];
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       su += __shfl_xor_sync(FULL, su, o);
       sv += __shfl_xor_sync(FULL, sv, o);
     }
     double tju = 0.0, tjv = 0.0;
-    if (du) warp_reflector(cu, j, mu, su, tju, lane);
-    if (dv) warp_reflector(cv, j, mv, sv, tjv, lane);
+    if (du) warp_reflector<MR>(cu, j, mu, su, tju, lane);
+    if (dv) warp_reflector<MR>(cv, j, mv, sv, tjv, lane);
     if (lane == 0) {
       if (du) tu[j] = tju;
       if (dv) tv[j] = tjv;
@@ -914,8 +935,19 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
       double* ccu = Wu + (long long)c * mu;
       double* ccv = Wv + (long long)c * mv;
       double wu = 0.0, wv = 0.0;
-      if (au) for (int i = j + 1 + lane; i < mu; i += 32) wu += cu[i] * ccu[i];
-      if (av) for (int i = j + 1 + lane; i < mv; i += 32) wv += cv[i] * ccv[i];
+      if constexpr (MR > 0) {
+#pragma unroll
+        for (int h = 0; h < MR; ++h) {
+          const int i = lane + 32 * h;
+          if (i > j) {
+            if (au) wu += cu[i] * ccu[i];
+            if (av) wv += cv[i] * ccv[i];
+          }
+        }
+      } else {
+        if (au) for (int i = j + 1 + lane; i < mu; i += 32) wu += cu[i] * ccu[i];
+        if (av) for (int i = j + 1 + lane; i < mv; i += 32) wv += cv[i] * ccv[i];
+      }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         wu += __shfl_xor_sync(FULL, wu, o);
@@ -923,12 +955,24 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
       }
       if (au) {
         wu = (wu + ccu[j]) * tju;
-        for (int i = j + 1 + lane; i < mu; i += 32) ccu[i] -= wu * cu[i];
+        if constexpr (MR > 0) {
+#pragma unroll
+          for (int h = 0; h < MR; ++h)
+            if (lane + 32 * h > j) ccu[lane + 32 * h] -= wu * cu[lane + 32 * h];
+        } else {
+          for (int i = j + 1 + lane; i < mu; i += 32) ccu[i] -= wu * cu[i];
+        }
         if (lane == 0) ccu[j] -= wu;
       }
       if (av) {
         wv = (wv + ccv[j]) * tjv;
-        for (int i = j + 1 + lane; i < mv; i += 32) ccv[i] -= wv * cv[i];
+        if constexpr (MR > 0) {
+#pragma unroll
+          for (int h = 0; h < MR; ++h)
+            if (lane + 32 * h > j) ccv[lane + 32 * h] -= wv * cv[lane + 32 * h];
+        } else {
+          for (int i = j + 1 + lane; i < mv; i += 32) ccv[i] -= wv * cv[i];
+        }
         if (lane == 0) ccv[j] -= wv;
       }
     }
@@ -937,6 +981,7 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
 }
 
 // xu := Qu xu and xv := Qv xv, interleaved
+template <int MR>
 __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu,
                               double* xu, const double* Wv, int mv, int pv,
                               const double* tv, double* xv, int lane) {
@@ -948,8 +993,19 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
     const double* vu = Wu + (long long)j * mu;
     const double* vv = Wv + (long long)j * mv;
     double wu = 0.0, wv = 0.0;
-    if (tju != 0.0) for (int i = j + 1 + lane; i < mu; i += 32) wu += vu[i] * xu[i];
-    if (tjv != 0.0) for (int i = j + 1 + lane; i < mv; i += 32) wv += vv[i] * xv[i];
+    if constexpr (MR > 0) {
+#pragma unroll
+      for (int h = 0; h < MR; ++h) {
+        const int i = lane + 32 * h;
+        if (i > j) {
+          if (tju != 0.0) wu += vu[i] * xu[i];
+          if (tjv != 0.0) wv += vv[i] * xv[i];
+        }
+      }
+    } else {
+      if (tju != 0.0) for (int i = j + 1 + lane; i < mu; i += 32) wu += vu[i] * xu[i];
+      if (tjv != 0.0) for (int i = j + 1 + lane; i < mv; i += 32) wv += vv[i] * xv[i];
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       wu += __shfl_xor_sync(FULL, wu, o);
@@ -957,11 +1013,23 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
     }
     if (tju != 0.0) {
       wu = (wu + xu[j]) * tju;
-      for (int i = j + 1 + lane; i < mu; i += 32) xu[i] -= wu * vu[i];
+      if constexpr (MR > 0) {
+#pragma unroll
+        for (int h = 0; h < MR; ++h)
+          if (lane + 32 * h > j) xu[lane + 32 * h] -= wu * vu[lane + 32 * h];
+      } else {
+        for (int i = j + 1 + lane; i < mu; i += 32) xu[i] -= wu * vu[i];
+      }
     }
     if (tjv != 0.0) {
       wv = (wv + xv[j]) * tjv;
-      for (int i = j + 1 + lane; i < mv; i += 32) xv[i] -= wv * vv[i];
+      if constexpr (MR > 0) {
+#pragma unroll
+        for (int h = 0; h < MR; ++h)
+          if (lane + 32 * h > j) xv[lane + 32 * h] -= wv * vv[lane + 32 * h];
+      } else {
+        for (int i = j + 1 + lane; i < mv; i += 32) xv[i] -= wv * vv[i];
+      }
     }
     __syncwarp();
     if (lane == 0) {
@@ -1097,7 +1165,11 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     __syncwarp();
   }
   ACR_PH(0);
-  warp_qr2(Uw, um, tauU, Vw, vm, tauV, R, lane);
+  const int mrl = (um == vm && (um & 31) == 0) ? um >> 5 : 0;   // rows per lane
+  if (mrl == 2) warp_qr2<2>(Uw, um, tauU, Vw, vm, tauV, R, lane);
+  else if (mrl == 4) warp_qr2<4>(Uw, um, tauU, Vw, vm, tauV, R, lane);
+  else if (mrl == 1) warp_qr2<1>(Uw, um, tauU, Vw, vm, tauV, R, lane);
+  else warp_qr2<0>(Uw, um, tauU, Vw, vm, tauV, R, lane);
   ACR_PH(1);
   double nu2 = 0.0, nv2 = 0.0;
   for (int idx = lane; idx < pu * R; idx += 32) {
@@ -1177,7 +1249,10 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
       ob2[i] = v;
     }
     __syncwarp();
-    warp_apply_q2(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
+    if (mrl == 2) warp_apply_q2<2>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
+    else if (mrl == 4) warp_apply_q2<4>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
+    else if (mrl == 1) warp_apply_q2<1>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
+    else warp_apply_q2<0>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
     double* du = tc.Uo + (long long)c * n;
     for (int i = lane; i < um; i += 32) du[i] = ob[i];
     double* dv = tc.Vo + (long long)c * n;
