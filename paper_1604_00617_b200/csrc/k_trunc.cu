@@ -192,7 +192,11 @@ __device__ __forceinline__ int rr_player(int step, int x, int np) {
 template <int NT>
 __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
   const int tid = threadIdx.x;
-  for (int i = tid; i < pc * pc; i += NT) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
+  const int lb = pr | 1, lj = pc | 1;      // odd column strides: no bank conflicts
+  for (int i = tid; i < pc * pc; i += NT) {
+    const int c = i / pc, r = i - c * pc;
+    J[c * lj + r] = (r == c) ? 1.0 : 0.0;
+  }
   __syncthreads();
   if (pc < 2) return 0;
   const int np = pc + (pc & 1), npairs = np / 2;
@@ -204,7 +208,10 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
   // columns below eps64 * |B|_F cannot move any singular value that a
   // relative threshold >= 1e-14 keeps: rotations involving them are skipped
   double nb = 0.0;
-  for (int i = tid; i < pr * pc; i += NT) nb += B[i] * B[i];
+  for (int i = tid; i < pr * pc; i += NT) {
+    const double x = B[(i / pr) * lb + i % pr];
+    nb += x * x;
+  }
   __shared__ double s_nb[(NT / 32)];
   nb = warp_sum(nb);
   if ((tid & 31) == 0) s_nb[tid >> 5] = nb;
@@ -226,8 +233,8 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
           valid = i < pc && j < pc;
         }
         double a = 0.0, b = 0.0, c = 0.0;
-        double* bi = B + (long long)i * pr;
-        double* bj = B + (long long)j * pr;
+        double* bi = B + (long long)i * lb;
+        double* bj = B + (long long)j * lb;
         if (valid)
           for (int r = sub; r < pr; r += gs) {
             double x = bi[r], y = bj[r];
@@ -253,8 +260,8 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
             bi[r] = cs * x - sn * y;
             bj[r] = sn * x + cs * y;
           }
-          double* ji = J + (long long)i * pc;
-          double* jj = J + (long long)j * pc;
+          double* ji = J + (long long)i * lj;
+          double* jj = J + (long long)j * lj;
           for (int r = sub; r < pc; r += gs) {
             double x = ji[r], y = jj[r];
             ji[r] = cs * x - sn * y;
@@ -332,11 +339,11 @@ __device__ __forceinline__ bool task_is_full(const TruncArgs& A, const TaskCtx& 
 }
 
 __host__ __device__ long long trunc_need_doubles(int um, int vm, int R) {
-  return (long long)(um + vm) * R + 4LL * R * R + 4LL * R + 8;
+  return (long long)(um + vm) * R + 4LL * R * R + 6LL * R + 8;
 }
 
 __host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
-  return (long long)(um + vm) * R + 2LL * R * R + 4LL * R + um + vm + 8;
+  return (long long)(um + vm) * R + 2LL * R * R + 6LL * R + um + vm + 8;
 }
 
 __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane);
@@ -359,8 +366,8 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   double* Uw = wk;
   double* Vw = Uw + (long long)um * R;
   double* Bm = Vw + (long long)vm * R;
-  double* Jm = Bm + (long long)R * R;
-  double* Cu = Jm + (long long)R * R;          // pu x keep coefficients
+  double* Jm = Bm + (long long)R * (R + 1);   // odd-strided cores (pr | 1, pc | 1)
+  double* Cu = Jm + (long long)R * (R + 1);          // pu x keep coefficients
   double* Cv = Cu + (long long)R * R;          // pv x keep
   double* tauU = Cv + (long long)R * R;
   double* tauV = tauU + R;
@@ -414,8 +421,8 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
     double s = 0.0;
     for (int l = l0; l < R; ++l)
       s += Uw[(long long)l * um + i] * Vw[(long long)l * vm + j];
-    if (!tr) Bm[(long long)j * pr + i] = s;
-    else Bm[(long long)i * pr + j] = s;
+    if (!tr) Bm[(long long)j * (pr | 1) + i] = s;
+    else Bm[(long long)i * (pr | 1) + j] = s;
   }
   __syncthreads();
   ACR_PH(2);
@@ -436,7 +443,7 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   ACR_PH(3);
   for (int j = tid; j < pc; j += NT) {
     double s = 0.0;
-    const double* bj = Bm + (long long)j * pr;
+    const double* bj = Bm + (long long)j * (pr | 1);
     for (int r = 0; r < pr; ++r) s += bj[r] * bj[r];
     sig[j] = sqrt(s);
   }
@@ -484,12 +491,12 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   for (int idx = tid; idx < pu * keep; idx += NT) {
     const int c = idx / pu, i = idx - c * pu;
     const int j = ord[c];
-    Cu[idx] = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
+    Cu[idx] = tr ? sig[j] * Jm[(long long)j * (pc | 1) + i] : Bm[(long long)j * (pr | 1) + i];
   }
   for (int idx = tid; idx < pv * keep; idx += NT) {
     const int c = idx / pv, i = idx - c * pv;
     const int j = ord[c];
-    Cv[idx] = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
+    Cv[idx] = tr ? Bm[(long long)j * (pr | 1) + i] / sig[j] : Jm[(long long)j * (pc | 1) + i];
   }
   {
     const int half = tid >= NT / 2 ? 1 : 0;
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_trunc_big(TruncArgs A, const i
 // its output factor.  Same arithmetic as trunc_block_full.
 // ---------------------------------------------------------------------------
 __host__ __device__ long long pair_need_doubles(int m, int R) {
-  return (long long)m * R + 4LL * R * R + 3LL * R + 8;
+  return (long long)m * R + 4LL * R * R + 5LL * R + 8;
 }
 
 __device__ __forceinline__ bool task_trivial(const TruncArgs& A, const TaskCtx& c) {
@@ -649,8 +656,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     double* W = sm;
     double* Rs = W + (long long)m * R;        // own R factor, [l][i] = Rs[l * R + i]
     double* Bm = Rs + (long long)R * R;
-    double* Jm = Bm + (long long)R * R;
-    double* Cs = Jm + (long long)R * R;       // own coefficients p x keep
+    double* Jm = Bm + (long long)R * (R + 1);   // odd-strided cores (pr | 1, pc | 1)
+    double* Cs = Jm + (long long)R * (R + 1);       // own coefficients p x keep
     double* tau = Cs + (long long)R * R;
     double* sig = tau + R;
     int* ord = reinterpret_cast<int*>(sig + R);
@@ -697,8 +704,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
         const int l0 = i > j ? i : j;
         double sacc = 0.0;
         for (int l = l0; l < R; ++l) sacc += Rs[l * R + i] * Rv[l * R + j];
-        if (!tr) Bm[(long long)j * pr + i] = sacc;
-        else Bm[(long long)i * pr + j] = sacc;
+        if (!tr) Bm[(long long)j * (pr | 1) + i] = sacc;
+        else Bm[(long long)i * (pr | 1) + j] = sacc;
       }
       __syncthreads();
       ACR_PH(2);
@@ -717,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
       ACR_PH(3);
       for (int j = tid; j < pc; j += TT) {
         double sacc = 0.0;
-        const double* bj = Bm + (long long)j * pr;
+        const double* bj = Bm + (long long)j * (pr | 1);
         for (int r = 0; r < pr; ++r) sacc += bj[r] * bj[r];
         sig[j] = sqrt(sacc);
       }
@@ -747,12 +754,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
       for (int idx = tid; idx < pu * keep; idx += TT) {
         const int cc = idx / pu, i = idx - cc * pu;
         const int j = ord[cc];
-        Cs[idx] = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
+        Cs[idx] = tr ? sig[j] * Jm[(long long)j * (pc | 1) + i] : Bm[(long long)j * (pr | 1) + i];
       }
       for (int idx = tid; idx < pv * keep; idx += TT) {
         const int cc = idx / pv, i = idx - cc * pv;
         const int j = ord[cc];
-        Cv[idx] = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
+        Cv[idx] = tr ? Bm[(long long)j * (pr | 1) + i] / sig[j] : Jm[(long long)j * (pc | 1) + i];
       }
       if (tid == 0) {
         misc[1] = keep;
@@ -1045,7 +1052,11 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
 // one-sided Jacobi on B (pr x pc col-major), J (pc x pc); pairs of a
 // round-robin step are spread over lane groups of size gs
 __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
-  for (int i = lane; i < pc * pc; i += 32) J[i] = (i / pc == i % pc) ? 1.0 : 0.0;
+  const int lb = pr | 1, lj = pc | 1;      // odd column strides: no bank conflicts
+  for (int i = lane; i < pc * pc; i += 32) {
+    const int c = i / pc, r = i - c * pc;
+    J[c * lj + r] = (r == c) ? 1.0 : 0.0;
+  }
   __syncwarp();
   if (pc < 2) return 0;
   const int np = pc + (pc & 1), npairs = np / 2;
@@ -1055,7 +1066,10 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
   const double tol = sqrt((double)pr) * 2.220446049250313e-16;
   const int sub = lane & (gs - 1), grp = lane / gs;
   double nb = 0.0;
-  for (int i = lane; i < pr * pc; i += 32) nb += B[i] * B[i];
+  for (int i = lane; i < pr * pc; i += 32) {
+    const double x = B[(i / pr) * lb + i % pr];
+    nb += x * x;
+  }
   const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
   for (int sweep = 0; sweep < 40; ++sweep) {
     bool rot = false;
@@ -1070,8 +1084,8 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
           valid = i < pc && j < pc;
         }
         double a = 0.0, b = 0.0, c = 0.0;
-        double* bi = B + (long long)i * pr;
-        double* bj = B + (long long)j * pr;
+        double* bi = B + (long long)i * lb;
+        double* bj = B + (long long)j * lb;
         if (valid)
           for (int r = sub; r < pr; r += gs) {
             double x = bi[r], y = bj[r];
@@ -1097,8 +1111,8 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
             bi[r] = cs * x - sn * y;
             bj[r] = sn * x + cs * y;
           }
-          double* ji = J + (long long)i * pc;
-          double* jj = J + (long long)j * pc;
+          double* ji = J + (long long)i * lj;
+          double* jj = J + (long long)j * lj;
           for (int r = sub; r < pc; r += gs) {
             double x = ji[r], y = jj[r];
             ji[r] = cs * x - sn * y;
@@ -1148,8 +1162,8 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   double* Uw = wk;
   double* Vw = Uw + (long long)um * R;
   double* Bm = Vw + (long long)vm * R;
-  double* Jm = Bm + (long long)R * R;
-  double* tauU = Jm + (long long)R * R;
+  double* Jm = Bm + (long long)R * (R + 1);   // odd-strided cores (pr | 1, pc | 1)
+  double* tauU = Jm + (long long)R * (R + 1);
   double* tauV = tauU + R;
   double* sig = tauV + R;
   int* ord = reinterpret_cast<int*>(sig + R);
@@ -1189,8 +1203,8 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     int l0 = i > j ? i : j;
     double s = 0.0;
     for (int l = l0; l < R; ++l) s += Uw[(long long)l * um + i] * Vw[(long long)l * vm + j];
-    if (!tr) Bm[(long long)j * pr + i] = s;
-    else Bm[(long long)i * pr + j] = s;
+    if (!tr) Bm[(long long)j * (pr | 1) + i] = s;
+    else Bm[(long long)i * (pr | 1) + j] = s;
   }
   __syncwarp();
   ACR_PH(2);
@@ -1198,7 +1212,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   ACR_PH(3);
   for (int j = lane; j < pc; j += 32) {
     double s = 0.0;
-    const double* bj = Bm + (long long)j * pr;
+    const double* bj = Bm + (long long)j * (pr | 1);
     for (int r = 0; r < pr; ++r) s += bj[r] * bj[r];
     sig[j] = sqrt(s);
   }
@@ -1240,12 +1254,12 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     const int j = ord[c];
     for (int i = lane; i < um; i += 32) {
       double v = 0.0;
-      if (i < pu) v = tr ? sig[j] * Jm[(long long)j * pc + i] : Bm[(long long)j * pr + i];
+      if (i < pu) v = tr ? sig[j] * Jm[(long long)j * (pc | 1) + i] : Bm[(long long)j * (pr | 1) + i];
       ob[i] = v;
     }
     for (int i = lane; i < vm; i += 32) {
       double v = 0.0;
-      if (i < pv) v = tr ? Bm[(long long)j * pr + i] / sig[j] : Jm[(long long)j * pc + i];
+      if (i < pv) v = tr ? Bm[(long long)j * (pr | 1) + i] / sig[j] : Jm[(long long)j * (pc | 1) + i];
       ob2[i] = v;
     }
     __syncwarp();
