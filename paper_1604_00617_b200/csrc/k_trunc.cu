@@ -347,6 +347,7 @@ __host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
 }
 
 __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane);
+__device__ int blk_jacobi(double* B, int pr, int pc, double* J, int lane);
 
 // ---------------------------------------------------------------------------
 // block path (one CTA per queued task; used for tasks too large for a warp)
@@ -432,7 +433,7 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   if (pc <= 64 && pr <= 128) {
     __shared__ int s_sw;
     if (tid < 32) {
-      const int sw = warp_jacobi(Bm, pr, pc, Jm, tid);
+      const int sw = blk_jacobi(Bm, pr, pc, Jm, tid);
       if (tid == 0) s_sw = sw;
     }
     __syncthreads();
@@ -713,7 +714,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
       if (pc <= 64 && pr <= 128) {
         __shared__ int s_sw;
         if (tid < 32) {
-          const int sw = warp_jacobi(Bm, pr, pc, Jm, tid);
+          const int sw = blk_jacobi(Bm, pr, pc, Jm, tid);
           if (tid == 0) s_sw = sw;
         }
         __syncthreads();
@@ -1048,6 +1049,118 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
 }
 
 
+
+// Single-warp Jacobi of the block and CTA-pair paths (one warp on the task's
+// critical path, 128 registers available): same pairing, lane groups,
+// arithmetic and order as warp_jacobi, with the row loops unrolled to RPL rows
+// per lane and each lane's elements kept in registers between the norms and
+// the rotation, so the loads of a step issue together instead of one
+// dependent shared-memory round trip per row.
+template <int RPL>
+__device__ int blk_jacobi_t(double* B, int pr, int pc, double* J, int lane, int gs) {
+  const int lb = pr | 1, lj = pc | 1;
+  const int np = pc + (pc & 1), npairs = np / 2;
+  const int per = 32 / gs;
+  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  const int sub = lane & (gs - 1), grp = lane / gs;
+  double nb = 0.0;
+  for (int i = lane; i < pr * pc; i += 32) {
+    const double x = B[(i / pr) * lb + i % pr];
+    nb += x * x;
+  }
+  const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rot = false;
+    for (int step = 0; step < np - 1; ++step) {
+      for (int base = 0; base < npairs; base += per) {
+        const int k = base + grp;
+        int i = 0, j = 0;
+        bool valid = k < npairs;
+        if (valid) {
+          i = rr_player(step, k, np);
+          j = rr_player(step, np - 1 - k, np);
+          valid = i < pc && j < pc;
+        }
+        double* bi = B + (long long)i * lb;
+        double* bj = B + (long long)j * lb;
+        double xr[RPL], yr[RPL];
+#pragma unroll
+        for (int h = 0; h < RPL; ++h) {
+          const int r = sub + gs * h;
+          const bool in = valid && r < pr;
+          xr[h] = in ? bi[r] : 0.0;
+          yr[h] = in ? bj[r] : 0.0;
+        }
+        double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+        for (int h = 0; h < RPL; ++h) {
+          if (sub + gs * h < pr) {
+            a += xr[h] * xr[h];
+            b += yr[h] * yr[h];
+            c += xr[h] * yr[h];
+          }
+        }
+        for (int o = gs >> 1; o; o >>= 1) {
+          a += __shfl_xor_sync(FULL, a, o);
+          b += __shfl_xor_sync(FULL, b, o);
+          c += __shfl_xor_sync(FULL, c, o);
+        }
+        if (valid && a > tiny && b > tiny && c != 0.0 &&
+            c * c > tol * tol * a * b) {
+          const double d = b - a, e = 2.0 * c;
+          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
+          double* ji = J + (long long)i * lj;
+          double* jj = J + (long long)j * lj;
+          double xj[RPL], yj[RPL];
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) {
+            const int r = sub + gs * h;
+            xj[h] = r < pc ? ji[r] : 0.0;
+            yj[h] = r < pc ? jj[r] : 0.0;
+          }
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) {
+            const int r = sub + gs * h;
+            if (r < pr) {
+              bi[r] = cs * xr[h] - sn * yr[h];
+              bj[r] = sn * xr[h] + cs * yr[h];
+            }
+            if (r < pc) {
+              ji[r] = cs * xj[h] - sn * yj[h];
+              jj[r] = sn * xj[h] + cs * yj[h];
+            }
+          }
+          rot = true;
+        }
+        __syncwarp();
+      }
+    }
+    if (!__any_sync(FULL, rot)) return sweep + 1;
+  }
+  return 40;
+}
+
+__device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane);
+
+__device__ int blk_jacobi(double* B, int pr, int pc, double* J, int lane) {
+  if (pc < 2 || pr > 4 * 32) return warp_jacobi(B, pr, pc, J, lane);
+  const int lj = pc | 1;
+  for (int i = lane; i < pc * pc; i += 32) {
+    const int c = i / pc, r = i - c * pc;
+    J[c * lj + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  const int npairs = (pc + (pc & 1)) / 2;
+  int gs = 32;
+  while (gs > 1 && gs * npairs > 32) gs >>= 1;
+  const int rpl = (pr + gs - 1) / gs;
+  if (rpl <= 1) return blk_jacobi_t<1>(B, pr, pc, J, lane, gs);
+  if (rpl <= 2) return blk_jacobi_t<2>(B, pr, pc, J, lane, gs);
+  if (rpl <= 4) return blk_jacobi_t<4>(B, pr, pc, J, lane, gs);
+  return warp_jacobi(B, pr, pc, J, lane);
+}
 
 // one-sided Jacobi on B (pr x pc col-major), J (pc x pc); pairs of a
 // round-robin step are spread over lane groups of size gs
