@@ -239,44 +239,71 @@ struct HBRoots {
   int lam, cnt, cp;
   int off[16], cols[16], mus[16];
   int steps[16];              // mu = anc(lam, steps)
+  int slot[16];               // mm_slot(mu): output panel slot of the root
 };
 
-__device__ __forceinline__ bool hb_roots(const TreeDev& T, const MMJob& J, int g, int path,
-                                         HBRoots& R) {
-  R.cnt = 0;
+// The root table of a CTA, built once in shared memory by its first warp: in
+// path mode lane t looks at ancestor t of the leaf (the tree-metadata and rank
+// loads of all ancestors are issued together instead of one dependent chain
+// per ancestor in every thread), the nonzero roots are compacted in t order
+// (ballot) and their column offsets formed by a warp scan: the same table,
+// in the same order, as the sequential walk of hb_roots.
+__device__ __forceinline__ void hb_roots_shared(const TreeDev& T, const MMJob& J, int g,
+                                                int path, HBRoots& R) {
+  const int lane = threadIdx.x & 31;
   if (path) {
-    R.lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
-    const int* an = T.anc + R.lam * (T.maxdepth + 1);
-    const int dl = T.depth[R.lam];
-    for (int t = 0; t < dl && t < 16; ++t) {
-      const int mu = an[t];
-      if (mu < J.mu0 || mu >= J.mu1) continue;
-      const int c = mm_cols(J, T, g, mu);
-      if (!c) continue;
-      R.mus[R.cnt] = mu;
-      R.cols[R.cnt] = c;
-      R.steps[R.cnt] = t;
-      R.off[R.cnt] = R.cnt == 0 ? 0 : R.off[R.cnt - 1] + ((R.cols[R.cnt - 1] + 1) & ~1);
-      ++R.cnt;
+    const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
+    const int dl = T.depth[lam];
+    int mu = -1, c = 0, slot = 0;
+    if (lane < dl && lane < 16) {
+      mu = T.anc[lam * (T.maxdepth + 1) + lane];
+      if (mu >= J.mu0 && mu < J.mu1) {
+        c = mm_cols(J, T, g, mu);
+        slot = mm_slot(T, mu);
+      }
     }
-  } else {
-    const int b0 = T.startB[J.mu0], nB = T.startB[J.mu1] - b0;
-    if ((int)blockIdx.x >= nB) return false;
-    const int mu = T.listB[(b0 + blockIdx.x) * 2];
-    R.lam = T.listB[(b0 + blockIdx.x) * 2 + 1];
-    const int c = mm_cols(J, T, g, mu);
+    const unsigned m = __ballot_sync(0xffffffffu, c != 0);
+    const int pos = __popc(m & ((1u << lane) - 1u));
+    const int padded = c ? ((c + 1) & ~1) : 0;
+    int incl = padded;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
     if (c) {
-      R.mus[0] = mu;
-      R.cols[0] = c;
-      R.off[0] = 0;
-      R.steps[0] = T.depth[R.lam] - T.depth[mu];
-      R.cnt = 1;
+      R.mus[pos] = mu;
+      R.cols[pos] = c;
+      R.steps[pos] = lane;
+      R.off[pos] = incl - padded;
+      R.slot[pos] = slot;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 0) {
+      R.lam = lam;
+      R.cnt = __popc(m);
+      R.cp = tot;
+    }
+  } else if (lane == 0) {
+    R.cnt = 0;
+    const int b0 = T.startB[J.mu0], nB = T.startB[J.mu1] - b0;
+    if ((int)blockIdx.x < nB) {
+      const int mu = T.listB[(b0 + blockIdx.x) * 2];
+      R.lam = T.listB[(b0 + blockIdx.x) * 2 + 1];
+      const int c = mm_cols(J, T, g, mu);
+      if (c) {
+        R.mus[0] = mu;
+        R.cols[0] = c;
+        R.off[0] = 0;
+        R.steps[0] = T.depth[R.lam] - T.depth[mu];
+        R.slot[0] = mm_slot(T, mu);
+        R.cnt = 1;
+        R.cp = (c + 1) & ~1;
+      }
     }
   }
-  if (!R.cnt) return false;
-  R.cp = R.off[R.cnt - 1] + ((R.cols[R.cnt - 1] + 1) & ~1);
-  return true;
 }
+
 
 // ancestor walk of every root, tabulated once per CTA (k = steps above lam)
 struct HBAnc {
@@ -329,7 +356,7 @@ __device__ __forceinline__ void hb_finish_tab(const TreeDev& T, const MMJob& J, 
     y0 = y0 + z0;
     y1 = y1 + z1;
   }
-  const int slot = mm_slot(T, R.mus[q]);
+  const int slot = R.slot[q];
   src_col(J.Y, n, g, slot, b0)[lo + i] = J.alpha * y0;
   if (nb > 1) src_col(J.Y, n, g, slot, b0 + 1)[lo + i] = J.alpha * y1;
 }
@@ -341,8 +368,10 @@ __global__ void __launch_bounds__(NTB) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int pat
   extern __shared__ double sm[];
   const MMJob& J = JJ.j[blockIdx.z];
   const int g = blockIdx.y, bw = T.bw;
-  HBRoots R;
-  if (!hb_roots(T, J, g, path, R)) return;
+  __shared__ HBRoots R;
+  if (threadIdx.x < 32) hb_roots_shared(T, J, g, path, R);
+  __syncthreads();
+  if (!R.cnt) return;
   const HB h = J.H[g];
   const int lam = R.lam, lo = T.lo[lam], s = T.hi[lam] - lo, cp = R.cp;
   const int ld = s + 1;
@@ -358,7 +387,7 @@ __global__ void __launch_bounds__(NTB) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int pat
   for (int w0 = 0; w0 < cp; w0 += xc) {
     const int wc = cp - w0 < xc ? cp - w0 : xc;
     for (int q = 0; q < R.cnt; ++q) {
-      const int slot = mm_slot(T, R.mus[q]);
+      const int slot = R.slot[q];
       const int q0 = R.off[q], q1 = q0 + ((R.cols[q] + 1) & ~1);
       const int c0 = q0 > w0 ? q0 : w0, c1 = q1 < w0 + wc ? q1 : w0 + wc;
       for (int pos = c0 + warp; pos < c1; pos += NTB / 32) {
