@@ -378,16 +378,36 @@ __device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* 
   long long ph[6] = {0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
 #define ACR_PH(i) do { if (A.ctr) { long long t_ = clock64(); ph[i] += t_ - t_ph; t_ph = t_; } } while (0)
-  for (int idx = tid; idx < um * R; idx += NT) {
-    int c = idx / um, i = idx - c * um;
-    Uw[idx] = c < a.r ? a.sc * a.U[(long long)c * n + i]
-                      : b.sc * b.U[(long long)(c - a.r) * n + i];
+  // operands by asynchronous copies (every element of a thread in flight at
+  // once); the exact sign scales of the U columns applied after the wait.
+  // Work areas in global scratch (tasks larger than shared memory) load
+  // synchronously.
+  if (!__isShared(Uw)) {
+    for (int idx = tid; idx < um * R; idx += NT) {
+      int c = idx / um, i = idx - c * um;
+      Uw[idx] = c < a.r ? a.sc * a.U[(long long)c * n + i]
+                        : b.sc * b.U[(long long)(c - a.r) * n + i];
+    }
+    for (int idx = tid; idx < vm * R; idx += NT) {
+      int c = idx / vm, i = idx - c * vm;
+      Vw[idx] = c < a.r ? a.V[(long long)c * n + i] : b.V[(long long)(c - a.r) * n + i];
+    }
+    __syncthreads();
+  } else {
+  for (int c = 0; c < R; ++c) {
+    const double* su = c < a.r ? a.U + (long long)c * n : b.U + (long long)(c - a.r) * n;
+    const double* sv = c < a.r ? a.V + (long long)c * n : b.V + (long long)(c - a.r) * n;
+    for (int i = tid; i < um; i += NT) cp_async8(Uw + (long long)c * um + i, su + i, true);
+    for (int i = tid; i < vm; i += NT) cp_async8(Vw + (long long)c * vm + i, sv + i, true);
   }
-  for (int idx = tid; idx < vm * R; idx += NT) {
-    int c = idx / vm, i = idx - c * vm;
-    Vw[idx] = c < a.r ? a.V[(long long)c * n + i] : b.V[(long long)(c - a.r) * n + i];
-  }
+  cp_async_wait_all();
   __syncthreads();
+  if (a.sc != 1.0 || b.sc != 1.0) {
+    for (int idx = tid; idx < um * R; idx += NT)
+      Uw[idx] *= idx < um * a.r ? a.sc : b.sc;
+    __syncthreads();
+  }
+  }
   ACR_PH(0);
   {
     const int half = tid >= NT / 2 ? 1 : 0;
@@ -665,17 +685,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     double* misc = sig + 2 * R;               // [0] |R|_F^2, [1] keep
     long long ph[6] = {0, 0, 0, 0, 0, 0};
     long long t_ph = clock64();
-    for (int idx = tid; idx < m * R; idx += TT) {
-      const int cc = idx / m, i = idx - cc * m;
-      double v;
-      if (side == 0)
-        v = cc < a.r ? a.sc * a.U[(long long)cc * n + i]
-                     : b.sc * b.U[(long long)(cc - a.r) * n + i];
-      else
-        v = cc < a.r ? a.V[(long long)cc * n + i] : b.V[(long long)(cc - a.r) * n + i];
-      W[idx] = v;
+    for (int cc = 0; cc < R; ++cc) {
+      const double* src = side == 0
+          ? (cc < a.r ? a.U + (long long)cc * n : b.U + (long long)(cc - a.r) * n)
+          : (cc < a.r ? a.V + (long long)cc * n : b.V + (long long)(cc - a.r) * n);
+      for (int i = tid; i < m; i += TT) cp_async8(W + (long long)cc * m + i, src + i, true);
     }
+    cp_async_wait_all();
     __syncthreads();
+    if (side == 0 && (a.sc != 1.0 || b.sc != 1.0)) {
+      for (int idx = tid; idx < m * R; idx += TT) W[idx] *= idx < m * a.r ? a.sc : b.sc;
+      __syncthreads();
+    }
     ACR_PH(0);
     const Grp gf{1, TT, tid, NWB, tid >> 5, tid & 31, red, nullptr};
     group_qr(W, m, R, tau, gf);
