@@ -342,8 +342,10 @@ __host__ __device__ long long trunc_need_doubles(int um, int vm, int R) {
   return (long long)(um + vm) * R + 4LL * R * R + 6LL * R + 8;
 }
 
+// panels (um + vm) R, cores B and J R (R + 1) each (odd strides), tau_u, tau_v,
+// sig R each, the rank order R ints, the output columns um + vm
 __host__ __device__ long long warp_need_doubles(int um, int vm, int R) {
-  return (long long)(um + vm) * R + 2LL * R * R + 6LL * R + um + vm + 8;
+  return (long long)(um + vm) * R + 2LL * R * (R + 1) + 3LL * R + (R + 1) / 2 + um + vm;
 }
 
 __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane);
@@ -1382,7 +1384,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
     atomicAdd(A.ctr + 9, 1ull);
     atomicAdd(A.ctr + 11, (unsigned long long)sweeps);
   }
-  double* ob = sig + 2 * R;          // one output column per side (um + vm)
+  double* ob = sig + R + (R + 1) / 2; // after the R ints of ord: one output column per side
   double* ob2 = ob + um;
   for (int c = 0; c < keep; ++c) {
     const int j = ord[c];
