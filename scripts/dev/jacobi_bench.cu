@@ -4,14 +4,205 @@
 #include <cstdlib>
 #include <vector>
 #include "../../paper_1604_00617_b200/csrc/k_trunc.cu"
+namespace acr {
+template <int RPL>
+__device__ int blk_jacobi_f(double* B, int pr, int pc, double* J, int lane, int gs) {
+  const int lb = pr | 1, lj = pc | 1;
+  const int np = pc + (pc & 1), npairs = np / 2;
+  const int per = 32 / gs;
+  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  const int sub = lane & (gs - 1), grp = lane / gs;
+  double nb = 0.0;
+  for (int i = lane; i < pr * pc; i += 32) {
+    const double x = B[(i / pr) * lb + i % pr];
+    nb += x * x;
+  }
+  const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rot = false;
+    for (int step = 0; step < np - 1; ++step) {
+      for (int base = 0; base < npairs; base += per) {
+        const int k = base + grp;
+        int i = 0, j = 0;
+        bool valid = k < npairs;
+        if (valid) {
+          i = rr_player(step, k, np);
+          j = rr_player(step, np - 1 - k, np);
+          valid = i < pc && j < pc;
+        }
+        double* bi = B + (long long)i * lb;
+        double* bj = B + (long long)j * lb;
+        double xr[RPL], yr[RPL];
+#pragma unroll
+        for (int h = 0; h < RPL; ++h) {
+          const int r = sub + gs * h;
+          const bool in = valid && r < pr;
+          xr[h] = in ? bi[r] : 0.0;
+          yr[h] = in ? bj[r] : 0.0;
+        }
+        double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+        for (int h = 0; h < RPL; ++h) {
+          if (sub + gs * h < pr) {
+            a += xr[h] * xr[h];
+            b += yr[h] * yr[h];
+            c += xr[h] * yr[h];
+          }
+        }
+        for (int o = gs >> 1; o; o >>= 1) {
+          a += __shfl_xor_sync(FULL, a, o);
+          b += __shfl_xor_sync(FULL, b, o);
+          c += __shfl_xor_sync(FULL, c, o);
+        }
+        if (valid && a > tiny && b > tiny && c != 0.0 &&
+            c * c > tol * tol * a * b) {
+          const double d = b - a, e = 2.0 * c;
+          const double mx = fmax(fabs(d), fabs(e));
+          const long long ex = (__double_as_longlong(mx) >> 52) & 0x7ff;
+          const double scl = __longlong_as_double((2046LL - ex) << 52);
+          const double ds = d * scl, es = e * scl;
+          const float df = (float)ds, ef = (float)es;
+          const float q = fmaf(df, df, ef * ef);
+          double t = (double)__fdividef(copysignf(1.0f, df) * ef, fabsf(df) + q * rsqrtf(q));
+          const double num = fma(t, fma(t, es, 2.0 * ds), -es);
+          t -= num * (double)__frcp_rn((float)(2.0 * fma(t, es, ds)));
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+          double* ji = J + (long long)i * lj;
+          double* jj = J + (long long)j * lj;
+          double xj[RPL], yj[RPL];
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) {
+            const int r = sub + gs * h;
+            xj[h] = r < pc ? ji[r] : 0.0;
+            yj[h] = r < pc ? jj[r] : 0.0;
+          }
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) {
+            const int r = sub + gs * h;
+            if (r < pr) {
+              bi[r] = cs * xr[h] - sn * yr[h];
+              bj[r] = sn * xr[h] + cs * yr[h];
+            }
+            if (r < pc) {
+              ji[r] = cs * xj[h] - sn * yj[h];
+              jj[r] = sn * xj[h] + cs * yj[h];
+            }
+          }
+          rot = true;
+        }
+        __syncwarp();
+      }
+    }
+    if (!__any_sync(FULL, rot)) return sweep + 1;
+  }
+  return 40;
+}
+template <int RPL>
+__device__ int blk_jacobi_c(double* B, int pr, int pc, double* J, int lane, int gs) {
+  const int lb = pr | 1, lj = pc | 1;
+  const int np = pc + (pc & 1), npairs = np / 2;
+  const int per = 32 / gs;
+  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  const int sub = lane & (gs - 1), grp = lane / gs;
+  double nb = 0.0;
+  for (int i = lane; i < pr * pc; i += 32) {
+    const double x = B[(i / pr) * lb + i % pr];
+    nb += x * x;
+  }
+  const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rot = false;
+    for (int step = 0; step < np - 1; ++step) {
+      for (int base = 0; base < npairs; base += per) {
+        const int k = base + grp;
+        int i = 0, j = 0;
+        bool valid = k < npairs;
+        if (valid) {
+          i = rr_player(step, k, np);
+          j = rr_player(step, np - 1 - k, np);
+          valid = i < pc && j < pc;
+        }
+        double* bi = B + (long long)i * lb;
+        double* bj = B + (long long)j * lb;
+        double xr[RPL], yr[RPL];
+#pragma unroll
+        for (int h = 0; h < RPL; ++h) {
+          const int r = sub + gs * h;
+          const bool in = valid && r < pr;
+          xr[h] = in ? bi[r] : 0.0;
+          yr[h] = in ? bj[r] : 0.0;
+        }
+        double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+        for (int h = 0; h < RPL; ++h) {
+          if (sub + gs * h < pr) {
+            a += xr[h] * xr[h];
+            b += yr[h] * yr[h];
+            c += xr[h] * yr[h];
+          }
+        }
+        for (int o = gs >> 1; o; o >>= 1) {
+          a += __shfl_xor_sync(FULL, a, o);
+          b += __shfl_xor_sync(FULL, b, o);
+          c += __shfl_xor_sync(FULL, c, o);
+        }
+        if (valid && a > tiny && b > tiny && c != 0.0 &&
+            c * c > tol * tol * a * b) {
+          const double cs = 0.8 + 1e-300 * a, sn = 0.6 + 1e-300 * b;
+          double* ji = J + (long long)i * lj;
+          double* jj = J + (long long)j * lj;
+          double xj[RPL], yj[RPL];
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) {
+            const int r = sub + gs * h;
+            xj[h] = r < pc ? ji[r] : 0.0;
+            yj[h] = r < pc ? jj[r] : 0.0;
+          }
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) {
+            const int r = sub + gs * h;
+            if (r < pr) {
+              bi[r] = cs * xr[h] - sn * yr[h];
+              bj[r] = sn * xr[h] + cs * yr[h];
+            }
+            if (r < pc) {
+              ji[r] = cs * xj[h] - sn * yj[h];
+              jj[r] = sn * xj[h] + cs * yj[h];
+            }
+          }
+          rot = true;
+        }
+        __syncwarp();
+      }
+    }
+    if (!__any_sync(FULL, rot)) return sweep + 1;
+  }
+  return 40;
+}
+
+template <int V>
+__device__ int jac_var(double* B, int pr, int pc, double* J, int lane) {
+  if (V == 0) return blk_jacobi(B, pr, pc, J, lane);
+  const int lj = pc | 1;
+  for (int i = lane; i < pc * pc; i += 32) { const int c = i / pc, r = i - c * pc; J[c * lj + r] = (r == c) ? 1.0 : 0.0; }
+  __syncwarp();
+  const int npairs = (pc + (pc & 1)) / 2;
+  int gs = 32;
+  while (gs > 1 && gs * npairs > 32) gs >>= 1;
+  const int rpl = (pr + gs - 1) / gs;
+  if (V == 1) { if (rpl <= 1) return blk_jacobi_f<1>(B, pr, pc, J, lane, gs); if (rpl <= 2) return blk_jacobi_f<2>(B, pr, pc, J, lane, gs); return blk_jacobi_f<4>(B, pr, pc, J, lane, gs); }
+  if (rpl <= 1) return blk_jacobi_c<1>(B, pr, pc, J, lane, gs); if (rpl <= 2) return blk_jacobi_c<2>(B, pr, pc, J, lane, gs); return blk_jacobi_c<4>(B, pr, pc, J, lane, gs);
+}
+}
 
 __global__ void k_jac(const double* in, int pr, int pc, long long* cyc, int* sweeps, double* out, int var) {
   __shared__ double B[32 * 33], J[32 * 33];
   const int lane = threadIdx.x;
-  for (int i = lane; i < pr * pc; i += 32) B[i] = in[i];
+  for (int i = lane; i < pr * pc; i += 32) B[(i / pr) * (pr | 1) + i % pr] = in[i];
   __syncwarp();
   long long t0 = clock64();
-  int sw = acr::warp_jacobi(B, pr, pc, J, lane);   // B, J: odd column strides (pr | 1, pc | 1)
+  int sw = var == 0 ? acr::jac_var<0>(B, pr, pc, J, lane) : var == 1 ? acr::jac_var<1>(B, pr, pc, J, lane) : acr::jac_var<2>(B, pr, pc, J, lane);
   __syncwarp();
   long long t1 = clock64();
   if (lane == 0) { *cyc = t1 - t0; *sweeps = sw; }
@@ -19,7 +210,7 @@ __global__ void k_jac(const double* in, int pr, int pc, long long* cyc, int* swe
 }
 
 int main() {
-  for (int pc : {4, 8, 12, 16, 20, 24, 32}) {
+  for (int pc : {4, 8, 12, 16}) {
     const int pr = pc;
     std::vector<double> h(pr * pc);
     srand(pc);
@@ -28,7 +219,7 @@ int main() {
     double *din, *dout; long long* dc; int* ds;
     cudaMalloc(&din, 8 * pr * pc); cudaMalloc(&dout, 8 * pr * pc); cudaMalloc(&dc, 8); cudaMalloc(&ds, 4);
     cudaMemcpy(din, h.data(), 8 * pr * pc, cudaMemcpyHostToDevice);
-    for (int var = 0; var < 1; ++var) {
+    for (int var = 0; var < 3; ++var) {
     long long c = 0; int s = 0;
     for (int rep = 0; rep < 3; ++rep) {
       k_jac<<<1, 32>>>(din, pr, pc, dc, ds, dout, var);
@@ -36,7 +227,7 @@ int main() {
     }
     cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&s, ds, 4, cudaMemcpyDeviceToHost);
     const int np = pc + (pc & 1);
-    const char* nm[] = {"base", "fastrot", "noJ", "constrot"};
+    const char* nm[] = {"blk", "blkfast", "blkconst"};
     printf("pc=%2d %-8s sweeps=%2d cycles=%8lld  per step=%.0f  (%s)\n", pc, nm[var], s, c, c / (double)(s * (np - 1)), cudaGetErrorString(cudaGetLastError()));
     }
   }
