@@ -355,7 +355,7 @@ __device__ int blk_jacobi(double* B, int pr, int pc, double* J, int lane);
 // block path (one CTA per queued task; used for tasks too large for a warp)
 // ---------------------------------------------------------------------------
 template <int NT>
-__device__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
+__device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
                                  double* red, int* iflag) {
   const int tid = threadIdx.x, n = A.T.n;
   const OpRes& a = tc.a;
@@ -622,15 +622,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_trunc_big(TruncArgs A, const i
     }
     const int R = c.a.r + c.b.r;
     const long long need = trunc_need_doubles(c.um, c.vm, R);
-    double* wk = sm;
     if (need > A.smem_doubles) {
       if (A.gscr == nullptr || need > A.gscr_stride) {
         if (threadIdx.x == 0) atomicMax(A.overflow, 1 << 29);
         continue;
       }
-      wk = A.gscr + (long long)blockIdx.x * A.gscr_stride;
+      trunc_block_full<NT>(A, c, A.gscr + (long long)blockIdx.x * A.gscr_stride, red, iflag);
+    } else {
+      // separate inlined copy on the shared-memory work area: LDS / STS
+      // instead of generic loads and stores
+      trunc_block_full<NT>(A, c, sm, red, iflag);
     }
-    trunc_block_full<NT>(A, c, wk, red, iflag);
     __syncthreads();
   }
 }
