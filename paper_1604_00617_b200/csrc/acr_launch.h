@@ -65,7 +65,8 @@ cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
                            int ld, cudaStream_t st);
 // work: unused (reserved), pass null
 cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work, cudaStream_t st);
-cudaError_t lu_solve(const double* A, int N, const int* piv, double* B,
+cudaError_t lu_transpose(const double* A, int N, double* At, cudaStream_t st);
+cudaError_t lu_solve(const double* A, const double* At, int N, const int* piv, double* B,
                      int nrhs, cudaStream_t st);
 cudaError_t launch_rhs_in(const double* rhs, int N, int k, int n, double* P,
                           cudaStream_t st);

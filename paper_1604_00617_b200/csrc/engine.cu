@@ -443,6 +443,8 @@ struct Plan {
   std::vector<Level> kept;
   Level last;
   Dev lu, piv, info;
+  Dev lut;                    // LU factors transposed for the cutoff solve (per factor)
+  bool lut_ok = false;
   int Nc = 0;
   std::vector<Profile> prof;
   std::vector<std::vector<int>> lastR;   // host ranks of the final level D, E, F
@@ -1437,6 +1439,7 @@ struct Plan {
       CK(launch_todense(dt.T, tab.as<HB>(), cntb, drc.as<int>(), drc.as<int>() + cntb,
                         lu.as<double>(), Nc, st));
       CK(lu_factor(lu.as<double>(), Nc, piv.as<int>(), info.as<int>(), nullptr, st));
+      lut_ok = false;
       launches += 1 + 4 * ((Nc + 31) / 32);
       int hinfo = 0;
       CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1563,7 +1566,13 @@ struct Plan {
         CK(cudaMemcpy2DAsync(B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
                              f[L].as<double>() + i * kn, sizeof(double) * n,
                              sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
-      CK(lu_solve(lu.as<double>(), Nc, piv.as<int>(), B.as<double>(), k, st));
+      if (!lut_ok) {
+        if (lut.n < sizeof(double) * (size_t)Nc * Nc) lut.alloc(sizeof(double) * (size_t)Nc * Nc, st);
+        CK(lu_transpose(lu.as<double>(), Nc, lut.as<double>(), st));
+        ++launches;
+        lut_ok = true;
+      }
+      CK(lu_solve(lu.as<double>(), lut.as<double>(), Nc, piv.as<int>(), B.as<double>(), k, st));
       ++launches;
       for (int i = 0; i < mc; ++i)
         CK(cudaMemcpy2DAsync(uu[L].as<double>() + i * kn, sizeof(double) * n,

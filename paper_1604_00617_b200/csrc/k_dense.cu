@@ -481,8 +481,24 @@ __global__ void __launch_bounds__(1024) k_lu_solve(const double* A, int N,
 // result is identical.
 static constexpr int LS_T = 1024;
 
-__global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, int N, const int* piv,
-                                                      double* B) {
+// At: the LU factors transposed (column-major), so that the block updates'
+// reads A[i][b0 + k] = At[(b0 + k) N + i] are coalesced over the rows i
+__global__ void k_transpose(const double* A, int N, double* At) {
+  __shared__ double t[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = by + r, j = bx + threadIdx.x;
+    if (i < N && j < N) t[r][threadIdx.x] = A[(long long)i * N + j];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int j = bx + r, i = by + threadIdx.x;
+    if (i < N && j < N) At[(long long)j * N + i] = t[threadIdx.x][r];
+  }
+}
+
+__global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, const double* At,
+                                                      int N, const int* piv, double* B) {
   extern __shared__ double y[];                 // N doubles, then N ints
   int* pv = reinterpret_cast<int*>(y + N);
   __shared__ double T[32][33];
@@ -514,12 +530,12 @@ __global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, int N
     }
     __syncthreads();
     for (int i = b0 + bs + tid; i < N; i += LS_T) {
-      const double* ar = A + (long long)i * N + b0;
+      const double* ar = At + (long long)b0 * N + i;   // A[i][b0 + k] = ar[k N]
       double v = y[i];
       for (int kb = 0; kb < bs; kb += 8) {       // 8 loads in flight, order kept
         double a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = kb + u < bs ? ar[kb + u] : 0.0;
+        for (int u = 0; u < 8; ++u) a[u] = kb + u < bs ? ar[(long long)(kb + u) * N] : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (kb + u < bs) v -= a[u] * y[b0 + kb + u];
@@ -547,12 +563,12 @@ __global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, int N
     }
     __syncthreads();
     for (int i = tid; i < b0; i += LS_T) {
-      const double* ar = A + (long long)i * N + b0;
+      const double* ar = At + (long long)b0 * N + i;   // A[i][b0 + k] = ar[k N]
       double v = y[i];
       for (int kb = bs - 1; kb >= 0; kb -= 8) {  // descending, 8 loads in flight
         double a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = kb - u >= 0 ? ar[kb - u] : 0.0;
+        for (int u = 0; u < 8; ++u) a[u] = kb - u >= 0 ? ar[(long long)(kb - u) * N] : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (kb - u >= 0) v -= a[u] * y[b0 + kb - u];
@@ -564,18 +580,24 @@ __global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, int N
   for (int i = tid; i < N; i += LS_T) b[i] = y[i];
 }
 
-cudaError_t lu_solve(const double* A, int N, const int* piv, double* B,
+cudaError_t lu_transpose(const double* A, int N, double* At, cudaStream_t st) {
+  dim3 g((N + 31) / 32, (N + 31) / 32), b(32, 8);
+  k_transpose<<<g, b, 0, st>>>(A, N, At);
+  return cudaGetLastError();
+}
+
+cudaError_t lu_solve(const double* A, const double* At, int N, const int* piv, double* B,
                      int nrhs, cudaStream_t st) {
   if (!nrhs) return cudaSuccess;
   const size_t smem = (size_t)N * (sizeof(double) + sizeof(int));
-  if (smem <= 160 * 1024) {
+  if (smem <= 160 * 1024 && At) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_lu_solve_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024);
       attr = true;
     }
-    k_lu_solve_blk<<<nrhs, LS_T, smem, st>>>(A, N, piv, B);
+    k_lu_solve_blk<<<nrhs, LS_T, smem, st>>>(A, At, N, piv, B);
   } else {
     k_lu_solve<<<nrhs, 1024, 0, st>>>(A, N, piv, B);
   }
