@@ -241,7 +241,7 @@ def run_ours(args):
     u_d = torch.zeros_like(rhs_d)
     h2d = sum(h.numel() * 8 for h in host) + rhs_h.numel() * 8
     d2h = u_h.numel() * 8
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(args.steps, 5))
 
     copy_stream = torch.cuda.Stream()
 
@@ -263,11 +263,48 @@ def run_ours(args):
     e2e_step()                                      # untimed: first-use buffers
     torch.cuda.synchronize()
     barrier()
+    # timed: the same per-step work through the public API, double-buffered
+    # as an application would pipeline it -- step i+1's bands upload (copy
+    # stream) and step i's u download (second copy stream) overlap the
+    # factorisations; every step still copies its inputs from pinned host
+    # memory and its result back, inside the timed region
+    dev2 = [dev, [torch.empty_like(h, device="cuda") for h in host]]
+    up_stream, down_stream = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_bands = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_used = [None, None]
     a0 = torch.cuda.Event(enable_timing=True)
     a1 = torch.cuda.Event(enable_timing=True)
     a0.record(stream)
-    for _ in range(e2e_steps):
-        u = e2e_step()
+    up_stream.wait_stream(stream)
+    with torch.cuda.stream(up_stream):
+        for d, h in zip(dev2[0], host):
+            d.copy_(h, non_blocking=True)
+        ev_bands[0].record(up_stream)
+    for i in range(e2e_steps):
+        kb = i % 2
+        if i + 1 < e2e_steps:                       # prefetch the next step's bands
+            if ev_used[1 - kb] is not None:
+                up_stream.wait_event(ev_used[1 - kb])
+            with torch.cuda.stream(up_stream):
+                for d, h in zip(dev2[1 - kb], host):
+                    d.copy_(h, non_blocking=True)
+                ev_bands[1 - kb].record(up_stream)
+        stream.wait_event(ev_bands[kb])
+        copy_stream.wait_stream(stream)             # rhs_d free (previous solve done)
+        with torch.cuda.stream(copy_stream):
+            rhs_d.copy_(rhs_h, non_blocking=True)
+        solver.factor(dev2[kb])
+        ev_used[kb] = torch.cuda.Event()
+        ev_used[kb].record(stream)
+        stream.wait_stream(copy_stream)
+        uu = solver.solve(rhs_d) if ws == 1 else solver.solve(rhs_d, u_d)
+        down_stream.wait_stream(stream)
+        with torch.cuda.stream(down_stream):
+            u_h.copy_(uu, non_blocking=True)
+        uu.record_stream(down_stream)
+        u = uu
+    stream.wait_stream(down_stream)
+    stream.wait_stream(up_stream)
     a1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = a0.elapsed_time(a1) / e2e_steps
@@ -390,6 +427,9 @@ def run_ours(args):
         "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms, "solve_ms": solve_ms,
+                "pipelining": "double-buffered: next step's bands H2D and this step's u D2H "
+                              "on copy streams overlap the factorisations; first upload and "
+                              "last download exposed", "steps": e2e_steps,
                 "residual_max_col": res_max, "residual_fro": res_fro},
         "gpu_launches": launches_per_factor * args.steps,
         "roofline": roofline, "roofline_fp64": roofline_fp64, "roofline_e2e": roofline_e2e,
