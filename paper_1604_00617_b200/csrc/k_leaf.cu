@@ -468,6 +468,39 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
       cp_async8(sb + i * GLD + j, in ? Lb + (long long)i * bw + j : Lb, in);
     }
   }
+  // ancestor table (parent first), built once per CTA by the first warp while
+  // the leaves land: lane t holds ancestor t + 1 of the leaf; its rank, slot
+  // and staging offset (prefix of padded ranks over the nonzero ones)
+  __shared__ int a_r[32], a_slot[32], a_off[32], a_cnt, a_tot;
+  const int* cr = rank_base(xr, g);
+  if (warp == 0) {
+    const int* an = T.anc + lam * (T.maxdepth + 1);
+    const int dl = T.depth[lam];
+    int r = 0, slot = 0;
+    if (lane < dl) {
+      const int al = an[lane + 1], ch = an[lane];
+      r = cr[al * 2 + (ch == T.c0[al] ? 0 : 1)];
+      slot = T.depth[al];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, r != 0);
+    const int pos = __popc(m & ((1u << lane) - 1u));
+    const int rp = (r + 3) & ~3;
+    int incl = rp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (r) {
+      a_r[pos] = r;
+      a_slot[pos] = slot;
+      a_off[pos] = incl - rp;
+    }
+    if (lane == 31) {
+      a_cnt = __popc(m);
+      a_tot = incl;
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
   const int gi = lane >> 2, ti = lane & 3;
@@ -480,23 +513,14 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
   dmma_block(acc, sa, sb, r0, c0, S, gi, ti);
   // ancestor cross terms, parent first: acc += P Q^T, one ancestor at a time
   const HB bb = B[g];
-  const int* cr = rank_base(xr, g);
   // every ancestor's P and Q^T in one staging phase when their padded ranks
   // fit the 64 columns of sa / sb (the usual case); the products are still
   // formed and added one ancestor at a time, parent first
-  int tot = 0;
-  {
-    int ch = lam;
-    for (int al = T.parent[lam]; al >= 0; ch = al, al = T.parent[al])
-      tot += (cr[al * 2 + (ch == T.c0[al] ? 0 : 1)] + 3) & ~3;
-  }
+  const int tot = a_tot, na = a_cnt;
   if (tot > 0 && tot <= 64) {
     __syncthreads();                             // main product done with sa / sb
-    int off = 0, ch = lam;
-    for (int al = T.parent[lam]; al >= 0; ch = al, al = T.parent[al]) {
-      const int r = cr[al * 2 + (ch == T.c0[al] ? 0 : 1)];
-      if (!r) continue;
-      const int rp = (r + 3) & ~3, slot = T.depth[al];
+    for (int t = 0; t < na; ++t) {
+      const int r = a_r[t], rp = (r + 3) & ~3, slot = a_slot[t], off = a_off[t];
       const double* P = src_col(PX, n, g, slot, 0) + lo;
       const double* Q = bb.V + (long long)slot * bb.R * n + lo;
       for (int idx = tid; idx < 64 * rp; idx += GT) {
@@ -505,16 +529,11 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
         cp_async8(sa + i * GLD + off + c, in ? P + (long long)c * n + i : P, in);
         cp_async8(sb + (off + c) * GLD + i, in ? Q + (long long)c * n + i : Q, in);
       }
-      off += rp;
     }
     cp_async_wait_all();
     __syncthreads();
-    off = 0;
-    ch = lam;
-    for (int al = T.parent[lam]; al >= 0; ch = al, al = T.parent[al]) {
-      const int r = cr[al * 2 + (ch == T.c0[al] ? 0 : 1)];
-      if (!r) continue;
-      const int rp = (r + 3) & ~3;
+    for (int t = 0; t < na; ++t) {
+      const int rp = (a_r[t] + 3) & ~3, off = a_off[t];
       double z[2][4][2];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
@@ -528,7 +547,6 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
           acc[a][q][0] = acc[a][q][0] + z[a][q][0];
           acc[a][q][1] = acc[a][q][1] + z[a][q][1];
         }
-      off += rp;
     }
   }
   int child = lam;
