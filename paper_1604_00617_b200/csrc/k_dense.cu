@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel_blk(double* A, int N, int j0
     }
     const int c0 = js + sb, nr = j0 + jb - c0;   // panel columns to the right
     if (nr > 0) {
-      // U12 = L11^{-1} A12 (unit lower), one thread per column
+      // U12 = L11^{-1} A12 (unit lower), one thread per column; also kept in
+      // shared memory for the update below (read once per element otherwise)
+      __shared__ double u12[LU_SB][LU_NB];
       if (tid < nr) {
         const int c = c0 + tid;
         double x[LU_SB];
@@ -344,15 +346,16 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel_blk(double* A, int N, int j0
             for (int q = 0; q < k; ++q) v -= S[q * Ms + k] * x[q];
             x[k] = v;
             A[(long long)(js + k) * N + c] = v;
+            u12[k][tid] = v;
           }
         }
       }
       __syncthreads();
       // A22 -= L21 U12 for the panel columns to the right
       for (int idx = tid; idx < (Ms - sb) * nr; idx += LU_PT) {
-        const int r = sb + idx / nr, c = c0 + idx % nr;
+        const int r = sb + idx / nr, cc = idx % nr, c = c0 + cc;
         double v = A[(long long)(js + r) * N + c];
-        for (int k = 0; k < sb; ++k) v -= S[k * Ms + r] * A[(long long)(js + k) * N + c];
+        for (int k = 0; k < sb; ++k) v -= S[k * Ms + r] * u12[k][cc];
         A[(long long)(js + r) * N + c] = v;
       }
     }
