@@ -119,16 +119,15 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
   }
 }
 
-// Register-tiled Gauss-Jordan for leaves of size <= S (S in {16, 32, 64}):
-// (S/4)^2 threads, each owning a 4x4 tile in registers; the pivot sequence
-// equals getrf's (first index of the largest |a_ik| among the remaining
-// rows), rows k and p are exchanged implicitly.  The special cases are off the
-// common path: every element does one FMA x -= a_rk * (row_p / pivot); the
-// owner of column k zeroes it first (x_rk := -a_rk / pivot), and only the
-// threads holding rows k and p fix those rows.  Shared memory carries just
-// the pivot column (published with the pivot search by its owner group) and
-// rows p and k (published after the pivot is known): two barriers per step,
-// no full-matrix copy.
+// Register-tiled Gauss-Jordan for leaves of size <= S (S in {16, 32, 64})
+// with implicit row pivoting: rows never move; step k's pivot row is the
+// unused row with the largest |a_ik| (first physical index on ties -- the
+// same candidates as getrf's remaining rows), and the permutation is applied
+// when the inverse is stored.  Every element does one FMA
+// x -= a_rk * (row_p / pivot) (the owner of column k zeroes it first, the
+// pivot row becomes the scaled row).  Shared memory carries the pivot column
+// (published with the pivot search by its owner group) and the pivot row:
+// two barriers per step, no full-matrix copy.
 // TR x TC register tiles, S/TR row groups (<= 32: one warp segment holds a
 // column group) x S/TC column groups; (4, 4) with 256 threads for batched
 // (throughput) launches, (2, 2) with 1024 threads for launches with fewer
@@ -139,8 +138,8 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
   constexpr int TGY = S / TR, TGX = S / TC, NT = TGX * TGY;
   static_assert(TGY <= 32, "a column group must fit one warp");
   constexpr unsigned MASK = TGY >= 32 ? 0xffffffffu : (NT >= 32 ? 0xffffffffu : (1u << NT) - 1u);
-  __shared__ double colbuf[2][S], rowP[S], rowK[S];
-  __shared__ int piv[S + 1], inv_[S];
+  __shared__ double colbuf[2][S], rowP[S];
+  __shared__ int piv[S + 1], kpos[S];
   const int g = blockIdx.x, tid = threadIdx.x;
   const int tx = tid / TGY, ty = tid - tx * TGY;   // column group, row group
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
@@ -174,13 +173,14 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
     if (tx == 0 && ty == 0) piv[0] = pb;
   }
   bool bad = false;
+  unsigned used = 0;                            // bit a: row ty TR + a has been a pivot
   for (int k = 0; k < s; ++k) {
     __syncthreads();                            // colbuf[k & 1], piv[k]
     const int p = piv[k];
     const double* cb = colbuf[k & 1];
     const double pv = cb[p];
     if (pv == 0.0) { bad = true; break; }       // uniform
-    if (ty == p / TR) {                         // old row p (select chain: x stays in registers)
+    if (ty == p / TR) {                         // pivot row p (select chain: x stays in registers)
       const int ap = p % TR;
 #pragma unroll
       for (int b = 0; b < TC; ++b) {
@@ -189,16 +189,7 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
         for (int a = 1; a < TR; ++a) v = ap == a ? x[a][b] : v;
         rowP[tx * TC + b] = v;
       }
-    }
-    if (ty == k / TR) {                         // old row k
-      const int ak = k % TR;
-#pragma unroll
-      for (int b = 0; b < TC; ++b) {
-        double v = x[0][b];
-#pragma unroll
-        for (int a = 1; a < TR; ++a) v = ak == a ? x[a][b] : v;
-        rowK[tx * TC + b] = v;
-      }
+      used |= 1u << ap;
     }
     __syncthreads();
     const double inv = 1.0 / pv;
@@ -206,7 +197,7 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
 #pragma unroll
     for (int b = 0; b < TC; ++b) {
       const int c = tx * TC + b;
-      rk[b] = (c == k) ? inv : rowP[c] * inv;   // new row k = old row p / pv
+      rk[b] = (c == k) ? inv : rowP[c] * inv;   // the pivot row, scaled
     }
     if (tx == k / TC) {                         // column k acts as zero
       const int bk = k % TC;
@@ -218,27 +209,9 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
 #pragma unroll
     for (int a = 0; a < TR; ++a) {
       const double f = cb[ty * TR + a];
+      const bool isp = ty * TR + a == p;
 #pragma unroll
-      for (int b = 0; b < TC; ++b) x[a][b] -= f * rk[b];
-    }
-    if (ty == k / TR || ty == p / TR) {
-      const double fk = cb[k];                  // old a_kk: row k moves to p
-#pragma unroll
-      for (int a = 0; a < TR; ++a) {
-        const int r = ty * TR + a;
-        if (r == p && p != k) {
-#pragma unroll
-          for (int b = 0; b < TC; ++b) {
-            const int c = tx * TC + b;
-            const double ok = (c == k) ? 0.0 : rowK[c];
-            x[a][b] = ok - fk * rk[b];
-          }
-        }
-        if (r == k) {
-#pragma unroll
-          for (int b = 0; b < TC; ++b) x[a][b] = rk[b];
-        }
-      }
+      for (int b = 0; b < TC; ++b) x[a][b] = isp ? rk[b] : x[a][b] - f * rk[b];
     }
     const int kn = k + 1;                       // next pivot by column kn's owners
     if (kn < s && (tid >> 5) == ((kn / TC) * TGY) >> 5) {
@@ -253,7 +226,7 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
         for (int b = 1; b < TC; ++b) v = bn == b ? x[a][b] : v;
         const int r = ty * TR + a;
         if (own) colbuf[kn & 1][r] = v;
-        if (r >= kn && r < s && fabs(v) > best) { best = fabs(v); pb = r; }
+        if (!((used >> a) & 1u) && r < s && fabs(v) > best) { best = fabs(v); pb = r; }
       }
 #pragma unroll
       for (int o = TGY / 2; o; o >>= 1) {
@@ -274,17 +247,9 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
     return;
   }
   __syncthreads();
-  // A^{-1} = X P: undo the column swaps in reverse order
-  if (tid == 0) {
-    int* pos = reinterpret_cast<int*>(rowP);   // S ints fit in S doubles
-    for (int j = 0; j < s; ++j) pos[j] = j;
-    for (int k = s - 1; k >= 0; --k) {
-      const int t = pos[k];
-      pos[k] = pos[piv[k]];
-      pos[piv[k]] = t;
-    }
-    for (int j = 0; j < s; ++j) inv_[pos[j]] = j;
-  }
+  // implicit pivoting: step k used physical row piv[k], so
+  // A^{-1}[kpos(r)][piv(c)] = X[r][c] with kpos(piv[k]) = k
+  for (int j = tid; j < s; j += NT) kpos[piv[j]] = j;
   __syncthreads();
   int nf = 0;
 #pragma unroll
@@ -294,7 +259,7 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
       const int r = ty * TR + a, c = tx * TC + b;
       if (r < s && c < s) {
         if (!isfinite(x[a][b])) nf = 1;
-        L[(long long)r * bw + inv_[c]] = x[a][b];
+        L[(long long)kpos[r] * bw + piv[c]] = x[a][b];
       }
     }
   if (__syncthreads_or(nf) && tid == 0) {
