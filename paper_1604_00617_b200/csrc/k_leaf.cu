@@ -273,12 +273,6 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
 template <int S>
 static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int leaf,
                                int* sing, cudaStream_t st) {
-  if constexpr (S == 64) {
-    if (nelem < 148) {                // latency-bound: 1024 threads, 2 x 2 tiles
-      k_leafinv_v2<S, 2, 2, 1><<<nelem, (S / 2) * (S / 2), 0, st>>>(T, H, leaf, sing);
-      return cudaGetLastError();
-    }
-  }
   k_leafinv_v2<S, 4, 4, 3><<<nelem, (S / 4) * (S / 4), 0, st>>>(T, H, leaf, sing);
   return cudaGetLastError();
 }
