@@ -452,7 +452,7 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
   // small cores: one warp, warp-level syncs per rotation step (a CTA barrier
   // per step costs more than the step); large cores: the whole CTA
   int sweeps;
-  if (pc <= 64 && pr <= 128) {
+  if (pc <= 16 && pr <= 128) {   // larger cores: every warp of the CTA
     __shared__ int s_sw;
     if (tid < 32) {
       const int sw = blk_jacobi(Bm, pr, pc, Jm, tid);
@@ -736,7 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
       __syncthreads();
       ACR_PH(2);
       int sweeps;
-      if (pc <= 64 && pr <= 128) {
+      if (pc <= 16 && pr <= 128) {   // larger cores: every warp of the CTA
         __shared__ int s_sw;
         if (tid < 32) {
           const int sw = blk_jacobi(Bm, pr, pc, Jm, tid);
@@ -1475,7 +1475,9 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     }
     const int R = a.r + b.r;
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
-    if (need > (long long)NSLOT * SLOT / 8) {   // large: block path queues
+    // large work areas, and cores above 16 columns (a single warp's Jacobi
+    // would walk whole column pairs per lane): block path queues
+    if (need > (long long)NSLOT * SLOT / 8 || (bigq != nullptr && R > 16)) {
       // queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM);
       // queue 1 (stored from bigq + nitems): one 512-thread CTA per SM
       if (lane == 0) {

@@ -56,18 +56,14 @@ __device__ int blk_jacobi_f(double* B, int pr, int pc, double* J, int lane, int 
         }
         if (valid && a > tiny && b > tiny && c != 0.0 &&
             c * c > tol * tol * a * b) {
+          // t = sign(d) e / q, q = |d| + r, r = sqrt(d^2 + e^2);
+          // 1 + t^2 = 2 r / q  ->  cs = sqrt(q) rsqrt(2 r), sn = cs sign(d) e / q
           const double d = b - a, e = 2.0 * c;
-          const double mx = fmax(fabs(d), fabs(e));
-          const long long ex = (__double_as_longlong(mx) >> 52) & 0x7ff;
-          const double scl = __longlong_as_double((2046LL - ex) << 52);
-          const double ds = d * scl, es = e * scl;
-          const float df = (float)ds, ef = (float)es;
-          const float q = fmaf(df, df, ef * ef);
-          double t = (double)__fdividef(copysignf(1.0f, df) * ef, fabsf(df) + q * rsqrtf(q));
-          const double num = fma(t, fma(t, es, 2.0 * ds), -es);
-          t -= num * (double)__frcp_rn((float)(2.0 * fma(t, es, ds)));
-          const double cs = rsqrt(fma(t, t, 1.0));
-          const double sn = cs * t;
+          const double r = sqrt(fma(d, d, e * e));
+          const double q = fabs(d) + r;
+          const double sq = sqrt(q), ir = rsqrt(2.0 * r), iq = 1.0 / q;
+          const double cs = sq * ir;
+          const double sn = cs * (copysign(1.0, d) * e) * iq;
           double* ji = J + (long long)i * lj;
           double* jj = J + (long long)j * lj;
           double xj[RPL], yj[RPL];
