@@ -355,8 +355,11 @@ __device__ int blk_jacobi(double* B, int pr, int pc, double* J, int lane);
 // block path (one CTA per queued task; used for tasks too large for a warp)
 // ---------------------------------------------------------------------------
 template <int NT>
+// score: when the work area is in global scratch, an optional shared-memory
+// area for the Jacobi core and rotations (B, J) -- the Jacobi is most of a
+// large task's time and should not run on global memory
 __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskCtx& tc, double* wk,
-                                 double* red, int* iflag) {
+                                 double* red, int* iflag, double* score = nullptr) {
   const int tid = threadIdx.x, n = A.T.n;
   const OpRes& a = tc.a;
   const OpRes& b = tc.b;
@@ -368,9 +371,9 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
   const int pu = um < R ? um : R, pv = vm < R ? vm : R;
   double* Uw = wk;
   double* Vw = Uw + (long long)um * R;
-  double* Bm = Vw + (long long)vm * R;
+  double* Bm = score ? score : Vw + (long long)vm * R;
   double* Jm = Bm + (long long)R * (R + 1);   // odd-strided cores (pr | 1, pc | 1)
-  double* Cu = Jm + (long long)R * (R + 1);          // pu x keep coefficients
+  double* Cu = Vw + (long long)vm * R + 2LL * R * (R + 1);   // pu x keep coefficients
   double* Cv = Cu + (long long)R * R;          // pv x keep
   double* tauU = Cv + (long long)R * R;
   double* tauV = tauU + R;
@@ -627,7 +630,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_trunc_big(TruncArgs A, const i
         if (threadIdx.x == 0) atomicMax(A.overflow, 1 << 29);
         continue;
       }
-      trunc_block_full<NT>(A, c, A.gscr + (long long)blockIdx.x * A.gscr_stride, red, iflag);
+      trunc_block_full<NT>(A, c, A.gscr + (long long)blockIdx.x * A.gscr_stride, red, iflag,
+                           2LL * R * (R + 1) <= A.smem_doubles ? sm : nullptr);
     } else {
       // separate inlined copy on the shared-memory work area: LDS / STS
       // instead of generic loads and stores
