@@ -449,6 +449,7 @@ struct Plan {
   std::vector<Profile> prof;
   std::vector<std::vector<int>> lastR;   // host ranks of the final level D, E, F
   double fms = 0, sms = 0;
+  bool sms_pending = false;
   long long launches = 0;
   bool factored = false;
   long long reserved = 0;
@@ -474,6 +475,7 @@ struct Plan {
   std::vector<Dev> scr;
   Dev ovf, sing;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t sev0 = nullptr, sev1 = nullptr;   // solve timing (read lazily)
 
   Plan(int m_, int n_, int leaf_, double eps_, int cap_, int cutoff_)
       : m(m_), n(n_), leaf(leaf_), cutoff(cutoff_), cap(cap_), eps(eps_) {
@@ -483,6 +485,8 @@ struct Plan {
   ~Plan() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (sev0) cudaEventDestroy(sev0);
+    if (sev1) cudaEventDestroy(sev1);
     for (auto e : evpool) cudaEventDestroy(e);
     if (st2) {
       cudaStreamSynchronize(st2);
@@ -1479,7 +1483,11 @@ struct Plan {
 
   void solve(const double* rhs, int k, double* u) {
     if (!factored) throw ArgError("acr_solve called before a successful acr_factor");
-    CK(cudaEventRecord(ev0, st));
+    if (!sev0) {
+      CK(cudaEventCreate(&sev0));
+      CK(cudaEventCreate(&sev1));
+    }
+    CK(cudaEventRecord(sev0, st));
     const long long kn = (long long)k * n;
     const int L = (int)recs.size();
     const int P = nranks();
@@ -1646,11 +1654,21 @@ struct Plan {
     }
     CK(launch_u_out(uu[0].as<double>(), mloc0 * n, k, n, u + (long long)first0 * n * k, st));
     ++launches;
-    CK(cudaEventRecord(ev1, st));
-    CK(cudaStreamSynchronize(st));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev0, ev1));
-    sms = ms;
+    CK(cudaEventRecord(sev1, st));
+    // asynchronous on the caller's stream: the elapsed time is read when
+    // asked for (solve_ms), not by blocking the host here
+    sms_pending = true;
+  }
+
+  double solve_ms() {
+    if (sms_pending) {
+      CK(cudaEventSynchronize(sev1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, sev0, sev1));
+      sms = ms;
+      sms_pending = false;
+    }
+    return sms;
   }
 
   long long storage_bytes(int k) const {
@@ -1920,7 +1938,14 @@ long long acr_device_bytes(const acr_plan_t* h) {
   return h && h->p ? h->p->device_bytes() : -1;
 }
 double acr_factor_ms(const acr_plan_t* h) { return h && h->p ? h->p->fms : -1.0; }
-double acr_solve_ms(const acr_plan_t* h) { return h && h->p ? h->p->sms : -1.0; }
+double acr_solve_ms(const acr_plan_t* h) {
+  if (!h || !h->p) return -1.0;
+  try {
+    return h->p->solve_ms();
+  } catch (...) {
+    return -1.0;
+  }
+}
 long long acr_kernel_launches(const acr_plan_t* h) { return h && h->p ? h->p->launches : -1; }
 
 int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
