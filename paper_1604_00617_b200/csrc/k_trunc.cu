@@ -28,6 +28,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Jacobi rotation (cos, sin) annihilating the off-diagonal 2c of the 2x2
+// Gram block [a c; c b], d = b - a, e = 2c: the smaller rotation angle,
+// tan(2 theta) = e / d, from the half-angle identities
+//   cos^2 = (1 + |d|/r) / 2,  sin = sign(d) (e/r) / (2 cos),  r = |(d, e)|,
+// two reciprocal square roots on the dependent chain (no sqrt, no division).
+__device__ __forceinline__ void jacobi_rot(double d, double e, double& cs, double& sn) {
+  const double ir = rsqrt(d * d + e * e);
+  const double h = fma(0.5 * fabs(d), ir, 0.5);
+  const double ih = rsqrt(h);
+  cs = h * ih;
+  sn = copysign(0.5, d) * e * ir * ih;
+}
+
+
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -249,12 +263,9 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
         }
         if (valid && a > tiny && b > tiny && c != 0.0 &&
             c * c > tol * tol * a * b) {
-          // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0,
-          // zeta = (b - a) / 2c, written with one sqrt and one division
           const double d = b - a, e = 2.0 * c;
-          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
-          const double cs = rsqrt(1.0 + t * t);
-          const double sn = cs * t;
+          double cs, sn;
+          jacobi_rot(d, e, cs, sn);
           for (int r = sub; r < pr; r += gs) {
             double x = bi[r], y = bj[r];
             bi[r] = cs * x - sn * y;
@@ -1137,9 +1148,8 @@ __device__ int blk_jacobi_t(double* B, int pr, int pc, double* J, int lane, int 
         if (valid && a > tiny && b > tiny && c != 0.0 &&
             c * c > tol * tol * a * b) {
           const double d = b - a, e = 2.0 * c;
-          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
-          const double cs = rsqrt(1.0 + t * t);
-          const double sn = cs * t;
+          double cs, sn;
+          jacobi_rot(d, e, cs, sn);
           double* ji = J + (long long)i * lj;
           double* jj = J + (long long)j * lj;
           double xj[RPL], yj[RPL];
@@ -1242,12 +1252,9 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
         }
         if (valid && a > tiny && b > tiny && c != 0.0 &&
             c * c > tol * tol * a * b) {
-          // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0,
-          // zeta = (b - a) / 2c, written with one sqrt and one division
           const double d = b - a, e = 2.0 * c;
-          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
-          const double cs = rsqrt(1.0 + t * t);
-          const double sn = cs * t;
+          double cs, sn;
+          jacobi_rot(d, e, cs, sn);
           for (int r = sub; r < pr; r += gs) {
             double x = bi[r], y = bj[r];
             bi[r] = cs * x - sn * y;
