@@ -28,6 +28,21 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Householder reflector of a column with head alpha and tail norm^2 ss > 0
+// (LAPACK dlarfg convention): beta = -sign(alpha) r, r = |(alpha, tail)|,
+// tau = (beta - alpha) / beta = 1 + |alpha| / r, tail scale 1 / (alpha - beta)
+// = sign(alpha) / (|alpha| + r); reciprocal square roots only on the chain.
+__device__ __forceinline__ void householder(double alpha, double ss, double& beta,
+                                            double& scal, double& tau) {
+  const double r2 = fma(alpha, alpha, ss);
+  const double ir = rsqrt(r2);
+  const double r = r2 * ir;
+  const double ix = rsqrt(fabs(alpha) + r);
+  beta = -copysign(r, alpha);
+  scal = copysign(ix * ix, alpha);
+  tau = fma(fabs(alpha), ir, 1.0);
+}
+
 // Jacobi rotation (cos, sin) annihilating the off-diagonal 2c of the 2x2
 // Gram block [a c; c b], d = b - a, e = 2c: the smaller rotation angle,
 // tan(2 theta) = e / d, from the half-angle identities
@@ -123,10 +138,7 @@ __device__ void group_qr(double* W, int mr, int R, double* tau, const Grp& g) {
     const double alpha = cj[j];
     double tj = 0.0, scal = 0.0, beta = alpha;
     if (ss != 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-      const double rb = 1.0 / beta;           // independent of the next division
-      scal = 1.0 / (alpha - beta);
-      tj = (beta - alpha) * rb;
+      householder(alpha, ss, beta, scal, tj);
     }
     gbar(g);                                  // everyone has read cj[j]
     if (tj != 0.0) {
@@ -921,10 +933,7 @@ __device__ __forceinline__ void warp_reflector(double* cj, int j, int mr, double
   double scal = 0.0, beta = alpha;
   tj = 0.0;
   if (ss != 0.0) {
-    beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-    const double rb = 1.0 / beta;             // independent of the next division
-    scal = 1.0 / (alpha - beta);
-    tj = (beta - alpha) * rb;
+    householder(alpha, ss, beta, scal, tj);
   }
   __syncwarp();
   if (tj != 0.0) {
