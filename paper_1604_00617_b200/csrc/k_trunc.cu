@@ -1099,6 +1099,127 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
 
 
 
+// Output factors for panels of MR * 32 rows per side (um == vm): KC kept
+// columns at a time live in registers (rows lane + 32 h), every reflector is
+// applied to all of them with one pass over its smem entries and independent
+// warp reductions, and the head element is folded into the reduction
+// (v_j[j] = 1), so there is no per-column shared-memory round trip or lane-0
+// step.  x := Q_u x (and Q_v on the other side), written straight to HBM.
+template <int MR, int KC>
+__device__ __forceinline__ void warp_out_reg(const double* Wu, const double* Wv, int m,
+                                             int pu, int pv, const double* tu,
+                                             const double* tv, const double* Bm,
+                                             const double* Jm, const double* sig,
+                                             const int* ord, int pr, int pc, bool tr,
+                                             int c0, int kk, double* Uo, double* Vo,
+                                             int n, int lane) {
+  double xu[KC][MR], xv[KC][MR];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    const int j = ord[c0 + (c < kk ? c : 0)];
+    const double sj = sig[j];
+#pragma unroll
+    for (int h = 0; h < MR; ++h) {
+      const int i = lane + 32 * h;
+      double u = 0.0, v = 0.0;
+      if (c < kk) {
+        if (i < pu) u = tr ? sj * Jm[(long long)j * (pc | 1) + i] : Bm[(long long)j * (pr | 1) + i];
+        if (i < pv) v = tr ? Bm[(long long)j * (pr | 1) + i] / sj : Jm[(long long)j * (pc | 1) + i];
+      }
+      xu[c][h] = u;
+      xv[c][h] = v;
+    }
+  }
+  const int p = pu > pv ? pu : pv;
+  for (int j = p - 1; j >= 0; --j) {
+    const double tju = j < pu ? tu[j] : 0.0;
+    const double tjv = j < pv ? tv[j] : 0.0;
+    const double* vu = Wu + (long long)j * m;
+    const double* vv = Wv + (long long)j * m;
+    double au[MR], av[MR];
+#pragma unroll
+    for (int h = 0; h < MR; ++h) {
+      const int i = lane + 32 * h;
+      au[h] = i > j ? vu[i] : (i == j ? 1.0 : 0.0);
+      av[h] = i > j ? vv[i] : (i == j ? 1.0 : 0.0);
+    }
+    double wu[KC], wv[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      wu[c] = 0.0;
+      wv[c] = 0.0;
+#pragma unroll
+      for (int h = 0; h < MR; ++h) {
+        wu[c] = fma(au[h], xu[c][h], wu[c]);
+        wv[c] = fma(av[h], xv[c][h], wv[c]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < KC; ++c) {
+        wu[c] += __shfl_xor_sync(FULL, wu[c], o);
+        wv[c] += __shfl_xor_sync(FULL, wv[c], o);
+      }
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      const double gu = wu[c] * tju, gv = wv[c] * tjv;
+#pragma unroll
+      for (int h = 0; h < MR; ++h) {
+        xu[c][h] = fma(-gu, au[h], xu[c][h]);
+        xv[c][h] = fma(-gv, av[h], xv[c][h]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KC; ++c)
+    if (c < kk) {
+      double* du = Uo + (long long)(c0 + c) * n;
+      double* dv = Vo + (long long)(c0 + c) * n;
+#pragma unroll
+      for (int h = 0; h < MR; ++h) {
+        du[lane + 32 * h] = xu[c][h];
+        dv[lane + 32 * h] = xv[c][h];
+      }
+    }
+}
+
+template <int MR>
+__device__ __forceinline__ void warp_out_regs(const double* Wu, const double* Wv, int m,
+                                              int pu, int pv, const double* tu,
+                                              const double* tv, const double* Bm,
+                                              const double* Jm, const double* sig,
+                                              const int* ord, int pr, int pc, bool tr,
+                                              int keep, double* Uo, double* Vo, int n,
+                                              int lane) {
+  constexpr int KM = MR >= 4 ? 1 : 4;   // register budget: KM x MR doubles per side
+  for (int c0 = 0; c0 < keep; c0 += KM) {
+    const int kk = keep - c0 < KM ? keep - c0 : KM;
+    if constexpr (KM == 1) {
+      warp_out_reg<MR, 1>(Wu, Wv, m, pu, pv, tu, tv, Bm, Jm, sig, ord, pr, pc, tr, c0, kk, Uo,
+                          Vo, n, lane);
+    } else {
+      if (kk > 2)
+        warp_out_reg<MR, 4>(Wu, Wv, m, pu, pv, tu, tv, Bm, Jm, sig, ord, pr, pc, tr, c0, kk,
+                            Uo, Vo, n, lane);
+      else
+        warp_out_reg<MR, 2>(Wu, Wv, m, pu, pv, tu, tv, Bm, Jm, sig, ord, pr, pc, tr, c0, kk,
+                            Uo, Vo, n, lane);
+    }
+  }
+}
+
+// 128-row panels: out of line (keeps the caller's register allocation)
+__device__ __noinline__ void warp_out_regs4(const double* Wu, const double* Wv, int m, int pu,
+                                            int pv, const double* tu, const double* tv,
+                                            const double* Bm, const double* Jm,
+                                            const double* sig, const int* ord, int pr, int pc,
+                                            bool tr, int keep, double* Uo, double* Vo, int n,
+                                            int lane) {
+  warp_out_regs<4>(Wu, Wv, m, pu, pv, tu, tv, Bm, Jm, sig, ord, pr, pc, tr, keep, Uo, Vo, n,
+                   lane);
+}
+
 // Single-warp Jacobi of the block and CTA-pair paths (one warp on the task's
 // critical path, 128 registers available): same pairing, lane groups,
 // arithmetic and order as warp_jacobi, with the row loops unrolled to RPL rows
@@ -1408,6 +1529,16 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   }
   double* ob = sig + R + (R + 1) / 2; // after the R ints of ord: one output column per side
   double* ob2 = ob + um;
+  if (mrl == 2)
+    warp_out_regs<2>(Uw, Vw, um, pu, pv, tauU, tauV, Bm, Jm, sig, ord, pr, pc, tr, keep, tc.Uo,
+                     tc.Vo, n, lane);
+  else if (mrl == 4)
+    warp_out_regs4(Uw, Vw, um, pu, pv, tauU, tauV, Bm, Jm, sig, ord, pr, pc, tr, keep, tc.Uo,
+                   tc.Vo, n, lane);
+  else if (mrl == 1)
+    warp_out_regs<1>(Uw, Vw, um, pu, pv, tauU, tauV, Bm, Jm, sig, ord, pr, pc, tr, keep, tc.Uo,
+                     tc.Vo, n, lane);
+  else
   for (int c = 0; c < keep; ++c) {
     const int j = ord[c];
     for (int i = lane; i < um; i += 32) {
@@ -1421,10 +1552,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
       ob2[i] = v;
     }
     __syncwarp();
-    if (mrl == 2) warp_apply_q2<2>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
-    else if (mrl == 4) warp_apply_q2<4>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
-    else if (mrl == 1) warp_apply_q2<1>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
-    else warp_apply_q2<0>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
+    warp_apply_q2<0>(Uw, um, pu, tauU, ob, Vw, vm, pv, tauV, ob2, lane);
     double* du = tc.Uo + (long long)c * n;
     for (int i = lane; i < um; i += 32) du[i] = ob[i];
     double* dv = tc.Vo + (long long)c * n;
