@@ -436,6 +436,8 @@ struct Plan {
   bool keep_levels = false;
   bool no_side = false;       // option 4: every launch on the plan's stream
   bool force_pair = false;    // option 3: CTA-pair recompression for every direct launch that fits
+  int warp_small = 0;         // option 6: launches of at most this many items use the warp kernel
+  int direct_max = -1;        // option 5: largest launch (items) run one CTA per task; -1 default
   HostTree ht;
   DeviceTree dt;
   cudaStream_t st = 0;
@@ -648,7 +650,18 @@ struct Plan {
       pworst = std::max(pworst, pair_need_doubles(std::max(um, vm), Rw));
     }
     const int nitems = a.ntasks * nelem;
-    const bool direct = nitems <= trunc_direct_max();
+    const bool direct = nitems <= (direct_max >= 0 ? direct_max : trunc_direct_max()) &&
+                        nitems > warp_small;
+    static const bool trace = getenv("ACR_TRACE_TRUNC") != nullptr;
+    if (trace) {
+      int mmax = 0;
+      for (int i = t0; i < t1; ++i) {
+        int bb = ht.listA[i * 3 + 1];
+        mmax = std::max(mmax, std::max(ht.mid[bb] - ht.lo[bb], ht.hi[bb] - ht.mid[bb]));
+      }
+      fprintf(stderr, "TRUNC mode %d tasks %d nelem %d mmax %d Rw %d direct %d\n", a.mode,
+              t1 - t0, nelem, mmax, Rw, (int)direct);
+    }
     const long long SMD = 28416;                 // 222 KB of doubles
     // latency-bound launches whose panels do not fit one CTA's shared memory:
     // one CTA per side (cluster pair) instead of the global-memory scratch
@@ -1885,6 +1898,14 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
   }
   if (option == 4) {
     h->p->no_side = value != 0;
+    return ACR_OK;
+  }
+  if (option == 5) {
+    h->p->direct_max = (int)value;
+    return ACR_OK;
+  }
+  if (option == 6) {
+    h->p->warp_small = (int)value;
     return ACR_OK;
   }
   return set_err(h, ACR_EARG, "unknown option");

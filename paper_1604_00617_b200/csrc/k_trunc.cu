@@ -1709,6 +1709,6 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   return cudaGetLastError();
 }
 
-int trunc_direct_max() { return 2 * 148; }
+int trunc_direct_max() { return 4 * 148; }
 
 }  // namespace acr
