@@ -37,6 +37,7 @@ struct MMJobs2 {
   MMJob j[2];
 };
 
+template <bool LAT>
 __global__ void __launch_bounds__(HT) k_hmatA(TreeDev T, MMJobs2 JJ) {
   const MMJob& J = JJ.j[blockIdx.z];
   if ((int)blockIdx.x >= J.nA) return;
@@ -66,6 +67,31 @@ __global__ void __launch_bounds__(HT) k_hmatA(TreeDev T, MMJobs2 JJ) {
   const double* X = src_col(J.X, n, g, mm_slot(T, mu), 0) + row;
   double* t = J.tbuf + ((long long)g * J.nA + blockIdx.x) * J.RT * J.CT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (LAT && c <= 16) {
+    // latency-bound launches (few elements): one warp per factor column a, all c panel columns at once: the factor
+    // element is loaded once for every column and the 16 accumulation chains
+    // (and their loads) are independent, so a long node's dot products keep
+    // many loads in flight instead of one serial chain per output
+    for (int a = warp; a < r; a += HT / 32) {
+      const double* fa = F + (long long)a * n;
+      double acc[16];
+#pragma unroll
+      for (int b = 0; b < 16; ++b) acc[b] = 0.0;
+      for (int i = lane; i < len; i += 32) {
+        const double f = fa[i];
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+          if (b < c) acc[b] += f * X[(long long)b * n + i];
+      }
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if (b < c) {
+          const double v = hwarp_sum(acc[b]);
+          if (lane == b) t[a * J.CT + b] = v;
+        }
+    }
+    return;
+  }
   for (int p = warp; p < r * c; p += HT / 32) {
     int a = p / c, b = p - a * c;
     const double* fa = F + (long long)a * n;
@@ -437,7 +463,8 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
   }
   if (nA > 0) {
     dim3 g(nA, nelem, njobs);
-    k_hmatA<<<g, HT, 0, st>>>(T, JJ);
+    if (nelem <= 32) k_hmatA<true><<<g, HT, 0, st>>>(T, JJ);
+    else k_hmatA<false><<<g, HT, 0, st>>>(T, JJ);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
