@@ -290,21 +290,29 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel_blk(double* A, int N, int j0
     {
       __shared__ int rws[2 * LU_SB], sa[LU_SB], sbb[LU_SB], nrw;
       __shared__ double tile[2 * LU_SB][LU_NB];
-      if (tid == 0) {
-        int cnt = 0;
-        for (int k = 0; k < sb; ++k) {
-          const int r1 = js + k, r2 = piv[js + k];
-          int q1 = -1, q2 = -1;
-          for (int q = 0; q < cnt; ++q) {
-            if (rws[q] == r1) q1 = q;
-            if (rws[q] == r2) q2 = q;
+      // slots 0..sb-1: the sub-panel rows; pivot rows below it get one extra
+      // slot each (duplicates share their first occurrence's slot): built by
+      // one warp with match/ballot instead of a serial scan by one thread
+      if (tid < 32) {
+        const bool act = tid < sb;
+        const int pr = act ? piv[js + tid] : -1;
+        const bool ext = act && pr >= js + sb;
+        const unsigned extm = __ballot_sync(0xffffffffu, ext);
+        const unsigned same = __match_any_sync(0xffffffffu, ext ? pr : -1 - tid);
+        const int leader = __ffs(same & extm) - 1;
+        const unsigned firsts = __ballot_sync(0xffffffffu, ext && leader == tid);
+        if (act) {
+          rws[tid] = js + tid;
+          sa[tid] = tid;
+          if (ext) {
+            const int slot = sb + __popc(firsts & ((1u << leader) - 1u));
+            sbb[tid] = slot;
+            if (leader == tid) rws[slot] = pr;
+          } else {
+            sbb[tid] = pr - js;
           }
-          if (q1 < 0) { rws[cnt] = r1; q1 = cnt++; }
-          if (q2 < 0) { if (r2 == r1) q2 = q1; else { rws[cnt] = r2; q2 = cnt++; } }
-          sa[k] = q1;
-          sbb[k] = q2;
         }
-        nrw = cnt;
+        if (tid == 0) nrw = sb + __popc(firsts);
       }
       __syncthreads();
       const int ncol = jb - sb;                   // panel columns outside the sub-panel
