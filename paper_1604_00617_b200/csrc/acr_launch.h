@@ -33,6 +33,10 @@ cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
                             int fside, cudaStream_t st);
 cudaError_t launch_leafadd(const TreeDev& T, const HB* A, const HB* B,
                            const HB* C, double sb, int nelem, cudaStream_t st);
+// int copy (e.g. device -> mapped pinned host memory, bypassing the copy
+// engines) and fill
+cudaError_t launch_copy_i32(int* dst, const int* src, long long n, cudaStream_t st);
+cudaError_t launch_fill_i32(int* dst, int v, long long n, cudaStream_t st);
 cudaError_t launch_negate(const TreeDev& T, const HB* H, int nelem,
                           cudaStream_t st);
 cudaError_t launch_copyhb(const TreeDev& T, const HB* S, const HB* D, int nelem,

@@ -476,6 +476,19 @@ struct Plan {
   // scratch pool
   std::vector<Dev> scr;
   Dev ovf, sing;
+  // Per-level flags and rank tables reach the host through mapped pinned
+  // memory written by a copy kernel, not through the copy engines: an
+  // application's bulk transfers on other streams (the next step's bands, the
+  // previous step's solution) would otherwise queue these small reads behind
+  // hundreds of MB and stall the factorisation at every level.
+  int* hmap = nullptr;       // host view
+  int* hmap_d = nullptr;     // device alias
+  size_t hmap_cap = 0, hmap_used = 0;
+  struct Pend {
+    std::vector<int>* out;
+    size_t off, n;
+  };
+  std::vector<Pend> pend;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t sev0 = nullptr, sev1 = nullptr;   // solve timing (read lazily)
 
@@ -485,6 +498,7 @@ struct Plan {
     scr.resize(32);
   }
   ~Plan() {
+    if (hmap) cudaFreeHost(hmap);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (sev0) cudaEventDestroy(sev0);
@@ -1080,11 +1094,38 @@ struct Plan {
   }
 
   // ---- helpers for reports ----
+  // n ints of the mapped staging buffer (grown only when nothing is pending)
+  size_t hmap_take(size_t n) {
+    if (hmap_used + n > hmap_cap) {
+      if (!pend.empty()) sync_fetch();
+      if (n > hmap_cap) {
+        CK(cudaStreamSynchronize(st));
+        if (hmap) CK(cudaFreeHost(hmap));
+        hmap_cap = std::max<size_t>(n, (size_t)12 * std::max(m, 1) * ht.nnodes + 2 * (size_t)m + 64);
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&hmap), hmap_cap * sizeof(int),
+                         cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hmap_d), hmap, 0));
+      }
+    }
+    const size_t off = hmap_used;
+    hmap_used += n;
+    return off;
+  }
+
   void fetch_ranks(const Batch& b, std::vector<int>& out) {
     out.resize((size_t)b.cnt * ht.nnodes * 2);
-    if (b.cnt)
-      CK(cudaMemcpyAsync(out.data(), b.rk.p, out.size() * sizeof(int),
-                         cudaMemcpyDeviceToHost, st));
+    if (!b.cnt) return;
+    const size_t off = hmap_take(out.size());
+    CK(launch_copy_i32(hmap_d + off, b.rk.as<int>(), (long long)out.size(), st));
+    pend.push_back({&out, off, out.size()});
+  }
+
+  // stream sync, then the fetched rank tables move to their host vectors
+  void sync_fetch() {
+    CK(cudaStreamSynchronize(st));
+    for (const Pend& p : pend) memcpy(p.out->data(), hmap + p.off, p.n * sizeof(int));
+    pend.clear();
+    hmap_used = 0;
   }
 
   long long hb_bytes(const int* rk) const {
@@ -1147,11 +1188,7 @@ struct Plan {
     const int nep = std::max(no - i0, 0);
     CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
     int* sg = sing.as<int>();
-    {
-      std::vector<int> init(std::max(ne, 1), INT_MAX);
-      CK(cudaMemcpyAsync(sg, init.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
-      CK(cudaStreamSynchronize(st));
-    }
+    CK(launch_fill_i32(sg, INT_MAX, (long long)ne, st));
     // 1. Dinv of the even blocks
     rec.m = mm;
     rec.first = first;
@@ -1233,9 +1270,17 @@ struct Plan {
     // overflow / singular checks (one sync per level)
     int h_ovf = 0;
     std::vector<int> hs(std::max(ne, 1));
-    CK(cudaMemcpyAsync(&h_ovf, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hs.data(), sg, sizeof(int) * ne, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    {
+      const size_t off = hmap_take((size_t)ne + 1);
+      CK(launch_copy_i32(hmap_d + off, ovf.as<int>(), 1, st));
+      CK(launch_copy_i32(hmap_d + off + 1, sg, (long long)ne, st));
+      CK(cudaStreamSynchronize(st));
+      h_ovf = hmap[off];
+      memcpy(hs.data(), hmap + off + 1, sizeof(int) * ne);
+      for (const Pend& p : pend) memcpy(p.out->data(), hmap + p.off, p.n * sizeof(int));
+      pend.clear();
+      hmap_used = 0;
+    }
     CK(cudaGetLastError());
     // singular leaves: report the first block in inversion order
     int bad = -1;
@@ -1375,7 +1420,7 @@ struct Plan {
     fetch_ranks(L.D, dR);
     fetch_ranks(L.E, eR);
     fetch_ranks(L.F, fR);
-    CK(cudaStreamSynchronize(st));
+    sync_fetch();
     profile_level(L.m, dR, eR, fR);
     int maxr = std::max(max_rank_of(dR), 1);
     int lvl = 0;
@@ -1389,7 +1434,7 @@ struct Plan {
         fetch_ranks(L.D, dR);
         fetch_ranks(L.E, eR);
         fetch_ranks(L.F, fR);
-        CK(cudaStreamSynchronize(st));
+        sync_fetch();
         maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
         continue;
       }
@@ -1413,7 +1458,7 @@ struct Plan {
       fetch_ranks(nx.D, dR);
       fetch_ranks(nx.E, eR);
       fetch_ranks(nx.F, fR);
-      CK(cudaStreamSynchronize(st));
+      sync_fetch();
       profile_level(nx.m, dR, eR, fR);
       maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
       if (keep_levels) kept.push_back(std::move(L));

@@ -706,6 +706,32 @@ __global__ void k_negate(TreeDev T, const HB* H) {
   }
 }
 
+__global__ void k_copy_i32(int* __restrict__ dst, const int* __restrict__ src, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void k_fill_i32(int* dst, int v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+cudaError_t launch_copy_i32(int* dst, const int* src, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const long long b = (n + 255) / 256;
+  k_copy_i32<<<(int)(b < 592 ? b : 592), 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_i32(int* dst, int v, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const long long b = (n + 255) / 256;
+  k_fill_i32<<<(int)(b < 592 ? b : 592), 256, 0, st>>>(dst, v, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_negate(const TreeDev& T, const HB* H, int nelem,
                           cudaStream_t st) {
   if (!nelem) return cudaSuccess;

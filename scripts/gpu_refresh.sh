@@ -1,6 +1,6 @@
 # bench lines (both arms), launch list and ncu --set full captures of the top kernels (cfg5)
 V=${V:-v7}
-python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$V.json 2> gpurun_out/bench_$V.err
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench_$V.json 2> gpurun_out/bench_$V.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$V.json 2>> gpurun_out/bench_$V.err
 python scripts/factor_once.py cfg5 > gpurun_out/plain_cfg5.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv --log-file gpurun_out/launches_cfg5_$V.csv python scripts/factor_once.py cfg5 > gpurun_out/ncu_l.log 2>&1
