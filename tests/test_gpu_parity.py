@@ -183,6 +183,29 @@ def test_run_to_run_bitwise(solver_mod):
     np.testing.assert_array_equal(a, b)
 
 
+def test_concurrent_bulk_copies_bitwise(solver_mod):
+    # the factorisation's per-level host reads bypass the copy engines (mapped
+    # pinned memory): results, ranks and the report must not depend on bulk
+    # transfers an application keeps in flight on other streams
+    s = P.make_config("cfg2")
+    c = P.CONFIGS["cfg2"]
+    a, ra = solver_mod.acr_solve(s, Tolerance(c["eps"]), leaf_size=c["leaf"])
+    h = torch.empty(64 << 20, dtype=torch.float64).pin_memory()
+    d = torch.empty_like(h, device="cuda")
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(up):
+        for _ in range(4):
+            d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(down):
+        for _ in range(4):
+            h.copy_(d, non_blocking=True)
+    b, rb = solver_mod.acr_solve(s, Tolerance(c["eps"]), leaf_size=c["leaf"])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a, b)
+    assert [p.to_dict() for p in ra.per_level_ranks] == [p.to_dict() for p in rb.per_level_ranks]
+    assert (ra.max_rank, ra.storage_bytes) == (rb.max_rank, rb.storage_bytes)
+
+
 def test_singular_pivot(solver_mod):
     s = P.random_system(4, 4, seed=6)
     s.D_diag[2] = 0.0
