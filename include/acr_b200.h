@@ -14,6 +14,17 @@
  * library owns its HODLR storage (stream-ordered cudaMallocAsync).  `stream`
  * is a cudaStream_t (NULL = legacy default stream).
  *
+ * Streams and threads: acr_factor, acr_solve and acr_block_to_dense are
+ * ordered on the stream they are given; acr_solve returns without waiting
+ * for the GPU (u is complete when the stream reaches the call).  Successive
+ * calls on one plan may name different streams: each call's stream first
+ * waits for everything the plan queued before, and the plan's buffers are
+ * recycled only on work ordered after their last use.  One plan must not be
+ * used from two host threads at once; independent plans may run on any
+ * number of threads concurrently (reference SPEC.md:213) -- the library has
+ * no unsynchronised global state (error text of plan-less calls is
+ * per thread).
+ *
  * Status codes: 0 ok, 1 bad argument (Python: ValueError), 2 singular pivot
  * (SingularBlockError / LinAlgError), 3 CUDA error, 4 internal limit.
  */
@@ -106,7 +117,8 @@ long long acr_kernel_launches(const acr_plan_t* p);
 int acr_kernel_stats(const acr_plan_t* p, int cls, long long* launches,
                      double* ms, unsigned long long* counters);
 int acr_last_error(const acr_plan_t* p, char* buf, int len);
-/* error of the last plan-less call (acr_plan_create failures) */
+/* error of the calling thread's last plan-less call (acr_plan_create,
+ * acr_residual, generators, kernel-level entry points) */
 int acr_global_error(char* buf, int len);
 
 /* Dense export of one block for tests: which 0 = D, 1 = E, 2 = F of the
@@ -148,7 +160,8 @@ int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
                         double eps, int max_rank_cap, double* Uo, double* Vo,
                         int* rank_out, void* stream);
 /* Test hook: recompression path used by acr_truncate_factor (0 = one CTA per
- * task (default), 1 = warp-per-task kernel, 2 = CTA pair).  Process-wide. */
+ * task (default), 1 = warp-per-task kernel, 2 = CTA pair).  Per calling
+ * thread. */
 int acr_set_truncate_path(int path);
 /* A: s x s row-major; X: inverse; *singular set to 1 on a zero pivot or a
  * non-finite result. */

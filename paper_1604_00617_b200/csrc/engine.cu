@@ -9,6 +9,7 @@
 // are decided per block on the device from device-resident ranks.  The
 // truncation schedule is the reference's.
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <chrono>
@@ -52,18 +53,28 @@ struct InternalError : std::runtime_error {
 // ---------------------------------------------------------------------------
 // stream-ordered device memory
 // ---------------------------------------------------------------------------
-static long long g_live = 0, g_peak = 0;   // bytes held through Dev
+// bytes held through Dev (all plans of the process; plans may run on several
+// host threads at once)
+static std::atomic<long long> g_live{0}, g_peak{0};
+static void note_alloc(long long b) {
+  const long long now = g_live.fetch_add(b) + b;
+  long long pk = g_peak.load();
+  while (now > pk && !g_peak.compare_exchange_weak(pk, now)) {
+  }
+}
 
 // Size-class caching allocator.  A factor requests the same sizes in the
 // same order every time, so after the first factor every request is served
-// from the cache (no new device mappings inside a timed factor).  All work of
-// a plan is on one stream, so handing a cached block to a later request is
-// stream-ordered.  Blocks are returned to the driver when the last plan dies.
+// from the cache (no new device mappings inside a timed factor).  Free blocks
+// are keyed by the stream they were last used on and only handed to requests
+// on that stream, so reuse is stream-ordered.  Blocks go back to the driver
+// (after a device synchronisation: they may have been used on any stream)
+// when an allocation fails or the last plan dies.
 struct DevCache {
   std::mutex mu;
   std::multimap<std::pair<size_t, cudaStream_t>, void*> free_;
   std::vector<void*> all;
-  int plans = 0;
+  std::atomic<int> plans{0};
   static size_t cls(size_t b) {
     if (b <= 4096) return (b + 255) & ~size_t(255);
     int lg = 63 - __builtin_clzll(b);
@@ -100,6 +111,9 @@ struct DevCache {
   }
   void trim(cudaStream_t s) {
     std::lock_guard<std::mutex> g(mu);
+    if (free_.empty()) return;
+    // a cached block's last use may be pending on another stream
+    cudaDeviceSynchronize();
     for (auto& kv : free_) {
       cudaFreeAsync(kv.second, s);
       all.erase(std::find(all.begin(), all.end(), kv.second));
@@ -122,8 +136,7 @@ struct Dev {
     n = bytes;
     if (bytes) {
       p = g_cache.get(bytes, &cap, s);
-      g_live += (long long)cap;
-      if (g_live > g_peak) g_peak = g_live;
+      note_alloc((long long)cap);
     }
   }
   void release() {
@@ -499,6 +512,7 @@ struct Plan {
   }
   ~Plan() {
     if (hmap) cudaFreeHost(hmap);
+    if (evsw) cudaEventDestroy(evsw);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (sev0) cudaEventDestroy(sev0);
@@ -535,6 +549,35 @@ struct Plan {
     if (s == st) return;
     CK(cudaEventRecord(evj, s));
     CK(cudaStreamWaitEvent(st, evj, 0));
+  }
+
+  // Every ABI call names its stream.  When it differs from the previous
+  // call's, the new stream waits for everything the plan queued so far, and
+  // every buffer the plan holds is re-tagged to the new stream so that, when
+  // released, the caching allocator only hands it to work ordered after its
+  // last use (solve is asynchronous on its stream).
+  bool st_set = false;
+  cudaEvent_t evsw = nullptr;
+  void retag(Dev& d, cudaStream_t s) { d.st = s; }
+  void retag(Batch& b, cudaStream_t s) {
+    retag(b.leaf, s); retag(b.U, s); retag(b.V, s); retag(b.rk, s);
+  }
+  void use_stream(cudaStream_t s) {
+    if (st_set && s == st) return;
+    if (st_set) {
+      if (!evsw) CK(cudaEventCreateWithFlags(&evsw, cudaEventDisableTiming));
+      CK(cudaEventRecord(evsw, st));
+      CK(cudaStreamWaitEvent(s, evsw, 0));
+    }
+    {
+      for (auto& r : recs) { retag(r.Dinv, s); retag(r.E, s); retag(r.F, s); }
+      for (auto& l : kept) { retag(l.D, s); retag(l.E, s); retag(l.F, s); }
+      retag(last.D, s); retag(last.E, s); retag(last.F, s);
+      for (Dev* d : {&lu, &piv, &info, &lut, &ovf, &sing, &dctr, &dt.buf}) retag(*d, s);
+      for (auto& d : scr) retag(d, s);
+    }
+    st = s;
+    st_set = true;
   }
 
   int nranks() const { return tp ? tp->size() : 1; }
@@ -1096,6 +1139,7 @@ struct Plan {
   // ---- helpers for reports ----
   // n ints of the mapped staging buffer (grown only when nothing is pending)
   size_t hmap_take(size_t n) {
+    if (pend.empty()) hmap_used = 0;
     if (hmap_used + n > hmap_cap) {
       if (!pend.empty()) sync_fetch();
       if (n > hmap_cap) {
@@ -1374,6 +1418,10 @@ struct Plan {
   // ---- factor ----
   void factor(const double* sub, const double* diag, const double* sup,
               const double* E, const double* F, int order) {
+    // a previous factor that threw between fetch_ranks and sync_fetch left
+    // entries pointing into its (gone) host vectors
+    pend.clear();
+    hmap_used = 0;
     recs.clear();
     kept.clear();
     prof.clear();
@@ -1772,7 +1820,10 @@ struct acr_plan {
   Plan* p;
 };
 
-static std::string g_err;
+// error text of the calling thread's last failed plan-less call (plans carry
+// their own); thread-local so concurrent independent calls do
+// not see each other's messages
+static thread_local std::string g_err;
 
 static int set_err(acr_plan_t* h, int code, const std::string& msg) {
   if (h && h->p) h->p->err = msg;
@@ -1964,7 +2015,7 @@ int acr_factor(acr_plan_t* h, const double* D_sub, const double* D_diag,
     return set_err(h, ACR_EARG, "unknown inversion_order");
   ACR_GUARD(h, {
     Plan& P = *h->p;
-    P.st = (cudaStream_t)stream;
+    P.use_stream((cudaStream_t)stream);
     P.factor(D_sub, D_diag, D_sup, E, F, inversion_order);
   });
   return ACR_OK;
@@ -1976,7 +2027,7 @@ int acr_solve(acr_plan_t* h, const double* rhs, int nrhs, double* u,
   if (nrhs < 1) return set_err(h, ACR_EARG, "nrhs must be >= 1");
   ACR_GUARD(h, {
     Plan& P = *h->p;
-    P.st = (cudaStream_t)stream;
+    P.use_stream((cudaStream_t)stream);
     P.solve(rhs, nrhs, u);
   });
   return ACR_OK;
@@ -2051,7 +2102,7 @@ int acr_block_to_dense(acr_plan_t* h, int level, int which, int block,
   if (!h || !h->p) return ACR_EARG;
   ACR_GUARD(h, {
     Plan& P = *h->p;
-    P.st = (cudaStream_t)stream;
+    P.use_stream((cudaStream_t)stream);
     const acr::Batch* b = nullptr;
     int L = (int)P.recs.size();
     if (which == 3) {
@@ -2144,7 +2195,7 @@ int acr_gen_uniform(const unsigned long long* pcg_state4, long long N, int k, do
   return ACR_OK;
 }
 
-static int g_trunc_path = 0;
+static thread_local int g_trunc_path = 0;   // test hook, per calling thread
 
 int acr_set_truncate_path(int path) {
   if (path < 0 || path > 2) return set_err(nullptr, ACR_EARG, "path must be 0, 1 or 2");

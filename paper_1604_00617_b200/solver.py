@@ -131,9 +131,16 @@ class AcrSolver:
                                  f"expected {s} float64 on CUDA")
         bands = [t.contiguous() for t in bands]
         self._bands = bands
+        cur = self.torch.cuda.current_stream()
+        other = stream is not None and stream != cur
+        if other:
+            stream.wait_stream(cur)
         rc = self.lib.acr_factor(self.plan, *[_ptr(t) for t in bands],
                                  1 if inversion_order == "reversed" else 0,
                                  _stream(self.torch, stream))
+        if other:
+            for t in bands:
+                t.record_stream(stream)
         if rc != 0:
             self.factored = False
             _raise(self.plan, rc)
@@ -154,10 +161,18 @@ class AcrSolver:
         rhs = rhs.to(torch.float64).contiguous()
         k = 1 if rhs.dim() == 1 else rhs.shape[1]
         u = torch.empty_like(rhs)
+        cur = torch.cuda.current_stream()
+        if stream is not None and stream != cur:
+            # rhs (possibly a converted temporary) and u were allocated on the
+            # current stream; the solve runs asynchronously on `stream`
+            stream.wait_stream(cur)
         rc = self.lib.acr_solve(self.plan, _ptr(rhs), int(k), _ptr(u),
                                 _stream(torch, stream))
         if rc != 0:
             _raise(self.plan, rc)
+        if stream is not None and stream != cur:
+            rhs.record_stream(stream)
+            u.record_stream(stream)
         self._nrhs = k
         return u
 

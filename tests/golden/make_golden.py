@@ -139,6 +139,90 @@ def config(name, stride=1, nrhs=1):
           "storage", rep.storage_bytes, "reduce_ms", rep.reduce_ms, "wall", wall)
 
 
+def projections(u, nproj=8, seed=1234, chunk=1 << 20):
+    """G @ u for a seeded Gaussian G (nproj x N): a size-independent
+    fingerprint of EVERY entry of the solution (the committed fixtures keep
+    only a subsample).  tests/ regenerate G with the same numpy stream."""
+    rng = np.random.default_rng(seed)
+    N = u.shape[0]
+    acc = np.zeros((nproj,) + u.shape[1:])
+    for c0 in range(0, N, chunk):
+        c1 = min(N, c0 + chunk)
+        G = rng.standard_normal((nproj, c1 - c0))
+        acc += G @ u[c0:c1]
+    return acc
+
+
+def multi_rhs(name, nrhs=16, stride=512, check_col0=True):
+    """k-column reference solution by the SURVEY.md 8(c) shim: replay
+    ``acr_solve``'s body (reduction.py:273-326) with the reference's own
+    functions, the level RHS replaced by (n, k) segments and
+    ``acrsolve.reduction.matvec`` rebound to ``acrsolve.algebra.matmat``
+    (2-D capable, algebra.py:52-62) for the forward sweep (:204-216) and
+    back-substitution (:235-256).  The factorisation never reads f, so it is
+    the single-column run's; each column differs from a per-column
+    ``acr_solve`` only by GEMM-vs-GEMV roundoff (checked on column 0 against
+    ``{name}.npz`` when ``check_col0``)."""
+    import scipy.linalg
+    import acrsolve.reduction as RR
+    from acrsolve.problems import assemble_full
+    c = P.CONFIGS[name]
+    s = P.make_config(name, nrhs=nrhs)
+    m, n = s.n_blocks, s.block_dim
+    F = s.rhs.reshape(m * n, nrhs)
+    rs = R.BlockTridiagSystem(m, n, s.D_sub, s.D_diag, s.D_sup, s.E, s.F,
+                              np.ascontiguousarray(F[:, 0]))
+    tol = R.Tolerance(c["eps"])
+    orig = RR.matvec
+    RR.matvec = RA.matmat
+    try:
+        t0 = time.perf_counter()
+        level = RR.lift_system(rs, c["leaf"])
+        level.f = [np.ascontiguousarray(F[i * n:(i + 1) * n]) for i in range(m)]
+        record = RR.EliminationRecord()
+        while level.n_blocks > 1:
+            level, entry = RR.reduce_level(level, tol)
+            record.entries.append(entry)
+        t_red = time.perf_counter()
+        A_small = level.to_dense()
+        f_small = np.concatenate(level.f)
+        lu, piv = scipy.linalg.lu_factor(A_small)
+        u_small = scipy.linalg.lu_solve((lu, piv), f_small)
+        segs = [u_small[i * n:(i + 1) * n] for i in range(level.n_blocks)]
+        u = RR.backsubstitute(record, segs)
+        t_end = time.perf_counter()
+    finally:
+        RR.matvec = orig
+    A = assemble_full(rs).tocsr()
+    res = np.linalg.norm(A @ u - F, axis=0) / np.linalg.norm(F, axis=0)
+    out = {"u_stride": stride, "u": u[::stride], "u_norm": np.linalg.norm(u, axis=0),
+           "u_sum": u.sum(axis=0), "residual": res, "nrhs": nrhs,
+           "u_proj": projections(u),
+           "reduce_ms": (t_red - t0) * 1e3, "backsub_ms": (t_end - t_red) * 1e3}
+    if check_col0:
+        z = np.load(os.path.join(HERE, f"{name}.npz"))
+        st = int(z["u_stride"])
+        d = np.linalg.norm(u[::st, 0] - z["u"]) / np.linalg.norm(z["u"])
+        out["col0_vs_single"] = d
+        out["col0_residual_single"] = float(z["residual"])
+        print(name, "column 0 vs single-column acr_solve (rel, subsampled):", d)
+    np.savez_compressed(os.path.join(HERE, f"{name}x{nrhs}.npz"), **out)
+    print(name, f"x{nrhs}", "residual per column", res, "reduce_ms", out["reduce_ms"])
+
+
+def mmio_files():
+    """Reference ``acr export`` output (cli.py:288-309 via mmio.py:19-62) for
+    two small problems: the byte-for-byte target of this package's writer."""
+    from acrsolve import cli as RC
+    for argv, stem in ((["--problem", "poisson", "--n", "6", "--kappa",
+                         "checkerboard:100:2"], "mmio_poisson6"),
+                       (["--problem", "convdiff", "--n", "5", "--alpha", "30"],
+                        "mmio_convdiff5")):
+        rc = RC.main(["export", *argv, "--out", os.path.join(HERE, stem)])
+        assert rc == 0
+        print("mmio:", stem)
+
+
 def kernels():
     """truncate_factor and leaf-inverse vectors captured from a config-1
     solve (both module bindings patched)."""
@@ -210,5 +294,13 @@ if __name__ == "__main__":
             config(w, stride=8)
         elif w in ("cfg4", "cfg5"):
             config(w, stride=64)
+        elif w == "mmio":
+            mmio_files()
+        elif w == "cfg1x16":
+            multi_rhs("cfg1", stride=1)
+        elif w == "cfg2x16":
+            multi_rhs("cfg2", stride=16)
+        elif w == "cfg5x16":
+            multi_rhs("cfg5", stride=512)
         else:
             raise SystemExit(f"unknown target {w}")
