@@ -128,6 +128,54 @@ int acr_global_error(char* buf, int len);
 int acr_block_to_dense(acr_plan_t* p, int level, int which, int block,
                        double* out, void* stream);
 
+/* Raw storage of one block of the factorisation (same level / which / block
+ * addressing as acr_block_to_dense), for the host HODLR objects of
+ * paper_1604_00617_b200.hodlr (reference HodlrMatrix / LowRankFactor,
+ * hodlr.py:47-173).  Layout: leaf n x bw (row i of
+ * the leaf holding i, column j - lo), U and V nd x R x n (depth slot k, column
+ * c, row i: node [lo,mid,hi) at depth k has off12 = U[k][:r12, lo:mid]^T
+ * V[k][:r12, mid:hi] and off21 = U[k][:r21, mid:hi]^T V[k][:r21, lo:mid]),
+ * ranks 2 x nnodes (off12, off21 of each node).  Device buffers; pass all
+ * four as NULL to only receive R (column capacity) and the block count. */
+int acr_block_export(acr_plan_t* p, int level, int which, int block, double* leaf,
+                     double* U, double* V, int* ranks, int* R_out, int* count_out,
+                     void* stream);
+
+/* Stepwise API: the reference's lower-level surface (reduction.py:156-256),
+ * used by its own tests (test_reduction.py:46-151), on device-resident levels
+ * and elimination-record entries named by integer handles owned by the plan.
+ *   acr_step_lift    lift_system (reduction.py:156-166) of the plan's (m, n,
+ *                    leaf) system -> level handle (level 0)
+ *   acr_step_reduce  reduce_level (reduction.py:173-232) of a level with the
+ *                    given eps / cap; inversion_order: NULL or a permutation
+ *                    of the even-block indices (only changes which singular
+ *                    pivot is reported first) -> new level + record handles.
+ *                    The input level is not modified.
+ *   acr_step_rhs     the level's forward RHS update (reduction.py:204-216):
+ *                    f (m_l n, k) -> f' (floor(m_l/2) n, k), row-major
+ *   acr_step_backsub one back-substitution level (reduction.py:235-256): the
+ *                    level's f and the odd blocks' u -> u of every block
+ *   acr_step_info    block count / column capacity of which 0 D, 1 E, 2 F of a
+ *                    level handle, 3 Dinv, 4 E, 5 F of a record handle; the
+ *                    level index and its block count
+ *   acr_step_export  raw storage of one block as acr_block_export
+ *   acr_step_free    release a handle */
+int acr_step_lift(acr_plan_t* p, const double* D_sub, const double* D_diag,
+                  const double* D_sup, const double* E, const double* F, int* level_out,
+                  void* stream);
+int acr_step_reduce(acr_plan_t* p, int level, double eps, int max_rank_cap,
+                    const int* inversion_order, int* level_out, int* record_out,
+                    void* stream);
+int acr_step_rhs(acr_plan_t* p, int record, const double* f, int nrhs, double* f_out,
+                 void* stream);
+int acr_step_backsub(acr_plan_t* p, int record, const double* f, const double* u_odd,
+                     int nrhs, double* u, void* stream);
+int acr_step_info(acr_plan_t* p, int handle, int which, int* count, int* R, int* level,
+                  int* m_level);
+int acr_step_export(acr_plan_t* p, int handle, int which, int block, double* leaf,
+                    double* U, double* V, int* ranks, void* stream);
+int acr_step_free(acr_plan_t* p, int handle);
+
 /* ||A u - f||_2 per column and ||f||_2 per column straight from the bands
  * (oracles.py:34-49); u, f (m*n, k) row-major; out_r, out_f host arrays[k]. */
 int acr_residual(int m, int n, int k, const double* D_sub, const double* D_diag,

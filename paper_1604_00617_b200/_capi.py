@@ -57,6 +57,17 @@ _SIGS = [
                                       C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                       C.c_void_p, C.POINTER(C.c_int), C.c_void_p]),
     ("acr_set_truncate_path", C.c_int, [C.c_int]),
+    ("acr_block_export", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4 +
+     [C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p]),
+    ("acr_step_lift", C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.POINTER(C.c_int), C.c_void_p]),
+    ("acr_step_reduce", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p]),
+    ("acr_step_rhs", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    ("acr_step_backsub", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                   C.c_void_p, C.c_void_p]),
+    ("acr_step_info", C.c_int, [C.c_void_p, C.c_int, C.c_int] + [C.POINTER(C.c_int)] * 4),
+    ("acr_step_export", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 5),
+    ("acr_step_free", C.c_int, [C.c_void_p, C.c_int]),
     ("acr_leaf_inverse", C.c_int, [C.c_int, C.c_void_p, C.c_void_p,
                                    C.POINTER(C.c_int), C.c_void_p]),
 ]

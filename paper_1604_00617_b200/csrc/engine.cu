@@ -370,6 +370,7 @@ struct Seg {
 struct Level {
   int m = 0, first = 0, mg = 0;
   int R = 1;
+  int lvl = 0;                      // reduction level index (0 = lifted system)
   Batch D, E, F;
 };
 
@@ -1215,11 +1216,58 @@ struct Plan {
     prof.push_back(p);
   }
 
+  Batch clone(const Batch& b) {
+    Batch c;
+    c.alloc(ht, b.cnt, b.R, st);
+    const size_t cnt = (size_t)std::max(b.cnt, 1);
+    CK(cudaMemcpyAsync(c.leaf.p, b.leaf.p, sizeof(double) * b.sl * cnt, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c.U.p, b.U.p, sizeof(double) * b.sf * cnt, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c.V.p, b.V.p, sizeof(double) * b.sf * cnt, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c.rk.p, b.rk.p, sizeof(int) * b.sr * cnt, cudaMemcpyDeviceToDevice, st));
+    return c;
+  }
+
+  // column capacity of a level's output from the input's max rank (a
+  // truncation that would exceed it flags overflow and the level is redone)
+  int rout_for(int maxr, int LR) const {
+    int Rout = std::max(4, (3 * maxr + 1) / 2 + 4);
+    if (cap > 0) Rout = std::min(Rout, std::max(cap, 1));
+    return std::max(Rout, LR);
+  }
+
+  // ---- lift (reference lift_system reduction.py:156-166, from_tridiagonal
+  //      hodlr.py:242-291, from_diagonal :294-314) of the global blocks
+  //      [first, first + mloc) ----
+  void lift(Level& L, int first, int mloc, const double* sub, const double* diag,
+            const double* sup, const double* E, const double* F) {
+    L.m = mloc;
+    L.first = first;
+    L.mg = m;
+    L.R = 1;
+    L.lvl = 0;
+    L.D.alloc(ht, L.m, 1, st);
+    L.E.alloc(ht, L.m, 1, st);
+    L.F.alloc(ht, L.m, 1, st);
+    const int e0 = first == 0 ? 1 : 0;                        // E exists for g >= 1
+    const int ne_ = L.m - e0;
+    const int nf_ = std::min(L.m, m - 1 - first);             // F exists for g <= m-2
+    Dev tD = make_tab({{&L.D, 0, 1, L.m}});
+    CK(launch_lift(dt.T, sub + (long long)first * (n - 1), diag + (long long)first * n,
+                   sup + (long long)first * (n - 1), tD.as<HB>(), L.m, st));
+    Dev tE = make_tab({{&L.E, e0, 1, ne_}});
+    CK(launch_liftdiag(dt.T, E + (long long)(first + e0 - 1) * n, tE.as<HB>(), ne_, st));
+    Dev tF = make_tab({{&L.F, 0, 1, nf_}});
+    CK(launch_liftdiag(dt.T, F + (long long)first * n, tF.as<HB>(), nf_, st));
+    Dev tZ = make_tab({{&L.E, 0, 1, e0}, {&L.F, nf_, 1, L.m - nf_}});
+    CK(launch_zerohb(dt.T, tZ.as<HB>(), e0 + L.m - nf_, st));
+    launches += 4;
+  }
+
   // ---- one reduction level (reference reduction.py:173-232) ----
   // Local window [first, first+m) of a global level of mg blocks; the last
   // local odd block takes {Dinv, E, F} of the right neighbour's first block.
   bool reduce(Level& L, int Rout, int lvl, int order, Level& nx, Record& rec,
-              int& need, bool dlev) {
+              int& need, bool dlev, const int* perm = nullptr, bool keep_input = false) {
     const int mm = L.m, first = L.first, mg = L.mg, ne = (mm + 1) / 2, no = mm / 2;
     const bool right = first + mm < mg;
     int nq = 0, nq_loc = 0, nq_h = 0, nf = 0, nf_loc = 0, nf_h = 0;
@@ -1329,7 +1377,7 @@ struct Plan {
     // singular leaves: report the first block in inversion order
     int bad = -1;
     for (int k = 0; k < ne; ++k) {
-      int e = order ? ne - 1 - k : k;
+      int e = perm ? perm[k] : order ? ne - 1 - k : k;
       if (hs[e] != INT_MAX) { bad = e; break; }
     }
     if (dlev) {
@@ -1365,9 +1413,15 @@ struct Plan {
       need = h_ovf;
       return false;
     }
-    // keep the level's couplings for the solve sweep
-    rec.E = std::move(L.E);
-    rec.F = std::move(L.F);
+    // keep the level's couplings for the solve sweep (copies when the input
+    // level must stay intact: the stepwise API is pure like the reference)
+    if (keep_input) {
+      rec.E = clone(L.E);
+      rec.F = clone(L.F);
+    } else {
+      rec.E = std::move(L.E);
+      rec.F = std::move(L.F);
+    }
     return true;
   }
 
@@ -1382,6 +1436,7 @@ struct Plan {
       F.first = 0;
       F.mg = L.mg;
       F.R = L.R;
+      F.lvl = L.lvl;
       F.D.alloc(ht, F.m, F.R, st);
       F.E.alloc(ht, F.m, F.R, st);
       F.F.alloc(ht, F.m, F.R, st);
@@ -1441,29 +1496,7 @@ struct Plan {
     first0 = P > 1 ? b0[me()] : 0;
     mloc0 = P > 1 ? b0[me() + 1] - b0[me()] : m;
     Level L;
-    L.m = mloc0;
-    L.first = first0;
-    L.mg = m;
-    L.R = 1;
-    L.D.alloc(ht, L.m, 1, st);
-    L.E.alloc(ht, L.m, 1, st);
-    L.F.alloc(ht, L.m, 1, st);
-    {
-      // bands of the global blocks [first0, first0 + mloc0)
-      const int e0 = first0 == 0 ? 1 : 0;                       // E exists for g >= 1
-      const int ne_ = L.m - e0;
-      const int nf_ = std::min(L.m, m - 1 - first0);            // F exists for g <= m-2
-      Dev tD = make_tab({{&L.D, 0, 1, L.m}});
-      CK(launch_lift(dt.T, sub + (long long)first0 * (n - 1), diag + (long long)first0 * n,
-                     sup + (long long)first0 * (n - 1), tD.as<HB>(), L.m, st));
-      Dev tE = make_tab({{&L.E, e0, 1, ne_}});
-      CK(launch_liftdiag(dt.T, E + (long long)(first0 + e0 - 1) * n, tE.as<HB>(), ne_, st));
-      Dev tF = make_tab({{&L.F, 0, 1, nf_}});
-      CK(launch_liftdiag(dt.T, F + (long long)first0 * n, tF.as<HB>(), nf_, st));
-      Dev tZ = make_tab({{&L.E, 0, 1, e0}, {&L.F, nf_, 1, L.m - nf_}});
-      CK(launch_zerohb(dt.T, tZ.as<HB>(), e0 + L.m - nf_, st));
-      launches += 4;
-    }
+    lift(L, first0, mloc0, sub, diag, sup, E, F);
     std::vector<int> dR, eR, fR;
     fetch_ranks(L.D, dR);
     fetch_ranks(L.E, eR);
@@ -1486,9 +1519,7 @@ struct Plan {
         maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
         continue;
       }
-      int Rout = std::max(4, (3 * maxr + 1) / 2 + 4);
-      if (cap > 0) Rout = std::min(Rout, std::max(cap, 1) + 0);
-      Rout = std::max(Rout, L.R);
+      int Rout = rout_for(maxr, L.R);
       if (distributed) Rout = (int)tp->allreduce_max(Rout, st);
       Record rec;
       Level nx;
@@ -1513,6 +1544,7 @@ struct Plan {
       recs.push_back(std::move(rec));
       L = std::move(nx);
       ++lvl;
+      L.lvl = lvl;
     }
     if (P > 1 && me() != 0) {
       // this rank's part ends at the consolidation level
@@ -1775,6 +1807,199 @@ struct Plan {
       sms_pending = false;
     }
     return sms;
+  }
+
+  // ---- stepwise API: the reference's lower-level surface (lift_system,
+  //      reduce_level, forward RHS update, backsubstitute; reduction.py:156-256)
+  //      on device-resident levels and records held by handle ----
+  std::map<int, Level> slev;
+  std::map<int, Record> srec;
+  int snext = 1;
+
+  void step_prep() {
+    if (!ovf.p) ovf.alloc(sizeof(int), st);
+    if (sing.n < sizeof(int) * (size_t)std::max(m, 1)) sing.alloc(sizeof(int) * std::max(m, 1), st);
+  }
+
+  int step_lift(const double* sub, const double* diag, const double* sup, const double* E,
+                const double* F) {
+    step_prep();
+    Level L;
+    lift(L, 0, m, sub, diag, sup, E, F);
+    const int id = snext++;
+    slev[id] = std::move(L);
+    return id;
+  }
+
+  Level& step_level(int id) {
+    auto it = slev.find(id);
+    if (it == slev.end()) throw ArgError("unknown level handle " + std::to_string(id));
+    return it->second;
+  }
+  Record& step_record(int id) {
+    auto it = srec.find(id);
+    if (it == srec.end()) throw ArgError("unknown record handle " + std::to_string(id));
+    return it->second;
+  }
+
+  // one level of reduce_level(level, tol, inversion_order) with the given
+  // tolerance; the input level is left intact
+  void step_reduce(int lid, double eps_, int cap_, const int* perm, int* nid, int* rid) {
+    Level& L = step_level(lid);
+    if (L.m < 2) throw ArgError("need at least 2 blocks to reduce, got " + std::to_string(L.m));
+    const int ne = (L.m + 1) / 2;
+    if (perm) {
+      std::vector<int> q(perm, perm + ne);
+      std::sort(q.begin(), q.end());
+      for (int i = 0; i < ne; ++i)
+        if (q[i] != i) throw ArgError("inversion_order must permute the even-block indices");
+    }
+    step_prep();
+    const double eps0 = eps;
+    const int cap0 = cap;
+    eps = eps_;
+    cap = cap_;
+    struct Restore {
+      Plan* p;
+      double e;
+      int c;
+      ~Restore() { p->eps = e; p->cap = c; }
+    } restore{this, eps0, cap0};
+    std::vector<int> dR, eR, fR;
+    fetch_ranks(L.D, dR);
+    fetch_ranks(L.E, eR);
+    fetch_ranks(L.F, fR);
+    sync_fetch();
+    const int maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
+    int Rout = rout_for(maxr, L.R);
+    Record rec;
+    Level nx;
+    int need = 0, tries = 0;
+    while (!reduce(L, Rout, L.lvl, 0, nx, rec, need, false, perm, true)) {
+      Rout = std::max(need, 2 * Rout);
+      rec = Record();
+      nx = Level();
+      if (++tries > 8) throw InternalError("rank capacity retries exhausted");
+    }
+    nx.lvl = L.lvl + 1;
+    fetch_ranks(rec.Dinv, rec.hDinv);
+    fetch_ranks(rec.E, rec.hE);
+    fetch_ranks(rec.F, rec.hF);
+    sync_fetch();
+    *nid = snext++;
+    slev[*nid] = std::move(nx);
+    *rid = snext++;
+    srec[*rid] = std::move(rec);
+  }
+
+  // forward RHS update of one level (reduction.py:204-216): f (mm*n, k) of the
+  // level -> fo (no*n, k) of the reduced level, row-major like acr_solve
+  void step_rhs(int rid, const double* f, int k, double* fo) {
+    Record& r = step_record(rid);
+    const long long kn = (long long)k * n;
+    const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
+    int nq = 0;
+    for (int j = 1; j < mm; j += 2)
+      if (j + 1 <= mm - 1) ++nq;
+    Dev fl(sizeof(double) * kn * mm, st);
+    CK(launch_rhs_in(f, mm * n, k, n, fl.as<double>(), st));
+    Dev z(sizeof(double) * kn * (ne + 1), st), a(sizeof(double) * kn * std::max(no, 1), st),
+        bb(sizeof(double) * kn * std::max(nq, 1), st);
+    Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
+    hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl.as<double>(), 2 * kn, k),
+              s_pan(z.as<double>(), kn, k), k);
+    Dev tE = make_tab({{&r.E, 1, 2, no}});
+    hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
+    Dev tF = make_tab({{&r.F, 1, 2, nq}});
+    hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k),
+              s_pan(bb.as<double>(), kn, k), k);
+    Dev fn(sizeof(double) * kn * std::max(no, 1), st);
+    const double* f1 = fl.as<double>() + kn;
+    CK(launch_rhs_combine(f1, 2 * kn, a.as<double>(), kn, bb.as<double>(), kn, fn.as<double>(),
+                          kn, nq, (int)kn, st));
+    CK(launch_rhs_combine(f1 + 2 * kn * nq, 2 * kn, a.as<double>() + kn * nq, kn, nullptr, 0,
+                          fn.as<double>() + kn * nq, kn, no - nq, (int)kn, st));
+    if (no) CK(launch_u_out(fn.as<double>(), no * n, k, n, fo, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // one back-substitution level (reduction.py:235-256): u of the odd blocks
+  // (no*n, k) and the level's f (mm*n, k) -> u (mm*n, k)
+  void step_backsub(int rid, const double* f, const double* uodd, int k, double* u) {
+    Record& r = step_record(rid);
+    const long long kn = (long long)k * n;
+    const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
+    Dev fl(sizeof(double) * kn * mm, st), ul(sizeof(double) * kn * mm, st);
+    CK(launch_rhs_in(f, mm * n, k, n, fl.as<double>(), st));
+    Dev uo(sizeof(double) * kn * std::max(no, 1), st);
+    if (no) {
+      CK(launch_rhs_in(uodd, no * n, k, n, uo.as<double>(), st));
+      CK(cudaMemcpy2DAsync(ul.as<double>() + kn, sizeof(double) * 2 * kn, uo.as<double>(),
+                           sizeof(double) * kn, sizeof(double) * kn, no,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    int nb = 0;
+    for (int i = 0; i <= mm - 1; i += 2)
+      if (i <= mm - 2) ++nb;
+    Dev a(sizeof(double) * kn * ne, st), b(sizeof(double) * kn * ne, st), rr(sizeof(double) * kn * ne, st);
+    CK(cudaMemsetAsync(a.p, 0, sizeof(double) * kn * ne, st));
+    CK(cudaMemsetAsync(b.p, 0, sizeof(double) * kn * ne, st));
+    double* up = ul.as<double>();
+    Dev tE = make_tab({{&r.E, 2, 2, ne - 1}});
+    hmat_full(tE.as<HB>(), ne - 1, r.E.R, s_pan(up + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
+    Dev tF = make_tab({{&r.F, 0, 2, nb}});
+    hmat_full(tF.as<HB>(), nb, r.F.R, s_pan(up + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
+    CK(launch_rhs_combine(fl.as<double>(), 2 * kn, a.as<double>(), kn, b.as<double>(), kn,
+                          rr.as<double>(), kn, ne, (int)kn, st));
+    Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
+    hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(rr.as<double>(), kn, k), s_pan(up, 2 * kn, k), k);
+    CK(launch_u_out(up, mm * n, k, n, u, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // storage of one block for export: which 0 D, 1 E, 2 F of a level handle;
+  // 3 Dinv, 4 E, 5 F of a record handle
+  const Batch* step_batch(int handle, int which) {
+    if (which <= 2) {
+      Level& L = step_level(handle);
+      return which == 0 ? &L.D : which == 1 ? &L.E : &L.F;
+    }
+    Record& r = step_record(handle);
+    return which == 3 ? &r.Dinv : which == 4 ? &r.E : &r.F;
+  }
+
+  // raw storage of one block (leaf n x bw, U/V nd x R x n column panels,
+  // ranks 2 x nnodes) into caller device buffers; null buffers: sizes only
+  void export_block(const Batch* b, int block, double* leaf, double* U, double* V, int* rk,
+                    int* R_out, int* cnt_out) {
+    if (R_out) *R_out = b->R;
+    if (cnt_out) *cnt_out = b->cnt;
+    if (!leaf && !U && !V && !rk) return;
+    if (block < 0 || block >= b->cnt) throw ArgError("block out of range");
+    if (leaf) CK(cudaMemcpyAsync(leaf, b->leaf.as<double>() + block * b->sl, sizeof(double) * b->sl,
+                                 cudaMemcpyDeviceToDevice, st));
+    if (U) CK(cudaMemcpyAsync(U, b->U.as<double>() + block * b->sf, sizeof(double) * b->sf,
+                              cudaMemcpyDeviceToDevice, st));
+    if (V) CK(cudaMemcpyAsync(V, b->V.as<double>() + block * b->sf, sizeof(double) * b->sf,
+                              cudaMemcpyDeviceToDevice, st));
+    if (rk) CK(cudaMemcpyAsync(rk, b->rk.as<int>() + block * b->sr, sizeof(int) * b->sr,
+                               cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // factor()'s storage: which 0 D, 1 E, 2 F of level `level`, 3 Dinv
+  const Batch* factor_batch(int level, int which) {
+    const int L = (int)recs.size();
+    if (which == 3) {
+      if (level < 0 || level >= L) throw ArgError("level out of range");
+      return &recs[level].Dinv;
+    }
+    if (which < 0 || which > 3) throw ArgError("which must be 0..3");
+    if (level == L) return which == 0 ? &last.D : which == 1 ? &last.E : &last.F;
+    if (level >= 0 && level < (int)kept.size())
+      return which == 0 ? &kept[level].D : which == 1 ? &recs[level].E : &recs[level].F;
+    if (level >= 0 && level < L && which != 0) return which == 1 ? &recs[level].E : &recs[level].F;
+    throw ArgError("level not retained (set option 1 before acr_factor)");
   }
 
   long long storage_bytes(int k) const {
@@ -2103,23 +2328,7 @@ int acr_block_to_dense(acr_plan_t* h, int level, int which, int block,
   ACR_GUARD(h, {
     Plan& P = *h->p;
     P.use_stream((cudaStream_t)stream);
-    const acr::Batch* b = nullptr;
-    int L = (int)P.recs.size();
-    if (which == 3) {
-      if (level < 0 || level >= L) throw acr::ArgError("level out of range");
-      b = &P.recs[level].Dinv;
-    } else {
-      if (level == L) {
-        b = which == 0 ? &P.last.D : which == 1 ? &P.last.E : &P.last.F;
-      } else if (level >= 0 && level < (int)P.kept.size()) {
-        b = which == 0 ? &P.kept[level].D
-                       : which == 1 ? &P.recs[level].E : &P.recs[level].F;
-      } else if (level >= 0 && level < L && which != 0) {
-        b = which == 1 ? &P.recs[level].E : &P.recs[level].F;
-      } else {
-        throw acr::ArgError("level not retained (set option 1 before acr_factor)");
-      }
-    }
+    const acr::Batch* b = P.factor_batch(level, which);
     if (block < 0 || block >= b->cnt) throw acr::ArgError("block out of range");
     acr::Dev tab = P.make_tab({{b, block, 1, 1}});
     acr::Dev rc(sizeof(int) * 2, P.st);
@@ -2334,6 +2543,109 @@ int acr_leaf_inverse(int s, const double* A, double* X, int* singular,
     CK(cudaMemcpyAsync(&hs, sg.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *singular = hs != INT_MAX ? 1 : 0;
+  });
+  return ACR_OK;
+}
+
+int acr_block_export(acr_plan_t* h, int level, int which, int block, double* leaf,
+                     double* U, double* V, int* ranks, int* R_out, int* count_out,
+                     void* stream) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    P.export_block(P.factor_batch(level, which), block, leaf, U, V, ranks, R_out, count_out);
+  });
+  return ACR_OK;
+}
+
+int acr_step_lift(acr_plan_t* h, const double* D_sub, const double* D_diag,
+                  const double* D_sup, const double* E, const double* F, int* level_out,
+                  void* stream) {
+  if (!h || !h->p || !level_out) return set_err(h, ACR_EARG, "null plan or output");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    *level_out = P.step_lift(D_sub, D_diag, D_sup, E, F);
+    CK(cudaStreamSynchronize(P.st));
+  });
+  return ACR_OK;
+}
+
+int acr_step_reduce(acr_plan_t* h, int level, double eps, int max_rank_cap,
+                    const int* inversion_order, int* level_out, int* record_out,
+                    void* stream) {
+  if (!h || !h->p || !level_out || !record_out) return set_err(h, ACR_EARG, "null plan or output");
+  if (!(eps > 0)) return set_err(h, ACR_EARG, "eps must be > 0");
+  if (max_rank_cap < 0) return set_err(h, ACR_EARG, "max_rank_cap must be positive");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    P.step_reduce(level, eps, max_rank_cap, inversion_order, level_out, record_out);
+  });
+  return ACR_OK;
+}
+
+int acr_step_rhs(acr_plan_t* h, int record, const double* f, int nrhs, double* f_out,
+                 void* stream) {
+  if (!h || !h->p || nrhs < 1) return set_err(h, ACR_EARG, "null plan or nrhs < 1");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    P.step_rhs(record, f, nrhs, f_out);
+  });
+  return ACR_OK;
+}
+
+int acr_step_backsub(acr_plan_t* h, int record, const double* f, const double* u_odd,
+                     int nrhs, double* u, void* stream) {
+  if (!h || !h->p || nrhs < 1) return set_err(h, ACR_EARG, "null plan or nrhs < 1");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    P.step_backsub(record, f, u_odd, nrhs, u);
+  });
+  return ACR_OK;
+}
+
+int acr_step_info(acr_plan_t* h, int handle, int which, int* count, int* R, int* level,
+                  int* m_level) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    const acr::Batch* b = P.step_batch(handle, which);
+    if (count) *count = b->cnt;
+    if (R) *R = b->R;
+    if (which <= 2) {
+      acr::Level& L = P.step_level(handle);
+      if (level) *level = L.lvl;
+      if (m_level) *m_level = L.m;
+    } else {
+      acr::Record& r = P.step_record(handle);
+      if (level) *level = -1;
+      if (m_level) *m_level = r.m;
+    }
+  });
+  return ACR_OK;
+}
+
+int acr_step_export(acr_plan_t* h, int handle, int which, int block, double* leaf, double* U,
+                    double* V, int* ranks, void* stream) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    P.export_block(P.step_batch(handle, which), block, leaf, U, V, ranks, nullptr, nullptr);
+  });
+  return ACR_OK;
+}
+
+int acr_step_free(acr_plan_t* h, int handle) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    if (!P.slev.erase(handle) && !P.srec.erase(handle))
+      throw acr::ArgError("unknown handle " + std::to_string(handle));
   });
   return ACR_OK;
 }

@@ -210,6 +210,26 @@ class AcrSolver:
     def kernel_launches(self) -> int:
         return int(self.lib.acr_kernel_launches(self.plan))
 
+    def export_hodlr(self, level: int, which: str, block: int):
+        """One block of the factorisation as a reference-shaped host
+        ``HodlrMatrix`` (``hodlr.py``; reference ``hodlr.py:102-173``):
+        which in D, E, F (level system) or Dinv (elimination record)."""
+        from .hodlr import export_block
+        code = {"D": 0, "E": 1, "F": 2, "Dinv": 3}[which]
+        R, cnt = C.c_int(), C.c_int()
+        st = _stream(self.torch)
+        rc = self.lib.acr_block_export(self.plan, level, code, block, None, None, None, None,
+                                       C.byref(R), C.byref(cnt), st)
+        if rc != 0:
+            _raise(self.plan, rc)
+
+        def call(leaf, U, V, rk):
+            rc_ = self.lib.acr_block_export(self.plan, level, code, block, leaf, U, V, rk,
+                                            None, None, st)
+            if rc_ != 0:
+                _raise(self.plan, rc_)
+        return export_block(self.lib, self.plan, self.n, self.leaf_size, R.value, call, st)
+
     def block_dense(self, level: int, which: str, block: int):
         """Dense copy of one block (tests): which in D, E, F, Dinv."""
         code = {"D": 0, "E": 1, "F": 2, "Dinv": 3}[which]
