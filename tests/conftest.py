@@ -52,3 +52,16 @@ def golden_profiles(z, prefix):
 @pytest.fixture(scope="session")
 def small_golden():
     return load_npz("small_systems.npz")
+
+
+def projections(u, nproj=8, seed=1234, chunk=1 << 20):
+    """G @ u for the seeded Gaussian G of tests/golden/make_golden.py
+    ``projections`` (same numpy stream): compares every entry of a solution
+    whose fixture keeps only a subsample."""
+    rng = np.random.default_rng(seed)
+    N = u.shape[0]
+    acc = np.zeros((nproj,) + u.shape[1:])
+    for c0 in range(0, N, chunk):
+        c1 = min(N, c0 + chunk)
+        acc += rng.standard_normal((nproj, c1 - c0)) @ u[c0:c1]
+    return acc

@@ -132,6 +132,7 @@ def config(name, stride=1, nrhs=1):
     out["u_stride"] = stride
     out["u"] = u[::stride]
     out["u_norm"] = np.linalg.norm(u)
+    out["u_proj"] = projections(u)
     out["wall_s"] = wall
     out["backsub_ms"] = rep.backsub_ms
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
@@ -291,7 +292,7 @@ if __name__ == "__main__":
         elif w in ("cfg1", "cfg2"):
             config(w)
         elif w == "cfg3":
-            config(w, stride=8)
+            config(w, stride=1)
         elif w in ("cfg4", "cfg5"):
             config(w, stride=64)
         elif w == "mmio":

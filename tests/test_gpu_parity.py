@@ -47,6 +47,22 @@ def _rank_counts(m0, n, leaf, levels, cutoff=1):
     return out
 
 
+def _rank_flips(rep, z, prefix, shape):
+    """Lower bound on the rank decisions that differ from the reference's:
+    sum over (level, depth) of |mean rank difference| x decisions there
+    (each flipped decision moves the mean by at least 1/decisions), and the
+    largest per-(level, depth) max-rank difference."""
+    prof = golden_profiles(z, prefix)
+    counts = _rank_counts(*shape, rep.levels)
+    flips, dmax = 0.0, 0
+    for lv, (p, q) in enumerate(zip(rep.per_level_ranks, prof)):
+        assert len(p.max_by_depth) == len(q[0])
+        for d, (a, b) in enumerate(zip(p.mean_by_depth, q[1])):
+            flips += abs(a - b) * counts[lv][d]
+        dmax = max([dmax] + [abs(a - b) for a, b in zip(p.max_by_depth, q[0])])
+    return int(round(flips)), dmax
+
+
 def _check_against_golden(rep, u, z, prefix, eps, u_ref=None, stride=1,
                           shape=None, flip_frac=1e-3):
     if u_ref is None:
@@ -60,8 +76,8 @@ def _check_against_golden(rep, u, z, prefix, eps, u_ref=None, stride=1,
     # rank decisions: a decision whose singular value sits within roundoff of
     # the threshold -- or of the noise guard sigma_1 <= R eps |Ru| |Rv|, which
     # fires hundreds of times on config 3 and compares roundoff-level numbers
-    # by construction -- may flip between LAPACK and the GPU; allow <= 0.1% of
-    # decisions to flip (the solution / residual bars above are the contract)
+    # by construction -- may flip between LAPACK and the GPU.  Generic bound
+    # here; the config tests pin the measured counts (PINNED_FLIPS)
     flips, total = 0.0, 0
     counts = _rank_counts(*shape, rep.levels) if shape else None
     for lv, (p, q) in enumerate(zip(rep.per_level_ranks, prof)):
@@ -167,6 +183,17 @@ def test_config_against_reference(solver_mod, cfg):
     stride = int(z["u_stride"])
     _check_against_golden(rep, u, z, "", c["eps"], stride=stride,
                           shape=(c["n"], c["n"], c["leaf"]))
+    flips, dmax = _rank_flips(rep, z, "", (c["n"], c["n"], c["leaf"]))
+    print(f"{cfg}: rank flips >= {flips}, max-rank difference {dmax}")
+    assert flips <= PINNED_FLIPS[cfg] and dmax <= min(PINNED_FLIPS[cfg], 1)
+    if "u_proj" in z.files:
+        from conftest import projections
+        assert _rel(projections(u), z["u_proj"]) <= 10 * c["eps"]
+
+
+# rank decisions measured to differ from the reference's (noise-guard /
+# threshold ties at roundoff; _rank_flips), pinned
+PINNED_FLIPS = {"cfg1": 0, "cfg2": 0, "cfg3": 29, "cfg5": 0}
 
 
 def test_forward_reversed_bitwise(solver_mod):
@@ -294,6 +321,9 @@ def test_config5_column0_against_reference(solver_mod):
     stride = int(z["u_stride"])
     _check_against_golden(rep, u, z, "", c["eps"], stride=stride,
                           shape=(c["n"], c["n"], c["leaf"]))
+    flips, dmax = _rank_flips(rep, z, "", (c["n"], c["n"], c["leaf"]))
+    print(f"cfg5: rank flips >= {flips}, max-rank difference {dmax}")
+    assert flips <= PINNED_FLIPS["cfg5"] and dmax <= 1
 
 
 def test_cta_pair_recompression_path(solver_mod):
@@ -356,3 +386,63 @@ def test_multi_rhs_columns_match_single_solves(solver_mod):
     for j in range(3):
         uj = sol.solve(f[:, j].contiguous()).cpu().numpy()
         assert _rel(u3[:, j], uj) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg5"])
+def test_config_16_rhs_against_reference(solver_mod, cfg):
+    """BASELINE config 5 as benchmarked: 16 right-hand-side columns against
+    the reference-shim solution (make_golden.py multi_rhs: acr_solve's body
+    with reduction.matvec rebound to algebra.matmat, SURVEY.md 8(c);
+    column 0 matches the reference's own single-column run to 4.5e-16).
+    Every column: solution within 10 x eps (subsample, norms and Gaussian
+    projections of every entry) and residual <= 2x the reference's."""
+    from conftest import projections
+    z = load_npz(f"{cfg}x16.npz")
+    c = P.CONFIGS[cfg]
+    s = P.make_config(cfg, nrhs=16)
+    sol = solver_mod.AcrSolver(s.n_blocks, s.block_dim, Tolerance(c["eps"]), 1, c["leaf"])
+    bands = sol.device_bands(s)
+    sol.factor(bands)
+    f = torch.as_tensor(s.rhs, device="cuda")
+    ud = sol.solve(f)
+    u = ud.cpu().numpy()
+    eps = c["eps"]
+    st = int(z["u_stride"])
+    ref = z["u"]
+    for j in range(16):
+        assert _rel(u[::st, j], ref[:, j]) <= 10 * eps, j
+    norms = np.linalg.norm(u, axis=0)
+    assert np.all(np.abs(norms - z["u_norm"]) <= 10 * eps * z["u_norm"])
+    pu, pr = projections(u), z["u_proj"]
+    for j in range(16):
+        assert _rel(pu[:, j], pr[:, j]) <= 10 * eps, j
+    res = []
+    for j in range(16):
+        r, _ = solver_mod.relative_residual_gpu(bands, ud[:, j].contiguous(),
+                                                f[:, j].contiguous(), s.n_blocks, s.block_dim)
+        res.append(r)
+    res = np.array(res)
+    assert np.all(res <= 2 * z["residual"]), (res / z["residual"]).max()
+    print(f"{cfg}x16: max residual ratio {(res / z['residual']).max():.3f}, "
+          f"max subsample rel {max(_rel(u[::st, j], ref[:, j]) for j in range(16)):.2e}")
+
+
+def test_singular_cutoff_block(solver_mod):
+    """Nonsingular pivots but a singular remaining block: the cutoff LU
+    raises LinAlgError("matrix is singular to working precision") like the
+    reference's dense_lu_solve (oracles.py:28-30), not SingularBlockError."""
+    n = 8
+    for leaf in (8, 2):
+        s = P.random_system(2, n, seed=1)
+        s.D_diag[0] = 1.0
+        s.D_sub[0] = s.D_sup[0] = 0.0
+        s.E[0] = 2.0
+        s.F[0] = 3.0
+        s.D_diag[1] = 6.0            # S = D_1 - E_0 D_0^-1 F_0 = 0
+        s.D_sub[1] = s.D_sup[1] = 0.0
+        with pytest.raises(np.linalg.LinAlgError,
+                           match="matrix is singular to working precision") as ei:
+            solver_mod.acr_solve(s, Tolerance(1e-12), leaf_size=leaf)
+        assert not isinstance(ei.value, SingularBlockError)
+        with pytest.raises(np.linalg.LinAlgError, match="matrix is singular"):
+            O.acr_solve(s, Tolerance(1e-12), leaf_size=leaf)
