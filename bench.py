@@ -179,9 +179,16 @@ def run_reference(args):
 def run_ours(args):
     import torch
     ws, rank, local = _dist()
+    if ws > torch.cuda.device_count():
+        print(f"bench.py: {ws} ranks but {torch.cuda.device_count()} visible GPU(s)",
+              file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1604_00617_b200.solver import AcrSolver, relative_residual_gpu
@@ -422,7 +429,8 @@ def run_ours(args):
                    f"leaf {c['leaf']}, eps {c['eps']}, factor with bands in HBM",
                    "global_unknowns": N, "nrhs_e2e": k,
                    "parallelism": (f"block-row shards x{ws} (NCCL neighbour halo, "
-                                   "top levels on rank 0)") if ws > 1 else "single",
+                                   "progressive consolidation of the top levels)")
+                   if ws > 1 else "single",
                    "l2": "inputs 168 MB and HODLR working set exceed the 126 MB L2; no flush"},
         "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -449,6 +457,21 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _spawn_ranks(args) -> int:
+    """``bench.py --gpus N`` (N > 1) started without torchrun: re-launch this
+    script as N ranks, one process per GPU (the driver's own launch line),
+    and return their exit status.  Rank 0 prints the JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -458,6 +481,16 @@ def main():
     ap.add_argument("--config", default="cfg5", choices=sorted(P.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # NCCL communicator lines (nranks, transport) on stderr, JSON on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        sys.exit(_spawn_ranks(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and ws != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws} ranks",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     else:

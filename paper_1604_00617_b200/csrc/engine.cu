@@ -474,7 +474,6 @@ struct Plan {
   Transport* tp = nullptr;
   bool own_tp = false;
   std::vector<int> bnd0;
-  int Ld = 0;                 // number of distributed levels (then rank 0 alone)
   int first0 = 0, mloc0 = 0;  // this rank's level-0 window
   // per-kernel-class instrumentation (option 2)
   bool prof_on = false;
@@ -524,6 +523,12 @@ struct Plan {
       cudaStreamDestroy(st2);
       cudaEventDestroy(evf);
       cudaEventDestroy(evj);
+    }
+    if (stc) {
+      cudaStreamSynchronize(stc);
+      cudaStreamDestroy(stc);
+      cudaEventDestroy(evcf);
+      cudaEventDestroy(evcj);
     }
     if (own_tp) delete tp;
   }
@@ -581,31 +586,112 @@ struct Plan {
     st_set = true;
   }
 
+  // comm stream for halo transfers that overlap compute (sharded plans)
+  cudaStream_t stc = nullptr;
+  cudaEvent_t evcf = nullptr, evcj = nullptr;
+  bool ef_pending = false;
+  int nb_left = -1, nb_right = -1;   // active neighbours at the current level
+  cudaStream_t comm_stream() {
+    if (!stc) {
+      CK(cudaStreamCreateWithFlags(&stc, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&evcf, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&evcj, cudaEventDisableTiming));
+    }
+    return stc;
+  }
+  void comm_fork() {
+    cudaStream_t c = comm_stream();
+    CK(cudaEventRecord(evcf, st));
+    CK(cudaStreamWaitEvent(c, evcf, 0));
+  }
+  void comm_join() {
+    CK(cudaEventRecord(evcj, stc));
+    CK(cudaStreamWaitEvent(st, evcj, 0));
+  }
+
   int nranks() const { return tp ? tp->size() : 1; }
   int me() const { return tp ? tp->rank() : 0; }
 
-  // block boundaries of every rank at level l (b[P] = global block count)
-  std::vector<int> bounds(int l) const {
-    const int P = nranks();
-    std::vector<int> b(P + 1);
-    int mg = m;
-    for (int t = 0; t < l; ++t) mg /= 2;
-    for (int r = 0; r < P; ++r) b[r] = bnd0.empty() ? 0 : (bnd0[r] >> l);
-    b[P] = mg;
-    return b;
+  // ---- sharding schedule; host-only and identical on
+  //      every rank (mirrored by paper_1604_00617_b200/dist.py schedule) ----
+  // wins[l]: block boundaries of every rank at level l after that level's
+  // merges (b[P] = global block count; a retired rank has an empty window).
+  // Before reducing level l the active windows must each start even, hold
+  // >= 2 blocks and (except the last) have even length; while they do not,
+  // active ranks merge pairwise (the 2i+1-th active rank hands its window
+  // to the 2i-th), so the upper levels consolidate onto P/2, P/4, ... GPUs
+  // as the block count halves.  At the cutoff everything merges onto rank 0.
+  struct MergeStep {
+    int lvl;
+    std::vector<int> before, after;
+  };
+  std::vector<std::vector<int>> wins;
+  std::vector<MergeStep> msteps;
+  int Lsched = 0;
+
+  static std::vector<int> active_of(const std::vector<int>& b) {
+    std::vector<int> a;
+    for (size_t r = 0; r + 1 < b.size(); ++r)
+      if (b[r + 1] > b[r]) a.push_back((int)r);
+    return a;
   }
-  // level l can be reduced distributed: every window starts even, has >= 2
-  // blocks and (except the last) an even length
-  bool dist_ok(int l) const {
-    const int P = nranks();
-    if (P <= 1) return false;
-    std::vector<int> b = bounds(l);
-    for (int r = 0; r < P; ++r) {
-      const int c = b[r + 1] - b[r];
+  static bool win_ok(const std::vector<int>& b) {
+    std::vector<int> a = active_of(b);
+    for (size_t i = 0; i < a.size(); ++i) {
+      const int r = a[i], c = b[r + 1] - b[r];
       if ((b[r] & 1) || c < 2) return false;
-      if (r < P - 1 && (c & 1)) return false;
+      if (i + 1 < a.size() && (c & 1)) return false;
     }
     return true;
+  }
+  static std::vector<int> merge_pairs(const std::vector<int>& b) {
+    std::vector<int> a = active_of(b), nb = b;
+    for (size_t i = 0; 2 * i + 1 < a.size(); ++i) {
+      const int dst = a[2 * i], src = a[2 * i + 1];
+      for (int x = dst + 1; x <= src; ++x) nb[x] = b[src + 1];
+    }
+    return nb;
+  }
+  void schedule() {
+    wins.clear();
+    msteps.clear();
+    const int P = nranks();
+    std::vector<int> cur = P > 1 ? bnd0 : std::vector<int>{0, m};
+    int mg = m, l = 0;
+    while (true) {
+      const bool last = mg <= cutoff;
+      while (active_of(cur).size() > 1 && (last || !win_ok(cur))) {
+        std::vector<int> nb = merge_pairs(cur);
+        msteps.push_back({l, cur, nb});
+        cur = nb;
+      }
+      wins.push_back(cur);
+      if (last) break;
+      mg /= 2;
+      ++l;
+      for (int r = 0; r < P; ++r) cur[r] >>= 1;
+      cur[P] = mg;
+    }
+    Lsched = l;
+  }
+  int nactive(int l) const { return (int)active_of(wins[l]).size(); }
+  bool active_at(int l) const { return wins[l][me() + 1] > wins[l][me()]; }
+  // previous / next active rank at level l (-1 if none)
+  int left_nb(int l) const {
+    for (int r = me() - 1; r >= 0; --r)
+      if (wins[l][r + 1] > wins[l][r]) return r;
+    return -1;
+  }
+  int right_nb(int l) const {
+    for (int r = me() + 1; r + 1 < (int)wins[l].size(); ++r)
+      if (wins[l][r + 1] > wins[l][r]) return r;
+    return -1;
+  }
+  // active rank whose window (boundaries b) holds block position pos
+  static int owner(const std::vector<int>& b, int pos) {
+    for (size_t r = 0; r + 1 < b.size(); ++r)
+      if (b[r] <= pos && pos < b[r + 1]) return (int)r;
+    return -1;
   }
 
   void block_msgs(std::vector<Msg>& msgs, const Batch& b, int e, int peer, bool send) {
@@ -1281,6 +1367,25 @@ struct Plan {
     CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
     int* sg = sing.as<int>();
     CK(launch_fill_i32(sg, INT_MAX, (long long)ne, st));
+    // 0. halo E, F of the right neighbour's first even block (level inputs):
+    //    on the comm stream, overlapped with the invert below
+    Batch hE, hF;
+    if (dlev) {
+      std::vector<Msg> msgs;
+      if (first > 0) {
+        block_msgs(msgs, L.E, 0, nb_left, true);
+        block_msgs(msgs, L.F, 0, nb_left, true);
+      }
+      if (right) {
+        hE.alloc(ht, 1, L.R, st);
+        hF.alloc(ht, 1, L.R, st);
+        block_msgs(msgs, hE, 0, nb_right, false);
+        block_msgs(msgs, hF, 0, nb_right, false);
+      }
+      comm_fork();
+      tp->exchange(msgs, comm_stream());
+      ef_pending = true;
+    }
     // 1. Dinv of the even blocks
     rec.m = mm;
     rec.first = first;
@@ -1295,23 +1400,21 @@ struct Plan {
       invert(tDi.as<HB>(), ne, rec.Dinv.R, sg);
     }
     // 1b. halo: our first even block to the left, the right neighbour's to us
-    Batch hDi, hE, hF;
+    Batch hDi;
     if (dlev) {
+      // Dinv of the first even block leaves once the invert is done; its E
+      // and F (level inputs) already went out on the comm stream before the
+      // invert (reduce step 0), so only a third of the halo is exposed
       std::vector<Msg> msgs;
-      if (first > 0) {
-        block_msgs(msgs, rec.Dinv, 0, me() - 1, true);
-        block_msgs(msgs, L.E, 0, me() - 1, true);
-        block_msgs(msgs, L.F, 0, me() - 1, true);
-      }
+      if (first > 0) block_msgs(msgs, rec.Dinv, 0, nb_left, true);
       if (right) {
         hDi.alloc(ht, 1, Rout, st);
-        hE.alloc(ht, 1, L.R, st);
-        hF.alloc(ht, 1, L.R, st);
-        block_msgs(msgs, hDi, 0, me() + 1, false);
-        block_msgs(msgs, hE, 0, me() + 1, false);
-        block_msgs(msgs, hF, 0, me() + 1, false);
+        block_msgs(msgs, hDi, 0, nb_right, false);
       }
-      tp->exchange(msgs, st);
+      comm_fork();
+      tp->exchange(msgs, comm_stream());
+      comm_join();
+      ef_pending = false;
     }
     // 2. P_j = E_j Dinv_{j-1}, Q_j = F_j Dinv_{j+1}
     Batch PQ;
@@ -1324,6 +1427,10 @@ struct Plan {
                lvl == 0 ? 1 : 0);
     }
     // 3. X = P F_{j-1}, Y = Q E_{j+1}, E' = -P E_{j-1}, F' = -Q F_{j+1}
+    if (ef_pending) {
+      comm_join();
+      ef_pending = false;
+    }
     nx.m = no;
     nx.first = first / 2;
     nx.mg = mg / 2;
@@ -1425,21 +1532,37 @@ struct Plan {
     return true;
   }
 
-  // gather every rank's window of level l onto rank 0 (rank 0 continues alone)
-  void consolidate(Level& L, int l) {
-    std::vector<int> b = bounds(l);
-    const int P = nranks();
-    std::vector<Msg> msgs;
-    Level F;
-    if (me() == 0) {
-      F.m = L.mg;
-      F.first = 0;
-      F.mg = L.mg;
-      F.R = L.R;
-      F.lvl = L.lvl;
-      F.D.alloc(ht, F.m, F.R, st);
-      F.E.alloc(ht, F.m, F.R, st);
-      F.F.alloc(ht, F.m, F.R, st);
+  // merges scheduled before reducing level l (progressive consolidation):
+  // a retiring rank sends its whole window (D, E, F) to the active rank that
+  // takes it over and returns false; a growing rank receives and
+  // concatenates.  Windows are contiguous, so the merged level is the two
+  // windows back to back.
+  bool apply_merges(Level& L, int l) {
+    const int r = me();
+    for (const MergeStep& ms : msteps) {
+      if (ms.lvl != l) continue;
+      const bool was = ms.before[r + 1] > ms.before[r];
+      if (!was) continue;
+      const bool now = ms.after[r + 1] > ms.after[r];
+      std::vector<Msg> msgs;
+      if (!now) {
+        const int dst = owner(ms.after, ms.before[r]);
+        range_msgs(msgs, L.D, 0, L.m, dst, true);
+        range_msgs(msgs, L.E, 0, L.m, dst, true);
+        range_msgs(msgs, L.F, 0, L.m, dst, true);
+        tp->exchange(msgs, st);
+        CK(cudaStreamSynchronize(st));
+        L = Level();
+        return false;
+      }
+      if (ms.after[r + 1] == ms.before[r + 1]) continue;   // not involved
+      Level G;
+      G.m = ms.after[r + 1] - ms.after[r];
+      G.first = L.first;
+      G.mg = L.mg;
+      G.R = L.R;
+      G.lvl = L.lvl;
+      for (Batch* d : {&G.D, &G.E, &G.F}) d->alloc(ht, G.m, G.R, st);
       auto cp = [&](Batch& dst, const Batch& src, int cnt) {
         CK(cudaMemcpyAsync(dst.leaf.p, src.leaf.p, sizeof(double) * src.sl * cnt,
                            cudaMemcpyDeviceToDevice, st));
@@ -1450,24 +1573,36 @@ struct Plan {
         CK(cudaMemcpyAsync(dst.rk.p, src.rk.p, sizeof(int) * src.sr * cnt,
                            cudaMemcpyDeviceToDevice, st));
       };
-      cp(F.D, L.D, L.m);
-      cp(F.E, L.E, L.m);
-      cp(F.F, L.F, L.m);
-      for (int r = 1; r < P; ++r) {
-        const int c = b[r + 1] - b[r];
-        range_msgs(msgs, F.D, b[r], c, r, false);
-        range_msgs(msgs, F.E, b[r], c, r, false);
-        range_msgs(msgs, F.F, b[r], c, r, false);
+      cp(G.D, L.D, L.m);
+      cp(G.E, L.E, L.m);
+      cp(G.F, L.F, L.m);
+      for (int q = r + 1; q + 1 < (int)ms.before.size(); ++q) {
+        const int c = ms.before[q + 1] - ms.before[q];
+        if (c <= 0) continue;
+        if (ms.before[q] >= ms.after[r + 1]) break;
+        const int off = ms.before[q] - ms.after[r];
+        range_msgs(msgs, G.D, off, c, q, false);
+        range_msgs(msgs, G.E, off, c, q, false);
+        range_msgs(msgs, G.F, off, c, q, false);
       }
-    } else {
-      range_msgs(msgs, L.D, 0, L.m, 0, true);
-      range_msgs(msgs, L.E, 0, L.m, 0, true);
-      range_msgs(msgs, L.F, 0, L.m, 0, true);
+      tp->exchange(msgs, st);
+      L = std::move(G);
     }
-    tp->exchange(msgs, st);
-    CK(cudaStreamSynchronize(st));
-    if (me() == 0) L = std::move(F);
-    else L = Level();
+    return true;
+  }
+
+  // a rank that retired before level l still takes part in the level's
+  // collectives (capacity and singular / overflow agreement), contributing
+  // neutral values, so the active ranks' all-reduces complete
+  void shadow_level(int l) {
+    if (nactive(l) <= 1) return;
+    tp->allreduce_max(0, st);                                 // Rout
+    while (true) {
+      if (tp->allreduce_max(0, st)) throw SingularError("singular dense leaf on another rank");
+      const long long ov = tp->allreduce_max(0, st);
+      if (!ov) break;
+      if (ov >= (1 << 29) || ov > 4 * n + 64) throw InternalError("truncation overflow on another rank");
+    }
   }
 
   // ---- factor ----
@@ -1483,7 +1618,6 @@ struct Plan {
     launches = 0;
     prof_reset();
     factored = false;
-    Ld = 0;
     if (!ovf.p) ovf.alloc(sizeof(int), st);
     sing.alloc(sizeof(int) * std::max(m, 1), st);
     if (!ev0) {
@@ -1492,62 +1626,67 @@ struct Plan {
     }
     CK(cudaEventRecord(ev0, st));
     const int P = nranks();
-    std::vector<int> b0 = bounds(0);
-    first0 = P > 1 ? b0[me()] : 0;
-    mloc0 = P > 1 ? b0[me() + 1] - b0[me()] : m;
+    schedule();
+    first0 = P > 1 ? bnd0[me()] : 0;
+    mloc0 = P > 1 ? bnd0[me() + 1] - bnd0[me()] : m;
     Level L;
     lift(L, first0, mloc0, sub, diag, sup, E, F);
     std::vector<int> dR, eR, fR;
-    fetch_ranks(L.D, dR);
-    fetch_ranks(L.E, eR);
-    fetch_ranks(L.F, fR);
-    sync_fetch();
-    profile_level(L.m, dR, eR, fR);
-    int maxr = std::max(max_rank_of(dR), 1);
+    int maxr = 1;
     int lvl = 0;
-    bool distributed = P > 1;
-    while (L.mg > cutoff || distributed) {
-      if (distributed && (L.mg <= cutoff || !dist_ok(lvl))) {
-        consolidate(L, lvl);
-        distributed = false;
-        Ld = lvl;
-        if (me() != 0) break;
-        fetch_ranks(L.D, dR);
-        fetch_ranks(L.E, eR);
-        fetch_ranks(L.F, fR);
-        sync_fetch();
-        maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
-        continue;
+    bool alive = true;
+    auto ranks_of = [&](bool prof_it) {
+      fetch_ranks(L.D, dR);
+      fetch_ranks(L.E, eR);
+      fetch_ranks(L.F, fR);
+      sync_fetch();
+      if (prof_it) profile_level(L.m, dR, eR, fR);
+      maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
+    };
+    ranks_of(true);
+    while (true) {
+      if (P > 1 && !msteps.empty()) {
+        const int m_before = L.m;
+        if (!apply_merges(L, lvl)) {
+          alive = false;
+          break;
+        }
+        if (L.m != m_before) ranks_of(false);
+      }
+      if (L.mg <= cutoff) break;
+      const bool dlev = P > 1 && nactive(lvl) > 1;
+      if (dlev) {
+        nb_left = left_nb(lvl);
+        nb_right = right_nb(lvl);
       }
       int Rout = rout_for(maxr, L.R);
-      if (distributed) Rout = (int)tp->allreduce_max(Rout, st);
+      if (dlev) Rout = (int)tp->allreduce_max(Rout, st);
       Record rec;
       Level nx;
       int need = 0;
       int tries = 0;
-      while (!reduce(L, Rout, lvl, order, nx, rec, need, distributed)) {
+      while (!reduce(L, Rout, lvl, order, nx, rec, need, dlev)) {
         Rout = std::max(need, 2 * Rout);
         rec = Record();
         nx = Level();
         if (++tries > 8) throw InternalError("rank capacity retries exhausted");
       }
+      // the fetched rank tables land in rec's / dR.. host vectors at the sync:
+      // sync before rec moves into recs
       fetch_ranks(rec.Dinv, rec.hDinv);
       fetch_ranks(rec.E, rec.hE);
       fetch_ranks(rec.F, rec.hF);
-      fetch_ranks(nx.D, dR);
-      fetch_ranks(nx.E, eR);
-      fetch_ranks(nx.F, fR);
-      sync_fetch();
-      profile_level(nx.m, dR, eR, fR);
-      maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
       if (keep_levels) kept.push_back(std::move(L));
-      recs.push_back(std::move(rec));
       L = std::move(nx);
       ++lvl;
       L.lvl = lvl;
+      ranks_of(true);
+      recs.push_back(std::move(rec));
     }
-    if (P > 1 && me() != 0) {
-      // this rank's part ends at the consolidation level
+    if (!alive) {
+      // retired at level lvl: shadow the collectives of the levels still
+      // reduced by several ranks, then this rank's part is done
+      for (int l = lvl; l < Lsched; ++l) shadow_level(l);
       CK(cudaEventRecord(ev1, st));
       CK(cudaStreamSynchronize(st));
       float ms = 0;
@@ -1627,48 +1766,66 @@ struct Plan {
     }
     CK(cudaEventRecord(sev0, st));
     const long long kn = (long long)k * n;
-    const int L = (int)recs.size();
     const int P = nranks();
+    const int Lt = P > 1 ? Lsched : (int)recs.size();   // level of the cutoff system
     const bool root = me() == 0;
-    std::vector<Dev> f(L + 1);
+    std::vector<Dev> f(Lt + 1);
     f[0].alloc(sizeof(double) * kn * std::max(mloc0, 1), st);
     CK(launch_rhs_in(rhs + (long long)first0 * n * k, mloc0 * n, k, n, f[0].as<double>(), st));
     ++launches;
-    for (int l = 0; l < L; ++l) {
-      if (P > 1 && l == Ld) {
-        // gather the consolidation level's right-hand side on rank 0
-        std::vector<int> b = bounds(l);
-        std::vector<Msg> msgs;
-        if (root) {
-          Dev full(sizeof(double) * kn * b[P], st);
-          CK(cudaMemcpyAsync(full.p, f[l].p, sizeof(double) * kn * (b[1] - b[0]),
+    // windows (block counts) this rank holds at level l before / after merges
+    auto wcount = [&](const std::vector<int>& b) { return b[me() + 1] - b[me()]; };
+    int lret = Lt;                     // level at which this rank retired (Lt: never)
+    // forward sweep (reduction.py:204-216) with the factor's merges replayed
+    for (int l = 0; l <= Lt; ++l) {
+      if (P > 1) {
+        bool out = false;
+        for (const MergeStep& ms : msteps) {
+          if (ms.lvl != l || wcount(ms.before) <= 0) continue;
+          std::vector<Msg> msgs;
+          if (wcount(ms.after) <= 0) {
+            msgs.push_back({owner(ms.after, ms.before[me()]), f[l].p,
+                            sizeof(double) * kn * wcount(ms.before), true});
+            tp->exchange(msgs, st);
+            out = true;
+            break;
+          }
+          if (ms.after[me() + 1] == ms.before[me() + 1]) continue;
+          Dev g(sizeof(double) * kn * wcount(ms.after), st);
+          CK(cudaMemcpyAsync(g.p, f[l].p, sizeof(double) * kn * wcount(ms.before),
                              cudaMemcpyDeviceToDevice, st));
-          for (int r = 1; r < P; ++r)
-            msgs.push_back({r, full.as<double>() + kn * b[r],
-                            sizeof(double) * kn * (b[r + 1] - b[r]), false});
+          for (int q = me() + 1; q + 1 < (int)ms.before.size(); ++q) {
+            const int c = ms.before[q + 1] - ms.before[q];
+            if (c <= 0) continue;
+            if (ms.before[q] >= ms.after[me() + 1]) break;
+            msgs.push_back({q, g.as<double>() + kn * (ms.before[q] - ms.after[me()]),
+                            sizeof(double) * kn * c, false});
+          }
           tp->exchange(msgs, st);
-          f[l] = std::move(full);
-        } else {
-          msgs.push_back({0, f[l].p, sizeof(double) * kn * (b[me() + 1] - b[me()]), true});
-          tp->exchange(msgs, st);
+          f[l] = std::move(g);
+        }
+        if (out) {
+          lret = l;
+          break;
         }
       }
+      if (l == Lt) break;
       Record& r = recs[l];
+      const bool dlev = P > 1 && nactive(l) > 1;
       const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
-      int nq = 0, nq_loc = 0;
+      int nq = 0;
       for (int j = 1; j < mm; j += 2)
-        if (r.first + j + 1 <= r.mg - 1) { ++nq; if (j + 1 < mm) ++nq_loc; }
-      const int nq_h = nq - nq_loc;
+        if (r.first + j + 1 <= r.mg - 1) ++nq;
       double* fl = f[l].as<double>();
       Dev z(sizeof(double) * kn * (std::max(ne, 1) + 1), st);   // + halo slot
       Dev a(sizeof(double) * kn * std::max(no, 1), st);
       Dev bb(sizeof(double) * kn * std::max(nq, 1), st);
       Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
       hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl, 2 * kn, k), s_pan(z.as<double>(), kn, k), k);
-      if (P > 1 && l < Ld) {
+      if (dlev) {
         std::vector<Msg> msgs;
-        if (r.first > 0) msgs.push_back({me() - 1, z.p, sizeof(double) * kn, true});
-        if (r.right) msgs.push_back({me() + 1, z.as<double>() + kn * ne, sizeof(double) * kn, false});
+        if (r.first > 0) msgs.push_back({left_nb(l), z.p, sizeof(double) * kn, true});
+        if (r.right) msgs.push_back({right_nb(l), z.as<double>() + kn * ne, sizeof(double) * kn, false});
         tp->exchange(msgs, st);
       }
       Dev tE = make_tab({{&r.E, 1, 2, no}});
@@ -1676,7 +1833,6 @@ struct Plan {
       // F_j z_{j+1}: z index i+1 (the halo slot ne for the right neighbour's block)
       Dev tF = make_tab({{&r.F, 1, 2, nq}});
       hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k), s_pan(bb.as<double>(), kn, k), k);
-      (void)nq_h;
       f[l + 1].alloc(sizeof(double) * kn * std::max(no, 1), st);
       double* fn = f[l + 1].as<double>();
       CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, bb.as<double>(), kn, fn, kn, nq, (int)kn, st));
@@ -1684,33 +1840,15 @@ struct Plan {
                             fn + kn * nq, kn, no - nq, (int)kn, st));
       launches += 2;
     }
-    if (P > 1 && L == Ld) {
-      // distributed levels only reach the cutoff: gather for the dense solve
-      std::vector<int> b = bounds(L);
-      std::vector<Msg> msgs;
-      if (root) {
-        Dev full(sizeof(double) * kn * b[P], st);
-        CK(cudaMemcpyAsync(full.p, f[L].p, sizeof(double) * kn * (b[1] - b[0]),
-                           cudaMemcpyDeviceToDevice, st));
-        for (int r = 1; r < P; ++r)
-          msgs.push_back({r, full.as<double>() + kn * b[r],
-                          sizeof(double) * kn * (b[r + 1] - b[r]), false});
-        tp->exchange(msgs, st);
-        f[L] = std::move(full);
-      } else {
-        msgs.push_back({0, f[L].p, sizeof(double) * kn * (b[me() + 1] - b[me()]), true});
-        tp->exchange(msgs, st);
-      }
-    }
-    std::vector<Dev> uu(L + 1);
+    std::vector<Dev> uu(Lt + 1);
     if (root) {
-      // cutoff solve
+      // cutoff solve (reduction.py:305-310)
       const int mc = last.m;
-      uu[L].alloc(sizeof(double) * kn * std::max(mc, 1), st);
+      uu[Lt].alloc(sizeof(double) * kn * std::max(mc, 1), st);
       Dev B(sizeof(double) * (size_t)Nc * k, st);
       for (int i = 0; i < mc; ++i)
         CK(cudaMemcpy2DAsync(B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
-                             f[L].as<double>() + i * kn, sizeof(double) * n,
+                             f[Lt].as<double>() + i * kn, sizeof(double) * n,
                              sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
       if (!lut_ok) {
         if (lut.n < sizeof(double) * (size_t)Nc * Nc) lut.alloc(sizeof(double) * (size_t)Nc * Nc, st);
@@ -1721,49 +1859,58 @@ struct Plan {
       CK(lu_solve(lu.as<double>(), lut.as<double>(), Nc, piv.as<int>(), B.as<double>(), k, st));
       ++launches;
       for (int i = 0; i < mc; ++i)
-        CK(cudaMemcpy2DAsync(uu[L].as<double>() + i * kn, sizeof(double) * n,
+        CK(cudaMemcpy2DAsync(uu[Lt].as<double>() + i * kn, sizeof(double) * n,
                              B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
                              sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
     }
-    // back-substitution
-    for (int l = L - 1; l >= -1; --l) {
-      if (P > 1 && l + 1 == Ld) {
-        // scatter the consolidation level's solution back to the owners
-        std::vector<int> b = bounds(Ld);
-        std::vector<Msg> msgs;
-        const int c = b[me() + 1] - b[me()];
-        if (root) {
-          for (int r = 1; r < P; ++r)
-            msgs.push_back({r, uu[Ld].as<double>() + kn * b[r],
-                            sizeof(double) * kn * (b[r + 1] - b[r]), true});
+    // back-substitution (reduction.py:235-256): undo level l's merges (the
+    // solution goes back to the ranks that held those blocks), then level l-1
+    for (int l = lret; l >= 0; --l) {
+      if (P > 1) {
+        for (auto it = msteps.rbegin(); it != msteps.rend(); ++it) {
+          const MergeStep& ms = *it;
+          if (ms.lvl != l || wcount(ms.before) <= 0) continue;
+          std::vector<Msg> msgs;
+          if (wcount(ms.after) <= 0) {             // this rank retired here: receive
+            uu[l].alloc(sizeof(double) * kn * wcount(ms.before), st);
+            msgs.push_back({owner(ms.after, ms.before[me()]), uu[l].p,
+                            sizeof(double) * kn * wcount(ms.before), false});
+            tp->exchange(msgs, st);
+            continue;
+          }
+          if (ms.after[me() + 1] == ms.before[me() + 1]) continue;
+          for (int q = me() + 1; q + 1 < (int)ms.before.size(); ++q) {
+            const int c = ms.before[q + 1] - ms.before[q];
+            if (c <= 0) continue;
+            if (ms.before[q] >= ms.after[me() + 1]) break;
+            msgs.push_back({q, uu[l].as<double>() + kn * (ms.before[q] - ms.after[me()]),
+                            sizeof(double) * kn * c, true});
+          }
           tp->exchange(msgs, st);
-          Dev mine(sizeof(double) * kn * std::max(c, 1), st);
-          CK(cudaMemcpyAsync(mine.p, uu[Ld].p, sizeof(double) * kn * c,
+          Dev mine(sizeof(double) * kn * std::max(wcount(ms.before), 1), st);
+          CK(cudaMemcpyAsync(mine.p, uu[l].p, sizeof(double) * kn * wcount(ms.before),
                              cudaMemcpyDeviceToDevice, st));
           CK(cudaStreamSynchronize(st));
-          uu[Ld] = std::move(mine);
-        } else {
-          uu[Ld].alloc(sizeof(double) * kn * std::max(c, 1), st);
-          msgs.push_back({0, uu[Ld].p, sizeof(double) * kn * c, false});
-          tp->exchange(msgs, st);
+          uu[l] = std::move(mine);
         }
       }
-      if (l < 0) break;
-      if (P > 1 && !root && l >= Ld) continue;
-      Record& r = recs[l];
+      if (l == 0) break;
+      const int lv = l - 1;
+      Record& r = recs[lv];
+      const bool dlev = P > 1 && nactive(lv) > 1;
       const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
-      uu[l].alloc(sizeof(double) * kn * mm, st);
-      double* ul = uu[l].as<double>();
+      uu[lv].alloc(sizeof(double) * kn * mm, st);
+      double* ul = uu[lv].as<double>();
       if (no)
-        CK(cudaMemcpy2DAsync(ul + kn, sizeof(double) * 2 * kn, uu[l + 1].as<double>(),
+        CK(cudaMemcpy2DAsync(ul + kn, sizeof(double) * 2 * kn, uu[l].as<double>(),
                              sizeof(double) * kn, sizeof(double) * kn, no,
                              cudaMemcpyDeviceToDevice, st));
       Dev uleft(sizeof(double) * kn, st);
-      if (P > 1 && l < Ld) {
+      if (dlev) {
         // the left neighbour's last odd block feeds our first even block
         std::vector<Msg> msgs;
-        if (r.right) msgs.push_back({me() + 1, ul + kn * (mm - 1), sizeof(double) * kn, true});
-        if (r.first > 0) msgs.push_back({me() - 1, uleft.p, sizeof(double) * kn, false});
+        if (r.right) msgs.push_back({right_nb(lv), ul + kn * (mm - 1), sizeof(double) * kn, true});
+        if (r.first > 0) msgs.push_back({left_nb(lv), uleft.p, sizeof(double) * kn, false});
         tp->exchange(msgs, st);
       }
       int nb = 0;
@@ -1783,12 +1930,12 @@ struct Plan {
       Dev tF = make_tab({{&r.F, 0, 2, nb}});
       hmat_full(tF.as<HB>(), nb, r.F.R, s_pan(ul + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
       Dev rr(sizeof(double) * kn * ne, st);
-      CK(launch_rhs_combine(f[l].as<double>(), 2 * kn, a.as<double>(), kn, b.as<double>(), kn,
+      CK(launch_rhs_combine(f[lv].as<double>(), 2 * kn, a.as<double>(), kn, b.as<double>(), kn,
                             rr.as<double>(), kn, ne, (int)kn, st));
       ++launches;
       Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
       hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(rr.as<double>(), kn, k), s_pan(ul, 2 * kn, k), k);
-      uu[l + 1].release();
+      uu[l].release();
     }
     CK(launch_u_out(uu[0].as<double>(), mloc0 * n, k, n, u + (long long)first0 * n * k, st));
     ++launches;

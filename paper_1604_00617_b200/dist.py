@@ -3,11 +3,12 @@
 Each rank owns a contiguous, even-aligned range of block rows.  Per
 reduction level the only exchange is the right neighbour's first even
 block ({Dinv, E, F}; one n x k vector per boundary in the solve), so each
-level's odd-block Schur updates stay local.  When a rank would hold fewer
-than two blocks (or alignment breaks) the level is gathered on rank 0, which
-finishes the top levels and the cutoff LU (the reference's algorithm is
+level's odd-block Schur updates stay local.  When the windows would hold
+fewer than two blocks (or alignment breaks) active ranks merge pairwise --
+the upper levels consolidate onto P/2, P/4, ... GPUs as the block count
+halves -- and rank 0 finishes the cutoff LU (the reference's algorithm is
 unchanged: same blocks, same products, same truncations -> the sharded
-result is bitwise the single-GPU one).
+result is the single-GPU one).
 
 ``block_partition`` is the pure host rule (tested on CPU); ``DistAcrSolver``
 drives the C ABI with NCCL between one process per GPU (torch.distributed
@@ -25,7 +26,7 @@ import numpy as np
 from . import _capi
 from .system import BlockTridiagSystem, Tolerance
 
-__all__ = ["block_partition", "level_bounds", "distributed_levels",
+__all__ = ["block_partition", "level_bounds", "distributed_levels", "schedule",
            "DistAcrSolver", "loopback_solve"]
 
 
@@ -65,13 +66,71 @@ def distributed_ok(b0: List[int], m: int, level: int) -> bool:
 
 
 def distributed_levels(m: int, P: int, cutoff: int = 1) -> int:
-    """Number of levels reduced sharded before consolidation on rank 0."""
+    """Number of levels reduced with every rank active (before the first
+    merge)."""
     b0 = block_partition(m, P)
     lv, mg = 0, m
     while mg > cutoff and distributed_ok(b0, m, lv):
         mg //= 2
         lv += 1
     return lv
+
+
+def _active(b: List[int]) -> List[int]:
+    return [r for r in range(len(b) - 1) if b[r + 1] > b[r]]
+
+
+def windows_ok(b: List[int]) -> bool:
+    """Active windows start even, hold >= 2 blocks, and all but the last
+    have even length (Plan::win_ok)."""
+    a = _active(b)
+    for i, r in enumerate(a):
+        c = b[r + 1] - b[r]
+        if b[r] % 2 or c < 2 or (i + 1 < len(a) and c % 2):
+            return False
+    return True
+
+
+def merge_pairs(b: List[int]) -> List[int]:
+    """The (2i+1)-th active rank hands its window to the 2i-th
+    (Plan::merge_pairs)."""
+    a, nb = _active(b), list(b)
+    for i in range(len(a) // 2):
+        dst, src = a[2 * i], a[2 * i + 1]
+        for x in range(dst + 1, src + 1):
+            nb[x] = b[src + 1]
+    return nb
+
+
+def schedule(m: int, P: int, cutoff: int = 1):
+    """Progressive consolidation schedule (Plan::schedule, csrc/engine.cu):
+    returns (wins, steps, L) with wins[l] every rank's window boundaries at
+    level l after that level's merges, steps = [(level, before, after)] the
+    pairwise merges in order, L the cutoff level.  Upper levels move onto
+    P/2, P/4, ... ranks as the block count halves; at the cutoff everything
+    is on rank 0."""
+    cur = block_partition(m, P) if P > 1 else [0, m]
+    wins, steps = [], []
+    mg, lv = m, 0
+    while True:
+        last = mg <= cutoff
+        while len(_active(cur)) > 1 and (last or not windows_ok(cur)):
+            nb = merge_pairs(cur)
+            steps.append((lv, list(cur), nb))
+            cur = nb
+        wins.append(list(cur))
+        if last:
+            return wins, steps, lv
+        mg //= 2
+        lv += 1
+        cur = [x >> 1 for x in cur[:-1]] + [mg]
+
+
+def owner(b: List[int], pos: int) -> int:
+    for r in range(len(b) - 1):
+        if b[r] <= pos < b[r + 1]:
+            return r
+    return -1
 
 
 def loopback_solve(sys: BlockTridiagSystem, tol: Tolerance, P: int,

@@ -1,7 +1,8 @@
-"""N>1 host logic on CPU (gloo, world size 2 and 3).
+"""N>1 host logic on CPU (gloo, world sizes 2, 3, 4).
 
 An emulation of the sharded schedule of csrc/engine.cu (Plan::reduce halo,
-Plan::consolidate, Plan::solve halo vectors) written with the CPU oracle's
+Plan::apply_merges progressive consolidation, Plan::solve halo vectors and
+merge replay) written with the CPU oracle's
 HODLR operations and torch.distributed point-to-point messages.  The same
 partition rules (paper_1604_00617_b200.dist) decide windows and the
 consolidation level.  Because each block's arithmetic is unchanged by the
@@ -20,7 +21,7 @@ import torch.multiprocessing as mp
 
 from oracle import acr_oracle as O
 from paper_1604_00617_b200 import problems as P
-from paper_1604_00617_b200.dist import block_partition, distributed_ok, level_bounds
+from paper_1604_00617_b200.dist import block_partition, owner, schedule
 from paper_1604_00617_b200.system import Tolerance
 
 
@@ -43,102 +44,117 @@ def _recv(src):
 
 
 def sharded_solve(sys_, tol, leaf, cutoff=1):
-    """Rank-local part of the sharded factor + solve (oracle arithmetic)."""
+    """Rank-local part of the sharded factor + solve (oracle arithmetic),
+    following the engine's schedule: halo of the right active neighbour's
+    first even block per level, pairwise merges (progressive consolidation)
+    before a level whose windows break the alignment rules, everything on
+    rank 0 at the cutoff; the solve replays the merges forward and undoes
+    them backward."""
     rank, Pn = dist.get_rank(), dist.get_world_size()
     m = sys_.n_blocks
     t = O.build_node_table(sys_.block_dim, leaf)
+    wins, steps, Lt = schedule(m, Pn, cutoff)
     b0 = block_partition(m, Pn)
     full = O.lift(sys_, t)
     lo, hi = b0[rank], b0[rank + 1]
-    # window of level 0; E/F None outside the global system
     D, E, F = full.D[lo:hi], full.E[lo:hi], full.F[lo:hi]
     f = [x.copy() for x in full.f[lo:hi]]
+    cnt = lambda b: b[rank + 1] - b[rank]                       # noqa: E731
+    act = lambda b, r: b[r + 1] > b[r]                          # noqa: E731
     first, mg = lo, m
     records = []
-    lvl = 0
-    while mg > cutoff and distributed_ok(b0, m, lvl):
+    lret = Lt
+    for lvl in range(Lt + 1):
+        out = False
+        for (sl, before, after) in steps:
+            if sl != lvl or cnt(before) <= 0:
+                continue
+            if cnt(after) <= 0:
+                _send((D, E, F, f), owner(after, before[rank]))
+                out = True
+                break
+            if after[rank + 1] == before[rank + 1]:
+                continue
+            for q in range(rank + 1, Pn):
+                if before[q + 1] - before[q] <= 0:
+                    continue
+                if before[q] >= after[rank + 1]:
+                    break
+                d2, e2, f2_, ff = _recv(q)
+                D, E, F, f = D + d2, E + e2, F + f2_, f + ff
+        if out:
+            lret = lvl
+            break
+        if lvl == Lt:
+            break
+        w = wins[lvl]
+        left = next((r for r in range(rank - 1, -1, -1) if act(w, r)), -1)
+        rightnb = next((r for r in range(rank + 1, Pn) if act(w, r)), -1)
         mm = len(D)
         right = first + mm < mg
         even = list(range(0, mm, 2))
         Dinv = {i: O.invert(D[i], t, tol) for i in even}
-        # halo: our first even block to the left, the right neighbour's to us
         if first > 0:
-            _send((Dinv[0], E[0], F[0]), rank - 1)
+            _send((Dinv[0], E[0], F[0], f[0]), left)
         if right:
-            hD, hE, hF = _recv(rank + 1)
-            Dinv[mm], Eh, Fh = hD, hE, hF
-        get_E = lambda i: E[i] if i < mm else Eh
-        get_F = lambda i: F[i] if i < mm else Fh
-        D2, E2, F2 = [], [], []
+            hD, Eh, Fh, fh = _recv(rightnb)
+            Dinv[mm] = hD
+        get_E = lambda i: E[i] if i < mm else Eh               # noqa: E731
+        get_F = lambda i: F[i] if i < mm else Fh               # noqa: E731
+        get_f = lambda i: f[i] if i < mm else fh               # noqa: E731
+        D2, E2, F2, f2 = [], [], [], []
         for j in range(1, mm, 2):
             jg = first + j
             Pj = O.multiply(E[j], Dinv[j - 1], t, tol)
             Dp = O.add(D[j], O.negate(O.multiply(Pj, F[j - 1], t, tol)), t, tol)
+            fp = f[j] - O.hmat(E[j], t, 0, O.hmat(Dinv[j - 1], t, 0, f[j - 1]))
             Ep = O.negate(O.multiply(Pj, E[j - 1], t, tol)) if jg >= 2 else None
             Fp = None
             if jg + 1 <= mg - 1:
                 Qj = O.multiply(F[j], Dinv[j + 1], t, tol)
                 Dp = O.add(Dp, O.negate(O.multiply(Qj, get_E(j + 1), t, tol)), t, tol)
+                fp = fp - O.hmat(F[j], t, 0, O.hmat(Dinv[j + 1], t, 0, get_f(j + 1)))
                 if jg + 2 <= mg - 1:
                     Fp = O.negate(O.multiply(Qj, get_F(j + 1), t, tol))
-            D2.append(Dp); E2.append(Ep); F2.append(Fp)
-        records.append(dict(m=mm, first=first, mg=mg, right=right,
-                            Dinv=[Dinv[i] for i in even], E=E, F=F))
-        D, E, F = D2, E2, F2
+            D2.append(Dp); E2.append(Ep); F2.append(Fp); f2.append(fp)
+        records.append(dict(m=mm, first=first, mg=mg, right=right, left=left,
+                            rightnb=rightnb, Dinv=[Dinv[i] for i in even], E=E, F=F, f=f))
+        D, E, F, f = D2, E2, F2, f2
         first, mg = first // 2, mg // 2
-        lvl += 1
-    Ld = lvl
-    # consolidation of level Ld on rank 0
-    gathered = [None] * Pn if rank == 0 else None
-    dist.gather_object((D, E, F), gathered, dst=0)
-    # ---- solve: forward sweep over the sharded levels ----
-    for rec in records:
-        mm, fr, mgl = rec["m"], rec["first"], rec["mg"]
-        z = {i: O.hmat(rec["Dinv"][i // 2], t, 0, f[i]) for i in range(0, mm, 2)}
-        if fr > 0:
-            _send(z[0], rank - 1)
-        if rec["right"]:
-            z[mm] = _recv(rank + 1)
-        f2 = []
-        for j in range(1, mm, 2):
-            fp = f[j] - O.hmat(rec["E"][j], t, 0, z[j - 1])
-            if fr + j + 1 <= mgl - 1:
-                fp = fp - O.hmat(rec["F"][j], t, 0, z[j + 1])
-            f2.append(fp)
-        rec["f"] = f
-        f = f2
-    fg = [None] * Pn if rank == 0 else None
-    dist.gather_object(f, fg, dst=0)
+    u = None
     if rank == 0:
-        D = [b for part in gathered for b in part[0]]
-        E = [b for part in gathered for b in part[1]]
-        F = [b for part in gathered for b in part[2]]
-        ff = [x for part in fg for x in part]
-        lv = O.Level(Ld, D, E, F, ff)
-        top = []
-        while lv.m > cutoff:
-            lv, rec = O.reduce_level(lv, t, tol)
-            top.append(rec)
+        lv = O.Level(Lt, D, E, F, f)
         us = O.dense_lu_solve(lv.to_dense(t), np.concatenate(lv.f))
         n = t.n
-        u_top = O.backsubstitute(top, t, [us[i * n:(i + 1) * n] for i in range(lv.m)])
-        bnd = level_bounds(b0, m, Ld)
-        segs = [u_top[i * n:(i + 1) * n] for i in range(bnd[-1])]
-        parts = [segs[bnd[r]:bnd[r + 1]] for r in range(Pn)]
-    else:
-        parts = None
-    box = [None]
-    dist.scatter_object_list(box, parts, src=0)
-    u = box[0]
-    # ---- back-substitution over the sharded levels ----
-    for rec in reversed(records):
+        u = [us[i * n:(i + 1) * n] for i in range(lv.m)]
+    for lvl in range(lret, -1, -1):
+        for (sl, before, after) in reversed(steps):
+            if sl != lvl or cnt(before) <= 0:
+                continue
+            if cnt(after) <= 0:
+                u = _recv(owner(after, before[rank]))
+                continue
+            if after[rank + 1] == before[rank + 1]:
+                continue
+            for q in range(rank + 1, Pn):
+                c = before[q + 1] - before[q]
+                if c <= 0:
+                    continue
+                if before[q] >= after[rank + 1]:
+                    break
+                off = before[q] - after[rank]
+                _send(u[off:off + c], q)
+            u = u[:cnt(before)]
+        if lvl == 0:
+            break
+        rec = records[lvl - 1]
         mm, fr, mgl = rec["m"], rec["first"], rec["mg"]
         full_u = [None] * mm
         for k, j in enumerate(range(1, mm, 2)):
             full_u[j] = u[k]
         if rec["right"]:
-            _send(full_u[mm - 1], rank + 1)
-        uleft = _recv(rank - 1) if fr > 0 else None
+            _send(full_u[mm - 1], rec["rightnb"])
+        uleft = _recv(rec["left"]) if fr > 0 else None
         for i in range(0, mm, 2):
             r = rec["f"][i].copy()
             if fr + i >= 1:
@@ -168,10 +184,11 @@ CASES = {
     "rand16": (P.random_system(16, 16, seed=31), Tolerance(1e-10), 4, 1),
     "rand13_c2": (P.random_system(13, 8, seed=2), Tolerance(1e-10), 4, 2),
     "poisson32": (P.poisson_const(32, seed=1), Tolerance(1e-8), 8, 1),
+    "rand32_c3": (P.random_system(32, 8, seed=5), Tolerance(1e-10), 4, 3),
 }
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_sharded_schedule_matches_single_process(world, name):
     s, tol, leaf, cutoff = CASES[name]
