@@ -13,8 +13,12 @@ through the public API with pinned host buffers: H2D of the bands and the
 
 ``--impl reference`` times the CPU restatement of the reference
 (oracle/acr_oracle.py, the reference's own algorithm and LAPACK calls) on a
-bounded sample of the same workload: the first 32 block rows of the config-5
-system (same n, leaf, eps), so every step stays within seconds.
+bounded sample of the same workload: the first 64 block rows of the config-5
+system (same n, leaf, eps; 6 of the 11 levels), one BLAS thread (the
+reference is single-threaded; all-core BLAS is reported beside it and is
+slower on these block sizes), so every step stays within seconds.  The
+reference package itself cannot travel to the GPU box; its own full-config
+factor time measured in the build container is reported as context.
 """
 
 from __future__ import annotations
@@ -38,7 +42,7 @@ from paper_1604_00617_b200.system import (BlockTridiagSystem,  # noqa: E402
 
 METRIC = "ACR factor unknowns/s (fp64 5-pt 2D)"
 UNIT = "unknowns/s"
-SAMPLE_BLOCKS = 32
+SAMPLE_BLOCKS = 64          # 6 of config 5's 11 levels; ~5-10 s per step on one core
 
 
 def _dist():
@@ -110,57 +114,91 @@ class ClockSampler:
                 "reasons": sorted(seen), "samples": len(sm)}
 
 
-def sample_system(cfg: str) -> BlockTridiagSystem:
-    """First SAMPLE_BLOCKS block rows of the config (same n, leaf, eps)."""
+def sample_system(cfg: str, blocks: int = None) -> BlockTridiagSystem:
+    """First ``blocks`` block rows of the config (same n, leaf, eps)."""
     s = P.make_config(cfg, nrhs=1)
-    k = min(SAMPLE_BLOCKS, s.n_blocks)
+    k = min(blocks or SAMPLE_BLOCKS, s.n_blocks)
     n = s.block_dim
     return BlockTridiagSystem(k, n, s.D_sub[:k], s.D_diag[:k], s.D_sup[:k],
                               s.E[:k - 1], s.F[:k - 1], s.rhs[:k * n],
                               name=f"{s.name}[:{k}]")
 
 
-def cpu_reference_step(cfg: str, sub: BlockTridiagSystem):
-    """One bounded sample of the reference algorithm on the host (oracle)."""
+def cpu_reference_step(cfg: str, sub: BlockTridiagSystem, threads: int = 1):
+    """One bounded sample of the reference algorithm on the host (oracle: the
+    reference's algorithm with its LAPACK call sequence), BLAS limited to
+    ``threads`` threads."""
+    from threadpoolctl import threadpool_limits
     from oracle import acr_oracle as O
     c = P.CONFIGS[cfg]
-    _, rep = O.acr_solve(sub, Tolerance(c["eps"]), leaf_size=c["leaf"])
+    with threadpool_limits(threads):
+        _, rep = O.acr_solve(sub, Tolerance(c["eps"]), leaf_size=c["leaf"])
     return sub.n_unknowns / (rep.reduce_ms / 1e3), rep
 
 
-def host_threads():
+def cpu_model() -> str:
     try:
-        from threadpoolctl import threadpool_info
-        return max((i.get("num_threads", 1) for i in threadpool_info()
-                    if i.get("internal_api") in ("openblas", "mkl", "blis")),
-                   default=os.cpu_count() or 1)
-    except Exception:
-        return os.cpu_count() or 1
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_context(cfg: str) -> dict:
+    """The real reference's own full-config factor time, measured in the
+    build container on one core (tests/golden/<cfg>.npz reduce_ms, from
+    make_golden.py running acrsolve.acr_solve unmodified)."""
+    out = {}
+    try:
+        z = np.load(os.path.join(REPO, "tests", "golden", f"{cfg}.npz"))
+        N = P.CONFIGS[cfg]["n"] ** 2
+        ms = float(z["reduce_ms"])
+        out = {"reference_full_config_reduce_ms": ms,
+               "reference_full_config_unknowns_per_s": N / (ms / 1e3),
+               "where": "build container, 1 core (8-core Intel Xeon), acrsolve unmodified"}
+    except (OSError, KeyError):
+        pass
+    return out
+
+
+def cpu_baseline_block(cfg: str, steps: int = 1):
+    """1 BLAS thread (the reference is single-threaded) as the
+    primary figure, plus one all-host-cores run; nproc and CPU model."""
+    sub = sample_system(cfg)
+    nproc = os.cpu_count() or 1
+    vals, reds = [], []
+    for _ in range(steps):
+        v, rep = cpu_reference_step(cfg, sub, 1)
+        vals.append(v)
+        reds.append(rep.reduce_ms)
+    v1 = sub.n_unknowns * steps / (sum(reds) / 1e3)
+    va, rep_a = cpu_reference_step(cfg, sub, nproc)
+    return sub, v1, {
+        "value": v1, "unit": UNIT, "cores": 1, "kind": "port",
+        "sample": (f"{cfg} first {sub.n_blocks} of {P.CONFIGS[cfg]['n']} block rows "
+                   f"({sub.n_unknowns} unknowns, n={sub.block_dim}, "
+                   f"{len(reds)} x reduce phase of oracle/acr_oracle.py = the reference's "
+                   f"algorithm and LAPACK calls, {sum(reds) / 1e3:.1f} s)"),
+        "all_cores": {"value": va, "cores": nproc, "reduce_ms": rep_a.reduce_ms},
+        "nproc": nproc, "cpu_model": cpu_model(),
+        "context": reference_context(cfg)}
 
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    sub = sample_system(args.config)
+    # warm-up: one config-1 solve per warm-up step (SURVEY.md 8(d))
+    w1 = P.make_config("cfg1")
     for _ in range(args.warmup):
-        cpu_reference_step(args.config, sub)
-    vals, reds = [], []
-    for _ in range(args.steps):
-        v, rep = cpu_reference_step(args.config, sub)
-        vals.append(v)
-        reds.append(rep.reduce_ms)
-    total_s = sum(reds) / 1e3
-    value = sub.n_unknowns * args.steps / total_s
-    cores = host_threads()
-    sample = (f"{args.config} first {sub.n_blocks} block rows "
-              f"({sub.n_unknowns} unknowns, n={sub.block_dim}); "
-              "reduce phase of oracle/acr_oracle.py (reference algorithm, "
-              "numpy/LAPACK), per step")
+        cpu_reference_step("cfg1", w1, 1)
+    sub, value, cb = cpu_baseline_block(args.config, args.steps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_s / args.steps,
+        "ms_per_step": 1e3 * sub.n_unknowns / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generator, BASELINE cfg5 formulas)",
         "impl": "reference",
@@ -168,8 +206,7 @@ def run_reference(args):
                    f"{P.CONFIGS[args.config]['n']} block rows",
                    "n": sub.block_dim, "leaf": P.CONFIGS[args.config]["leaf"],
                    "eps": P.CONFIGS[args.config]["eps"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
-                         "kind": "port", "sample": sample},
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -330,14 +367,19 @@ def run_ours(args):
     inst_factor_ms = float(solver.lib.acr_factor_ms(solver.plan))
     import ctypes as C
     stats = {}
-    for cls, name in enumerate(["k_trunc", "k_leafinv", "k_leafgemm", "k_hmat",
-                                "k_leafgemm_diag"]):
+    names = ["k_trunc", "k_leafinv", "k_leafgemm", "k_hmat", "k_leafgemm_diag", "k_gp",
+             "k_leaflr", "k_elementwise", "k_lu_cutoff"]
+    for cls, name in enumerate(names):
         nl = C.c_longlong()
         kms = C.c_double()
         ctr = (C.c_ulonglong * 16)()
         solver.lib.acr_kernel_stats(solver.plan, cls, C.byref(nl), C.byref(kms), ctr)
         stats[name] = {"launches": nl.value, "ms": kms.value,
                        "flops": ctr[0], "bytes": ctr[1]}
+    # level-0 leaf products with a diagonal operand (E, F of the lifted
+    # system): no FLOPs to speak of; its counter carries algorithmic bytes
+    dg = stats["k_leafgemm_diag"]
+    dg["bytes"], dg["flops"] = dg["flops"], 0
     tr = stats["k_trunc"]
     peaks = {}
     try:
@@ -345,12 +387,44 @@ def run_ours(args):
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # FP64 peaks measured on this GPU model (scripts/fp64_peak.cu ->
+    # profiles/r01_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)
+    fp64 = {}
+    try:
+        fp64 = json.load(open(os.path.join(REPO, "profiles", "r01_fp64_peak.json")))
+    except OSError:
+        pass
+    dfma = float(fp64.get("dfma_tflops", 34.16)) * 1e3
+    dmma = float(fp64.get("dmma_tflops", 37.20)) * 1e3
+    pipes = {"k_trunc": ("DFMA", dfma, "Householder QR, Jacobi SVD, apply-Q"),
+             "k_leafinv": ("DFMA", dfma, "register-tiled Gauss-Jordan"),
+             "k_leafgemm": ("DMMA", dmma, "m8n8k4 dense leaf products"),
+             "k_hmat": ("DFMA", dfma, "HODLR x panel (leaf_matmat + lr_apply)"),
+             "k_leafgemm_diag": ("DFMA", dfma, "level-0 exact diagonal leaf products"),
+             "k_gp": ("DFMA", dfma, "panel x (panel^T panel)"),
+             "k_leaflr": ("DFMA", dfma, "leaf += U V^T (leaf_add_uvT)"),
+             "k_elementwise": ("DFMA", dfma, "leaf add / negate / copy"),
+             "k_lu_cutoff": ("DFMA", dfma, "blocked LU of the cutoff block")}
+    for name, st_ in stats.items():
+        pipe, pk, what = pipes[name]
+        sec = st_["ms"] / 1e3
+        gbs = st_["bytes"] / sec / 1e9 if sec > 0 else 0.0
+        gfs = st_["flops"] / sec / 1e9 if sec > 0 else 0.0
+        t_roof = max(st_["bytes"] / (hbm_peak * 1e9), st_["flops"] / (pk * 1e9))
+        st_.update({"achieved_gbs": gbs, "achieved_gflops": gfs, "pipe": pipe, "what": what,
+                    "bound": "hbm" if st_["bytes"] / (hbm_peak * 1e9) >= st_["flops"] / (pk * 1e9)
+                    else "fp64",
+                    "hbm_frac": gbs / hbm_peak, "fp64_frac": gfs / pk,
+                    "roofline_frac": t_roof / sec if sec > 0 else 0.0})
     avg_ms = tr["ms"] / max(tr["launches"], 1)
     per_launch_bytes = tr["bytes"] / max(tr["launches"], 1)
     achieved = per_launch_bytes / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
     traffic = None
     try:
-        dr = json.load(open(os.path.join(REPO, "profiles", "r01_trunc_dram.json")))
+        fn = os.path.join(REPO, "profiles", "r02_trunc_dram.json")
+        if not os.path.exists(fn):
+            fn = os.path.join(REPO, "profiles", "r01_trunc_dram.json")
+        dr = json.load(open(fn))
         if cfg == "cfg5" and ws == 1:
             traffic = dr["dram_bytes_total"] / max(tr["launches"], 1)
     except (OSError, KeyError, ValueError):
@@ -361,7 +435,7 @@ def run_ours(args):
         "frac": achieved / hbm_peak,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
         "traffic": traffic,
-        "traffic_source": "profiles/r01_trunc_dram.json (ncu dram__bytes_read+write over every "
+        "traffic_source": "profiles/r02_trunc_dram.json (ncu dram__bytes_read+write over every "
                           "k_trunc launch of one config-5 factor, per instrumented launch)"
         if traffic is not None else None,
         "algorithmic_bytes_per_launch": per_launch_bytes,
@@ -369,42 +443,18 @@ def run_ours(args):
         "fp64_gflops_achieved": (tr["flops"] / max(tr["launches"], 1)) / (avg_ms / 1e3) / 1e9
         if avg_ms > 0 else 0.0,
         "share_of_factor": tr["ms"] / max(inst_factor_ms, 1e-9),
+        "instrumented_factor_ms": inst_factor_ms,
         "kernel_classes": stats,
+        "class_census": "algorithmic FLOP/bytes per SURVEY.md Appendix C: device counters "
+                        "(k_trunc in-kernel; k_hmat / k_gp / k_leaflr census kernels over the "
+                        "device ranks) or host counts (leaf classes, elementwise, LU)",
+        "fp64_peak_source": "profiles/r01_fp64_peak.json (measured DFMA %.2f / DMMA %.2f TFLOP/s)"
+                            % (dfma / 1e3, dmma / 1e3),
     }
-    # FP64 view of the same classes against the FP64 peaks measured on this
-    # GPU model (scripts/fp64_peak.cu -> profiles/r01_fp64_peak.json)
-    fp64 = {}
-    try:
-        fp64 = json.load(open(os.path.join(REPO, "profiles", "r01_fp64_peak.json")))
-    except OSError:
-        pass
-    dfma = float(fp64.get("dfma_tflops", 34.16)) * 1e3
-    dmma = float(fp64.get("dmma_tflops", 37.20)) * 1e3
-
-    def _gfs(st):
-        return st["flops"] / (st["ms"] / 1e3) / 1e9 if st["ms"] > 0 else 0.0
-    roofline_fp64 = {
-        "unit": "GFLOP/s", "peak_source": "profiles/r01_fp64_peak.json (measured DFMA / DMMA)",
-        "k_trunc": {"achieved": _gfs(tr), "peak": dfma, "frac": _gfs(tr) / dfma,
-                    "pipe": "DFMA (Householder QR, Jacobi, apply-Q)"},
-        "k_leafgemm": {"achieved": _gfs(stats["k_leafgemm"]), "peak": dmma,
-                       "frac": _gfs(stats["k_leafgemm"]) / dmma,
-                       "pipe": "DMMA m8n8k4 (dense leaf products)"},
-        "k_leafinv": {"achieved": _gfs(stats["k_leafinv"]), "peak": dfma,
-                      "frac": _gfs(stats["k_leafinv"]) / dfma,
-                      "pipe": "DFMA (register-tiled Gauss-Jordan)"},
-    }
-    # level-0 leaf products with a diagonal operand (E, F of the lifted
-    # system): no FLOPs to speak of, HBM-bound; its 'flops' counter carries
-    # algorithmic bytes (leaf + diagonal read, product written)
-    dg = stats.pop("k_leafgemm_diag")
-    dg["bytes"], dg["flops"] = dg["flops"], 0
-    stats["k_leafgemm_diag"] = dg
-    roofline_fp64["k_leafgemm_diag"] = {
-        "achieved_gbs": dg["bytes"] / (dg["ms"] / 1e3) / 1e9 if dg["ms"] > 0 else 0.0,
-        "peak_gbs": hbm_peak,
-        "frac": (dg["bytes"] / (dg["ms"] / 1e3) / 1e9 / hbm_peak) if dg["ms"] > 0 else 0.0,
-        "pipe": "HBM (level-0 exact diagonal leaf products)"}
+    roofline_fp64 = {n_: {"achieved": v["achieved_gflops"], "peak": pipes[n_][1],
+                          "frac": v["fp64_frac"], "pipe": pipes[n_][0]}
+                     for n_, v in stats.items()}
+    roofline_fp64["unit"] = "GFLOP/s"
 
     # end-to-end roofline of the whole factor: T_roof =
     # max(census FLOPs / FP64 peak, compulsory bytes / HBM peak) over the
@@ -444,13 +494,7 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        sub = sample_system(cfg)
-        v, rep = cpu_reference_step(cfg, sub)
-        line["cpu_baseline"] = {
-            "value": v, "unit": UNIT, "cores": host_threads(), "kind": "port",
-            "sample": f"{cfg} first {sub.n_blocks} block rows ({sub.n_unknowns} "
-                      f"unknowns), reduce phase of oracle/acr_oracle.py, "
-                      f"{rep.reduce_ms / 1e3:.1f} s"}
+        _, _, line["cpu_baseline"] = cpu_baseline_block(cfg, 1)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -103,17 +103,21 @@ long long acr_device_bytes(const acr_plan_t* p);
 double acr_factor_ms(const acr_plan_t* p);
 double acr_solve_ms(const acr_plan_t* p);
 long long acr_kernel_launches(const acr_plan_t* p);
-/* Instrumented factor only (option 2): class 0 recompression (k_trunc),
- * 1 leaf inverse, 2 leaf GEMM, 3 HODLR x panel.  counters[16] (class 0):
- * [0] algorithmic FLOPs, [1] algorithmic bytes,
- * [2..7] block-path clock64 cycles per phase (load, QR, core, Jacobi, select,
- * output), [8] block-path full tasks, [9] warp-path full tasks, [10]/[11]
- * Jacobi sweeps (block / warp), [12..15] warp-path cycles (load, QR, core,
- * Jacobi).  Classes 1 and 2: counters[0] = dense-leaf FLOPs (2 s^3 per leaf
- * inverse / product, 2 s^2 on the exact diagonal path).  cls 100: the raw
- * 160 device counters ([16..65] warp-path histogram, [66]/[67] warp-path
- * select / output cycles, [72..146] block-path histogram: counts, cycles,
- * Jacobi cycles by rank x rows bucket). */
+/* Instrumented factor only (option 2): per kernel class, launches, summed
+ * CUDA-event time and algorithmic counters (SURVEY.md Appendix C formulas
+ * over the run's actual shapes and ranks).  Classes: 0 recompression
+ * (k_trunc), 1 leaf inverse, 2 dense leaf GEMM (DMMA), 3 HODLR x panel
+ * (k_hmat: leaf_matmat + lr_apply), 4 level-0 exact diagonal leaf products,
+ * 5 small panel products (k_gp), 6 low-rank leaf updates (k_leaflr:
+ * leaf_add_uvT), 7 elementwise block ops (leaf add, negate, copy), 8 cutoff
+ * LU.  counters[16]: [0] algorithmic FLOPs, [1] algorithmic bytes (class 4:
+ * [0] holds its bytes).  Class 0 also: [2..7] block-path clock64 cycles per
+ * phase (load, QR, core, Jacobi, select, output), [8] block-path full tasks,
+ * [9] warp-path full tasks, [10]/[11] Jacobi sweeps (block / warp), [12..15]
+ * warp-path cycles (load, QR, core, Jacobi).  cls 100: the raw 160 device
+ * counters ([16..65] warp-path histogram, [66]/[67] warp-path select /
+ * output cycles, [72..146] block-path histogram: counts, cycles, Jacobi
+ * cycles by rank x rows bucket, [150..155] census of classes 3, 5, 6). */
 int acr_kernel_stats(const acr_plan_t* p, int cls, long long* launches,
                      double* ms, unsigned long long* counters);
 int acr_last_error(const acr_plan_t* p, char* buf, int len);

@@ -63,6 +63,15 @@ cudaError_t launch_rhs_combine(const double* f, long long fs, const double* a,
                                double* out, long long os, int count, int len,
                                cudaStream_t st);
 
+// census of the low-rank / panel kernels for the instrumented factor
+// (k_census.cu; counter slots 150..155)
+cudaError_t launch_census_hmat(const TreeDev& T, const MMJob* jobs, int njobs, int nelem,
+                               unsigned long long* ctr, cudaStream_t st);
+cudaError_t launch_census_gp(const TreeDev& T, const GPJob* jobs, int njobs, const int* nodes,
+                             int nnodes, int nelem, unsigned long long* ctr, cudaStream_t st);
+cudaError_t launch_census_leaflr(const TreeDev& T, RankRef rr, int node, int fside, int mu,
+                                 int nelem, unsigned long long* ctr, cudaStream_t st);
+
 // dense kernels (k_dense.cu)
 cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
                            const int* rowblk, const int* colblk, double* A,

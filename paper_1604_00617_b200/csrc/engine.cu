@@ -477,7 +477,11 @@ struct Plan {
   int first0 = 0, mloc0 = 0;  // this rank's level-0 window
   // per-kernel-class instrumentation (option 2)
   bool prof_on = false;
-  enum { NCLS = 8 };
+  // classes: 0 recompression, 1 leaf inverse, 2 leaf GEMM (DMMA), 3 HODLR x
+  // panel, 4 level-0 diagonal leaf products, 5 small panel products (k_gp),
+  // 6 low-rank leaf updates (k_leaflr), 7 elementwise block ops (leaf add,
+  // negate, copy, zero), 8 cutoff LU
+  enum { NCLS = 10 };
   std::vector<cudaEvent_t> evpool;
   size_t evused = 0;
   std::vector<std::pair<int, size_t>> evmarks;   // (class, index of start event)
@@ -485,6 +489,7 @@ struct Plan {
   long long kcnt[NCLS] = {0};
   unsigned long long kctr[160] = {0};
   double hflops[NCLS] = {0};   // host-side FLOP counts (leaf classes), per factor
+  double hbytes[NCLS] = {0};   // host-side algorithmic byte counts
   Dev dctr;
   // scratch pool
   std::vector<Dev> scr;
@@ -727,10 +732,41 @@ struct Plan {
     if (!prof_on) return;
     CK(cudaEventRecord(next_event(), st));
   }
+  unsigned long long* ctrp() { return prof_on ? dctr.as<unsigned long long>() : nullptr; }
+  // instrumented launch wrappers: class events around the kernel, census
+  // kernel (algorithmic FLOP / bytes from the device ranks) after it
+  void hmat(const MMJob* J, int nj, int G, cudaStream_t s) {
+    kbegin(3);
+    CK(launch_hmat(dt.T, J, nj, G, s));
+    kend();
+    launches += 2;
+    if (prof_on) CK(launch_census_hmat(dt.T, J, nj, G, ctrp(), s));
+  }
+  void gp(const GPJob* J, int nj, const int* nodes, int nnodes, int G, int kcap, cudaStream_t s) {
+    kbegin(5);
+    CK(launch_gp(dt.T, J, nj, nodes, nnodes, G, kcap, s));
+    kend();
+    ++launches;
+    if (prof_on) CK(launch_census_gp(dt.T, J, nj, nodes, nnodes, G, ctrp(), s));
+  }
+  void leaflr(const HB* H, int G, int mu, Src U, Src V, RankRef rr, int node, int fside,
+              cudaStream_t s) {
+    kbegin(6);
+    CK(launch_leaflr_n(dt.T, H, G, mu, ht.nleaves_under(mu), U, V, rr, node, fside, s));
+    kend();
+    ++launches;
+    if (prof_on) CK(launch_census_leaflr(dt.T, rr, node, fside, mu, G, ctrp(), s));
+  }
+  // elementwise block ops: bytes = blocks x words touched (leaf panel n x bw
+  // plus factor panels where the op reads / writes them)
+  void elem_bytes(int G, double words_per_block) {
+    if (prof_on) hbytes[7] += 8.0 * G * words_per_block;
+  }
+
   void prof_reset() {
     evused = 0;
     evmarks.clear();
-    for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; hflops[i] = 0; }
+    for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; hflops[i] = 0; hbytes[i] = 0; }
     for (auto& c : kctr) c = 0;
     if (prof_on) {
       if (!dctr.p) dctr.alloc(160 * sizeof(unsigned long long), st);
@@ -951,9 +987,7 @@ struct Plan {
       }
       j[0].hx = 1; j[0].hw = 0; j[0].sx = 0; j[0].sy = 1;
       j[1].hx = 0; j[1].hw = 1; j[1].sx = 1; j[1].sy = 0;
-      CK(launch_gp(dt.T, j, 2, dt.d_branches, (int)ht.branches.size(), G,
-                   RA * RB, st));
-      ++launches;
+      gp(j, 2, dt.d_branches, (int)ht.branches.size(), G, RA * RB, st);
     }
     const cudaStream_t s2 = side();
     fork(s2);
@@ -966,7 +1000,10 @@ struct Plan {
         if (ht.isleaf[v]) {
           const double sz = ht.hi[v] - ht.lo[v];
           if (diag) hflops[4] += (double)G * 8.0 * (2.0 * sz * sz + sz);
-          else hflops[2] += (double)G * 2.0 * sz * sz * sz;
+          else {
+            hflops[2] += (double)G * 2.0 * sz * sz * sz;
+            hbytes[2] += (double)G * 24.0 * sz * sz;      // leaf_gemm: A, B read, C written
+          }
         }
     CK(launch_leafgemm(dt.T, A, B, C, G, s_pan(PX, ps * RB, RB), r_arr(cr, nn * 2), diag,
                        s2));
@@ -1007,10 +1044,7 @@ struct Plan {
       j.nA = nA1;
       j.nB = ht.startB[nn] - ht.startB[1];
     }
-    kbegin(3);
-    CK(launch_hmat(dt.T, J, 2, G, st));
-    kend();
-    launches += 2;
+    hmat(J, 2, G, st);
     // M2: off12 = combine(f1, f2), off21 = combine(g1, g2)
     TruncArgs a;
     memset(&a, 0, sizeof(a));
@@ -1040,7 +1074,10 @@ struct Plan {
     if (G <= 0) return;
     const cudaStream_t s2 = side();
     fork(s2);
+    kbegin(7);
     CK(launch_leafadd(dt.T, A, B, C, sb, G, s2));
+    kend();
+    elem_bytes(G, 3.0 * n * ht.bw);          // read A, B leaves, write C
     ++launches;
     if (!ht.branches.empty()) {
       TruncArgs a;
@@ -1120,10 +1157,7 @@ struct Plan {
     // the two jobs need distinct t-buffers
     double* tb2 = scratch<double>(11, (size_t)c.G * std::max(J[0].nA, 1) * c.R * c.R);
     J[1].tbuf = tb2;
-    kbegin(3);
-    CK(launch_hmat(dt.T, J, 2, c.G, st));
-    kend();
-    launches += 2;
+    hmat(J, 2, c.G, st);
   }
 
   // add_lowrank(H_mu, (U, V)) with rank (nu, fside) if (nu, 1-fside) != 0:
@@ -1131,9 +1165,7 @@ struct Plan {
   // data); the caller joins s2
   void inv_lowrank(InvCtx& c, int nu, int mu, Src U, Src V, int fside, cudaStream_t s2) {
     fork(s2);
-    CK(launch_leaflr_n(dt.T, c.H, c.G, mu, ht.nleaves_under(mu), U, V, r_hb(c.H),
-                       nu, fside, s2));
-    ++launches;
+    leaflr(c.H, c.G, mu, U, V, r_hb(c.H), nu, fside, s2);
     int t0 = ht.startA[mu], t1 = ht.startA[mu + 1];
     if (t1 > t0) {
       TruncArgs a;
@@ -1154,6 +1186,7 @@ struct Plan {
       if (prof_on) {   // Gauss-Jordan inverse: 2 s^3
         const double sz = ht.hi[nu] - ht.lo[nu];
         hflops[1] += (double)c.G * 2.0 * sz * sz * sz;
+        hbytes[1] += (double)c.G * 16.0 * sz * sz;        // leaf_inv: read + write
       }
       CK(launch_leafinv(dt.T, c.H, c.G, nu, c.sing, st));
       kend();
@@ -1175,16 +1208,13 @@ struct Plan {
       j.W = s_hbU(c.H); j.hw = 1;
       j.Z = P3;
       j.alpha = -1.0;
-      CK(launch_gp(dt.T, &j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st));
-      ++launches;
+      gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st);
     }
     const cudaStream_t s2 = side();
     {                                                  // S = H22 + W V12^T
       // leaves on the main stream, off-diagonal combines on the side stream:
       // the first leaf inverse of sinv below overlaps the recompressions
-      CK(launch_leaflr_n(dt.T, c.H, c.G, a1, ht.nleaves_under(a1), P3, s_hbV(c.H),
-                         r_hb(c.H), nu, 0, st));
-      ++launches;
+      leaflr(c.H, c.G, a1, P3, s_hbV(c.H), r_hb(c.H), nu, 0, st);
       const int t0 = ht.startA[a1], t1 = ht.startA[a1 + 1];
       if (t1 > t0) {
         fork(s2);
@@ -1211,8 +1241,7 @@ struct Plan {
       j.W = P1; j.hw = 0;
       j.Z = P3;
       j.alpha = 1.0;
-      CK(launch_gp(dt.T, &j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st));
-      ++launches;
+      gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st);
     }
     inv_lowrank(c, nu, a0, P3, P2, 1, s2);             // b11 = x11 + G Hh^T
     TruncArgs a;                                       // b12, b21 (independent of b11)
@@ -1395,7 +1424,10 @@ struct Plan {
     {
       Dev tDe = make_tab({{&L.D, 0, 2, ne}});
       Dev tDi = make_tab({{&rec.Dinv, 0, 1, ne}});
+      kbegin(7);
       CK(launch_copyhb(dt.T, tDe.as<HB>(), tDi.as<HB>(), ne, ovf.as<int>(), st));
+      kend();
+      elem_bytes(ne, 2.0 * n * ht.bw);       // leaves copied (+ factors below the rank)
       ++launches;
       invert(tDi.as<HB>(), ne, rec.Dinv.R, sg);
     }
@@ -1450,7 +1482,10 @@ struct Plan {
       multiply(tA.as<HB>(), tB.as<HB>(), tC.as<HB>(), G, PQ.R, L.R, Rout,
                lvl == 0 ? 2 : 0);
       Dev tE = make_tab({{&nx.E, i0, 1, nep}, {&nx.F, 0, 1, nf}});
+      kbegin(7);
       CK(launch_negate(dt.T, tE.as<HB>(), nep + nf, st));
+      kend();
+      elem_bytes(nep + nf, 2.0 * n * ht.bw);
       ++launches;
       const int nz_e = std::min(i0, no);
       Dev tZ = make_tab({{&nx.E, 0, 1, nz_e}, {&nx.F, nf, 1, no - nf}});
@@ -1719,7 +1754,13 @@ struct Plan {
       CK(cudaMemsetAsync(lu.p, 0, sizeof(double) * (size_t)Nc * Nc, st));
       CK(launch_todense(dt.T, tab.as<HB>(), cntb, drc.as<int>(), drc.as<int>() + cntb,
                         lu.as<double>(), Nc, st));
+      kbegin(8);
       CK(lu_factor(lu.as<double>(), Nc, piv.as<int>(), info.as<int>(), nullptr, st));
+      kend();
+      if (prof_on) {   // 2/3 N^3 FLOP; the N x N factor read and written once per panel sweep
+        hflops[8] += 2.0 / 3.0 * (double)Nc * Nc * Nc;
+        hbytes[8] += 16.0 * (double)Nc * Nc;
+      }
       lut_ok = false;
       launches += 1 + 4 * ((Nc + 31) / 32);
       int hinfo = 0;
@@ -1754,8 +1795,7 @@ struct Plan {
     J.RT = R;
     J.CT = k;
     J.tbuf = scratch<double>(12, (size_t)G * std::max(J.nA, 1) * R * k);
-    CK(launch_hmat(dt.T, &J, 1, G, st));
-    launches += 2;
+    hmat(&J, 1, G, st);
   }
 
   void solve(const double* rhs, int k, double* u) {
@@ -2445,8 +2485,15 @@ int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
   *ms = cls == 100 ? 0.0 : P.kms[cls];
   if (counters)
     for (int i = 0; i < 16; ++i) counters[i] = cls == 0 ? P.kctr[i] : 0;
-  if (counters && cls > 0 && cls < Plan::NCLS)
+  if (counters && cls > 0 && cls < Plan::NCLS) {
     counters[0] = (unsigned long long)P.hflops[cls];
+    counters[1] = (unsigned long long)P.hbytes[cls];
+    const int dev_slot = cls == 3 ? 150 : cls == 5 ? 152 : cls == 6 ? 154 : -1;
+    if (dev_slot >= 0) {
+      counters[0] = P.kctr[dev_slot];
+      counters[1] = P.kctr[dev_slot + 1];
+    }
+  }
   if (counters && cls == 100)
     for (int i = 0; i < 160; ++i) counters[i] = P.kctr[i];
   return ACR_OK;
