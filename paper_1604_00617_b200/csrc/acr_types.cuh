@@ -112,6 +112,8 @@ struct TruncArgs {
   int gscr_ntasks;          // tasks [0, gscr_ntasks) of the slice own a global area
   int smem_doubles;         // dynamic smem capacity in doubles
   unsigned long long* ctr;  // optional [flops, bytes] algorithmic counters
+  int* wq;                  // warp path: dynamic work counter (null: static striding)
+  int task_major;           // warp path item order: 0 element-major, 1 task-major
 };
 
 // HODLR x panel product over subtrees (reference algebra.py:52-83):

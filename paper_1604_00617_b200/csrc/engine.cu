@@ -452,6 +452,7 @@ struct Plan {
   bool force_pair = false;    // option 3: CTA-pair recompression for every direct launch that fits
   int warp_small = 0;         // option 6: launches of at most this many items use the warp kernel
   int direct_max = -1;        // option 5: largest launch (items) run one CTA per task; -1 default
+  int warp_sched = 2;         // option 8: warp-path items 0 static, 1 dynamic, 2 dynamic task-major
   HostTree ht;
   DeviceTree dt;
   cudaStream_t st = 0;
@@ -856,14 +857,21 @@ struct Plan {
     const bool may_big = !direct && wworst > trunc_warp_pool_doubles();
     int* q = nullptr;
     int* qc = nullptr;
+    a.wq = nullptr;
+    a.task_major = warp_sched == 2 ? 1 : 0;
+    if (!direct && warp_sched > 0) {
+      qc = scratch<int>(alt ? 17 : 14, 8);
+      a.wq = qc + 2;
+    }
     a.smem_doubles = (int)std::min(bworst, SMD);
     a.gscr = nullptr;
     a.gscr_stride = 0;
     a.gscr_ntasks = 0;
     if (may_big) {
       q = scratch<int>(alt ? 16 : 13, 2 * (size_t)nitems + 2);
-      qc = scratch<int>(alt ? 17 : 14, 4);
+      qc = scratch<int>(alt ? 17 : 14, 8);
     }
+    if (!direct && warp_sched > 0) a.wq = qc + 2;
     if ((direct || may_big) && bworst > SMD) {
       const int nblk = direct ? nitems : std::min(nitems, 148);
       a.gscr = scratch<double>(alt ? 15 : 10, (size_t)nblk * bworst);
@@ -2414,6 +2422,10 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
   }
   if (option == 6) {
     h->p->warp_small = (int)value;
+    return ACR_OK;
+  }
+  if (option == 8) {
+    h->p->warp_sched = (int)value;
     return ACR_OK;
   }
   return set_err(h, ACR_EARG, "unknown option");

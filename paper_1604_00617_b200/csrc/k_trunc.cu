@@ -637,7 +637,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_trunc_big(TruncArgs A, const i
   __shared__ double red[(NT / 32) + 4];
   __shared__ int iflag[2];
   const int cnt = q ? *qcount : nitems;
-  for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+  __shared__ int s_next;
+  for (int i = blockIdx.x;; i += gridDim.x) {
+    if (q) {
+      // queue mode: the next queued task from a counter (qcount + 3; tasks
+      // differ widely in size, static striding left CTAs idle at the tail)
+      __syncthreads();
+      if (threadIdx.x == 0) s_next = atomicAdd(const_cast<int*>(qcount) + 3, 1);
+      __syncthreads();
+      i = s_next;
+    }
+    if (i >= cnt) break;
     const int item = q ? q[i] : i;
     const int task = item % A.ntasks, g = item / A.ntasks;
     TaskCtx c = resolve_task(A, task, g);
@@ -1582,8 +1592,19 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = A.T.n;
-  for (int item = blockIdx.x * TW + warp; item < nitems; item += gridDim.x * TW) {
-    const int task = item % A.ntasks, g = item / A.ntasks;
+  const int nelem = nitems / A.ntasks;
+  for (int it = blockIdx.x * TW + warp;; it += gridDim.x * TW) {
+    // dynamic: the next item from a global counter (tasks differ in size by
+    // orders of magnitude; static striding left warps idle at the tail)
+    int item = it;
+    if (A.wq) {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(A.wq, 1);
+      item = __shfl_sync(FULL, v, 0);
+    }
+    if (item >= nitems) break;
+    const int task = A.task_major ? item / nelem : item % A.ntasks;
+    const int g = A.task_major ? item - task * nelem : item / A.ntasks;
     TaskCtx tc = resolve_task(A, task, g);
     __syncwarp();
     const OpRes& a = tc.a;
@@ -1628,11 +1649,12 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     if (need > (long long)NSLOT * SLOT / 8 || (bigq != nullptr && R > 16)) {
       // queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM);
       // queue 1 (stored from bigq + nitems): one 512-thread CTA per SM
-      if (lane == 0) {
+      if (lane == 0) {   // queued as element-major items (k_trunc_big decodes so)
+        const int em = g * A.ntasks + task;
         if (trunc_need_doubles(tc.um, tc.vm, R) <= QHALF_D)
-          bigq[atomicAdd(bigcount, 1)] = item;
+          bigq[atomicAdd(bigcount, 1)] = em;
         else
-          bigq[nitems + atomicAdd(bigcount + 1, 1)] = item;
+          bigq[nitems + atomicAdd(bigcount + 1, 1)] = em;
       }
       continue;
     }
@@ -1681,8 +1703,10 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
       k_trunc_big<512><<<nitems, 512, bsm, st>>>(a, nullptr, nullptr, nitems);
     return cudaGetLastError();
   }
-  if (may_big) {
-    cudaError_t e = cudaMemsetAsync(bigcount, 0, 2 * sizeof(int), st);
+  if (may_big || a.wq) {
+    // [0], [1] queue lengths, [2] warp-path item counter, [3], [4] queue
+    // fetch counters
+    cudaError_t e = cudaMemsetAsync(bigcount, 0, 5 * sizeof(int), st);
     if (e != cudaSuccess) return e;
   }
   int blocks = (nitems + TW - 1) / TW;
