@@ -270,6 +270,161 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked Gauss-Jordan leaf inverse for 33..64-row leaves, trailing updates
+// on the FP64 tensor pipe (mma.sync.m8n8k4.f64 -> DMMA).  Same pivot rule
+// and implicit row pivoting as k_leafinv_v2 (step k's pivot is the unused row
+// with the largest |x_ik|, first index on ties; rows never move; the
+// permutation is applied at the store).  Columns are taken in panels of 8:
+//   1. one warp runs the 8 unblocked Gauss-Jordan steps on the 64 x 8 panel
+//      (rows lane and lane + 32 in registers, warp-shuffle pivot search and
+//      pivot-row broadcast: no CTA barrier on the pivot chain);
+//   2. T = the panel's pivot rows of every other column (8 x 64, copied);
+//   3. every other 8 x 8 tile: X <- (X with the panel's pivot rows zeroed)
+//      + P T, two DMMAs per tile (k = 8) -- the 8 elementary GJ transforms
+//      composed, E = I + (E - I)[:, pivots], whose columns are exactly the
+//      panel's final values (in-place GJ stores E e_p in column k).
+// The non-panel columns therefore get one rank-8 update per panel instead of
+// eight rank-1 updates: the same algorithm up to the FP summation order.
+// ---------------------------------------------------------------------------
+static constexpr int BGJ_LD = 68;       // padded row stride (doubles)
+
+__global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, int leaf,
+                                                       int* sing) {
+  __shared__ __align__(16) double X[64 * BGJ_LD];
+  __shared__ __align__(16) double Tb[8 * BGJ_LD];
+  __shared__ int piv[64], kpos[64], pflag[64];
+  __shared__ int s_bad;
+  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
+  double* L = H[g].leaf + (long long)lo * bw;
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int r = idx >> 6, c = idx & 63;
+    X[r * BGJ_LD + c] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
+  }
+  if (tid < 64) pflag[tid] = -1;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  unsigned used = 0;                        // warp 0: bit h = row lane + 32 h pivoted
+  const int gi = lane >> 2, ti = lane & 3;
+  for (int pb = 0; pb * 8 < s; ++pb) {
+    const int k0 = pb * 8;
+    // ---- 1. panel: 8 unblocked GJ steps by warp 0 ----
+    if (warp == 0) {
+      double x[2][8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[h][c] = X[(lane + 32 * h) * BGJ_LD + k0 + c];
+      bool bad = false;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (k0 + t < s && !bad) {
+          double best = -1.0;
+          int pi = 64;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            const double v = fabs(x[h][t]);
+            if (r < s && !((used >> h) & 1u) && v > best) { best = v; pi = r; }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, pi, o);
+            if (ov > best || (ov == best && oi < pi)) { best = ov; pi = oi; }
+          }
+          const int hp = pi >> 5, lp = pi & 31;
+          double rowp[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            rowp[c] = __shfl_sync(0xffffffffu, hp ? x[1][c] : x[0][c], lp);
+          const double pv = rowp[t];
+          if (pv == 0.0) {
+            bad = true;                     // uniform
+          } else {
+            const double inv = 1.0 / pv;
+            double rk[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) rk[c] = c == t ? inv : rowp[c] * inv;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const bool isp = lane + 32 * h == pi;
+              const double f = x[h][t];
+              x[h][t] = 0.0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) x[h][c] = isp ? rk[c] : x[h][c] - f * rk[c];
+            }
+            if (lane == lp) used |= 1u << hp;
+            if (lane == 0) {
+              piv[k0 + t] = pi;
+              pflag[pi] = pb;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) X[(lane + 32 * h) * BGJ_LD + k0 + c] = x[h][c];
+      if (bad && lane == 0) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) break;                        // uniform
+    // ---- 2. T = pivot rows of the other columns ----
+    const int np = s - k0 < 8 ? s - k0 : 8;
+    for (int idx = tid; idx < 8 * 64; idx += 256) {
+      const int t = idx >> 6, c = idx & 63;
+      Tb[t * BGJ_LD + c] = t < np ? X[piv[k0 + t] * BGJ_LD + c] : 0.0;
+    }
+    __syncthreads();
+    // ---- 3. rank-8 update of every other tile on DMMA ----
+    for (int tl = warp; tl < 64; tl += 8) {
+      const int rb = tl >> 3, cb = tl & 7;
+      if (cb == pb) continue;
+      const int r = rb * 8 + gi, c = cb * 8 + 2 * ti;
+      const bool zr = pflag[r] == pb;
+      double d0 = zr ? 0.0 : X[r * BGJ_LD + c];
+      double d1 = zr ? 0.0 : X[r * BGJ_LD + c + 1];
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 4) {
+        const double a = X[r * BGJ_LD + k0 + kk + ti];
+        const double b = Tb[(kk + ti) * BGJ_LD + cb * 8 + gi];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+                     "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                     : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+      }
+      X[r * BGJ_LD + c] = d0;
+      X[r * BGJ_LD + c + 1] = d1;
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) {
+      int ps = 0;
+      for (int v = 0; v < T.nnodes; ++v)
+        if (T.isleaf[v] && T.lo[v] < lo) ++ps;
+      atomicMin(sing + g, ps);
+    }
+    return;
+  }
+  for (int j = tid; j < s; j += 256) kpos[piv[j]] = j;
+  __syncthreads();
+  int nf = 0;
+  for (int idx = tid; idx < s * s; idx += 256) {
+    const int r = idx / s, c = idx - r * s;
+    const double v = X[r * BGJ_LD + c];
+    if (!isfinite(v)) nf = 1;
+    L[(long long)kpos[r] * bw + piv[c]] = v;
+  }
+  if (__syncthreads_or(nf) && tid == 0) {
+    int ps = 0;
+    for (int v = 0; v < T.nnodes; ++v)
+      if (T.isleaf[v] && T.lo[v] < lo) ++ps;
+    atomicMin(sing + g, ps);
+  }
+}
+
 template <int S>
 static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int leaf,
                                int* sing, cudaStream_t st) {
@@ -283,7 +438,14 @@ cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
   int s = T.bw;
   if (s <= 16) return leafinv_reg<16>(T, H, nelem, leaf, sing, st);
   if (s <= 32) return leafinv_reg<32>(T, H, nelem, leaf, sing, st);
-  if (s <= 64) return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
+  if (s <= 64) {
+    static const int bgj = getenv("ACR_LEAFINV_GJ") ? 0 : 1;   // A/B aid: 0 = unblocked v2
+    if (bgj && s > 32) {
+      k_leafinv_bgj<<<nelem, 256, 0, st>>>(T, H, leaf, sing);
+      return cudaGetLastError();
+    }
+    return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
+  }
   size_t smem = (size_t)s * (s + 1) * 8 + (size_t)s * 8 + (size_t)s * 4 + 16;
   static bool attr = false;
   if (!attr) {

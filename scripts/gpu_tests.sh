@@ -1,5 +1,5 @@
-# GPU tests only (run under gpurun); optional pytest selection in $1
+# GPU tests (run under gpurun); extra pytest arguments are passed through
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -q -m gpu -x ${1:-} > gpurun_out/tgpu.log 2>&1; echo "exit $?" >> gpurun_out/tgpu.log
+timeout 1200 python -m pytest tests -q -m gpu -x "$@" > gpurun_out/tgpu.log 2>&1; echo "exit $?" >> gpurun_out/tgpu.log
 tail -30 gpurun_out/tgpu.log

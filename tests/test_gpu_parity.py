@@ -446,3 +446,38 @@ def test_singular_cutoff_block(solver_mod):
         assert not isinstance(ei.value, SingularBlockError)
         with pytest.raises(np.linalg.LinAlgError, match="matrix is singular"):
             O.acr_solve(s, Tolerance(1e-12), leaf_size=leaf)
+
+
+@pytest.mark.parametrize("s", [64, 48, 33, 40])
+def test_blocked_leaf_inverse(solver_mod, s):
+    """The blocked Gauss-Jordan leaf inverse (DMMA rank-8 updates) for
+    33..64-row leaves against numpy's inverse (LAPACK gesv, the reference's
+    algebra.py:199-207), including ill-conditioned and pivoting-heavy cases;
+    exact zeros -> singular."""
+    from paper_1604_00617_b200 import _capi
+    import ctypes as C
+    lib = _capi.load()
+    rng = np.random.default_rng(s)
+    cases = [rng.standard_normal((s, s)),
+             rng.standard_normal((s, s)) + 8 * np.eye(s),
+             np.tril(rng.standard_normal((s, s)), -1) + np.diag(rng.uniform(1e-3, 1, s)),
+             rng.standard_normal((s, s))[rng.permutation(s)] * np.logspace(0, 6, s)]
+    for A in cases:
+        dA = torch.tensor(A, device="cuda")
+        dX = torch.empty_like(dA)
+        sg = C.c_int()
+        assert lib.acr_leaf_inverse(s, C.c_void_p(dA.data_ptr()), C.c_void_p(dX.data_ptr()),
+                                    C.byref(sg), None) == 0
+        assert sg.value == 0
+        ref = np.linalg.inv(A)
+        X = dX.cpu().numpy()
+        cond = np.linalg.cond(A)
+        assert np.abs(X - ref).max() <= 1e-15 * cond * np.abs(ref).max() * s, cond
+    A = rng.standard_normal((s, s))
+    A[:, 5] = 0.0
+    dA = torch.tensor(A, device="cuda")
+    dX = torch.empty_like(dA)
+    sg = C.c_int()
+    lib.acr_leaf_inverse(s, C.c_void_p(dA.data_ptr()), C.c_void_p(dX.data_ptr()),
+                         C.byref(sg), None)
+    assert sg.value == 1
