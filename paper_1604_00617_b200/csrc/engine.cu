@@ -228,6 +228,7 @@ struct HostTree {
       }
       iota.push_back(v);
     }
+    bw = (bw + 1) & ~1;   // leaf panel width even: 16-byte vector access to every block
     const int D1 = maxdepth + 1;
     anc.assign((size_t)nnodes * D1, -1);
     for (int v = 0; v < nnodes; ++v) {

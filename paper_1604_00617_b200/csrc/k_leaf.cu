@@ -320,6 +320,11 @@ __global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, 
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         if (k0 + t < s && !bad) {
+          // warp argmax of |x| over the unused rows, first index on ties, by
+          // integer warp reductions on the bit pattern (monotone for
+          // non-negative doubles): max of the high words, then of the low
+          // words among the lanes holding that high word, then the smallest
+          // row index holding both -- exact, no floating compares on the chain
           double best = -1.0;
           int pi = 64;
 #pragma unroll
@@ -328,12 +333,11 @@ __global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, 
             const double v = fabs(x[h][t]);
             if (r < s && !((used >> h) & 1u) && v > best) { best = v; pi = r; }
           }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, pi, o);
-            if (ov > best || (ov == best && oi < pi)) { best = ov; pi = oi; }
-          }
+          const unsigned long long bb = best < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(best) + 1ull;
+          const unsigned hi = (unsigned)(bb >> 32), lw = (unsigned)bb;
+          const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+          const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lw : 0u);
+          pi = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lw == mlo) ? (unsigned)pi : 64u);
           const int hp = pi >> 5, lp = pi & 31;
           double rowp[8];
 #pragma unroll
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, 
           if (pv == 0.0) {
             bad = true;                     // uniform
           } else {
-            const double inv = 1.0 / pv;
+            const double inv = __drcp_rn(pv);   // == 1.0 / pv (both correctly rounded)
             double rk[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) rk[c] = c == t ? inv : rowp[c] * inv;
@@ -829,9 +833,14 @@ __global__ void k_leafadd(int len, const HB* A, const HB* B, const HB* C,
   const double* a = A[g].leaf;
   const double* b = B[g].leaf;
   double* c = C[g].leaf;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
-       i += gridDim.x * blockDim.x)
-    c[i] = a[i] + sb * b[i];
+  const double2* a2 = reinterpret_cast<const double2*>(a);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  double2* c2 = reinterpret_cast<double2*>(c);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len / 2;
+       i += gridDim.x * blockDim.x) {
+    const double2 x = a2[i], y = b2[i];
+    c2[i] = make_double2(x.x + sb * y.x, x.y + sb * y.y);
+  }
 }
 
 cudaError_t launch_leafadd(const TreeDev& T, const HB* A, const HB* B,
@@ -848,9 +857,12 @@ __global__ void k_negate(TreeDev T, const HB* H) {
   const int g = blockIdx.y, n = T.n;
   const HB h = H[g];
   const int len = n * T.bw;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
-       i += gridDim.x * blockDim.x)
-    h.leaf[i] = -1.0 * h.leaf[i];
+  double2* h2 = reinterpret_cast<double2*>(h.leaf);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len / 2;
+       i += gridDim.x * blockDim.x) {
+    const double2 x = h2[i];
+    h2[i] = make_double2(-1.0 * x.x, -1.0 * x.y);
+  }
   // factors: U columns below the rank, per branch node and side
   for (int v = blockIdx.x; v < T.nnodes; v += gridDim.x) {
     if (T.isleaf[v]) continue;
@@ -905,9 +917,13 @@ __global__ void k_copyhb(TreeDev T, const HB* S, const HB* D, int* overflow) {
   const int g = blockIdx.y, n = T.n;
   const HB s = S[g], d = D[g];
   const int len = n * T.bw;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
-       i += gridDim.x * blockDim.x)
-    d.leaf[i] = s.leaf[i];
+  {
+    const double2* s2 = reinterpret_cast<const double2*>(s.leaf);
+    double2* d2 = reinterpret_cast<double2*>(d.leaf);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len / 2;
+         i += gridDim.x * blockDim.x)
+      d2[i] = s2[i];
+  }
   for (int v = blockIdx.x; v < T.nnodes; v += gridDim.x) {
     if (T.isleaf[v]) {
       if (threadIdx.x < 2) d.rk[v * 2 + threadIdx.x] = 0;
@@ -947,9 +963,10 @@ __global__ void k_zerohb(TreeDev T, const HB* D) {
   const int g = blockIdx.y;
   const HB d = D[g];
   const int len = T.n * T.bw;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
+  double2* d2 = reinterpret_cast<double2*>(d.leaf);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len / 2;
        i += gridDim.x * blockDim.x)
-    d.leaf[i] = 0.0;
+    d2[i] = make_double2(0.0, 0.0);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * T.nnodes;
        i += gridDim.x * blockDim.x)
     d.rk[i] = 0;
@@ -965,29 +982,66 @@ cudaError_t launch_zerohb(const TreeDev& T, const HB* D, int nelem,
 // ---------------------------------------------------------------------------
 // lift (hodlr.py:242-314): bands -> leaves + rank<=1 corner factors
 // ---------------------------------------------------------------------------
+// row -> (first row, size) of its leaf for every row of the block, in shared
+// memory, built once per CTA from the leaf list
+__device__ __forceinline__ void leaf_map(const TreeDev& T, int* mlo, int* msz) {
+  const int b0 = T.startB[0], nb = T.startB[1] - b0;
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+    const int v = T.listB[(b0 + q) * 2 + 1];
+    const int lo = T.lo[v], hi = T.hi[v];
+    for (int i = lo; i < hi; ++i) {
+      mlo[i] = lo;
+      msz[i] = hi - lo;
+    }
+  }
+  __syncthreads();
+}
+
+// exact lift of the tridiagonal bands (hodlr.py:242-291): dense tridiagonal
+// leaves (two columns per thread, 16-byte stores) and, at every branch depth,
+// factor column 0 zero except the corners off12 = a e_{mid-1} e_mid^T,
+// off21 = b e_mid e_{mid-1}^T (a = sup[mid-1], b = sub[mid-1]; rank 0 if 0)
 __global__ void k_lift(TreeDev T, const double* sub, const double* diag,
                        const double* sup, const HB* D) {
+  extern __shared__ int lmap[];
   const int g = blockIdx.y, n = T.n, bw = T.bw;
   const HB d = D[g];
   const double* sb = sub + (long long)g * (n - 1);
   const double* dg = diag + (long long)g * n;
   const double* sp = sup + (long long)g * (n - 1);
-  // leaves
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * bw;
+  int* mlo = lmap;
+  int* msz = lmap + n;
+  leaf_map(T, mlo, msz);
+  double2* L2 = reinterpret_cast<double2*>(d.leaf);
+  const int half = bw >> 1;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * half;
        idx += gridDim.x * blockDim.x) {
-    int i = idx / bw, jj = idx - i * bw;
-    // leaf containing row i: walk the tree
-    int v = 0;
-    while (!T.isleaf[v]) v = (i < T.mid[v]) ? T.c0[v] : T.c1[v];
-    int lo = T.lo[v], s = T.hi[v] - lo;
-    double val = 0.0;
-    if (jj < s) {
-      int j = lo + jj;
-      if (j == i) val = dg[i];
-      else if (j == i + 1) val = sp[i];
-      else if (j == i - 1) val = sb[j];
+    const int i = idx / half, jj = 2 * (idx - i * half);
+    const int lo = mlo[i], s = msz[i];
+    double v2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lo + jj + q;
+      v2[q] = jj + q >= s ? 0.0 : j == i ? dg[i] : j == i + 1 ? sp[i] : j == i - 1 ? sb[j] : 0.0;
     }
-    d.leaf[idx] = val;
+    L2[idx] = make_double2(v2[0], v2[1]);
+  }
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < T.nd * n;
+       idx += gridDim.x * blockDim.x) {
+    const int k = idx / n, i = idx - k * n;
+    int node = 0;                               // the depth-k node holding row i
+    for (int t = 0; t < k && !T.isleaf[node]; ++t)
+      node = i < T.mid[node] ? T.c0[node] : T.c1[node];
+    double u = 0.0, v = 0.0;
+    if (!T.isleaf[node] && T.depth[node] == k) {
+      const int mid = T.mid[node];
+      const double a = sp[mid - 1], b = sb[mid - 1];
+      if (i == mid - 1) { u = a; v = b != 0.0 ? 1.0 : 0.0; }
+      if (i == mid) { u = b; v = a != 0.0 ? 1.0 : 0.0; }
+    }
+    const long long slot = (long long)k * d.R * n;
+    d.U[slot + i] = u;
+    d.V[slot + i] = v;
   }
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < T.nnodes;
        v += gridDim.x * blockDim.x) {
@@ -995,16 +1049,9 @@ __global__ void k_lift(TreeDev T, const double* sub, const double* diag,
       d.rk[v * 2] = d.rk[v * 2 + 1] = 0;
       continue;
     }
-    int lo = T.lo[v], hi = T.hi[v], mid = T.mid[v];
-    long long slot = (long long)T.depth[v] * d.R * n;
-    double a = sp[mid - 1];   // entry (mid-1, mid): U = a e_last, V = e_0
-    double b = sb[mid - 1];   // entry (mid, mid-1): U = b e_0, V = e_last
-    // zero the first column over the node rows, then place the corner
-    for (int i = lo; i < hi; ++i) { d.U[slot + i] = 0.0; d.V[slot + i] = 0.0; }
-    d.rk[v * 2] = a != 0.0 ? 1 : 0;
-    d.rk[v * 2 + 1] = b != 0.0 ? 1 : 0;
-    if (a != 0.0) { d.U[slot + mid - 1] = a; d.V[slot + mid] = 1.0; }
-    if (b != 0.0) { d.U[slot + mid] = b; d.V[slot + mid - 1] = 1.0; }
+    const int mid = T.mid[v];
+    d.rk[v * 2] = sp[mid - 1] != 0.0 ? 1 : 0;
+    d.rk[v * 2 + 1] = sb[mid - 1] != 0.0 ? 1 : 0;
   }
 }
 
@@ -1012,20 +1059,26 @@ cudaError_t launch_lift(const TreeDev& T, const double* sub, const double* diag,
                         const double* sup, const HB* D, int nelem,
                         cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_lift<<<dim3(8, nelem), 256, 0, st>>>(T, sub, diag, sup, D);
+  k_lift<<<dim3(8, nelem), 256, 2 * T.n * sizeof(int), st>>>(T, sub, diag, sup, D);
   return cudaGetLastError();
 }
 
+// exact diagonal block (hodlr.py:294-314): dense diagonal leaves, rank 0
 __global__ void k_liftdiag(TreeDev T, const double* dd, const HB* D) {
+  extern __shared__ int lmap[];
   const int g = blockIdx.y, n = T.n, bw = T.bw;
   const HB d = D[g];
   const double* dg = dd + (long long)g * n;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * bw;
+  int* mlo = lmap;
+  int* msz = lmap + n;
+  leaf_map(T, mlo, msz);
+  double2* L2 = reinterpret_cast<double2*>(d.leaf);
+  const int half = bw >> 1;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * half;
        idx += gridDim.x * blockDim.x) {
-    int i = idx / bw, jj = idx - i * bw;
-    int v = 0;
-    while (!T.isleaf[v]) v = (i < T.mid[v]) ? T.c0[v] : T.c1[v];
-    d.leaf[idx] = (T.lo[v] + jj == i) ? dg[i] : 0.0;
+    const int i = idx / half, jj = 2 * (idx - i * half);
+    const int c = i - mlo[i];                   // the diagonal's column in the leaf
+    L2[idx] = make_double2(c == jj ? dg[i] : 0.0, c == jj + 1 ? dg[i] : 0.0);
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * T.nnodes;
        i += gridDim.x * blockDim.x)
@@ -1035,7 +1088,7 @@ __global__ void k_liftdiag(TreeDev T, const double* dd, const HB* D) {
 cudaError_t launch_liftdiag(const TreeDev& T, const double* d, const HB* D,
                             int nelem, cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_liftdiag<<<dim3(8, nelem), 256, 0, st>>>(T, d, D);
+  k_liftdiag<<<dim3(8, nelem), 256, 2 * T.n * sizeof(int), st>>>(T, d, D);
   return cudaGetLastError();
 }
 

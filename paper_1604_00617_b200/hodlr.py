@@ -131,7 +131,7 @@ def export_block(lib, plan, n: int, leaf_size: int, R: int, call, stream) -> Hod
     import torch
     t = build_node_table(n, leaf_size)
     nd = max(t.n_depths, 1)
-    bw = t.max_leaf
+    bw = (t.max_leaf + 1) & ~1          # the engine's leaf panel width (even)
     f64 = dict(dtype=torch.float64, device="cuda")
     leaf = torch.empty((n, bw), **f64)
     U = torch.empty((nd, max(R, 1), n), **f64)
