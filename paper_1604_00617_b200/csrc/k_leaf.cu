@@ -555,18 +555,17 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
   double* Lc = C[g].leaf + (long long)lo * bw;
   if (diag) {                      // exact: C = diag(a) B or A diag(b)
     if (s == 64 && (bw & 1) == 0) {  // 16-byte rows, shifts instead of divisions
+      // the diagonal operand's 64 values staged once (each was otherwise a
+      // separate sector load repeated by every thread of its row / column)
+      const double* Ld = diag == 1 ? La : Lb;
+      if (tid < 64) sa[tid] = Ld[(long long)tid * bw + tid];
+      __syncthreads();
+      const double* Lm = diag == 1 ? Lb : La;
       for (int idx = tid; idx < 64 * 32; idx += GT) {
         const int i = idx >> 5, j = (idx & 31) * 2;
-        double2 v;
-        if (diag == 1) {
-          const double d = La[(long long)i * bw + i];
-          const double2 b = *reinterpret_cast<const double2*>(Lb + (long long)i * bw + j);
-          v = make_double2(d * b.x, d * b.y);
-        } else {
-          const double2 a = *reinterpret_cast<const double2*>(La + (long long)i * bw + j);
-          v = make_double2(a.x * Lb[(long long)j * bw + j],
-                           a.y * Lb[(long long)(j + 1) * bw + j + 1]);
-        }
+        const double2 x = *reinterpret_cast<const double2*>(Lm + (long long)i * bw + j);
+        const double2 v = diag == 1 ? make_double2(sa[i] * x.x, sa[i] * x.y)
+                                    : make_double2(x.x * sa[j], x.y * sa[j + 1]);
         *reinterpret_cast<double2*>(Lc + (long long)i * bw + j) = v;
       }
       return;
@@ -720,11 +719,50 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
     }
 }
 
+// level-0 leaf products with an exact diagonal operand (E, F lifted from the
+// bands: rank-0 factors, diagonal leaves): C = diag(a) B (diag 1) or
+// A diag(b) (diag 2), a streaming kernel (no tensor work, small footprint so
+// that many CTAs per SM keep the HBM busy)
+__global__ void __launch_bounds__(256) k_leafgemm_diag(TreeDev T, const HB* A, const HB* B,
+                                                       const HB* C, int diag) {
+  __shared__ double dv[128];
+  const int g = blockIdx.y, tid = threadIdx.x;
+  const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
+  const int lo = T.lo[lam], s = T.hi[lam] - lo, bw = T.bw;
+  const double* La = A[g].leaf + (long long)lo * bw;
+  const double* Lb = B[g].leaf + (long long)lo * bw;
+  double* Lc = C[g].leaf + (long long)lo * bw;
+  const double* Ld = diag == 1 ? La : Lb;
+  const double* Lm = diag == 1 ? Lb : La;
+  if (tid < s) dv[tid] = Ld[(long long)tid * bw + tid];
+  __syncthreads();
+  if ((s & 1) == 0) {                          // bw is even: 16-byte rows
+    const int h = s >> 1;
+    for (int idx = tid; idx < s * h; idx += 256) {
+      const int i = idx / h, j = 2 * (idx - i * h);
+      const double2 x = *reinterpret_cast<const double2*>(Lm + (long long)i * bw + j);
+      const double2 v = diag == 1 ? make_double2(dv[i] * x.x, dv[i] * x.y)
+                                  : make_double2(x.x * dv[j], x.y * dv[j + 1]);
+      *reinterpret_cast<double2*>(Lc + (long long)i * bw + j) = v;
+    }
+    return;
+  }
+  for (int idx = tid; idx < s * s; idx += 256) {
+    const int i = idx / s, j = idx - i * s;
+    const double x = Lm[(long long)i * bw + j];
+    Lc[(long long)i * bw + j] = diag == 1 ? dv[i] * x : x * dv[j];
+  }
+}
+
 cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
                             const HB* C, int nelem, Src PX, RankRef xr, int diag,
                             cudaStream_t st) {
   if (!nelem) return cudaSuccess;
   dim3 grid(T.nleaves, nelem);
+  if (diag && T.bw <= 128) {
+    k_leafgemm_diag<<<grid, 256, 0, st>>>(T, A, B, C, diag);
+    return cudaGetLastError();
+  }
   if (T.bw <= 64) {
     const size_t smem = 2ull * 64 * GLD * 8;
     static bool attr = false;
