@@ -289,8 +289,10 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
 // ---------------------------------------------------------------------------
 static constexpr int BGJ_LD = 68;       // padded row stride (doubles)
 
-__global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, int leaf,
-                                                       int* sing) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H, int leaf,
+                                                         int* sing) {
+  constexpr int NW = NT / 32;
   __shared__ __align__(16) double X[64 * BGJ_LD];
   __shared__ __align__(16) double Tb[8 * BGJ_LD];
   __shared__ int piv[64], kpos[64], pflag[64];
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, 
   const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
   double* L = H[g].leaf + (long long)lo * bw;
-  for (int idx = tid; idx < 64 * 64; idx += 256) {
+  for (int idx = tid; idx < 64 * 64; idx += NT) {
     const int r = idx >> 6, c = idx & 63;
     X[r * BGJ_LD + c] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
   }
@@ -377,13 +379,13 @@ __global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, 
     if (s_bad) break;                        // uniform
     // ---- 2. T = pivot rows of the other columns ----
     const int np = s - k0 < 8 ? s - k0 : 8;
-    for (int idx = tid; idx < 8 * 64; idx += 256) {
+    for (int idx = tid; idx < 8 * 64; idx += NT) {
       const int t = idx >> 6, c = idx & 63;
       Tb[t * BGJ_LD + c] = t < np ? X[piv[k0 + t] * BGJ_LD + c] : 0.0;
     }
     __syncthreads();
     // ---- 3. rank-8 update of every other tile on DMMA ----
-    for (int tl = warp; tl < 64; tl += 8) {
+    for (int tl = warp; tl < 64; tl += NW) {
       const int rb = tl >> 3, cb = tl & 7;
       if (cb == pb) continue;
       const int r = rb * 8 + gi, c = cb * 8 + 2 * ti;
@@ -412,10 +414,10 @@ __global__ void __launch_bounds__(256, 3) k_leafinv_bgj(TreeDev T, const HB* H, 
     }
     return;
   }
-  for (int j = tid; j < s; j += 256) kpos[piv[j]] = j;
+  for (int j = tid; j < s; j += NT) kpos[piv[j]] = j;
   __syncthreads();
   int nf = 0;
-  for (int idx = tid; idx < s * s; idx += 256) {
+  for (int idx = tid; idx < s * s; idx += NT) {
     const int r = idx / s, c = idx - r * s;
     const double v = X[r * BGJ_LD + c];
     if (!isfinite(v)) nf = 1;
@@ -445,7 +447,11 @@ cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
   if (s <= 64) {
     static const int bgj = getenv("ACR_LEAFINV_GJ") ? 0 : 1;   // A/B aid: 0 = unblocked v2
     if (bgj && s > 32) {
-      k_leafinv_bgj<<<nelem, 256, 0, st>>>(T, H, leaf, sing);
+      // batched launches: 128-thread CTAs, five per SM (more panels in
+      // flight while each CTA's other warps wait on its panel warp);
+      // latency-bound launches: 256 threads (shorter per-panel update)
+      if (nelem >= 2 * 148) k_leafinv_bgj<128, 5><<<nelem, 128, 0, st>>>(T, H, leaf, sing);
+      else k_leafinv_bgj<256, 3><<<nelem, 256, 0, st>>>(T, H, leaf, sing);
       return cudaGetLastError();
     }
     return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
