@@ -114,6 +114,7 @@ struct TruncArgs {
   unsigned long long* ctr;  // optional [flops, bytes] algorithmic counters
   int* wq;                  // warp path: dynamic work counter (null: static striding)
   int task_major;           // warp path item order: 0 element-major, 1 task-major
+  int direct_tag;           // instrumentation: direct (one CTA per item) launch
 };
 
 // HODLR x panel product over subtrees (reference algebra.py:52-83):

@@ -489,7 +489,7 @@ struct Plan {
   std::vector<std::pair<int, size_t>> evmarks;   // (class, index of start event)
   double kms[NCLS] = {0};
   long long kcnt[NCLS] = {0};
-  unsigned long long kctr[160] = {0};
+  unsigned long long kctr[256] = {0};
   double hflops[NCLS] = {0};   // host-side FLOP counts (leaf classes), per factor
   double hbytes[NCLS] = {0};   // host-side algorithmic byte counts
   Dev dctr;
@@ -771,8 +771,8 @@ struct Plan {
     for (int i = 0; i < NCLS; ++i) { kms[i] = 0; kcnt[i] = 0; hflops[i] = 0; hbytes[i] = 0; }
     for (auto& c : kctr) c = 0;
     if (prof_on) {
-      if (!dctr.p) dctr.alloc(160 * sizeof(unsigned long long), st);
-      CK(cudaMemsetAsync(dctr.p, 0, 160 * sizeof(unsigned long long), st));
+      if (!dctr.p) dctr.alloc(256 * sizeof(unsigned long long), st);
+      CK(cudaMemsetAsync(dctr.p, 0, 256 * sizeof(unsigned long long), st));
     }
   }
   void prof_collect() {   // after a stream sync
@@ -2508,7 +2508,7 @@ int acr_kernel_stats(const acr_plan_t* h, int cls, long long* launches,
     }
   }
   if (counters && cls == 100)
-    for (int i = 0; i < 160; ++i) counters[i] = P.kctr[i];
+    for (int i = 0; i < 256; ++i) counters[i] = P.kctr[i];
   return ACR_OK;
 }
 

@@ -572,6 +572,18 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
   }
   if (tid == 0) *ro = keep;
   ACR_PH(5);
+  if (A.ctr && tid == 0 && A.direct_tag) {   // direct (latency-bound) launches apart
+    atomicAdd(A.ctr + 160, 1ull);
+    for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 161 + i, (unsigned long long)ph[i]);
+    const int rb = R <= 8 ? 0 : R <= 16 ? 1 : R <= 32 ? 2 : R <= 64 ? 3 : 4;
+    const int mm = um > vm ? um : vm;
+    const int mb = mm <= 128 ? 0 : mm <= 256 ? 1 : mm <= 512 ? 2 : mm <= 1024 ? 3 : 4;
+    long long tot = 0;
+    for (int i = 0; i < 6; ++i) tot += ph[i];
+    atomicAdd(A.ctr + 170 + rb * 5 + mb, 1ull);
+    atomicAdd(A.ctr + 195 + rb * 5 + mb, (unsigned long long)tot);
+    atomicAdd(A.ctr + 220 + rb * 5 + mb, (unsigned long long)ph[1]);
+  }
   if (A.ctr && tid == 0) {
     for (int i = 0; i < 6; ++i) atomicAdd(A.ctr + 2 + i, (unsigned long long)ph[i]);
     // histogram: R bucket (<=8, <=16, <=32, <=64, >64) x m bucket (<=128, 256,
@@ -1696,11 +1708,13 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   const int nitems = a.ntasks * nelem;
   const size_t bsm = (size_t)a.smem_doubles * 8 + 64;
   if (direct) {
+    TruncArgs ad = a;
+    ad.direct_tag = 1;
     // more tasks than SMs: 256-thread CTAs, two per SM, when the work areas fit
     if (nitems > nsm && bsm <= QHALF)
-      k_trunc_big<256><<<nitems, 256, bsm, st>>>(a, nullptr, nullptr, nitems);
+      k_trunc_big<256><<<nitems, 256, bsm, st>>>(ad, nullptr, nullptr, nitems);
     else
-      k_trunc_big<512><<<nitems, 512, bsm, st>>>(a, nullptr, nullptr, nitems);
+      k_trunc_big<512><<<nitems, 512, bsm, st>>>(ad, nullptr, nullptr, nitems);
     return cudaGetLastError();
   }
   if (may_big || a.wq) {

@@ -21,7 +21,7 @@ sol.lib.acr_plan_set_option(sol.plan, 2, 1)
 sol.factor(bands)
 torch.cuda.synchronize()
 nl, ms = C.c_longlong(), C.c_double()
-ctr = (C.c_ulonglong * 160)()
+ctr = (C.c_ulonglong * 256)()
 sol.lib.acr_kernel_stats(sol.plan, 100, C.byref(nl), C.byref(ms), ctr)
 G = 1e9
 print(f"block path: tasks {ctr[8]}, sweeps {ctr[10]}; Gcyc load {ctr[2]/G:.2f} qr {ctr[3]/G:.2f} "
@@ -40,6 +40,17 @@ for rb in range(5):
     if row:
         print(f"  {rl[rb]}: " + "; ".join(row))
 print("warp-path histogram [16..65]:", list(ctr[16:66]))
+print(f"direct launches: tasks {ctr[160]}; Gcyc load {ctr[161]/G:.2f} qr {ctr[162]/G:.2f} core "
+      f"{ctr[163]/G:.2f} jacobi {ctr[164]/G:.2f} select {ctr[165]/G:.2f} output {ctr[166]/G:.2f}")
+print("direct histogram: count / Gcyc total / Gcyc QR")
+for rb in range(5):
+    row = []
+    for mb in range(5):
+        k = rb * 5 + mb
+        if ctr[170 + k]:
+            row.append(f"{ml[mb]}: {ctr[170+k]} / {ctr[195+k]/G:.3f} / {ctr[220+k]/G:.3f}")
+    if row:
+        print(f"  {rl[rb]}: " + "; ".join(row))
 for cls, nm in enumerate(["trunc", "leafinv", "leafgemm", "hmat", "diag", "gp", "leaflr", "elem", "lu"]):
     c16 = (C.c_ulonglong * 16)()
     sol.lib.acr_kernel_stats(sol.plan, cls, C.byref(nl), C.byref(ms), c16)
