@@ -447,11 +447,9 @@ cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
   if (s <= 64) {
     static const int bgj = getenv("ACR_LEAFINV_GJ") ? 0 : 1;   // A/B aid: 0 = unblocked v2
     if (bgj && s > 32) {
-      // batched launches: 128-thread CTAs, five per SM (more panels in
-      // flight while each CTA's other warps wait on its panel warp);
-      // latency-bound launches: 256 threads (shorter per-panel update)
-      if (nelem >= 2 * 148) k_leafinv_bgj<128, 5><<<nelem, 128, 0, st>>>(T, H, leaf, sing);
-      else k_leafinv_bgj<256, 3><<<nelem, 256, 0, st>>>(T, H, leaf, sing);
+      // 256 threads, three CTAs per SM (measured: 128-thread CTAs at five per
+      // SM are slower for batched launches too, 126 vs 85 us per 1024 leaves)
+      k_leafinv_bgj<256, 3><<<nelem, 256, 0, st>>>(T, H, leaf, sing);
       return cudaGetLastError();
     }
     return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
