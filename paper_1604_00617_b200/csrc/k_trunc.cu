@@ -478,11 +478,22 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
   // small cores: one warp, warp-level syncs per rotation step (a CTA barrier
   // per step costs more than the step); large cores: the whole CTA
   int sweeps;
-  if (pc <= 16 && pr <= 128) {   // larger cores: every warp of the CTA
+  const bool wj = pc <= 16 && pr <= 128;      // larger cores: every warp of the CTA
+  if (wj) {
     __shared__ int s_sw;
     if (tid < 32) {
       const int sw = blk_jacobi(Bm, pr, pc, Jm, tid);
       if (tid == 0) s_sw = sw;
+    } else {
+      // meanwhile the other warps form the explicit Q of both sides (it does
+      // not depend on the SVD; the core has been formed from the R factors)
+      const int t2 = tid - 32, nw2 = NT / 32 - 1, wu = nw2 / 2;
+      const int half = (t2 >> 5) >= wu ? 1 : 0;
+      const int nthr = (half ? nw2 - wu : wu) * 32;
+      const int t = half ? t2 - wu * 32 : t2;
+      Grp g{1 + half, nthr, t, nthr / 32, t >> 5, tid & 31, red + (half ? wu : 0), nullptr};
+      if (!half) group_form_q(Uw, um, pu, tauU, g);
+      else group_form_q(Vw, vm, pv, tauV, g);
     }
     __syncthreads();
     sweeps = s_sw;
@@ -547,7 +558,7 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
     const int j = ord[c];
     Cv[idx] = tr ? Bm[(long long)j * (pr | 1) + i] / sig[j] : Jm[(long long)j * (pc | 1) + i];
   }
-  {
+  if (!wj) {
     const int half = tid >= NT / 2 ? 1 : 0;
     const int t = tid - half * (NT / 2);
     Grp g{1 + half, NT / 2, t, (NT / 32) / 2, t >> 5, tid & 31, red + half * ((NT / 32) / 2),
