@@ -776,6 +776,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     nr2 = block_sum<TT>(nr2, red);
     if (tid == 0) misc[0] = nr2;
     cl.sync();                                 // both R factors published
+    // the explicit Q of each side does not depend on the SVD: side 1 forms
+    // its Q while side 0 runs the core and the Jacobi; side 0's other warps
+    // form Q_u during a single-warp Jacobi
+    bool qdone = false;
+    if (side == 1) {
+      group_form_q(W, m, p, tau, gf);
+      qdone = true;
+    }
     if (side == 0) {
       const double* Rv = cl.map_shared_rank(Rs, 1);
       const double* mv = cl.map_shared_rank(misc, 1);
@@ -801,9 +809,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
         if (tid < 32) {
           const int sw = blk_jacobi(Bm, pr, pc, Jm, tid);
           if (tid == 0) s_sw = sw;
+        } else {
+          const Grp gq{1, TT - 32, tid - 32, NWB - 1, (tid - 32) >> 5, tid & 31, red, nullptr};
+          group_form_q(W, m, p, tau, gq);
         }
         __syncthreads();
         sweeps = s_sw;
+        qdone = true;
       } else {
         sweeps = block_jacobi<TT>(Bm, pr, pc, Jm, iflag);
       }
@@ -865,7 +877,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     cl.sync();                                 // coefficients and keep published
     const int keep = (int)misc[1];
     if (keep > 0) {
-      group_form_q(W, m, p, tau, gf);
+      if (!qdone) group_form_q(W, m, p, tau, gf);
       __syncthreads();
       double* O = side ? c.Vo : c.Uo;
       for (int idx = tid; idx < m * keep; idx += TT) {
