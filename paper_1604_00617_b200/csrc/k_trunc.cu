@@ -205,6 +205,8 @@ __device__ void group_form_q(double* W, int mr, int p, const double* tau, const 
   }
 }
 
+__constant__ bool jacobi_skip_confirm = true;
+
 __device__ __forceinline__ int rr_player(int step, int x, int np) {
   if (x == 0) return 0;
   int t = x - 1 + step;              // < 2 (np - 1): one conditional wrap
@@ -1284,8 +1286,12 @@ __device__ int blk_jacobi_t(double* B, int pr, int pc, double* J, int lane, int 
     nb += x * x;
   }
   const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  // a sweep whose rotations were all below 1e-9 (|c| / sqrt(ab)) leaves
+  // off-diagonals O(1e-18) << tol: the confirmation sweep that would follow
+  // rotates nothing and is skipped (ACR_JACOBI_CONFIRM=1 keeps it)
+  const bool skipc = jacobi_skip_confirm;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    bool rot = false;
+    bool rot = false, big = false;
     for (int step = 0; step < np - 1; ++step) {
       for (int base = 0; base < npairs; base += per) {
         const int k = base + grp;
@@ -1347,11 +1353,13 @@ __device__ int blk_jacobi_t(double* B, int pr, int pc, double* J, int lane, int 
             }
           }
           rot = true;
+          big |= c * c > 1e-18 * a * b;
         }
         __syncwarp();
       }
     }
     if (!__any_sync(FULL, rot)) return sweep + 1;
+    if (skipc && !__any_sync(FULL, big)) return sweep + 1;
   }
   return 40;
 }
@@ -1398,8 +1406,12 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
     nb += x * x;
   }
   const double tiny = warp_sum(nb) * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  // a sweep whose rotations were all below 1e-9 (|c| / sqrt(ab)) leaves
+  // off-diagonals O(1e-18) << tol: the confirmation sweep that would follow
+  // rotates nothing and is skipped (ACR_JACOBI_CONFIRM=1 keeps it)
+  const bool skipc = jacobi_skip_confirm;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    bool rot = false;
+    bool rot = false, big = false;
     for (int step = 0; step < np - 1; ++step) {
       for (int base = 0; base < npairs; base += per) {
         const int k = base + grp;
@@ -1443,11 +1455,13 @@ __device__ int warp_jacobi(double* B, int pr, int pc, double* J, int lane) {
             jj[r] = sn * x + cs * y;
           }
           rot = true;
+          big |= c * c > 1e-18 * a * b;
         }
         __syncwarp();
       }
     }
     if (!__any_sync(FULL, rot)) return sweep + 1;
+    if (skipc && !__any_sync(FULL, big)) return sweep + 1;
   }
   return 40;
 }
@@ -1711,6 +1725,17 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
 
 int trunc_warp_pool_doubles() { return NSLOT * SLOT / 8; }
 
+// development aid: ACR_JACOBI_CONFIRM=1 keeps the confirmation sweep
+void trunc_init_flags() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (getenv("ACR_JACOBI_CONFIRM")) {
+    const bool v = false;
+    cudaMemcpyToSymbol(jacobi_skip_confirm, &v, sizeof(v));
+  }
+}
+
 cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
                          int* bigq, int* bigcount, cudaStream_t st) {
   if (a.ntasks == 0 || nelem == 0) return cudaSuccess;
@@ -1728,6 +1753,7 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
+  trunc_init_flags();
   const int nitems = a.ntasks * nelem;
   const size_t bsm = (size_t)a.smem_doubles * 8 + 64;
   if (direct) {
@@ -1771,5 +1797,6 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
 }
 
 int trunc_direct_max() { return 4 * 148; }
+
 
 }  // namespace acr
