@@ -115,6 +115,7 @@ struct TruncArgs {
   int* wq;                  // warp path: dynamic work counter (null: static striding)
   int task_major;           // warp path item order: 0 element-major, 1 task-major
   int direct_tag;           // instrumentation: direct (one CTA per item) launch
+  int warp_rmax;            // warp path takes tasks of at most this many columns
 };
 
 // HODLR x panel product over subtrees (reference algebra.py:52-83):

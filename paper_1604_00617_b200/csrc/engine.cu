@@ -454,6 +454,7 @@ struct Plan {
   int warp_small = 0;         // option 6: launches of at most this many items use the warp kernel
   int direct_max = -1;        // option 5: largest launch (items) run one CTA per task; -1 default
   int warp_sched = 2;         // option 8: warp-path items 0 static, 1 dynamic, 2 dynamic task-major
+  int warp_rmax = 16;         // option 9: widest core (columns) the warp path takes
   HostTree ht;
   DeviceTree dt;
   cudaStream_t st = 0;
@@ -860,6 +861,7 @@ struct Plan {
     int* qc = nullptr;
     a.wq = nullptr;
     a.task_major = warp_sched == 2 ? 1 : 0;
+    a.warp_rmax = warp_rmax;
     if (!direct && warp_sched > 0) {
       qc = scratch<int>(alt ? 17 : 14, 8);
       a.wq = qc + 2;
@@ -2427,6 +2429,10 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
   }
   if (option == 8) {
     h->p->warp_sched = (int)value;
+    return ACR_OK;
+  }
+  if (option == 9) {
+    h->p->warp_rmax = (int)value;
     return ACR_OK;
   }
   return set_err(h, ACR_EARG, "unknown option");

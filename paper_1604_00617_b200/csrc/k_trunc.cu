@@ -1695,7 +1695,7 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
     // large work areas, and cores above 16 columns (a single warp's Jacobi
     // would walk whole column pairs per lane): block path queues
-    if (need > (long long)NSLOT * SLOT / 8 || (bigq != nullptr && R > 16)) {
+    if (need > (long long)NSLOT * SLOT / 8 || (bigq != nullptr && R > A.warp_rmax)) {
       // queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM);
       // queue 1 (stored from bigq + nitems): one 512-thread CTA per SM
       if (lane == 0) {   // queued as element-major items (k_trunc_big decodes so)
