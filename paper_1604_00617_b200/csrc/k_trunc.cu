@@ -161,6 +161,64 @@ __device__ void group_qr(double* W, int mr, int R, double* tau, const Grp& g) {
   }
 }
 
+// Householder QR with look-ahead (same reflectors as group_qr up to the
+// summation order of the tail norms): warp 0 of the group owns the next
+// column -- it applies reflector j to column j + 1, then forms reflector
+// j + 1 from it (norm, dlarfg, scaling) -- while the other warps apply
+// reflector j to columns j + 2 .. R - 1.  One group barrier per reflector
+// instead of four; the critical path per step is warp 0's single-column
+// update plus two warp reductions.
+__device__ __forceinline__ void la_update(double* W, int mr, int j, int c, double tj, int lane) {
+  const double* v = W + (long long)j * mr;
+  double* cc = W + (long long)c * mr;
+  double w = 0.0;
+  for (int i = j + 1 + lane; i < mr; i += 32) w += v[i] * cc[i];
+  w = (warp_sum(w) + cc[j]) * tj;
+  for (int i = j + 1 + lane; i < mr; i += 32) cc[i] -= w * v[i];
+  __syncwarp();
+  if (lane == 0) cc[j] -= w;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void la_prep(double* W, int mr, int j, double* tau, int lane) {
+  double* cj = W + (long long)j * mr;
+  double ss = 0.0;
+  for (int i = j + 1 + lane; i < mr; i += 32) ss += cj[i] * cj[i];
+  ss = warp_sum(ss);
+  const double alpha = cj[j];
+  double tj = 0.0, scal = 0.0, beta = alpha;
+  if (ss != 0.0) householder(alpha, ss, beta, scal, tj);
+  __syncwarp();
+  if (tj != 0.0) {
+    for (int i = j + 1 + lane; i < mr; i += 32) cj[i] *= scal;
+    if (lane == 0) cj[j] = beta;
+  }
+  if (lane == 0) tau[j] = tj;
+  __syncwarp();
+}
+
+__device__ void group_qr_la(double* W, int mr, int R, double* tau, const Grp& g) {
+  const int p = mr < R ? mr : R;
+  if (p <= 0) return;
+  if (g.w == 0) la_prep(W, mr, 0, tau, g.lane);
+  gbar(g);
+  const int nwo = g.nw - 1;                  // warps on the trailing columns (groups have >= 2)
+  for (int j = 0; j < p; ++j) {
+    const double tj = tau[j];
+    if (g.w == 0) {
+      if (j + 1 < p) {
+        if (tj != 0.0) la_update(W, mr, j, j + 1, tj, g.lane);
+        la_prep(W, mr, j + 1, tau, g.lane);
+      }
+    } else if (tj != 0.0) {
+      // columns j + 2 .. R - 1 (and j + 1 when it is past the last reflector)
+      const int c0 = j + 1 < p ? j + 2 : j + 1;
+      for (int c = c0 + (g.w - 1); c < R; c += nwo) la_update(W, mr, j, c, tj, g.lane);
+    }
+    gbar(g);
+  }
+}
+
 __device__ void group_apply_q(const double* W, int mr, int p, const double* tau,
                               double* X, int nc, const Grp& g) {
   for (int j = p - 1; j >= 0; --j) {
@@ -206,6 +264,7 @@ __device__ void group_form_q(double* W, int mr, int p, const double* tau, const 
 }
 
 __constant__ bool jacobi_skip_confirm = true;
+__constant__ bool qr_lookahead = true;
 
 __device__ __forceinline__ int rr_player(int step, int x, int np) {
   if (x == 0) return 0;
@@ -444,8 +503,13 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
     const int t = tid - half * (NT / 2);
     Grp g{1 + half, NT / 2, t, (NT / 32) / 2, t >> 5, tid & 31, red + half * ((NT / 32) / 2),
           nullptr};
-    if (!half) group_qr(Uw, um, R, tauU, g);
-    else group_qr(Vw, vm, R, tauV, g);
+    if (qr_lookahead) {
+      if (!half) group_qr_la(Uw, um, R, tauU, g);
+      else group_qr_la(Vw, vm, R, tauV, g);
+    } else {
+      if (!half) group_qr(Uw, um, R, tauU, g);
+      else group_qr(Vw, vm, R, tauV, g);
+    }
   }
   __syncthreads();
   ACR_PH(1);
@@ -765,7 +829,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     }
     ACR_PH(0);
     const Grp gf{1, TT, tid, NWB, tid >> 5, tid & 31, red, nullptr};
-    group_qr(W, m, R, tau, gf);
+    if (qr_lookahead) group_qr_la(W, m, R, tau, gf);
+    else group_qr(W, m, R, tau, gf);
     __syncthreads();
     ACR_PH(1);
     double nr2 = 0.0;
@@ -907,9 +972,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
   }
 }
 
+void trunc_init_flags();
+
 cudaError_t launch_trunc_pair(const TruncArgs& a, int nelem, long long smem_doubles,
                               cudaStream_t st) {
   if (a.ntasks == 0 || nelem == 0) return cudaSuccess;
+  trunc_init_flags();
   const size_t bytes = (size_t)smem_doubles * 8 + 64;
   static size_t attr = 0;
   if (bytes > attr) {
@@ -1733,6 +1801,10 @@ void trunc_init_flags() {
   if (getenv("ACR_JACOBI_CONFIRM")) {
     const bool v = false;
     cudaMemcpyToSymbol(jacobi_skip_confirm, &v, sizeof(v));
+  }
+  if (getenv("ACR_QR_NOLA")) {                // development aid: plain group QR
+    const bool v = false;
+    cudaMemcpyToSymbol(qr_lookahead, &v, sizeof(v));
   }
 }
 
