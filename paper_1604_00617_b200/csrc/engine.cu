@@ -847,11 +847,22 @@ struct Plan {
     }
     const long long SMD = 28416;                 // 222 KB of doubles
     // latency-bound launches whose panels do not fit one CTA's shared memory:
-    // one CTA per side (cluster pair) instead of the global-memory scratch
-    if (direct && pworst <= SMD && (bworst > SMD || force_pair)) {
+    // one CTA per side (cluster pair) instead of the global-memory scratch.
+    // The sizes here come from capacities (Ra + Rb columns); a task whose
+    // actual panel still exceeds one CTA's shared memory keeps it in a
+    // per-CTA global area (rare)
+    const long long pair_small = 4LL * Rw * Rw + 5LL * Rw + 8;   // the pair kernel's non-panel arrays
+    if (direct && (bworst > SMD || force_pair) && pair_small <= SMD) {
+      a.smem_doubles = (int)std::min(pworst, SMD);
+      a.gscr = nullptr;
+      a.gscr_stride = 0;
+      if (pworst > SMD) {
+        a.gscr = scratch<double>(alt ? 15 : 10, (size_t)2 * nitems * pworst);
+        a.gscr_stride = pworst;
+      }
       fork(s);
       kbegin(0);
-      CK(launch_trunc_pair(a, nelem, pworst, s));
+      CK(launch_trunc_pair(a, nelem, a.smem_doubles, s));
       kend();
       launches += 1;
       return;

@@ -804,8 +804,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     const int R = a.r + b.r;
     const int m = side ? c.vm : c.um;
     const int p = m < R ? m : R;
-    double* W = sm;
-    double* Rs = W + (long long)m * R;        // own R factor, [l][i] = Rs[l * R + i]
+    // small arrays first (offsets depend on R only: the same in both CTAs,
+    // which address each other's through DSMEM), the panel after them -- or
+    // in a per-CTA global area when it does not fit (rare: capacities size
+    // the launch, actual ranks are usually far below them)
+    double* Rs = sm;                          // own R factor, [l][i] = Rs[l * R + i]
     double* Bm = Rs + (long long)R * R;
     double* Jm = Bm + (long long)R * (R + 1);   // odd-strided cores (pr | 1, pc | 1)
     double* Cs = Jm + (long long)R * (R + 1);       // own coefficients p x keep
@@ -813,13 +816,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     double* sig = tau + R;
     int* ord = reinterpret_cast<int*>(sig + R);
     double* misc = sig + 2 * R;               // [0] |R|_F^2, [1] keep
+    const long long small = 4LL * R * R + 5LL * R + 8;   // through misc[0..1]
+    const bool w_sm = small + (long long)m * R <= A.smem_doubles;
+    double* W = w_sm ? sm + small : A.gscr + (long long)blockIdx.x * A.gscr_stride;
     long long ph[6] = {0, 0, 0, 0, 0, 0};
     long long t_ph = clock64();
     for (int cc = 0; cc < R; ++cc) {
       const double* src = side == 0
           ? (cc < a.r ? a.U + (long long)cc * n : b.U + (long long)(cc - a.r) * n)
           : (cc < a.r ? a.V + (long long)cc * n : b.V + (long long)(cc - a.r) * n);
-      for (int i = tid; i < m; i += TT) cp_async8(W + (long long)cc * m + i, src + i, true);
+      if (w_sm)
+        for (int i = tid; i < m; i += TT) cp_async8(W + (long long)cc * m + i, src + i, true);
+      else
+        for (int i = tid; i < m; i += TT) W[(long long)cc * m + i] = src[i];
     }
     cp_async_wait_all();
     __syncthreads();
