@@ -519,6 +519,35 @@ __global__ void __launch_bounds__(LT) k_leafgemm(TreeDev T, const HB* A,
 static constexpr int GT = 256;
 static constexpr int GLD = 68;           // padded leading dimension (doubles)
 
+// TMA bulk copies (cp.async.bulk, global -> shared, completion counted in
+// bytes on an mbarrier) for the leaf staging of k_leafgemm_tc
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(a), "r"(phase) : "memory");
+}
+
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
                "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
@@ -582,11 +611,22 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
     }
     return;                        // level-0 couplings have rank-0 factors
   }
-  if (s == 64 && (bw & 1) == 0) {   // asynchronous staging, 16-byte copies
-    for (int idx = tid; idx < 64 * 32; idx += GT) {
-      const int i = idx >> 5, j = (idx & 31) * 2;
-      cp_async16(sa + i * GLD + j, La + (long long)i * bw + j);
-      cp_async16(sb + i * GLD + j, Lb + (long long)i * bw + j);
+  __shared__ __align__(8) unsigned long long lbar;
+  const bool tma = s == 64 && (bw & 1) == 0;
+  if (tma) {
+    // TMA: one 512-byte bulk copy per leaf row into the padded rows (GLD:
+    // conflict-free DMMA fragment reads), 128 copies on one mbarrier that
+    // counts the 64 KB of both leaves, issued by 16 lanes of every warp
+    if (tid == 32) {
+      mbar_init(&lbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 32) mbar_expect_tx(&lbar, 2u * 64u * 64u * 8u);
+    if (lane < 16) {                 // 128 row copies issued by 8 warps x 16 lanes
+      const int i = warp * 8 + (lane & 7);
+      if (lane < 8) bulk_g2s(sa + i * GLD, La + (long long)i * bw, 512u, &lbar);
+      else bulk_g2s(sb + i * GLD, Lb + (long long)i * bw, 512u, &lbar);
     }
   } else {
     for (int idx = tid; idx < 64 * 64; idx += GT) {
@@ -630,6 +670,7 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
     }
   }
   cp_async_wait_all();
+  if (tma) mbar_wait(&lbar, 0);
   __syncthreads();
   const int gi = lane >> 2, ti = lane & 3;
   const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;   // 4 x 2 warp grid
