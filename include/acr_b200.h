@@ -89,6 +89,18 @@ int acr_factor(acr_plan_t* p, const double* D_sub, const double* D_diag,
 int acr_solve(acr_plan_t* p, const double* rhs, int nrhs, double* u,
               void* stream);
 
+/* Factor with the forward sweep of a right-hand side fused in (the
+ * reference fuses its single RHS into the reduction, reduction.py:204-216):
+ * each level's RHS update runs on a side stream right after the level's
+ * record is complete, overlapping the next levels' factorisation.  rhs
+ * (m*n, nrhs) row-major, read during the call's stream work; single-GPU
+ * plans.  acr_solve_back then runs the cutoff solve and back-substitution
+ * into u (m*n, nrhs), once per fused factorisation. */
+int acr_factor_rhs(acr_plan_t* p, const double* D_sub, const double* D_diag,
+                   const double* D_sup, const double* E, const double* F,
+                   int inversion_order, const double* rhs, int nrhs, void* stream);
+int acr_solve_back(acr_plan_t* p, double* u, void* stream);
+
 /* Report (SolveReport fields, reduction.py:124-153). */
 int acr_levels(const acr_plan_t* p);
 int acr_cutoff_blocks(const acr_plan_t* p);

@@ -28,6 +28,9 @@ _SIGS = [
     ("acr_plan_set_option", C.c_int, [C.c_void_p, C.c_int, C.c_longlong]),
     ("acr_factor", C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int, C.c_void_p]),
     ("acr_solve", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    ("acr_factor_rhs", C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int, C.c_void_p, C.c_int,
+                                                                    C.c_void_p]),
+    ("acr_solve_back", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("acr_levels", C.c_int, [C.c_void_p]),
     ("acr_cutoff_blocks", C.c_int, [C.c_void_p]),
     ("acr_tree_depths", C.c_int, [C.c_void_p]),

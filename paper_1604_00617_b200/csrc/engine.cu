@@ -532,6 +532,12 @@ struct Plan {
       cudaEventDestroy(evf);
       cudaEventDestroy(evj);
     }
+    if (stf) {
+      cudaStreamSynchronize(stf);
+      cudaStreamDestroy(stf);
+      cudaEventDestroy(evfl);
+      cudaEventDestroy(evfj);
+    }
     if (stc) {
       cudaStreamSynchronize(stc);
       cudaStreamDestroy(stc);
@@ -589,6 +595,7 @@ struct Plan {
       retag(last.D, s); retag(last.E, s); retag(last.F, s);
       for (Dev* d : {&lu, &piv, &info, &lut, &ovf, &sing, &dctr, &dt.buf}) retag(*d, s);
       for (auto& d : scr) retag(d, s);
+      for (auto& d : ffs) retag(d, s);
     }
     st = s;
     st_set = true;
@@ -1675,6 +1682,8 @@ struct Plan {
     launches = 0;
     prof_reset();
     factored = false;
+    ff_ready = false;
+    const bool fused = frhs != nullptr && nranks() == 1 && !prof_on;
     if (!ovf.p) ovf.alloc(sizeof(int), st);
     sing.alloc(sizeof(int) * std::max(m, 1), st);
     if (!ev0) {
@@ -1688,6 +1697,7 @@ struct Plan {
     mloc0 = P > 1 ? bnd0[me() + 1] - bnd0[me()] : m;
     Level L;
     lift(L, first0, mloc0, sub, diag, sup, E, F);
+    if (fused) fwd_begin();
     std::vector<int> dR, eR, fR;
     int maxr = 1;
     int lvl = 0;
@@ -1739,7 +1749,15 @@ struct Plan {
       L.lvl = lvl;
       ranks_of(true);
       recs.push_back(std::move(rec));
+      // the forward sweep starts FWD_LAG levels behind: the first levels are
+      // throughput-bound and a concurrent sweep would only compete for the
+      // SMs; from level FWD_LAG on, the factorisation is a latency chain that
+      // leaves most of the GPU idle
+      if (fused)
+        while (fwd_next + fwd_lag <= lvl - 1) fwd_level(fwd_next++);
     }
+    if (fused)
+      while (fwd_next < (int)recs.size()) fwd_level(fwd_next++);
     if (!alive) {
       // retired at level lvl: shadow the collectives of the levels still
       // reduced by several ranks, then this rank's part is done
@@ -1787,6 +1805,7 @@ struct Plan {
       launches += 1 + 4 * ((Nc + 31) / 32);
       int hinfo = 0;
       CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      if (fused) fwd_end();
       CK(cudaEventRecord(ev1, st));
       CK(cudaStreamSynchronize(st));
       if (hinfo) throw SingularError("matrix is singular to working precision");
@@ -1800,7 +1819,9 @@ struct Plan {
   }
 
   // ---- solve (reference reduction.py:204-216, 305-311, 235-256) ----
-  void hmat_full(const HB* H, int G, int R, Src X, Src Y, int k) {
+  // tbuf: the phase-A buffer (nullptr: plan scratch slot 12); s: stream
+  void hmat_full(const HB* H, int G, int R, Src X, Src Y, int k, double* tbuf = nullptr,
+                 cudaStream_t s = nullptr) {
     if (G <= 0) return;
     MMJob J;
     memset(&J, 0, sizeof(J));
@@ -1816,12 +1837,105 @@ struct Plan {
     J.nB = ht.nleaves_under(0);
     J.RT = R;
     J.CT = k;
-    J.tbuf = scratch<double>(12, (size_t)G * std::max(J.nA, 1) * R * k);
-    hmat(&J, 1, G, st);
+    J.tbuf = tbuf ? tbuf : scratch<double>(12, (size_t)G * std::max(J.nA, 1) * R * k);
+    hmat(&J, 1, G, s ? s : st);
   }
 
+  // ---- forward sweep fused into factor() (single GPU): right after level
+  //      l's record is complete, its RHS update (reduction.py:204-216) runs
+  //      on a side stream, overlapping the factorisation of the next levels
+  //      (the upper levels leave the GPU mostly idle).  Every buffer is
+  //      allocated on the plan's stream before the event the side stream
+  //      waits for, and kept alive until the join at the end of factor(). ----
+  const double* frhs = nullptr;   // right-hand side of the next factor (acr_factor_rhs)
+  int fk = 0;
+  std::vector<Dev> ffs;           // f of every level, internal layout
+  bool ff_ready = false;
+  int ff_k = 0;
+  cudaStream_t stf = nullptr;
+  cudaEvent_t evfl = nullptr, evfj = nullptr;
+  std::vector<Dev> fkeep;         // tables / temporaries of the fused levels
+  int fwd_next = 0;               // next level whose forward sweep is issued
+  int fwd_lag = 5;                // levels the sweep trails the factorisation (ACR_FWD_LAG; measured 0..5: 5 best)
+
+  void fwd_begin() {
+    if (!stf) {
+      CK(cudaStreamCreateWithFlags(&stf, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&evfl, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&evfj, cudaEventDisableTiming));
+    }
+    // an earlier fused factor that failed may have left work on the side
+    // stream that reads these buffers: order their release after it
+    CK(cudaEventRecord(evfj, stf));
+    CK(cudaStreamWaitEvent(st, evfj, 0));
+    ffs.clear();
+    fkeep.clear();
+    ff_ready = false;
+    fwd_next = 0;
+    if (const char* e = getenv("ACR_FWD_LAG")) fwd_lag = atoi(e);
+    int L = 0;
+    for (int mg = m; mg > cutoff; mg /= 2) ++L;
+    ffs.resize(L + 1);
+    const long long kn = (long long)fk * n;
+    ffs[0].alloc(sizeof(double) * kn * std::max(m, 1), st);
+    CK(launch_rhs_in(frhs, m * n, fk, n, ffs[0].as<double>(), st));
+    ++launches;
+  }
+
+  void fwd_level(int l) {
+    Record& r = recs[l];
+    const int k = fk;
+    const long long kn = (long long)k * n;
+    const int mm = r.m, ne = (mm + 1) / 2, no = mm / 2;
+    int nq = 0;
+    for (int j = 1; j < mm; j += 2)
+      if (r.first + j + 1 <= r.mg - 1) ++nq;
+    Dev z(sizeof(double) * kn * (std::max(ne, 1) + 1), st);
+    Dev a(sizeof(double) * kn * std::max(no, 1), st);
+    Dev bb(sizeof(double) * kn * std::max(nq, 1), st);
+    ffs[l + 1].alloc(sizeof(double) * kn * std::max(no, 1), st);
+    const long long nA = std::max(ht.nA(0, 1), 1);
+    Dev t1(sizeof(double) * (size_t)std::max(ne, 1) * nA * r.Dinv.R * k, st);
+    Dev t2(sizeof(double) * (size_t)std::max(no, 1) * nA * r.E.R * k, st);
+    Dev t3(sizeof(double) * (size_t)std::max(nq, 1) * nA * r.F.R * k, st);
+    Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});
+    Dev tE = make_tab({{&r.E, 1, 2, no}});
+    Dev tF = make_tab({{&r.F, 1, 2, nq}});
+    CK(cudaEventRecord(evfl, st));
+    CK(cudaStreamWaitEvent(stf, evfl, 0));
+    double* fl = ffs[l].as<double>();
+    hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl, 2 * kn, k), s_pan(z.as<double>(), kn, k), k,
+              t1.as<double>(), stf);
+    hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k),
+              k, t2.as<double>(), stf);
+    hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k),
+              s_pan(bb.as<double>(), kn, k), k, t3.as<double>(), stf);
+    double* fn = ffs[l + 1].as<double>();
+    CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, bb.as<double>(), kn, fn, kn, nq,
+                          (int)kn, stf));
+    CK(launch_rhs_combine(fl + kn + 2 * kn * nq, 2 * kn, a.as<double>() + kn * nq, kn, nullptr, 0,
+                          fn + kn * nq, kn, no - nq, (int)kn, stf));
+    launches += 2;
+    for (Dev* d : {&z, &a, &bb, &t1, &t2, &t3, &tDi, &tE, &tF}) fkeep.push_back(std::move(*d));
+  }
+
+  void fwd_end() {
+    CK(cudaEventRecord(evfj, stf));
+    CK(cudaStreamWaitEvent(st, evfj, 0));
+    fkeep.clear();                 // released on st, ordered after the side stream's work
+    ff_ready = true;
+    ff_k = fk;
+  }
+
+  // rhs == nullptr: back-substitution after a factorisation that ran the
+  // forward sweep of its right-hand side (acr_factor_rhs / acr_solve_back)
   void solve(const double* rhs, int k, double* u) {
     if (!factored) throw ArgError("acr_solve called before a successful acr_factor");
+    const bool fused = rhs == nullptr;
+    if (fused) {
+      if (!ff_ready) throw ArgError("acr_solve_back needs a preceding acr_factor_rhs");
+      k = ff_k;
+    }
     if (!sev0) {
       CK(cudaEventCreate(&sev0));
       CK(cudaEventCreate(&sev1));
@@ -1832,14 +1946,19 @@ struct Plan {
     const int Lt = P > 1 ? Lsched : (int)recs.size();   // level of the cutoff system
     const bool root = me() == 0;
     std::vector<Dev> f(Lt + 1);
-    f[0].alloc(sizeof(double) * kn * std::max(mloc0, 1), st);
-    CK(launch_rhs_in(rhs + (long long)first0 * n * k, mloc0 * n, k, n, f[0].as<double>(), st));
-    ++launches;
+    if (fused) {
+      f = std::move(ffs);            // consumed: one back-substitution per fused factor
+      ff_ready = false;
+    } else {
+      f[0].alloc(sizeof(double) * kn * std::max(mloc0, 1), st);
+      CK(launch_rhs_in(rhs + (long long)first0 * n * k, mloc0 * n, k, n, f[0].as<double>(), st));
+      ++launches;
+    }
     // windows (block counts) this rank holds at level l before / after merges
     auto wcount = [&](const std::vector<int>& b) { return b[me() + 1] - b[me()]; };
     int lret = Lt;                     // level at which this rank retired (Lt: never)
     // forward sweep (reduction.py:204-216) with the factor's merges replayed
-    for (int l = 0; l <= Lt; ++l) {
+    for (int l = 0; l <= Lt && !fused; ++l) {
       if (P > 1) {
         bool out = false;
         for (const MergeStep& ms : msteps) {
@@ -2471,6 +2590,38 @@ int acr_solve(acr_plan_t* h, const double* rhs, int nrhs, double* u,
     Plan& P = *h->p;
     P.use_stream((cudaStream_t)stream);
     P.solve(rhs, nrhs, u);
+  });
+  return ACR_OK;
+}
+
+int acr_factor_rhs(acr_plan_t* h, const double* D_sub, const double* D_diag,
+                   const double* D_sup, const double* E, const double* F, int inversion_order,
+                   const double* rhs, int nrhs, void* stream) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  if (inversion_order != 0 && inversion_order != 1)
+    return set_err(h, ACR_EARG, "unknown inversion_order");
+  if (!rhs || nrhs < 1) return set_err(h, ACR_EARG, "need a right-hand side with nrhs >= 1");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    if (P.nranks() > 1) throw acr::ArgError("acr_factor_rhs: single-GPU plans only");
+    P.use_stream((cudaStream_t)stream);
+    P.frhs = rhs;
+    P.fk = nrhs;
+    struct Clear {
+      Plan& p;
+      ~Clear() { p.frhs = nullptr; }
+    } clear{P};
+    P.factor(D_sub, D_diag, D_sup, E, F, inversion_order);
+  });
+  return ACR_OK;
+}
+
+int acr_solve_back(acr_plan_t* h, double* u, void* stream) {
+  if (!h || !h->p) return set_err(h, ACR_EARG, "null plan");
+  ACR_GUARD(h, {
+    Plan& P = *h->p;
+    P.use_stream((cudaStream_t)stream);
+    P.solve(nullptr, 0, u);
   });
   return ACR_OK;
 }

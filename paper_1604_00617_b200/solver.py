@@ -114,9 +114,22 @@ class AcrSolver:
                                       device=dev)
         return [f(sys.D_sub), f(sys.D_diag), f(sys.D_sup), f(sys.E), f(sys.F)]
 
-    def factor(self, bands, inversion_order: str = "forward", stream=None):
+    def _as_rhs(self, rhs):
+        torch = self.torch
+        if not isinstance(rhs, torch.Tensor):
+            rhs = torch.as_tensor(np.ascontiguousarray(rhs, dtype=np.float64), device="cuda")
+        N = self.m * self.n
+        if rhs.shape[0] != N or rhs.dim() not in (1, 2):
+            raise ValueError(f"rhs has shape {tuple(rhs.shape)}, expected ({N},[k])")
+        return rhs.to(torch.float64).contiguous()
+
+    def factor(self, bands, inversion_order: str = "forward", stream=None, rhs=None):
         """``bands`` = [D_sub, D_diag, D_sup, E, F] CUDA float64 tensors or a
-        ``BlockTridiagSystem``."""
+        ``BlockTridiagSystem``.  With ``rhs`` ((N,) or (N, k)), the forward
+        sweep of that right-hand side runs inside the factorisation (each
+        level's RHS update overlapping the next levels, as the reference
+        fuses it, reduction.py:204-216); ``solve()`` without arguments then
+        finishes it (cutoff solve + back-substitution)."""
         if inversion_order not in ("forward", "reversed"):
             raise ValueError(f"unknown inversion_order {inversion_order!r}")
         if isinstance(bands, BlockTridiagSystem):
@@ -135,33 +148,55 @@ class AcrSolver:
         other = stream is not None and stream != cur
         if other:
             stream.wait_stream(cur)
-        rc = self.lib.acr_factor(self.plan, *[_ptr(t) for t in bands],
-                                 1 if inversion_order == "reversed" else 0,
-                                 _stream(self.torch, stream))
+        order = 1 if inversion_order == "reversed" else 0
+        self._fused = None
+        if rhs is not None:
+            rhs = self._as_rhs(rhs)
+            k = 1 if rhs.dim() == 1 else rhs.shape[1]
+            rc = self.lib.acr_factor_rhs(self.plan, *[_ptr(t) for t in bands], order, _ptr(rhs),
+                                         int(k), _stream(self.torch, stream))
+            if rc == 0:
+                self._fused = (tuple(rhs.shape), rhs.dtype)
+        else:
+            rc = self.lib.acr_factor(self.plan, *[_ptr(t) for t in bands], order,
+                                     _stream(self.torch, stream))
         if other:
             for t in bands:
                 t.record_stream(stream)
+            if rhs is not None:
+                rhs.record_stream(stream)
         if rc != 0:
             self.factored = False
             _raise(self.plan, rc)
         self.factored = True
         return self
 
-    def solve(self, rhs, stream=None):
-        """rhs: CUDA float64 tensor (N,) or (N, k); returns u of the same shape."""
+    def solve(self, rhs=None, stream=None):
+        """rhs: CUDA float64 tensor (N,) or (N, k); returns u of the same shape.
+        Without rhs: finish the right-hand side given to ``factor(rhs=...)``
+        (once per such factorisation)."""
         torch = self.torch
         if not self.factored:
             raise RuntimeError("factor() must succeed before solve()")
-        if not isinstance(rhs, torch.Tensor):
-            rhs = torch.as_tensor(np.ascontiguousarray(rhs, dtype=np.float64),
-                                  device="cuda")
-        N = self.m * self.n
-        if rhs.shape[0] != N or rhs.dim() not in (1, 2):
-            raise ValueError(f"rhs has shape {tuple(rhs.shape)}, expected ({N},[k])")
-        rhs = rhs.to(torch.float64).contiguous()
+        cur = torch.cuda.current_stream()
+        if rhs is None:
+            if not getattr(self, "_fused", None):
+                raise RuntimeError("solve() without a right-hand side needs factor(rhs=...)")
+            shape, dtype = self._fused
+            self._fused = None
+            u = torch.empty(shape, dtype=dtype, device="cuda")
+            if stream is not None and stream != cur:
+                stream.wait_stream(cur)
+            rc = self.lib.acr_solve_back(self.plan, _ptr(u), _stream(torch, stream))
+            if rc != 0:
+                _raise(self.plan, rc)
+            if stream is not None and stream != cur:
+                u.record_stream(stream)
+            self._nrhs = 1 if len(shape) == 1 else shape[1]
+            return u
+        rhs = self._as_rhs(rhs)
         k = 1 if rhs.dim() == 1 else rhs.shape[1]
         u = torch.empty_like(rhs)
-        cur = torch.cuda.current_stream()
         if stream is not None and stream != cur:
             # rhs (possibly a converted temporary) and u were allocated on the
             # current stream; the solve runs asynchronously on `stream`
@@ -277,8 +312,10 @@ def acr_solve(sys: BlockTridiagSystem, tol: Tolerance, cutoff_blocks: int = 1,
     solver = AcrSolver(sys.n_blocks, sys.block_dim, tol, cutoff_blocks, leaf_size)
     bands = solver.device_bands(sys)
     f = torch.as_tensor(sys.rhs, device="cuda")
-    solver.factor(bands, inversion_order)
-    u = solver.solve(f)
+    # the forward sweep rides with the factorisation (reduction.py:204-216);
+    # the report's reduce_ms therefore includes it, like the reference's
+    solver.factor(bands, inversion_order, rhs=f)
+    u = solver.solve()
     u_host = u.cpu().numpy()
     t1 = time.perf_counter()
     res, _ = relative_residual_gpu(bands, u, f, sys.n_blocks, sys.block_dim)

@@ -481,3 +481,24 @@ def test_blocked_leaf_inverse(solver_mod, s):
     lib.acr_leaf_inverse(s, C.c_void_p(dA.data_ptr()), C.c_void_p(dX.data_ptr()),
                          C.byref(sg), None)
     assert sg.value == 1
+
+
+def test_fused_forward_sweep_bitwise(solver_mod):
+    """factor(rhs=...) runs the forward sweep inside the factorisation (side
+    stream, level by level); solve() then back-substitutes.  Same kernels and
+    per-level order as factor() + solve(rhs): bitwise identical, and one
+    back-substitution per fused factorisation."""
+    c = P.CONFIGS["cfg2"]
+    s = P.make_config("cfg2", nrhs=3)
+    sol = solver_mod.AcrSolver(s.n_blocks, s.block_dim, Tolerance(c["eps"]), 1, c["leaf"])
+    bands = sol.device_bands(s)
+    f = torch.as_tensor(s.rhs, device="cuda")
+    sol.factor(bands)
+    ref = sol.solve(f).cpu().numpy()
+    sol.factor(bands, rhs=f)
+    got = sol.solve().cpu().numpy()
+    np.testing.assert_array_equal(got, ref)
+    with pytest.raises(RuntimeError):
+        sol.solve()                  # consumed
+    sol.factor(bands, rhs=f[:, 1].contiguous())
+    np.testing.assert_array_equal(sol.solve().cpu().numpy(), sol.solve(f[:, 1].contiguous()).cpu().numpy())
