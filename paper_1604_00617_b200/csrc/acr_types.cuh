@@ -116,6 +116,7 @@ struct TruncArgs {
   int task_major;           // warp path item order: 0 element-major, 1 task-major
   int direct_tag;           // instrumentation: direct (one CTA per item) launch
   int warp_rmax;            // warp path takes tasks of at most this many columns
+  long long warp_maxneed;   // ... and work areas of at most this many doubles
 };
 
 // HODLR x panel product over subtrees (reference algebra.py:52-83):

@@ -455,6 +455,7 @@ struct Plan {
   int direct_max = -1;        // option 5: largest launch (items) run one CTA per task; -1 default
   int warp_sched = 2;         // option 8: warp-path items 0 static, 1 dynamic, 2 dynamic task-major
   int warp_rmax = 16;         // option 9: widest core (columns) the warp path takes
+  long long warp_maxneed = 0; // option 10: largest warp-path work area (doubles); 0 = the pool
   HostTree ht;
   DeviceTree dt;
   cudaStream_t st = 0;
@@ -874,12 +875,15 @@ struct Plan {
       launches += 1;
       return;
     }
-    const bool may_big = !direct && wworst > trunc_warp_pool_doubles();
+    const long long wmax = warp_maxneed > 0 ? std::min<long long>(warp_maxneed, trunc_warp_pool_doubles())
+                                            : trunc_warp_pool_doubles();
+    const bool may_big = !direct && wworst > wmax;
     int* q = nullptr;
     int* qc = nullptr;
     a.wq = nullptr;
     a.task_major = warp_sched == 2 ? 1 : 0;
     a.warp_rmax = warp_rmax;
+    a.warp_maxneed = wmax;
     if (!direct && warp_sched > 0) {
       qc = scratch<int>(alt ? 17 : 14, 8);
       a.wq = qc + 2;
@@ -2563,6 +2567,10 @@ int acr_plan_set_option(acr_plan_t* h, int option, long long value) {
   }
   if (option == 9) {
     h->p->warp_rmax = (int)value;
+    return ACR_OK;
+  }
+  if (option == 10) {
+    h->p->warp_maxneed = value;
     return ACR_OK;
   }
   return set_err(h, ACR_EARG, "unknown option");

@@ -1772,7 +1772,8 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
     // large work areas, and cores above 16 columns (a single warp's Jacobi
     // would walk whole column pairs per lane): block path queues
-    if (need > (long long)NSLOT * SLOT / 8 || (bigq != nullptr && R > A.warp_rmax)) {
+    if (need > (long long)NSLOT * SLOT / 8 ||
+        (bigq != nullptr && (R > A.warp_rmax || need > A.warp_maxneed))) {
       // queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM);
       // queue 1 (stored from bigq + nitems): one 512-thread CTA per SM
       if (lane == 0) {   // queued as element-major items (k_trunc_big decodes so)
@@ -1785,7 +1786,9 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
       continue;
     }
     const int ns = (int)((need + SLOT - 1) / SLOT);
+    const long long t_acq = A.ctr ? clock64() : 0;
     const int s0 = acquire_slots(&mask, ns, lane);
+    if (A.ctr && lane == 0) atomicAdd(A.ctr + 68, (unsigned long long)(clock64() - t_acq));
     // order this warp's accesses to the slots after the previous owner's
     // (without this fence the hand-over raced once the tasks got shorter)
     __syncwarp();

@@ -27,7 +27,8 @@ G = 1e9
 print(f"block path: tasks {ctr[8]}, sweeps {ctr[10]}; Gcyc load {ctr[2]/G:.2f} qr {ctr[3]/G:.2f} "
       f"core {ctr[4]/G:.2f} jacobi {ctr[5]/G:.2f} select {ctr[6]/G:.2f} output {ctr[7]/G:.2f}")
 print(f"warp path: tasks {ctr[9]}, sweeps {ctr[11]}; Gcyc load {ctr[12]/G:.2f} qr {ctr[13]/G:.2f} "
-      f"core {ctr[14]/G:.2f} jacobi {ctr[15]/G:.2f} select {ctr[66]/G:.2f} output {ctr[67]/G:.2f}")
+      f"core {ctr[14]/G:.2f} jacobi {ctr[15]/G:.2f} select {ctr[66]/G:.2f} output {ctr[67]/G:.2f} "
+      f"slot-wait {ctr[68]/G:.2f}")
 rl = ["R<=8", "R<=16", "R<=32", "R<=64", "R>64"]
 ml = ["m<=128", "m<=256", "m<=512", "m<=1024", "m>1024"]
 print("block-path histogram: count / Gcyc total / Gcyc jacobi")
