@@ -5,6 +5,9 @@
 //                    scipy getrf/getrs semantics: first max pivot, singular if
 //                    a U diagonal entry is exactly 0)
 //   k_residual       ||A u - f|| / ||f|| from the bands (oracles.py:34-49)
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "acr_types.cuh"
 #include "acr_launch.h"
 
@@ -371,6 +374,143 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel_blk(double* A, int N, int j0
   }
 }
 
+// Panel factorisation on a thread-block cluster of LUC CTAs (distributed
+// shared memory): the whole jb-column panel stays on chip, split by rows
+// over the CTAs (a single SM streamed every sub-panel and its in-panel
+// update through L2, ~120 us per panel).  Row interchanges are implicit --
+// rows never move inside the panel; every CTA keeps the same position ->
+// physical-row map and each thread its own row's position -- and the panel
+// is written back in its final (swapped) order.  Per column: the CTAs' local
+// pivot candidates (largest |a|, first position on ties: getrf's rule),
+// one cluster barrier, the winner and the pivot row read through DSMEM, the
+// rank-1 update of the remaining panel columns (scale by the reciprocal of
+// the pivot, as dgetf2).  piv / info as the other panel kernels.
+static constexpr int LUC = 4;
+static constexpr int LUCT = 512;
+
+__global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
+    k_lu_panel_cl(double* A, int N, int j0, int jb, int* piv, int* info) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  const int crank = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Ms = N - j0;
+  const int RB = (Ms + LUC - 1) / LUC;
+  const int r0 = crank * RB;
+  const int nr = Ms - r0 < RB ? (Ms - r0 > 0 ? Ms - r0 : 0) : RB;
+  double* P = sm;                                        // [c][i], column c of own rows
+  int* p2r = reinterpret_cast<int*>(P + (size_t)jb * RB);  // position -> physical row
+  __shared__ double cval[2];
+  __shared__ int cpos[2], crow[2];
+  __shared__ double prow[LU_NB];
+  __shared__ double wv[LUCT / 32];
+  __shared__ int wpos[LUCT / 32], wrow[LUCT / 32];
+  __shared__ int s_pos, s_row;
+  for (int idx = tid; idx < nr * jb; idx += LUCT) {
+    const int i = idx / jb, c = idx - i * jb;
+    P[c * RB + i] = A[(long long)(j0 + r0 + i) * N + j0 + c];
+  }
+  for (int q = tid; q < Ms; q += LUCT) p2r[q] = q;
+  int my_pos = tid < nr ? r0 + tid : 0x7fffffff;
+  __syncthreads();
+  cl.sync();
+  for (int jj = 0; jj < jb; ++jj) {
+    // local candidate: rows not yet pivoted (position >= jj)
+    double best = -1.0;
+    int bpos = 0x7fffffff, brow = -1;
+    if (tid < nr && my_pos >= jj) {
+      best = fabs(P[jj * RB + tid]);
+      bpos = my_pos;
+      brow = r0 + tid;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
+    }
+    if (lane == 0) { wv[warp] = best; wpos[warp] = bpos; wrow[warp] = brow; }
+    __syncthreads();
+    if (warp == 0) {
+      best = lane < LUCT / 32 ? wv[lane] : -1.0;
+      bpos = lane < LUCT / 32 ? wpos[lane] : 0x7fffffff;
+      brow = lane < LUCT / 32 ? wrow[lane] : -1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
+      }
+      if (lane == 0) { cval[jj & 1] = best; cpos[jj & 1] = bpos; crow[jj & 1] = brow; }
+    }
+    cl.sync();                                  // every CTA's candidate (and rows) ready
+    if (warp == 0) {
+      // the winner among the CTAs' candidates, then the pivot row (DSMEM)
+      best = -1.0;
+      bpos = 0x7fffffff;
+      brow = -1;
+      if (lane < LUC) {
+        const double* rv = cl.map_shared_rank(cval, lane);
+        const int* rp = cl.map_shared_rank(cpos, lane);
+        const int* rr = cl.map_shared_rank(crow, lane);
+        best = rv[jj & 1];
+        bpos = rp[jj & 1];
+        brow = rr[jj & 1];
+      }
+#pragma unroll
+      for (int o = 2; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
+      }
+      bpos = __shfl_sync(0xffffffffu, bpos, 0);
+      brow = __shfl_sync(0xffffffffu, brow, 0);
+      const int owner = brow / RB, li = brow - owner * RB;
+      const double* op = cl.map_shared_rank(P, owner);
+      if (lane >= jj && lane < jb) prow[lane] = op[lane * RB + li];
+      if (lane == 0) {
+        s_pos = bpos;
+        s_row = brow;
+      }
+    }
+    __syncthreads();
+    const int ppos = s_pos, prw = s_row;
+    const int a = p2r[jj];                      // physical row now at position jj
+    if (tid < nr) {
+      if (r0 + tid == a) my_pos = ppos;
+      if (r0 + tid == prw) my_pos = jj;
+    }
+    __syncthreads();                            // everyone read p2r[jj]
+    if (tid == 0) {
+      p2r[jj] = prw;
+      p2r[ppos] = a;
+    }
+    const double pv = prow[jj];
+    if (crank == 0 && tid == 0) {
+      piv[j0 + jj] = j0 + ppos;
+      if (pv == 0.0 && *info == 0) *info = j0 + jj + 1;
+    }
+    if (tid < nr && my_pos > jj) {
+      const double rinv = pv != 0.0 ? 1.0 / pv : 0.0;
+      const double l = pv != 0.0 ? P[jj * RB + tid] * rinv : P[jj * RB + tid];
+      P[jj * RB + tid] = l;
+      for (int c = jj + 1; c < jb; ++c) P[c * RB + tid] = P[c * RB + tid] - l * prow[c];
+    }
+  }
+  cl.sync();                                    // remote reads of this CTA's rows done
+  __shared__ int fpos[LUCT];                    // each row's final position
+  fpos[tid] = tid < nr ? my_pos : 0;
+  __syncthreads();
+  for (int idx = tid; idx < nr * jb; idx += LUCT) {
+    const int i = idx / jb, c = idx - i * jb;
+    A[(long long)(j0 + fpos[i]) * N + j0 + c] = P[c * RB + i];
+  }
+}
+
 // Row interchanges of panel j0 applied to every column outside it (laswp):
 // a CTA stages the <= 2 jb touched rows of its 32 columns in shared memory,
 // replays the swaps there (thread per column) and writes the rows back.
@@ -437,7 +577,19 @@ cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work,
   for (int j0 = 0; j0 < N; j0 += LU_NB) {
     int jb = N - j0 < LU_NB ? N - j0 : LU_NB;
     const size_t sbytes = (size_t)LU_SB * (N - j0) * sizeof(double);
-    if (sbytes <= 200 * 1024) {   // sub-panels in shared memory
+    const int Ms = N - j0, RB = (Ms + LUC - 1) / LUC;
+    const size_t cbytes = (size_t)jb * RB * sizeof(double) + (size_t)Ms * sizeof(int);
+    static const bool nocl = getenv("ACR_LU_NOCLUSTER") != nullptr;   // A/B aid
+    if (!nocl && RB <= LUCT && cbytes <= 200 * 1024) {   // whole panel on a CTA cluster
+      static bool attr_c = false;
+      if (!attr_c) {
+        cudaFuncSetAttribute(k_lu_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr_c = true;
+      }
+      k_lu_panel_cl<<<LUC, LUCT, cbytes, st>>>(A, N, j0, jb, piv, info);
+      if (N - jb > 0) k_lu_laswp<<<(N - jb + 31) / 32, dim3(32, 8), 0, st>>>(A, N, j0, jb, piv);
+    } else if (sbytes <= 200 * 1024) {   // sub-panels in shared memory
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(k_lu_panel_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
