@@ -393,6 +393,7 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ double sm[];
+  constexpr int NW = LUCT / 32;
   const int crank = (int)cl.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int Ms = N - j0;
@@ -401,12 +402,12 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
   const int nr = Ms - r0 < RB ? (Ms - r0 > 0 ? Ms - r0 : 0) : RB;
   double* P = sm;                                        // [c][i], column c of own rows
   int* p2r = reinterpret_cast<int*>(P + (size_t)jb * RB);  // position -> physical row
-  __shared__ double cval[2];
-  __shared__ int cpos[2], crow[2];
+  // per-warp pivot candidates, double-buffered by column parity (read by
+  // every CTA of the cluster through DSMEM after the cluster barrier)
+  __shared__ double wv[2][NW];
+  __shared__ int wpos[2][NW], wrow[2][NW];
   __shared__ double prow[LU_NB];
-  __shared__ double wv[LUCT / 32];
-  __shared__ int wpos[LUCT / 32], wrow[LUCT / 32];
-  __shared__ int s_pos, s_row;
+  __shared__ int s_pos, s_row, s_a;
   for (int idx = tid; idx < nr * jb; idx += LUCT) {
     const int i = idx / jb, c = idx - i * jb;
     P[c * RB + i] = A[(long long)(j0 + r0 + i) * N + j0 + c];
@@ -414,9 +415,9 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
   for (int q = tid; q < Ms; q += LUCT) p2r[q] = q;
   int my_pos = tid < nr ? r0 + tid : 0x7fffffff;
   __syncthreads();
-  cl.sync();
   for (int jj = 0; jj < jb; ++jj) {
-    // local candidate: rows not yet pivoted (position >= jj)
+    const int par = jj & 1;
+    // warp candidate: rows not yet pivoted (position >= jj)
     double best = -1.0;
     int bpos = 0x7fffffff, brow = -1;
     if (tid < nr && my_pos >= jj) {
@@ -431,12 +432,25 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
       const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
       if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
     }
-    if (lane == 0) { wv[warp] = best; wpos[warp] = bpos; wrow[warp] = brow; }
-    __syncthreads();
+    if (lane == 0) { wv[par][warp] = best; wpos[par][warp] = bpos; wrow[par][warp] = brow; }
+    cl.sync();                                  // all candidates and rows of step jj ready
     if (warp == 0) {
-      best = lane < LUCT / 32 ? wv[lane] : -1.0;
-      bpos = lane < LUCT / 32 ? wpos[lane] : 0x7fffffff;
-      brow = lane < LUCT / 32 ? wrow[lane] : -1;
+      // the winner among the LUC x NW warp candidates (lane t reads CTA
+      // t / (32 / NW)'s... every CTA's NW slots, LUC * NW <= 64: two per lane)
+      best = -1.0;
+      bpos = 0x7fffffff;
+      brow = -1;
+#pragma unroll
+      for (int h = 0; h < (LUC * NW + 31) / 32; ++h) {
+        const int t = lane + 32 * h;
+        if (t < LUC * NW) {
+          const int cr = t / NW, w = t - cr * NW;
+          const double v = cl.map_shared_rank(&wv[par][0], cr)[w];
+          const int pp = cl.map_shared_rank(&wpos[par][0], cr)[w];
+          const int rr = cl.map_shared_rank(&wrow[par][0], cr)[w];
+          if (v > best || (v == best && pp < bpos)) { best = v; bpos = pp; brow = rr; }
+        }
+      }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -444,50 +458,23 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
         const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
         if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
       }
-      if (lane == 0) { cval[jj & 1] = best; cpos[jj & 1] = bpos; crow[jj & 1] = brow; }
-    }
-    cl.sync();                                  // every CTA's candidate (and rows) ready
-    if (warp == 0) {
-      // the winner among the CTAs' candidates, then the pivot row (DSMEM)
-      best = -1.0;
-      bpos = 0x7fffffff;
-      brow = -1;
-      if (lane < LUC) {
-        const double* rv = cl.map_shared_rank(cval, lane);
-        const int* rp = cl.map_shared_rank(cpos, lane);
-        const int* rr = cl.map_shared_rank(crow, lane);
-        best = rv[jj & 1];
-        bpos = rp[jj & 1];
-        brow = rr[jj & 1];
-      }
-#pragma unroll
-      for (int o = 2; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
-        const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
-        if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
-      }
-      bpos = __shfl_sync(0xffffffffu, bpos, 0);
-      brow = __shfl_sync(0xffffffffu, brow, 0);
       const int owner = brow / RB, li = brow - owner * RB;
-      const double* op = cl.map_shared_rank(P, owner);
-      if (lane >= jj && lane < jb) prow[lane] = op[lane * RB + li];
+      const double* opn = cl.map_shared_rank(P, owner);
+      if (lane >= jj && lane < jb) prow[lane] = opn[lane * RB + li];
       if (lane == 0) {
+        const int a = p2r[jj];                  // physical row now at position jj
         s_pos = bpos;
         s_row = brow;
+        s_a = a;
+        p2r[jj] = brow;
+        p2r[bpos] = a;
       }
     }
     __syncthreads();
-    const int ppos = s_pos, prw = s_row;
-    const int a = p2r[jj];                      // physical row now at position jj
+    const int ppos = s_pos, prw = s_row, a = s_a;
     if (tid < nr) {
       if (r0 + tid == a) my_pos = ppos;
       if (r0 + tid == prw) my_pos = jj;
-    }
-    __syncthreads();                            // everyone read p2r[jj]
-    if (tid == 0) {
-      p2r[jj] = prw;
-      p2r[ppos] = a;
     }
     const double pv = prow[jj];
     if (crank == 0 && tid == 0) {
@@ -500,6 +487,8 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
       P[jj * RB + tid] = l;
       for (int c = jj + 1; c < jb; ++c) P[c * RB + tid] = P[c * RB + tid] - l * prow[c];
     }
+    // prow is rewritten by warp 0 only after the next cluster barrier, which
+    // every thread of this CTA reaches after its update
   }
   cl.sync();                                    // remote reads of this CTA's rows done
   __shared__ int fpos[LUCT];                    // each row's final position
