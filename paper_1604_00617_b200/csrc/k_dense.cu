@@ -10,12 +10,14 @@
 
 #include "acr_types.cuh"
 #include "acr_launch.h"
+#include "acr_pdl.cuh"
 
 namespace acr {
 
 // one CTA per (dense block, row chunk); A row-major with leading dim ld
 __global__ void k_todense(TreeDev T, const HB* blk, const int* rowblk,
                           const int* colblk, double* A, int ld) {
+  ACR_PDL_ENTRY();
   const int b = blockIdx.y, n = T.n, bw = T.bw;
   const HB h = blk[b];
   double* Ab = A + (long long)rowblk[b] * n * ld + (long long)colblk[b] * n;
@@ -54,7 +56,7 @@ cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
   if (!nblk) return cudaSuccess;
   int bx = (T.n * T.n + 255) / 256;
   if (bx > 1024) bx = 1024;
-  k_todense<<<dim3(bx, nblk), 256, 0, st>>>(T, blk, rowblk, colblk, A, ld);
+  CK_PDL(launch_pdl(k_todense, dim3(dim3(bx, nblk)), dim3(256), 0, st, T, blk, rowblk, colblk, A, ld));
   return cudaGetLastError();
 }
 
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(LU_PT) k_lu_panel(double* A, int N, int j0,
 
 // A12 := L11^{-1} A12 (unit lower), one thread per column, L11 in smem
 __global__ void k_lu_trsm(double* A, int N, int j0, int jb) {
+  ACR_PDL_ENTRY();
   __shared__ double L[LU_NB][LU_NB + 1];
   for (int idx = threadIdx.x; idx < jb * jb; idx += blockDim.x) {
     int i = idx / jb, k = idx - i * jb;
@@ -162,6 +165,7 @@ __global__ void k_lu_trsm(double* A, int N, int j0, int jb) {
 
 // A22 -= A21 A12, 64x64 tiles, k = jb <= 32
 __global__ void __launch_bounds__(256) k_lu_gemm(double* A, int N, int j0, int jb) {
+  ACR_PDL_ENTRY();
   __shared__ double sa[64][LU_NB + 1];
   __shared__ double sb[LU_NB][64 + 1];
   const int r0 = j0 + jb + blockIdx.y * 64, c0 = j0 + jb + blockIdx.x * 64;
@@ -390,6 +394,7 @@ static constexpr int LUCT = 512;
 
 __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
     k_lu_panel_cl(double* A, int N, int j0, int jb, int* piv, int* info) {
+  ACR_PDL_ENTRY();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ double sm[];
@@ -504,6 +509,7 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
 // a CTA stages the <= 2 jb touched rows of its 32 columns in shared memory,
 // replays the swaps there (thread per column) and writes the rows back.
 __global__ void k_lu_laswp(double* A, int N, int j0, int jb, const int* piv) {
+  ACR_PDL_ENTRY();
   __shared__ double t[2 * LU_NB][33];
   __shared__ int rows[2 * LU_NB], sa[LU_NB], sb[LU_NB], nrows;
   // slots 0..jb-1: rows j0..j0+jb-1; pivot rows below the panel get extra
@@ -576,8 +582,8 @@ cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work,
                              200 * 1024);
         attr_c = true;
       }
-      k_lu_panel_cl<<<LUC, LUCT, cbytes, st>>>(A, N, j0, jb, piv, info);
-      if (N - jb > 0) k_lu_laswp<<<(N - jb + 31) / 32, dim3(32, 8), 0, st>>>(A, N, j0, jb, piv);
+      CK_PDL(launch_pdl(k_lu_panel_cl, dim3(LUC), dim3(LUCT), cbytes, st, A, N, j0, jb, piv, info));
+      if (N - jb > 0) CK_PDL(launch_pdl(k_lu_laswp, dim3((N - jb + 31) / 32), dim3(dim3(32, 8)), 0, st, A, N, j0, jb, piv));
     } else if (sbytes <= 200 * 1024) {   // sub-panels in shared memory
       static bool attr = false;
       if (!attr) {
@@ -586,15 +592,15 @@ cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work,
         attr = true;
       }
       k_lu_panel_blk<<<1, LU_PT, sbytes, st>>>(A, N, j0, jb, piv, info);
-      if (N - jb > 0) k_lu_laswp<<<(N - jb + 31) / 32, dim3(32, 8), 0, st>>>(A, N, j0, jb, piv);
+      if (N - jb > 0) CK_PDL(launch_pdl(k_lu_laswp, dim3((N - jb + 31) / 32), dim3(dim3(32, 8)), 0, st, A, N, j0, jb, piv));
     } else {
       k_lu_panel<<<1, LU_PT, 0, st>>>(A, N, j0, jb, piv, info);
     }
     int rest = N - j0 - jb;
     if (rest > 0) {
-      k_lu_trsm<<<(rest + 63) / 64, 64, 0, st>>>(A, N, j0, jb);
+      CK_PDL(launch_pdl(k_lu_trsm, dim3((rest + 63) / 64), dim3(64), 0, st, A, N, j0, jb));
       dim3 g((rest + 63) / 64, (rest + 63) / 64);
-      k_lu_gemm<<<g, 256, 0, st>>>(A, N, j0, jb);
+      CK_PDL(launch_pdl(k_lu_gemm, dim3(g), dim3(256), 0, st, A, N, j0, jb));
     }
   }
   return cudaGetLastError();

@@ -9,6 +9,7 @@
 //   subtree, deepest first -- the reference's recursion order)
 #include "acr_types.cuh"
 #include "acr_launch.h"
+#include "acr_pdl.cuh"
 #include <cstdlib>
 
 namespace acr {
@@ -39,6 +40,7 @@ struct MMJobs2 {
 
 template <bool LAT>
 __global__ void __launch_bounds__(HT) k_hmatA(TreeDev T, MMJobs2 JJ) {
+  ACR_PDL_ENTRY();
   const MMJob& J = JJ.j[blockIdx.z];
   if ((int)blockIdx.x >= J.nA) return;
   const int g = blockIdx.y, n = T.n;
@@ -391,6 +393,7 @@ __device__ __forceinline__ void hb_finish_tab(const TreeDev& T, const MMJob& J, 
 // X staged in windows of at most xc columns (bounded shared memory)
 template <int NTB>
 __global__ void __launch_bounds__(NTB) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int path, int xc) {
+  ACR_PDL_ENTRY();
   extern __shared__ double sm[];
   const MMJob& J = JJ.j[blockIdx.z];
   const int g = blockIdx.y, bw = T.bw;
@@ -463,8 +466,8 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
   }
   if (nA > 0) {
     dim3 g(nA, nelem, njobs);
-    if (nelem <= 32) k_hmatA<true><<<g, HT, 0, st>>>(T, JJ);
-    else k_hmatA<false><<<g, HT, 0, st>>>(T, JJ);
+    if (nelem <= 32) CK_PDL(launch_pdl(k_hmatA<true>, dim3(g), dim3(HT), 0, st, T, JJ));
+    else CK_PDL(launch_pdl(k_hmatA<false>, dim3(g), dim3(HT), 0, st, T, JJ));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -489,7 +492,7 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     const size_t smem = ((size_t)T.bw * cp + (size_t)T.bw * (T.bw + 1) + 1) * 8;
     dim3 g(path ? T.nleaves : nB, nelem, njobs);
     // 256 threads per leaf CTA (measured: 128 and 512 are slower)
-    k_hmatB_sm<256><<<g, 256, smem, st>>>(T, JJ, path, (int)cp);
+    CK_PDL(launch_pdl(k_hmatB_sm<256>, dim3(g), dim3(256), smem, st, T, JJ, path, (int)cp));
     return cudaGetLastError();
   }
   if (path) {
@@ -518,6 +521,7 @@ struct GPJobs2 {
 // GT threads: 256 for small (latency-bound) grids, 128 for large ones
 template <int GT>
 __global__ void __launch_bounds__(GT) k_gp(TreeDev T, GPJobs2 JJ, const int* nodes) {
+  ACR_PDL_ENTRY();
   extern __shared__ double K[];
   const GPJob& J = JJ.j[blockIdx.z];
   const int g = blockIdx.y, n = T.n;
@@ -581,8 +585,8 @@ cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
     attr = true;
   }
   dim3 g(nnodes, nelem, njobs);
-  if ((long long)nnodes * nelem * njobs < 148LL * 4) k_gp<256><<<g, 256, smem, st>>>(T, JJ, nodes);
-  else k_gp<128><<<g, 128, smem, st>>>(T, JJ, nodes);
+  if ((long long)nnodes * nelem * njobs < 148LL * 4) CK_PDL(launch_pdl(k_gp<256>, dim3(g), dim3(256), smem, st, T, JJ, nodes));
+  else CK_PDL(launch_pdl(k_gp<128>, dim3(g), dim3(128), smem, st, T, JJ, nodes));
   return cudaGetLastError();
 }
 
@@ -591,6 +595,7 @@ cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
 __global__ void k_rhs_combine(const double* f, long long fs, const double* a,
                               long long as, const double* b, long long bs,
                               double* out, long long os, int len) {
+  ACR_PDL_ENTRY();
   const int e = blockIdx.y;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
        i += gridDim.x * blockDim.x) {
@@ -608,7 +613,7 @@ cudaError_t launch_rhs_combine(const double* f, long long fs, const double* a,
   if (count <= 0) return cudaSuccess;
   int bx = (len + 255) / 256;
   if (bx > 64) bx = 64;
-  k_rhs_combine<<<dim3(bx, count), 256, 0, st>>>(f, fs, a, as, b, bs, out, os, len);
+  CK_PDL(launch_pdl(k_rhs_combine, dim3(dim3(bx, count)), dim3(256), 0, st, f, fs, a, as, b, bs, out, os, len));
   return cudaGetLastError();
 }
 

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include "acr_types.cuh"
 #include "acr_launch.h"
+#include "acr_pdl.cuh"
 
 namespace acr {
 
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(IT) k_leafinv(TreeDev T, const HB* H, int leaf
 template <int S, int TR, int TC, int MINB>
 __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDev T, const HB* H,
                                                                        int leaf, int* sing) {
+  ACR_PDL_ENTRY();
   constexpr int TGY = S / TR, TGX = S / TC, NT = TGX * TGY;
   static_assert(TGY <= 32, "a column group must fit one warp");
   constexpr unsigned MASK = TGY >= 32 ? 0xffffffffu : (NT >= 32 ? 0xffffffffu : (1u << NT) - 1u);
@@ -292,6 +294,7 @@ static constexpr int BGJ_LD = 68;       // padded row stride (doubles)
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H, int leaf,
                                                          int* sing) {
+  ACR_PDL_ENTRY();
   constexpr int NW = NT / 32;
   __shared__ __align__(16) double X[64 * BGJ_LD];
   __shared__ __align__(16) double Tb[8 * BGJ_LD];
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H
 template <int S>
 static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int leaf,
                                int* sing, cudaStream_t st) {
-  k_leafinv_v2<S, 4, 4, 3><<<nelem, (S / 4) * (S / 4), 0, st>>>(T, H, leaf, sing);
+  CK_PDL(launch_pdl(k_leafinv_v2<S, 4, 4, 3>, dim3(nelem), dim3((S / 4) * (S / 4)), 0, st, T, H, leaf, sing));
   return cudaGetLastError();
 }
 
@@ -449,7 +452,7 @@ cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
     if (bgj && s > 32) {
       // 256 threads, three CTAs per SM (measured: 128-thread CTAs at five per
       // SM are slower for batched launches too, 126 vs 85 us per 1024 leaves)
-      k_leafinv_bgj<256, 3><<<nelem, 256, 0, st>>>(T, H, leaf, sing);
+      CK_PDL(launch_pdl(k_leafinv_bgj<256, 3>, dim3(nelem), dim3(256), 0, st, T, H, leaf, sing));
       return cudaGetLastError();
     }
     return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
@@ -576,6 +579,7 @@ __device__ __forceinline__ void dmma_block(double (&acc)[2][4][2], const double*
 __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, const HB* B,
                                                       const HB* C, Src PX, RankRef xr,
                                                       int diag) {
+  ACR_PDL_ENTRY();
   extern __shared__ double sm[];
   double* sa = sm;                 // [64][GLD]  A rows       (P for cross terms)
   double* sb = sa + 64 * GLD;      // [64][GLD]  B rows       (Q^T for cross terms)
@@ -770,6 +774,7 @@ __global__ void __launch_bounds__(GT, 2) k_leafgemm_tc(TreeDev T, const HB* A, c
 // that many CTAs per SM keep the HBM busy)
 __global__ void __launch_bounds__(256) k_leafgemm_diag(TreeDev T, const HB* A, const HB* B,
                                                        const HB* C, int diag) {
+  ACR_PDL_ENTRY();
   __shared__ double dv[128];
   const int g = blockIdx.y, tid = threadIdx.x;
   const int lam = T.listB[(T.startB[0] + blockIdx.x) * 2 + 1];
@@ -805,7 +810,7 @@ cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
   if (!nelem) return cudaSuccess;
   dim3 grid(T.nleaves, nelem);
   if (diag && T.bw <= 128) {
-    k_leafgemm_diag<<<grid, 256, 0, st>>>(T, A, B, C, diag);
+    CK_PDL(launch_pdl(k_leafgemm_diag, dim3(grid), dim3(256), 0, st, T, A, B, C, diag));
     return cudaGetLastError();
   }
   if (T.bw <= 64) {
@@ -816,7 +821,7 @@ cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
                            (int)smem);
       attr = true;
     }
-    k_leafgemm_tc<<<grid, GT, smem, st>>>(T, A, B, C, PX, xr, diag);
+    CK_PDL(launch_pdl(k_leafgemm_tc, dim3(grid), dim3(GT), smem, st, T, A, B, C, PX, xr, diag));
     return cudaGetLastError();
   }
   size_t smem = 2ull * T.bw * T.bw * 8;
@@ -836,6 +841,7 @@ cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
 __global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
                                                Src Us, Src Vs, RankRef rr,
                                                int node, int fside) {
+  ACR_PDL_ENTRY();
   extern __shared__ double sm[];
   const int g = blockIdx.y, tid = threadIdx.x, n = T.n, bw = T.bw;
   const int* rb = rank_base(rr, g);
@@ -903,7 +909,7 @@ cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
     cudaFuncSetAttribute(k_leaflr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_leaflr<<<grid, LT, smem, st>>>(T, H, mu, U, V, rr, node, fside);
+  CK_PDL(launch_pdl(k_leaflr, dim3(grid), dim3(LT), smem, st, T, H, mu, U, V, rr, node, fside));
   return cudaGetLastError();
 }
 
@@ -912,6 +918,7 @@ cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
 // ---------------------------------------------------------------------------
 __global__ void k_leafadd(int len, const HB* A, const HB* B, const HB* C,
                           double sb) {
+  ACR_PDL_ENTRY();
   const int g = blockIdx.y;
   const double* a = A[g].leaf;
   const double* b = B[g].leaf;
@@ -932,11 +939,12 @@ cudaError_t launch_leafadd(const TreeDev& T, const HB* A, const HB* B,
   int len = T.n * T.bw;
   int bx = (len + 255) / 256;
   if (bx > 64) bx = 64;
-  k_leafadd<<<dim3(bx, nelem), 256, 0, st>>>(len, A, B, C, sb);
+  CK_PDL(launch_pdl(k_leafadd, dim3(dim3(bx, nelem)), dim3(256), 0, st, len, A, B, C, sb));
   return cudaGetLastError();
 }
 
 __global__ void k_negate(TreeDev T, const HB* H) {
+  ACR_PDL_ENTRY();
   const int g = blockIdx.y, n = T.n;
   const HB h = H[g];
   const int len = n * T.bw;
@@ -964,12 +972,14 @@ __global__ void k_negate(TreeDev T, const HB* H) {
 }
 
 __global__ void k_copy_i32(int* __restrict__ dst, const int* __restrict__ src, long long n) {
+  ACR_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
 
 __global__ void k_fill_i32(int* dst, int v, long long n) {
+  ACR_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     dst[i] = v;
@@ -978,25 +988,26 @@ __global__ void k_fill_i32(int* dst, int v, long long n) {
 cudaError_t launch_copy_i32(int* dst, const int* src, long long n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const long long b = (n + 255) / 256;
-  k_copy_i32<<<(int)(b < 592 ? b : 592), 256, 0, st>>>(dst, src, n);
+  CK_PDL(launch_pdl(k_copy_i32, dim3((int)(b < 592 ? b : 592)), dim3(256), 0, st, dst, src, n));
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill_i32(int* dst, int v, long long n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const long long b = (n + 255) / 256;
-  k_fill_i32<<<(int)(b < 592 ? b : 592), 256, 0, st>>>(dst, v, n);
+  CK_PDL(launch_pdl(k_fill_i32, dim3((int)(b < 592 ? b : 592)), dim3(256), 0, st, dst, v, n));
   return cudaGetLastError();
 }
 
 cudaError_t launch_negate(const TreeDev& T, const HB* H, int nelem,
                           cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_negate<<<dim3(32, nelem), 256, 0, st>>>(T, H);
+  CK_PDL(launch_pdl(k_negate, dim3(dim3(32, nelem)), dim3(256), 0, st, T, H));
   return cudaGetLastError();
 }
 
 __global__ void k_copyhb(TreeDev T, const HB* S, const HB* D, int* overflow) {
+  ACR_PDL_ENTRY();
   const int g = blockIdx.y, n = T.n;
   const HB s = S[g], d = D[g];
   const int len = n * T.bw;
@@ -1038,11 +1049,12 @@ __global__ void k_copyhb(TreeDev T, const HB* S, const HB* D, int* overflow) {
 cudaError_t launch_copyhb(const TreeDev& T, const HB* S, const HB* D, int nelem,
                           int* overflow, cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_copyhb<<<dim3(32, nelem), 256, 0, st>>>(T, S, D, overflow);
+  CK_PDL(launch_pdl(k_copyhb, dim3(dim3(32, nelem)), dim3(256), 0, st, T, S, D, overflow));
   return cudaGetLastError();
 }
 
 __global__ void k_zerohb(TreeDev T, const HB* D) {
+  ACR_PDL_ENTRY();
   const int g = blockIdx.y;
   const HB d = D[g];
   const int len = T.n * T.bw;
@@ -1058,7 +1070,7 @@ __global__ void k_zerohb(TreeDev T, const HB* D) {
 cudaError_t launch_zerohb(const TreeDev& T, const HB* D, int nelem,
                           cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_zerohb<<<dim3(16, nelem), 256, 0, st>>>(T, D);
+  CK_PDL(launch_pdl(k_zerohb, dim3(dim3(16, nelem)), dim3(256), 0, st, T, D));
   return cudaGetLastError();
 }
 
@@ -1086,6 +1098,7 @@ __device__ __forceinline__ void leaf_map(const TreeDev& T, int* mlo, int* msz) {
 // off21 = b e_mid e_{mid-1}^T (a = sup[mid-1], b = sub[mid-1]; rank 0 if 0)
 __global__ void k_lift(TreeDev T, const double* sub, const double* diag,
                        const double* sup, const HB* D) {
+  ACR_PDL_ENTRY();
   extern __shared__ int lmap[];
   const int g = blockIdx.y, n = T.n, bw = T.bw;
   const HB d = D[g];
@@ -1142,12 +1155,13 @@ cudaError_t launch_lift(const TreeDev& T, const double* sub, const double* diag,
                         const double* sup, const HB* D, int nelem,
                         cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_lift<<<dim3(8, nelem), 256, 2 * T.n * sizeof(int), st>>>(T, sub, diag, sup, D);
+  CK_PDL(launch_pdl(k_lift, dim3(dim3(8, nelem)), dim3(256), 2 * T.n * sizeof(int), st, T, sub, diag, sup, D));
   return cudaGetLastError();
 }
 
 // exact diagonal block (hodlr.py:294-314): dense diagonal leaves, rank 0
 __global__ void k_liftdiag(TreeDev T, const double* dd, const HB* D) {
+  ACR_PDL_ENTRY();
   extern __shared__ int lmap[];
   const int g = blockIdx.y, n = T.n, bw = T.bw;
   const HB d = D[g];
@@ -1171,13 +1185,14 @@ __global__ void k_liftdiag(TreeDev T, const double* dd, const HB* D) {
 cudaError_t launch_liftdiag(const TreeDev& T, const double* d, const HB* D,
                             int nelem, cudaStream_t st) {
   if (!nelem) return cudaSuccess;
-  k_liftdiag<<<dim3(8, nelem), 256, 2 * T.n * sizeof(int), st>>>(T, d, D);
+  CK_PDL(launch_pdl(k_liftdiag, dim3(dim3(8, nelem)), dim3(256), 2 * T.n * sizeof(int), st, T, d, D));
   return cudaGetLastError();
 }
 
 // HB table for a strided set of blocks: tab[i] = block (first + i*step)
 __global__ void k_build_tab(HB* tab, HB base, long long sl, long long sf,
                             long long sr, int first, int step, int count) {
+  ACR_PDL_ENTRY();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   long long e = first + (long long)i * step;
@@ -1193,8 +1208,8 @@ cudaError_t launch_build_tab(HB* tab, HB base, long long sl, long long sf,
                              long long sr, int first, int step, int count,
                              cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  k_build_tab<<<(count + 127) / 128, 128, 0, st>>>(tab, base, sl, sf, sr, first,
-                                                  step, count);
+  CK_PDL(launch_pdl(k_build_tab, dim3((count + 127) / 128), dim3(128), 0, st, tab, base, sl, sf, sr, first,
+                                                  step, count));
   return cudaGetLastError();
 }
 

@@ -16,6 +16,7 @@
 
 #include "acr_types.cuh"
 #include "acr_launch.h"
+#include "acr_pdl.cuh"
 
 namespace acr {
 
@@ -722,6 +723,7 @@ __device__ bool block_trivial(const TruncArgs& A, const TaskCtx& c, double* red)
 template <int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_trunc_big(TruncArgs A, const int* q,
                                                   const int* qcount, int nitems) {
+  ACR_PDL_ENTRY();
   extern __shared__ double sm[];
   __shared__ double red[(NT / 32) + 4];
   __shared__ int iflag[2];
@@ -783,6 +785,7 @@ __device__ __forceinline__ bool task_trivial(const TruncArgs& A, const TaskCtx& 
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     k_trunc_pair(TruncArgs A, int nitems) {
+  ACR_PDL_ENTRY();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ double sm[];
@@ -997,7 +1000,7 @@ cudaError_t launch_trunc_pair(const TruncArgs& a, int nelem, long long smem_doub
     attr = bytes;
   }
   const int nitems = a.ntasks * nelem;
-  k_trunc_pair<<<2 * nitems, TT, bytes, st>>>(a, nitems);
+  CK_PDL(launch_pdl(k_trunc_pair, dim3(2 * nitems), dim3(TT), bytes, st, a, nitems));
   return cudaGetLastError();
 }
 
@@ -1712,6 +1715,7 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
 
 __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nitems,
                                                           int* bigq, int* bigcount) {
+  ACR_PDL_ENTRY();
   extern __shared__ double pool[];
   __shared__ unsigned long long mask;
   if (threadIdx.x == 0) mask = 0ull;
@@ -1845,9 +1849,9 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
     ad.direct_tag = 1;
     // more tasks than SMs: 256-thread CTAs, two per SM, when the work areas fit
     if (nitems > nsm && bsm <= QHALF)
-      k_trunc_big<256><<<nitems, 256, bsm, st>>>(ad, nullptr, nullptr, nitems);
+      CK_PDL(launch_pdl(k_trunc_big<256>, dim3(nitems), dim3(256), bsm, st, ad, nullptr, nullptr, nitems));
     else
-      k_trunc_big<512><<<nitems, 512, bsm, st>>>(ad, nullptr, nullptr, nitems);
+      CK_PDL(launch_pdl(k_trunc_big<512>, dim3(nitems), dim3(512), bsm, st, ad, nullptr, nullptr, nitems));
     return cudaGetLastError();
   }
   if (may_big || a.wq) {
@@ -1858,7 +1862,7 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   }
   int blocks = (nitems + TW - 1) / TW;
   if (blocks > nsm) blocks = nsm;
-  k_trunc_warp<<<blocks, TW * 32, NSLOT * SLOT * 8, st>>>(a, nitems, bigq, bigcount);
+  CK_PDL(launch_pdl(k_trunc_warp, dim3(blocks), dim3(TW * 32), NSLOT * SLOT * 8, st, a, nitems, bigq, bigcount));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !may_big) return e;
   // queues of oversized tasks, split by each task's own work area: two
@@ -1869,13 +1873,13 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
     TruncArgs ah = a;
     ah.smem_doubles = QHALF_D;
     const int bb = nitems < 2 * nsm ? nitems : 2 * nsm;
-    k_trunc_big<256><<<bb, 256, QHALF, st>>>(ah, bigq, bigcount, nitems);
+    CK_PDL(launch_pdl(k_trunc_big<256>, dim3(bb), dim3(256), QHALF, st, ah, bigq, bigcount, nitems));
   }
   if (bsm > QHALF) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int bb = nitems < nsm ? nitems : nsm;
-    k_trunc_big<512><<<bb, 512, bsm, st>>>(a, bigq + nitems, bigcount + 1, nitems);
+    CK_PDL(launch_pdl(k_trunc_big<512>, dim3(bb), dim3(512), bsm, st, a, bigq + nitems, bigcount + 1, nitems));
   }
   return cudaGetLastError();
 }
