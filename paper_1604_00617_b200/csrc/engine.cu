@@ -1077,7 +1077,19 @@ struct Plan {
       j.nA = nA1;
       j.nB = ht.startB[nn] - ht.startB[1];
     }
-    hmat(J, 2, G, st);
+    if (diag) {
+      // level 0: one operand is an exact diagonal with rank-0 factors.  The
+      // job with the diagonal operand as H is a row scaling; the other one
+      // has no columns (rank 0) and is skipped (M2 passes the other operand
+      // through, algebra.py:93-96)
+      kbegin(3);
+      CK(launch_hmat_diag(dt.T, J[diag == 1 ? 0 : 1], G, st));
+      kend();
+      ++launches;
+      if (prof_on) CK(launch_census_hmat(dt.T, &J[diag == 1 ? 0 : 1], 1, G, ctrp(), st));
+    } else {
+      hmat(J, 2, G, st);
+    }
     // M2: off12 = combine(f1, f2), off21 = combine(g1, g2)
     TruncArgs a;
     memset(&a, 0, sizeof(a));

@@ -452,6 +452,42 @@ __global__ void __launch_bounds__(NTB) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int pat
   }
 }
 
+// HODLR x panel with a DIAGONAL HODLR operand (level 0: E, F lifted from the
+// bands, diagonal leaves, rank-0 factors): every subtree product reduces to a
+// row scaling, Y[slot(mu)][:, rows(mu)] = alpha diag(H) X[slot(mu)][:, rows(mu)],
+// for every root mu in [mu0, mu1) -- bitwise the dense leaf product (the
+// off-diagonal leaf entries are exact zeros and the factor terms vanish),
+// reading n diagonal values instead of the n x bw leaf panel.
+__global__ void k_hmat_diag(TreeDev T, MMJob J) {
+  ACR_PDL_ENTRY();
+  const int g = blockIdx.y, n = T.n, bw = T.bw;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const HB h = J.H[g];
+  // leaf of row i and the chain of nodes above it
+  int node = 0, path[17], np = 0;
+  while (!T.isleaf[node] && np < 16) {
+    path[np++] = node;
+    node = i < T.mid[node] ? T.c0[node] : T.c1[node];
+  }
+  path[np] = node;
+  const double d = h.leaf[(long long)i * bw + (i - T.lo[node])];
+  for (int q = 1; q <= np; ++q) {               // mu = path[q], slot = depth(parent)
+    const int mu = path[q];
+    if (mu < J.mu0 || mu >= J.mu1) continue;
+    const int c = mm_cols(J, T, g, mu);
+    const int slot = mm_slot(T, mu);
+    for (int b = 0; b < c; ++b)
+      src_col(J.Y, n, g, slot, b)[i] = J.alpha * (d * src_col(J.X, n, g, slot, b)[i]);
+  }
+}
+
+cudaError_t launch_hmat_diag(const TreeDev& T, const MMJob& job, int nelem, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  CK_PDL(launch_pdl(k_hmat_diag, dim3((T.n + 255) / 256, nelem), dim3(256), 0, st, T, job));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
                         int nelem, cudaStream_t st) {
   if (!nelem || !njobs) return cudaSuccess;
