@@ -1002,8 +1002,10 @@ struct Plan {
     double* tbY = scratch<double>(4, (size_t)G * std::max(nA1, 1) * RA * RB);
     double* tbZ = scratch<double>(5, (size_t)G * std::max(nA1, 1) * RA * RB);
     CK(cudaMemsetAsync(cr, 0, sizeof(int) * G * nn * 2, st));
-    // cross terms X11 = (U_A12 (V_A12^T U_B21), V_B21), X22 likewise
-    if (!ht.branches.empty()) {
+    // cross terms X11 = (U_A12 (V_A12^T U_B21), V_B21), X22 likewise (none
+    // when an operand is the level-0 diagonal: its factors have rank 0, the
+    // cross-term ranks stay 0 from the memset)
+    if (!ht.branches.empty() && !diag) {
       GPJob j[2];
       memset(j, 0, sizeof(j));
       for (int s = 0; s < 2; ++s) {
@@ -1097,8 +1099,9 @@ struct Plan {
     a.a = op_own(s_pan(Yp, ps * RB, RB), s_hbV(B), r_hb(B));
     a.b = op_own(s_hbU(A), s_pan(Zp, ps * RA, RA), r_hb(A));
     run_trunc(a, ht.startA[0], ht.startA[1], C, G, RB, RA);
-    // M3: ancestors' cross terms, parent first, root last
-    for (int t = 1; t < ht.nd; ++t) {
+    // M3: ancestors' cross terms, parent first, root last (all rank 0 with a
+    // diagonal operand: every combine would pass C through unchanged)
+    for (int t = 1; t < ht.nd && !diag; ++t) {
       int s0 = ht.startA[0];
       while (s0 < ht.startA[1] && ht.depth[ht.listA[s0 * 3 + 1]] < t) ++s0;
       if (s0 >= ht.startA[1]) break;
