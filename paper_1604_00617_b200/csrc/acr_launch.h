@@ -59,7 +59,7 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
 cudaError_t launch_hmat_diag(const TreeDev& T, const MMJob& job, int nelem, cudaStream_t st);
 cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
                       const int* nodes, int nnodes, int nelem, int kcap,
-                      cudaStream_t st);
+                      cudaStream_t st, int rxcap = 0, int rycap = 0);
 cudaError_t launch_rhs_combine(const double* f, long long fs, const double* a,
                                long long as, const double* b, long long bs,
                                double* out, long long os, int count, int len,

@@ -753,9 +753,10 @@ struct Plan {
     launches += 2;
     if (prof_on) CK(launch_census_hmat(dt.T, J, nj, G, ctrp(), s));
   }
-  void gp(const GPJob* J, int nj, const int* nodes, int nnodes, int G, int kcap, cudaStream_t s) {
+  void gp(const GPJob* J, int nj, const int* nodes, int nnodes, int G, int rxcap, int rycap,
+          cudaStream_t s) {
     kbegin(5);
-    CK(launch_gp(dt.T, J, nj, nodes, nnodes, G, kcap, s));
+    CK(launch_gp(dt.T, J, nj, nodes, nnodes, G, rxcap * rycap, s, rxcap, rycap));
     kend();
     ++launches;
     if (prof_on) CK(launch_census_gp(dt.T, J, nj, nodes, nnodes, G, ctrp(), s));
@@ -1022,7 +1023,7 @@ struct Plan {
       }
       j[0].hx = 1; j[0].hw = 0; j[0].sx = 0; j[0].sy = 1;
       j[1].hx = 0; j[1].hw = 1; j[1].sx = 1; j[1].sy = 0;
-      gp(j, 2, dt.d_branches, (int)ht.branches.size(), G, RA * RB, st);
+      gp(j, 2, dt.d_branches, (int)ht.branches.size(), G, RA, RB, st);
     }
     const cudaStream_t s2 = side();
     fork(s2);
@@ -1256,7 +1257,7 @@ struct Plan {
       j.W = s_hbU(c.H); j.hw = 1;
       j.Z = P3;
       j.alpha = -1.0;
-      gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st);
+      gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R, c.R, st);
     }
     const cudaStream_t s2 = side();
     {                                                  // S = H22 + W V12^T
@@ -1289,7 +1290,7 @@ struct Plan {
       j.W = P1; j.hw = 0;
       j.Z = P3;
       j.alpha = 1.0;
-      gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R * c.R, st);
+      gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R, c.R, st);
     }
     inv_lowrank(c, nu, a0, P3, P2, 1, s2);             // b11 = x11 + G Hh^T
     TruncArgs a;                                       // b12, b21 (independent of b11)

@@ -607,13 +607,143 @@ __global__ void __launch_bounds__(GT) k_gp(TreeDev T, GPJobs2 JJ, const int* nod
   if (J.orank && threadIdx.x == 0) J.orank[g * J.ors + nu * 2 + J.oside] = ry;
 }
 
+// K = X^T Y on the FP64 tensor pipe: the node's l1 rows split over the
+// warps, each warp accumulating every 8 x 8 tile of K with mma.sync m8n8k4
+// (A fragment = 8 columns of X at 4 rows, B = 8 columns of Y), the warps'
+// partial tiles summed in a fixed order through shared memory.  Every X / Y
+// element is read once (the scalar kernel re-read X for every column of Y
+// and paid a warp reduction per dot product).  Then Z = alpha W K as k_gp.
+// TMAX: tiles per side (ranks <= 8 TMAX).
+template <int NT, int TMAX>
+__global__ void __launch_bounds__(NT) k_gp_tc(TreeDev T, GPJobs2 JJ, const int* nodes) {
+  ACR_PDL_ENTRY();
+  extern __shared__ double smp[];
+  constexpr int NW = NT / 32;
+  const GPJob& J = JJ.j[blockIdx.z];
+  const int g = blockIdx.y, n = T.n;
+  const int nu = nodes[blockIdx.x];
+  const int rx = rank_base(J.rx, g)[nu * 2 + J.sx];
+  const int ry = rank_base(J.ry, g)[nu * 2 + J.sy];
+  if (!rx || !ry) {
+    if (J.orank && threadIdx.x == 0) J.orank[g * J.ors + nu * 2 + J.oside] = 0;
+    return;
+  }
+  const int lo = T.lo[nu], hi = T.hi[nu], mid = T.mid[nu];
+  const int slot = T.depth[nu];
+  const int r1 = J.hx ? mid : lo, l1 = J.hx ? hi - mid : mid - lo;
+  const int r2 = J.hw ? mid : lo, l2 = J.hw ? hi - mid : mid - lo;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = lane >> 2, ti = lane & 3;
+  const int ta = (rx + 7) >> 3, tb = (ry + 7) >> 3;
+  double acc[TMAX][TMAX][2];
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+    for (int b = 0; b < TMAX; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // this warp's rows: chunks of 4 rows, interleaved across warps
+  const double* xc[TMAX];
+  const double* yc[TMAX];
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a) {
+    const int ca = a * 8 + gi;
+    xc[a] = (a < ta && ca < rx) ? src_col(J.X, n, g, slot, ca) + r1 : nullptr;
+    yc[a] = (a < tb && ca < ry) ? src_col(J.Y, n, g, slot, ca) + r1 : nullptr;
+  }
+  for (int k0 = warp * 4; k0 < l1; k0 += NW * 4) {
+    const int k = k0 + ti;
+    double av[TMAX], bv[TMAX];
+#pragma unroll
+    for (int a = 0; a < TMAX; ++a) {
+      av[a] = (xc[a] && k < l1) ? xc[a][k] : 0.0;
+      bv[a] = (yc[a] && k < l1) ? yc[a][k] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+      for (int b = 0; b < TMAX; ++b)
+        if (a < ta && b < tb)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+                       "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1]) : "d"(av[a]), "d"(bv[b]));
+  }
+  // partial tiles -> smem [warp][a][b][64], then K[a][b] summed over warps in order
+  double* part = smp;
+  double* K = smp + (size_t)NW * TMAX * TMAX * 64;
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+    for (int b = 0; b < TMAX; ++b)
+      if (a < ta && b < tb) {
+        double* pt = part + (((size_t)warp * TMAX + a) * TMAX + b) * 64;
+        pt[gi * 8 + 2 * ti] = acc[a][b][0];
+        pt[gi * 8 + 2 * ti + 1] = acc[a][b][1];
+      }
+  __syncthreads();
+  for (int e = threadIdx.x; e < rx * ry; e += NT) {
+    const int x = e / ry, y = e - x * ry;
+    const int a = x >> 3, b = y >> 3, off = (x & 7) * 8 + (y & 7);
+    double sacc = 0.0;
+    for (int w = 0; w < NW; ++w) sacc += part[(((size_t)w * TMAX + a) * TMAX + b) * 64 + off];
+    K[e] = sacc;
+  }
+  __syncthreads();
+  // Z = alpha W K: thread per output row, W row in registers (8 at a time)
+  for (int i = threadIdx.x; i < l2; i += NT) {
+    for (int b0 = 0; b0 < ry; b0 += 8) {
+      const int nb = ry - b0 < 8 ? ry - b0 : 8;
+      double z[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) z[q] = 0.0;
+      for (int a = 0; a < rx; ++a) {
+        const double w = src_col(J.W, n, g, slot, a)[r2 + i];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < nb) z[q] += w * K[a * ry + b0 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nb) src_col(J.Z, n, g, slot, b0 + q)[r2 + i] = J.alpha * z[q];
+    }
+  }
+  if (J.orank && threadIdx.x == 0) J.orank[g * J.ors + nu * 2 + J.oside] = ry;
+}
+
 cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
                       const int* nodes, int nnodes, int nelem, int kcap,
-                      cudaStream_t st) {
+                      cudaStream_t st, int rxcap, int rycap) {
   if (!nelem || !njobs || !nnodes) return cudaSuccess;
   GPJobs2 JJ;
   JJ.j[0] = jobs[0];
   JJ.j[1] = njobs > 1 ? jobs[1] : jobs[0];
+  static const bool tc_off = getenv("ACR_GP_SCALAR") != nullptr;   // A/B aid
+  const int tmax = ((rxcap > rycap ? rxcap : rycap) + 7) / 8;
+  if (!tc_off && rxcap > 0 && tmax <= 4) {
+    const bool small = (long long)nnodes * nelem * njobs < 148LL * 4;
+    const int nw = small ? 8 : 4;
+    const int tm = tmax <= 1 ? 1 : tmax <= 2 ? 2 : 4;
+    const size_t smem = ((size_t)nw * tm * tm * 64 + (size_t)rxcap * rycap) * 8;
+    static bool attr_tc = false;
+    if (!attr_tc) {
+      cudaFuncSetAttribute(k_gp_tc<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_tc = true;
+    }
+    dim3 g(nnodes, nelem, njobs);
+    if (small) {
+      if (tm == 1) CK_PDL(launch_pdl(k_gp_tc<256, 1>, g, dim3(256), smem, st, T, JJ, nodes));
+      else if (tm == 2) CK_PDL(launch_pdl(k_gp_tc<256, 2>, g, dim3(256), smem, st, T, JJ, nodes));
+      else CK_PDL(launch_pdl(k_gp_tc<256, 4>, g, dim3(256), smem, st, T, JJ, nodes));
+    } else {
+      if (tm == 1) CK_PDL(launch_pdl(k_gp_tc<128, 1>, g, dim3(128), smem, st, T, JJ, nodes));
+      else if (tm == 2) CK_PDL(launch_pdl(k_gp_tc<128, 2>, g, dim3(128), smem, st, T, JJ, nodes));
+      else CK_PDL(launch_pdl(k_gp_tc<128, 4>, g, dim3(128), smem, st, T, JJ, nodes));
+    }
+    return cudaGetLastError();
+  }
   size_t smem = (size_t)kcap * 8;
   static bool attr = false;
   if (!attr) {
