@@ -105,6 +105,93 @@ __global__ void __launch_bounds__(HT) k_hmatA(TreeDev T, MMJobs2 JJ) {
   }
 }
 
+// Phase A on the FP64 tensor pipe: t = F^T X (r x c) over the node's rows,
+// rows split over the warps, every 8 x 8 tile of t accumulated with
+// mma.sync m8n8k4, the warps' partial tiles summed in a fixed order through
+// shared memory (same structure as k_gp_tc).  TMAX: tiles per side.
+template <int NT, int TMAX>
+__global__ void __launch_bounds__(NT) k_hmatA_tc(TreeDev T, MMJobs2 JJ) {
+  ACR_PDL_ENTRY();
+  constexpr int NW = NT / 32;
+  __shared__ double part[NW * TMAX * TMAX * 64];
+  const MMJob& J = JJ.j[blockIdx.z];
+  if ((int)blockIdx.x >= J.nA) return;
+  const int g = blockIdx.y, n = T.n;
+  const int e0 = T.startA[J.mu0];
+  const int* ent = T.listA + (e0 + blockIdx.x) * 3;
+  const int mu = ent[0], beta = ent[1], side = ent[2];
+  const int c = mm_cols(J, T, g, mu);
+  if (!c) return;
+  const HB h = J.H[g];
+  const int r = h.rk[beta * 2 + side];
+  if (!r) return;
+  const int lo = T.lo[beta], hi = T.hi[beta], mid = T.mid[beta];
+  int row, len;
+  const double* F;
+  const long long fs = (long long)T.depth[beta] * h.R * n;
+  if (!J.trans) {
+    row = side ? lo : mid;
+    len = side ? mid - lo : hi - mid;
+    F = h.V + fs + row;
+  } else {
+    row = side ? mid : lo;
+    len = side ? hi - mid : mid - lo;
+    F = h.U + fs + row;
+  }
+  const double* X = src_col(J.X, n, g, mm_slot(T, mu), 0) + row;
+  double* t = J.tbuf + ((long long)g * J.nA + blockIdx.x) * J.RT * J.CT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = lane >> 2, ti = lane & 3;
+  const int ta = (r + 7) >> 3, tb = (c + 7) >> 3;
+  double acc[TMAX][TMAX][2];
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+    for (int b = 0; b < TMAX; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const double* fc[TMAX];
+  const double* xc[TMAX];
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a) {
+    const int ca = a * 8 + gi;
+    fc[a] = (a < ta && ca < r) ? F + (long long)ca * n : nullptr;
+    xc[a] = (a < tb && ca < c) ? X + (long long)ca * n : nullptr;
+  }
+  for (int k0 = warp * 4; k0 < len; k0 += NW * 4) {
+    const int k = k0 + ti;
+    double av[TMAX], bv[TMAX];
+#pragma unroll
+    for (int a = 0; a < TMAX; ++a) {
+      av[a] = (fc[a] && k < len) ? fc[a][k] : 0.0;
+      bv[a] = (xc[a] && k < len) ? xc[a][k] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+      for (int b = 0; b < TMAX; ++b)
+        if (a < ta && b < tb)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+                       "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1]) : "d"(av[a]), "d"(bv[b]));
+  }
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+    for (int b = 0; b < TMAX; ++b)
+      if (a < ta && b < tb) {
+        double* pt = part + ((warp * TMAX + a) * TMAX + b) * 64;
+        pt[gi * 8 + 2 * ti] = acc[a][b][0];
+        pt[gi * 8 + 2 * ti + 1] = acc[a][b][1];
+      }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * c; e += NT) {
+    const int x = e / c, y = e - x * c;
+    const int a = x >> 3, b = y >> 3, off = (x & 7) * 8 + (y & 7);
+    double sacc = 0.0;
+    for (int w = 0; w < NW; ++w) sacc += part[((w * TMAX + a) * TMAX + b) * 64 + off];
+    t[x * J.CT + y] = sacc;
+  }
+}
+
 // Fallback phase B (trees deeper than 16; k_hmatB_sm below is the main path).
 // Register tile of phase B: one thread = one leaf row i x HB_CB columns of
 // one subtree root.  The leaf row and every ancestor U (V) row element are
@@ -500,9 +587,17 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     nB = jobs[k].nB > nB ? jobs[k].nB : nB;
     cmax = jobs[k].CT > cmax ? jobs[k].CT : cmax;
   }
+  int rtmax = 0;
+  for (int k = 0; k < njobs; ++k) rtmax = jobs[k].RT > rtmax ? jobs[k].RT : rtmax;
   if (nA > 0) {
     dim3 g(nA, nelem, njobs);
-    if (nelem <= 32) CK_PDL(launch_pdl(k_hmatA<true>, dim3(g), dim3(HT), 0, st, T, JJ));
+    static const bool tc_off = getenv("ACR_HMATA_SCALAR") != nullptr;   // A/B aid
+    const int tmax = ((rtmax > cmax ? rtmax : cmax) + 7) / 8;
+    if (!tc_off && tmax <= 4) {
+      if (tmax <= 1) CK_PDL(launch_pdl(k_hmatA_tc<128, 1>, g, dim3(128), 0, st, T, JJ));
+      else if (tmax <= 2) CK_PDL(launch_pdl(k_hmatA_tc<128, 2>, g, dim3(128), 0, st, T, JJ));
+      else CK_PDL(launch_pdl(k_hmatA_tc<128, 4>, g, dim3(128), 0, st, T, JJ));
+    } else if (nelem <= 32) CK_PDL(launch_pdl(k_hmatA<true>, dim3(g), dim3(HT), 0, st, T, JJ));
     else CK_PDL(launch_pdl(k_hmatA<false>, dim3(g), dim3(HT), 0, st, T, JJ));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
