@@ -291,40 +291,19 @@ __global__ void __launch_bounds__((S / TR) * (S / TC), MINB) k_leafinv_v2(TreeDe
 // ---------------------------------------------------------------------------
 static constexpr int BGJ_LD = 68;       // padded row stride (doubles)
 
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H, int leaf,
-                                                         int* sing) {
-  ACR_PDL_ENTRY();
-  constexpr int NW = NT / 32;
-  __shared__ __align__(16) double X[64 * BGJ_LD];
-  __shared__ __align__(16) double Tb[8 * BGJ_LD];
-  __shared__ int piv[64], kpos[64], pflag[64];
-  __shared__ int s_bad;
-  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
-  double* L = H[g].leaf + (long long)lo * bw;
-  for (int idx = tid; idx < 64 * 64; idx += NT) {
-    const int r = idx >> 6, c = idx & 63;
-    X[r * BGJ_LD + c] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
-  }
-  if (tid < 64) pflag[tid] = -1;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  unsigned used = 0;                        // warp 0: bit h = row lane + 32 h pivoted
-  const int gi = lane >> 2, ti = lane & 3;
-  for (int pb = 0; pb * 8 < s; ++pb) {
-    const int k0 = pb * 8;
-    // ---- 1. panel: 8 unblocked GJ steps by warp 0 ----
-    if (warp == 0) {
+// one 8-column panel of unblocked Gauss-Jordan steps by one warp (see above)
+__device__ __forceinline__ void bgj_panel(double* X, int pq, int s, int lane, unsigned& used,
+                                          int* piv, int* pflag, int* s_bad) {
+  const int kq = pq * 8;
       double x[2][8];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) x[h][c] = X[(lane + 32 * h) * BGJ_LD + k0 + c];
+        for (int c = 0; c < 8; ++c) x[h][c] = X[(lane + 32 * h) * BGJ_LD + kq + c];
       bool bad = false;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        if (k0 + t < s && !bad) {
+        if (kq + t < s && !bad) {
           // warp argmax of |x| over the unused rows, first index on ties, by
           // integer warp reductions on the bit pattern (monotone for
           // non-negative doubles): max of the high words, then of the low
@@ -366,8 +345,8 @@ __global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H
             }
             if (lane == lp) used |= 1u << hp;
             if (lane == 0) {
-              piv[k0 + t] = pi;
-              pflag[pi] = pb;
+              piv[kq + t] = pi;
+              pflag[pi] = pq;
             }
           }
         }
@@ -375,36 +354,81 @@ __global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) X[(lane + 32 * h) * BGJ_LD + k0 + c] = x[h][c];
-      if (bad && lane == 0) s_bad = 1;
+        for (int c = 0; c < 8; ++c) X[(lane + 32 * h) * BGJ_LD + kq + c] = x[h][c];
+      if (bad && lane == 0) *s_bad = 1;
     }
-    __syncthreads();
-    if (s_bad) break;                        // uniform
-    // ---- 2. T = pivot rows of the other columns ----
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H, int leaf,
+                                                         int* sing) {
+  ACR_PDL_ENTRY();
+  constexpr int NW = NT / 32;
+  __shared__ __align__(16) double X[64 * BGJ_LD];
+  __shared__ __align__(16) double Tb[8 * BGJ_LD];
+  __shared__ int piv[64], kpos[64], pflag[64];
+  __shared__ int s_bad;
+  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
+  double* L = H[g].leaf + (long long)lo * bw;
+  for (int idx = tid; idx < 64 * 64; idx += NT) {
+    const int r = idx >> 6, c = idx & 63;
+    X[r * BGJ_LD + c] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
+  }
+  if (tid < 64) pflag[tid] = -1;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  unsigned used = 0;                        // warp 0: bit h = row lane + 32 h pivoted
+  const int gi = lane >> 2, ti = lane & 3;
+  const int npan = (s + 7) / 8;
+  if (warp == 0) bgj_panel(X, 0, s, lane, used, piv, pflag, &s_bad);
+  __syncthreads();
+  for (int pb = 0; pb < npan && !s_bad; ++pb) {
+    const int k0 = pb * 8;
+    // ---- T = pivot rows of panel pb in every other column ----
     const int np = s - k0 < 8 ? s - k0 : 8;
     for (int idx = tid; idx < 8 * 64; idx += NT) {
       const int t = idx >> 6, c = idx & 63;
       Tb[t * BGJ_LD + c] = t < np ? X[piv[k0 + t] * BGJ_LD + c] : 0.0;
     }
     __syncthreads();
-    // ---- 3. rank-8 update of every other tile on DMMA ----
-    for (int tl = warp; tl < 64; tl += NW) {
-      const int rb = tl >> 3, cb = tl & 7;
-      if (cb == pb) continue;
+    // rank-8 update of tile (rb, cb) on DMMA: X <- (X, panel pb's pivot rows
+    // zeroed) + P T
+    auto upd = [&](int rb, int cb) {
       const int r = rb * 8 + gi, c = cb * 8 + 2 * ti;
       const bool zr = pflag[r] == pb;
       double d0 = zr ? 0.0 : X[r * BGJ_LD + c];
       double d1 = zr ? 0.0 : X[r * BGJ_LD + c + 1];
 #pragma unroll
       for (int kk = 0; kk < 8; kk += 4) {
-        const double a = X[r * BGJ_LD + k0 + kk + ti];
-        const double b = Tb[(kk + ti) * BGJ_LD + cb * 8 + gi];
+        const double av = X[r * BGJ_LD + k0 + kk + ti];
+        const double bv = Tb[(kk + ti) * BGJ_LD + cb * 8 + gi];
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
                      "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
-                     : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+                     : "+d"(d0), "+d"(d1) : "d"(av), "d"(bv));
       }
       X[r * BGJ_LD + c] = d0;
       X[r * BGJ_LD + c + 1] = d1;
+    };
+    if (pb + 1 < npan && NW == 8) {
+      // look-ahead: the next panel's column block first (one tile per warp),
+      // then warp 0 factors panel pb + 1 while the other warps update the rest
+      upd(warp, pb + 1);
+      __syncthreads();
+      if (warp == 0) {
+        bgj_panel(X, pb + 1, s, lane, used, piv, pflag, &s_bad);
+      } else {
+        for (int tl = warp - 1; tl < 64; tl += NW - 1) {
+          const int rb = tl >> 3, cb = tl & 7;
+          if (cb != pb && cb != pb + 1) upd(rb, cb);
+        }
+      }
+    } else {
+      for (int tl = warp; tl < 64; tl += NW) {
+        const int rb = tl >> 3, cb = tl & 7;
+        if (cb != pb) upd(rb, cb);
+      }
+      __syncthreads();
+      if (pb + 1 < npan && warp == 0) bgj_panel(X, pb + 1, s, lane, used, piv, pflag, &s_bad);
     }
     __syncthreads();
   }
