@@ -71,6 +71,9 @@ cudaError_t launch_census_hmat(const TreeDev& T, const MMJob* jobs, int njobs, i
                                unsigned long long* ctr, cudaStream_t st);
 cudaError_t launch_census_gp(const TreeDev& T, const GPJob* jobs, int njobs, const int* nodes,
                              int nnodes, int nelem, unsigned long long* ctr, cudaStream_t st);
+cudaError_t launch_rank_stats(const int* rD, const int* rE, const int* rF, long long sr, int mm,
+                              const int* branches, int nbr, const int* depth, int nd,
+                              unsigned* out, cudaStream_t st);
 cudaError_t launch_census_leaflr(const TreeDev& T, RankRef rr, int node, int fside, int mu,
                                  int nelem, unsigned long long* ctr, cudaStream_t st);
 

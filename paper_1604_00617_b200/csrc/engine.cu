@@ -1304,7 +1304,8 @@ struct Plan {
   // ---- helpers for reports ----
   // n ints of the mapped staging buffer (grown only when nothing is pending)
   size_t hmap_take(size_t n) {
-    if (pend.empty()) hmap_used = 0;
+    // (space is reclaimed at the syncs that drain it: a stats_launch region
+    // stays valid until the stats_read after the next sync)
     if (hmap_used + n > hmap_cap) {
       if (!pend.empty()) sync_fetch();
       if (n > hmap_cap) {
@@ -1332,9 +1333,51 @@ struct Plan {
   // stream sync, then the fetched rank tables move to their host vectors
   void sync_fetch() {
     CK(cudaStreamSynchronize(st));
+    drain_fetch();
+  }
+
+  // the stream has been synchronised: fetched tables move to their vectors
+  void drain_fetch() {
     for (const Pend& p : pend) memcpy(p.out->data(), hmap + p.off, p.n * sizeof(int));
     pend.clear();
     hmap_used = 0;
+  }
+
+  // rank statistics of a level computed on the device (k_rank_stats) and
+  // copied into the mapped buffer; stats_read after the next stream sync.
+  // The per-level host round trip then moves 4 nd + 2 words instead of the
+  // three m x nnodes rank tables (whose host scan was the largest GPU idle
+  // gap at the top levels)
+  size_t stats_launch(const Level& L) {
+    const int nd = std::max(ht.nd, 1);
+    const size_t nw = 4 * (size_t)nd + 2;
+    unsigned* d = scratch<unsigned>(18, nw);
+    CK(cudaMemsetAsync(d, 0, nw * sizeof(unsigned), st));
+    CK(launch_rank_stats(L.D.rk.as<int>(), L.E.rk.as<int>(), L.F.rk.as<int>(), L.D.sr, L.m,
+                         dt.d_branches, (int)ht.branches.size(), dt.T.depth, nd, d, st));
+    const size_t off = hmap_take(nw);
+    CK(launch_copy_i32(hmap_d + off, reinterpret_cast<const int*>(d), (long long)nw, st));
+    launches += 2;
+    return off;
+  }
+
+  // profile (profile_level's semantics) and capacity max of stats_launch's output
+  int stats_read(size_t off, bool prof_it) {
+    const int nd = std::max(ht.nd, 1);
+    const unsigned* w = reinterpret_cast<const unsigned*>(hmap + off);
+    if (prof_it) {
+      Profile p;
+      p.mx.assign(ht.nd, 0);
+      p.mean.assign(ht.nd, 0.0);
+      for (int d = 0; d < ht.nd; ++d) {
+        unsigned long long sum;
+        memcpy(&sum, w + 2 * nd + 2 + 2 * d, sizeof(sum));
+        p.mx[d] = (int)w[d];
+        p.mean[d] = w[nd + d] ? (double)(long long)sum / (double)(long long)w[nd + d] : 0.0;
+      }
+      prof.push_back(p);
+    }
+    return std::max((int)w[2 * nd], 1);
   }
 
   long long hb_bytes(const int* rk) const {
@@ -1353,31 +1396,6 @@ struct Plan {
     for (size_t b = 0; b + per <= r.size(); b += per)
       for (int v : ht.branches) mx = std::max({mx, r[b + v * 2], r[b + v * 2 + 1]});
     return mx;
-  }
-
-  void profile_level(int mm, const std::vector<int>& dR, const std::vector<int>& eR,
-                     const std::vector<int>& fR) {
-    Profile p;
-    int nd = ht.nd;
-    p.mx.assign(nd, 0);
-    std::vector<long long> sum(nd, 0), cnt(nd, 0);
-    auto acc = [&](const std::vector<int>& r, int blk) {
-      const int* rk = r.data() + (size_t)blk * ht.nnodes * 2;
-      for (int v : ht.branches) {
-        int d = ht.depth[v];
-        for (int s = 0; s < 2; ++s) {
-          p.mx[d] = std::max(p.mx[d], rk[v * 2 + s]);
-          sum[d] += rk[v * 2 + s];
-          cnt[d] += 1;
-        }
-      }
-    };
-    for (int i = 0; i < mm; ++i) acc(dR, i);
-    for (int i = 1; i < mm; ++i) acc(eR, i);
-    for (int i = 0; i + 1 < mm; ++i) acc(fR, i);
-    p.mean.assign(nd, 0.0);
-    for (int d = 0; d < nd; ++d) p.mean[d] = cnt[d] ? (double)sum[d] / (double)cnt[d] : 0.0;
-    prof.push_back(p);
   }
 
   Batch clone(const Batch& b) {
@@ -1431,7 +1449,8 @@ struct Plan {
   // Local window [first, first+m) of a global level of mg blocks; the last
   // local odd block takes {Dinv, E, F} of the right neighbour's first block.
   bool reduce(Level& L, int Rout, int lvl, int order, Level& nx, Record& rec,
-              int& need, bool dlev, const int* perm = nullptr, bool keep_input = false) {
+              int& need, bool dlev, const int* perm = nullptr, bool keep_input = false,
+              size_t* stats_off = nullptr) {
     const int mm = L.m, first = L.first, mg = L.mg, ne = (mm + 1) / 2, no = mm / 2;
     const bool right = first + mm < mg;
     int nq = 0, nq_loc = 0, nq_h = 0, nf = 0, nf_loc = 0, nf_h = 0;
@@ -1554,6 +1573,7 @@ struct Plan {
     int h_ovf = 0;
     std::vector<int> hs(std::max(ne, 1));
     {
+      if (stats_off) *stats_off = stats_launch(nx);
       const size_t off = hmap_take((size_t)ne + 1);
       CK(launch_copy_i32(hmap_d + off, ovf.as<int>(), 1, st));
       CK(launch_copy_i32(hmap_d + off + 1, sg, (long long)ne, st));
@@ -1723,12 +1743,9 @@ struct Plan {
     int lvl = 0;
     bool alive = true;
     auto ranks_of = [&](bool prof_it) {
-      fetch_ranks(L.D, dR);
-      fetch_ranks(L.E, eR);
-      fetch_ranks(L.F, fR);
+      const size_t off = stats_launch(L);
       sync_fetch();
-      if (prof_it) profile_level(L.m, dR, eR, fR);
-      maxr = std::max({max_rank_of(dR), max_rank_of(eR), max_rank_of(fR), 1});
+      maxr = stats_read(off, prof_it);
     };
     ranks_of(true);
     while (true) {
@@ -1752,22 +1769,21 @@ struct Plan {
       Level nx;
       int need = 0;
       int tries = 0;
-      while (!reduce(L, Rout, lvl, order, nx, rec, need, dlev)) {
+      size_t soff = 0;
+      while (!reduce(L, Rout, lvl, order, nx, rec, need, dlev, nullptr, false, &soff)) {
         Rout = std::max(need, 2 * Rout);
         rec = Record();
         nx = Level();
         if (++tries > 8) throw InternalError("rank capacity retries exhausted");
       }
-      // the fetched rank tables land in rec's / dR.. host vectors at the sync:
-      // sync before rec moves into recs
-      fetch_ranks(rec.Dinv, rec.hDinv);
-      fetch_ranks(rec.E, rec.hE);
-      fetch_ranks(rec.F, rec.hF);
+      // the record's host rank tables (storage accounting) are fetched
+      // lazily by storage_bytes; the next level's statistics came back with
+      // reduce's one sync
+      maxr = stats_read(soff, true);
       if (keep_levels) kept.push_back(std::move(L));
       L = std::move(nx);
       ++lvl;
       L.lvl = lvl;
-      ranks_of(true);
       recs.push_back(std::move(rec));
       // the forward sweep starts FWD_LAG levels behind: the first levels are
       // throughput-bound and a concurrent sweep would only compete for the
@@ -1793,7 +1809,11 @@ struct Plan {
       factored = true;
       return;
     }
-    lastR = {dR, eR, fR};
+    // the final level's full rank tables (storage accounting), drained at
+    // the end-of-factor sync
+    fetch_ranks(L.D, dR);
+    fetch_ranks(L.E, eR);
+    fetch_ranks(L.F, fR);
     // cutoff: dense LU of the remaining system
     const int mc = L.m;
     Nc = mc * n;
@@ -1828,6 +1848,8 @@ struct Plan {
       if (fused) fwd_end();
       CK(cudaEventRecord(ev1, st));
       CK(cudaStreamSynchronize(st));
+      drain_fetch();
+      lastR = {dR, eR, fR};
       if (hinfo) throw SingularError("matrix is singular to working precision");
     }
     float ms = 0;
@@ -2350,7 +2372,26 @@ struct Plan {
     throw ArgError("level not retained (set option 1 before acr_factor)");
   }
 
-  long long storage_bytes(int k) const {
+  // the records' host rank tables, fetched on first use (the factor no
+  // longer copies them out level by level)
+  void ensure_rec_ranks() {
+    bool any = false;
+    for (auto& r : recs) {
+      const std::pair<const Batch*, std::vector<int>*> t[3] = {
+          {&r.Dinv, &r.hDinv}, {&r.E, &r.hE}, {&r.F, &r.hF}};
+      for (auto& x : t) {
+        if (!x.second->empty() || x.first->cnt <= 0) continue;
+        x.second->resize((size_t)x.first->cnt * ht.nnodes * 2);
+        CK(cudaMemcpyAsync(x.second->data(), x.first->rk.p, sizeof(int) * x.second->size(),
+                           cudaMemcpyDeviceToHost, st));
+        any = true;
+      }
+    }
+    if (any) CK(cudaStreamSynchronize(st));
+  }
+
+  long long storage_bytes(int k) {
+    ensure_rec_ranks();
     long long s = 0;
     const long long seg = 8LL * n * k;
     for (auto& r : recs) {

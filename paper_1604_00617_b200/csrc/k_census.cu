@@ -12,6 +12,8 @@
 //   low-rank leaf update (k_leaflr): per leaf (s rows) of rank r
 //     leaf_add_uvT  2 s^2 r + s^2 FLOP, 8 (2 s^2 + 2 s r) B
 // Counter slots: [150]/[151] hmat FLOP/B, [152]/[153] gp, [154]/[155] leaflr.
+#include <algorithm>
+
 #include "acr_types.cuh"
 #include "acr_launch.h"
 
@@ -138,6 +140,69 @@ cudaError_t launch_census_leaflr(const TreeDev& T, RankRef rr, int node, int fsi
                                  int nelem, unsigned long long* ctr, cudaStream_t st) {
   if (!ctr || !nelem) return cudaSuccess;
   k_census_leaflr<<<(nelem + 127) / 128, 128, 0, st>>>(T, rr, node, fside, mu, nelem, ctr);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Rank statistics of one level (the host's profile_level / max_rank_of,
+// reference algebra.py:272-291, computed where the rank tables live so the
+// per-level host round trip moves nd numbers instead of three m x nnodes
+// tables).  Blocks of D (all), E (i >= 1) and F (i <= m-2) are profiled,
+// both sides of every branch node, bucketed by depth; the capacity maximum
+// runs over every block and side.  out (zeroed by the caller):
+//   u32 [0, nd) max, [nd, 2 nd) count, [2 nd] capacity max, [2 nd + 1] pad,
+//   u64 sums at u32 offset 2 nd + 2.
+// ---------------------------------------------------------------------------
+__global__ void k_rank_stats(const int* rD, const int* rE, const int* rF, long long sr, int mm,
+                             const int* branches, int nbr, const int* depth, int nd,
+                             unsigned* out) {
+  __shared__ unsigned smax[64], scnt[64];
+  __shared__ unsigned long long ssum[64];
+  __shared__ unsigned sg;
+  for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+    smax[d] = 0;
+    scnt[d] = 0;
+    ssum[d] = 0;
+  }
+  if (threadIdx.x == 0) sg = 0;
+  __syncthreads();
+  const long long per = (long long)mm * nbr, tot = 3 * per;
+  unsigned gmax = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int tb = (int)(t / per);
+    const long long rem = t - tb * per;
+    const int i = (int)(rem / nbr), v = branches[rem - (long long)i * nbr];
+    const int* rk = (tb == 0 ? rD : tb == 1 ? rE : rF) + (long long)i * sr + 2 * v;
+    const unsigned r0 = (unsigned)rk[0], r1 = (unsigned)rk[1];
+    gmax = max(gmax, max(r0, r1));
+    if (tb == 0 || (tb == 1 && i >= 1) || (tb == 2 && i + 1 < mm)) {
+      const int d = depth[v];
+      atomicMax(&smax[d], max(r0, r1));
+      atomicAdd(&scnt[d], 2u);
+      atomicAdd(&ssum[d], (unsigned long long)(r0 + r1));
+    }
+  }
+  atomicMax(&sg, gmax);
+  __syncthreads();
+  unsigned long long* osum = reinterpret_cast<unsigned long long*>(out + 2 * nd + 2);
+  for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+    if (!scnt[d]) continue;
+    atomicMax(out + d, smax[d]);
+    atomicAdd(out + nd + d, scnt[d]);
+    atomicAdd(osum + d, ssum[d]);
+  }
+  if (threadIdx.x == 0) atomicMax(out + 2 * nd, sg);
+}
+
+cudaError_t launch_rank_stats(const int* rD, const int* rE, const int* rF, long long sr, int mm,
+                              const int* branches, int nbr, const int* depth, int nd,
+                              unsigned* out, cudaStream_t st) {
+  if (nd > 64) return cudaErrorInvalidValue;
+  const long long tot = 3LL * mm * nbr;
+  if (tot <= 0) return cudaSuccess;
+  const int grid = (int)std::min<long long>((tot + 255) / 256, 148);
+  k_rank_stats<<<grid, 256, 0, st>>>(rD, rE, rF, sr, mm, branches, nbr, depth, nd, out);
   return cudaGetLastError();
 }
 
