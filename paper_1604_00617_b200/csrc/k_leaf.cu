@@ -370,9 +370,21 @@ __global__ void __launch_bounds__(NT, MINB) k_leafinv_bgj(TreeDev T, const HB* H
   const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = T.lo[leaf], s = T.hi[leaf] - lo, bw = T.bw;
   double* L = H[g].leaf + (long long)lo * bw;
-  for (int idx = tid; idx < 64 * 64; idx += NT) {
-    const int r = idx >> 6, c = idx & 63;
-    X[r * BGJ_LD + c] = (r < s && c < s) ? L[(long long)r * bw + c] : 0.0;
+  {
+    // every load of a thread in flight before the first shared store (a
+    // load-store loop kept one global round trip per element on the chain)
+    constexpr int PT = 64 * 64 / NT;
+    double v[PT];
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int idx = tid + u * NT, r = idx >> 6, c = idx & 63;
+      v[u] = (r < s && c < s) ? __ldg(L + (long long)r * bw + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int idx = tid + u * NT;
+      X[(idx >> 6) * BGJ_LD + (idx & 63)] = v[u];
+    }
   }
   if (tid < 64) pflag[tid] = -1;
   if (tid == 0) s_bad = 0;

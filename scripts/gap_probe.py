@@ -48,3 +48,13 @@ for lo, hi in ((0, 2), (2, 5), (5, 10), (10, 50), (50, 1e9)):
 big = sorted(((gaps[i], i) for i in range(len(gaps))), reverse=True)[:10]
 for x, i in big:
     print(f"gap {x:8.1f} us at {where[i][2]} ms: after {where[i][0]} before {where[i][1]}")
+# kernel time by name (concurrent kernels both count)
+from collections import defaultdict
+tot, cnt = defaultdict(float), defaultdict(int)
+for a, b, nm in iv:
+    k = nm.split("(")[0][:48]
+    tot[k] += b - a
+    cnt[k] += 1
+print("kernel totals:")
+for k in sorted(tot, key=lambda x: -tot[x])[:24]:
+    print(f"  {k:48s} n={cnt[k]:5d} ms={tot[k]/1e3:8.2f} avg_us={tot[k]/cnt[k]:8.1f}")
