@@ -12,8 +12,18 @@ int trunc_warp_pool_doubles();
 // to bigq and processed by a persistent block-level kernel (may_big)
 // direct: one 512-thread CTA per (task, element) -- small, latency-bound
 // launches; otherwise warp kernel, with oversized tasks queued to bigq
+// aux (required with may_big): cls = nitems bytes of device scratch for the
+// classification flags; q0 / q1 = streams for the two queue kernels, which
+// then run beside the warp kernel (events ef, ej0, ej1 order them around st);
+// null streams run the three kernels in turn on st
+struct TruncAux {
+  unsigned char* cls;
+  cudaStream_t q0, q1;
+  cudaEvent_t ef, ej0, ej1;
+};
 cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
-                         int* bigq, int* bigcount, cudaStream_t st);
+                         int* bigq, int* bigcount, cudaStream_t st,
+                         const TruncAux* aux = nullptr);
 int trunc_direct_max();
 long long warp_need_doubles(int um, int vm, int R);
 // CTA-pair (cluster of 2) recompression for direct launches of large tasks

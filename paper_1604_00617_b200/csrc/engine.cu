@@ -539,6 +539,16 @@ struct Plan {
       cudaEventDestroy(evfl);
       cudaEventDestroy(evfj);
     }
+    for (auto& qs : qstr)
+      if (qs.q0) {
+        cudaStreamSynchronize(qs.q0);
+        cudaStreamSynchronize(qs.q1);
+        cudaStreamDestroy(qs.q0);
+        cudaStreamDestroy(qs.q1);
+        cudaEventDestroy(qs.ef);
+        cudaEventDestroy(qs.ej0);
+        cudaEventDestroy(qs.ej1);
+      }
     if (stc) {
       cudaStreamSynchronize(stc);
       cudaStreamDestroy(stc);
@@ -547,6 +557,15 @@ struct Plan {
     }
     if (own_tp) delete tp;
   }
+
+  // streams of the recompression queue kernels (run beside the warp kernel),
+  // one set per launching stream (main / side)
+  struct QStreams {
+    cudaStream_t q0 = nullptr, q1 = nullptr;
+    cudaEvent_t ef = nullptr, ej0 = nullptr, ej1 = nullptr;
+  };
+  QStreams qstr[2];
+  bool no_qstreams = getenv("ACR_NO_QSTREAMS") != nullptr;   // development aid
 
   // second stream for independent launches at latency-bound levels (disabled
   // while instrumenting so per-class event timings stay on one stream)
@@ -905,7 +924,23 @@ struct Plan {
     }
     fork(s);
     kbegin(0);
-    CK(launch_trunc(a, nelem, direct, may_big, q, qc, s));
+    TruncAux aux;
+    memset(&aux, 0, sizeof(aux));
+    if (may_big) {
+      aux.cls = scratch<unsigned char>(alt ? 20 : 19, (size_t)nitems);
+      if (!prof_on && !no_qstreams) {          // instrumented runs keep one stream
+        QStreams& qs = qstr[alt ? 1 : 0];
+        if (!qs.q0) {
+          CK(cudaStreamCreateWithFlags(&qs.q0, cudaStreamNonBlocking));
+          CK(cudaStreamCreateWithFlags(&qs.q1, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&qs.ef, cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&qs.ej0, cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&qs.ej1, cudaEventDisableTiming));
+        }
+        aux.q0 = qs.q0; aux.q1 = qs.q1; aux.ef = qs.ef; aux.ej0 = qs.ej0; aux.ej1 = qs.ej1;
+      }
+    }
+    CK(launch_trunc(a, nelem, direct, may_big, q, qc, s, &aux));
     kend();
     launches += may_big ? ((long long)a.smem_doubles * 8 + 64 > 112 * 1024 ? 3 : 2) : 1;
     if (getenv("ACR_TDUMP")) tdump(a, t0, t1, out, nelem, direct, may_big);
@@ -2927,8 +2962,14 @@ int acr_truncate_factor(int m, int k, int R, const double* U, const double* V,
     if (g_trunc_path == 2 && acr::pair_need_doubles(std::max(m, k), Rc) <= 28416)
       CK(acr::launch_trunc_pair(a, 1, acr::pair_need_doubles(std::max(m, k), Rc), st));
     else
+    {
+      acr::Dev cl(16, st);
+      acr::TruncAux aux;
+      memset(&aux, 0, sizeof(aux));
+      aux.cls = cl.as<unsigned char>();
       CK(acr::launch_trunc(a, 1, g_trunc_path != 1, g_trunc_path == 1, q.as<int>(),
-                           qc.as<int>(), st));
+                           qc.as<int>(), st, &aux));
+    }
     int hr2[6];
     CK(cudaMemcpyAsync(hr2, rk.p, sizeof(hr2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -1713,8 +1713,45 @@ __device__ void trunc_warp_full(const TruncArgs& A, const TaskCtx& tc, double* w
   }
 }
 
+// Classification pass of a launch whose tasks may exceed the warp path (the
+// ranks, and so the work areas, are only known on the device): one thread per
+// item; large work areas, and cores above warp_rmax columns (a single warp's
+// Jacobi would walk whole column pairs per lane) go to the block-path queues
+// -- queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM),
+// queue 1 (stored from bigq + nitems): one 512-thread CTA per SM -- and are
+// flagged in cls so the warp kernel skips them.  The three kernels then run
+// concurrently on their own streams.
+__global__ void __launch_bounds__(256) k_trunc_classify(TruncArgs A, int nitems, int* bigq,
+                                                        int* bigcount, unsigned char* cls) {
+  ACR_PDL_ENTRY();
+  const int em = blockIdx.x * 256 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int which = -1;
+  if (em < nitems) {
+    const int task = em % A.ntasks, g = em / A.ntasks;
+    const TaskCtx tc = resolve_task(A, task, g);
+    if (task_is_full(A, tc)) {
+      const int R = tc.a.r + tc.b.r;
+      const long long need = warp_need_doubles(tc.um, tc.vm, R);
+      if (need > (long long)NSLOT * SLOT / 8 || R > A.warp_rmax || need > A.warp_maxneed)
+        which = trunc_need_doubles(tc.um, tc.vm, R) <= QHALF_D ? 0 : 1;
+    }
+    cls[em] = which >= 0 ? 1 : 0;
+  }
+  // warp-aggregated appends
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const unsigned m = __ballot_sync(FULL, which == k);
+    if (m == 0u) continue;
+    int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(bigcount + k, __popc(m));
+    base = __shfl_sync(FULL, base, __ffs(m) - 1);
+    if (which == k) bigq[(long long)k * nitems + base + __popc(m & ((1u << lane) - 1u))] = em;
+  }
+}
+
 __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nitems,
-                                                          int* bigq, int* bigcount) {
+                                                          const unsigned char* cls) {
   ACR_PDL_ENTRY();
   extern __shared__ double pool[];
   __shared__ unsigned long long mask;
@@ -1735,6 +1772,8 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     if (item >= nitems) break;
     const int task = A.task_major ? item / nelem : item % A.ntasks;
     const int g = A.task_major ? item - task * nelem : item / A.ntasks;
+    // tasks the classification pass sent to the block-path queues
+    if (cls != nullptr && cls[(long long)g * A.ntasks + task]) continue;
     TaskCtx tc = resolve_task(A, task, g);
     __syncwarp();
     const OpRes& a = tc.a;
@@ -1774,19 +1813,8 @@ __global__ void __launch_bounds__(TW * 32, 1) k_trunc_warp(TruncArgs A, int nite
     }
     const int R = a.r + b.r;
     const long long need = warp_need_doubles(tc.um, tc.vm, R);
-    // large work areas, and cores above 16 columns (a single warp's Jacobi
-    // would walk whole column pairs per lane): block path queues
-    if (need > (long long)NSLOT * SLOT / 8 ||
-        (bigq != nullptr && (R > A.warp_rmax || need > A.warp_maxneed))) {
-      // queue 0: work area fits a half-SM CTA (two 256-thread CTAs per SM);
-      // queue 1 (stored from bigq + nitems): one 512-thread CTA per SM
-      if (lane == 0) {   // queued as element-major items (k_trunc_big decodes so)
-        const int em = g * A.ntasks + task;
-        if (trunc_need_doubles(tc.um, tc.vm, R) <= QHALF_D)
-          bigq[atomicAdd(bigcount, 1)] = em;
-        else
-          bigq[nitems + atomicAdd(bigcount + 1, 1)] = em;
-      }
+    if (need > (long long)NSLOT * SLOT / 8) {   // cannot happen: sized by the host or classified
+      if (lane == 0) atomicMax(A.overflow, 1 << 29);
       continue;
     }
     const int ns = (int)((need + SLOT - 1) / SLOT);
@@ -1825,7 +1853,7 @@ void trunc_init_flags() {
 }
 
 cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_big,
-                         int* bigq, int* bigcount, cudaStream_t st) {
+                         int* bigq, int* bigcount, cudaStream_t st, const TruncAux* aux) {
   if (a.ntasks == 0 || nelem == 0) return cudaSuccess;
   static bool attr = false;
   static int nsm = 148;
@@ -1862,24 +1890,46 @@ cudaError_t launch_trunc(const TruncArgs& a, int nelem, bool direct, bool may_bi
   }
   int blocks = (nitems + TW - 1) / TW;
   if (blocks > nsm) blocks = nsm;
-  CK_PDL(launch_pdl(k_trunc_warp, dim3(blocks), dim3(TW * 32), NSLOT * SLOT * 8, st, a, nitems, bigq, bigcount));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || !may_big) return e;
-  // queues of oversized tasks, split by each task's own work area: two
-  // 256-thread CTAs per SM for those that fit half an SM's shared memory (one
-  // task's single-warp Jacobi overlaps the other's QR / output), one
-  // 512-thread CTA per SM for the rest
+  if (!may_big) {
+    CK_PDL(launch_pdl(k_trunc_warp, dim3(blocks), dim3(TW * 32), NSLOT * SLOT * 8, st, a, nitems,
+                      (const unsigned char*)nullptr));
+    return cudaGetLastError();
+  }
+  // Queued launch: classify, then the two block-path queue kernels and the
+  // warp kernel side by side (aux streams; without them, in turn on st).  The
+  // queue kernels go first: they hold the longest tasks, and the many short
+  // warp-path tasks fill the SMs their CTAs leave.  Queue 0: two 256-thread
+  // CTAs per SM for work areas within half an SM's shared memory; queue 1: one
+  // 512-thread CTA per SM for the rest.
+  CK_PDL(launch_pdl(k_trunc_classify, dim3((nitems + 255) / 256), dim3(256), 0, st, a, nitems,
+                    bigq, bigcount, aux ? aux->cls : nullptr));
+  const bool conc = aux != nullptr && aux->q0 != nullptr && aux->q0 != st;
+  cudaStream_t s0 = conc ? aux->q0 : st, s1 = conc ? aux->q1 : st;
+  const bool full = bsm > QHALF;
+  if (conc) {
+    cudaError_t e = cudaEventRecord(aux->ef, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, aux->ef, 0);
+    if (e == cudaSuccess && full) e = cudaStreamWaitEvent(s1, aux->ef, 0);
+    if (e != cudaSuccess) return e;
+  }
+  if (full) {
+    const int bb = nitems < nsm ? nitems : nsm;
+    CK_PDL(launch_pdl(k_trunc_big<512>, dim3(bb), dim3(512), bsm, s1, a, bigq + nitems, bigcount + 1, nitems));
+  }
   {
     TruncArgs ah = a;
     ah.smem_doubles = QHALF_D;
     const int bb = nitems < 2 * nsm ? nitems : 2 * nsm;
-    CK_PDL(launch_pdl(k_trunc_big<256>, dim3(bb), dim3(256), QHALF, st, ah, bigq, bigcount, nitems));
+    CK_PDL(launch_pdl(k_trunc_big<256>, dim3(bb), dim3(256), QHALF, s0, ah, bigq, bigcount, nitems));
   }
-  if (bsm > QHALF) {
-    e = cudaGetLastError();
+  CK_PDL(launch_pdl(k_trunc_warp, dim3(blocks), dim3(TW * 32), NSLOT * SLOT * 8, st, a, nitems,
+                    (const unsigned char*)(aux ? aux->cls : nullptr)));
+  if (conc) {
+    cudaError_t e = cudaEventRecord(aux->ej0, s0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, aux->ej0, 0);
+    if (e == cudaSuccess && full) e = cudaEventRecord(aux->ej1, s1);
+    if (e == cudaSuccess && full) e = cudaStreamWaitEvent(st, aux->ej1, 0);
     if (e != cudaSuccess) return e;
-    const int bb = nitems < nsm ? nitems : nsm;
-    CK_PDL(launch_pdl(k_trunc_big<512>, dim3(bb), dim3(512), bsm, st, a, bigq + nitems, bigcount + 1, nitems));
   }
   return cudaGetLastError();
 }

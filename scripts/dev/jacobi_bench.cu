@@ -193,29 +193,31 @@ __device__ int jac_var(double* B, int pr, int pc, double* J, int lane) {
 }
 
 __global__ void k_jac(const double* in, int pr, int pc, long long* cyc, int* sweeps, double* out, int var) {
-  __shared__ double B[32 * 33], J[32 * 33];
+  __shared__ double B[32 * 33], J[32 * 33], G[32 * 33], RL[64];
   const int lane = threadIdx.x;
   for (int i = lane; i < pr * pc; i += 32) B[(i / pr) * (pr | 1) + i % pr] = in[i];
   __syncwarp();
   long long t0 = clock64();
-  int sw = var == 0 ? acr::jac_var<0>(B, pr, pc, J, lane) : var == 1 ? acr::jac_var<1>(B, pr, pc, J, lane) : acr::jac_var<2>(B, pr, pc, J, lane);
+  int sw = var == 3 ? acr::precond_jacobi(B, pc, J, G, RL, lane) : var == 0 ? acr::jac_var<0>(B, pr, pc, J, lane) : var == 1 ? acr::jac_var<1>(B, pr, pc, J, lane) : acr::jac_var<2>(B, pr, pc, J, lane);
   __syncwarp();
   long long t1 = clock64();
   if (lane == 0) { *cyc = t1 - t0; *sweeps = sw; }
-  for (int i = lane; i < pr * pc; i += 32) out[i] = B[i];
+  for (int i = lane; i < (pr | 1) * pc; i += 32) out[i] = B[i];
 }
 
 int main() {
-  for (int pc : {4, 8, 12, 16}) {
+  for (int pc : {8, 12, 14, 16, 24}) {
     const int pr = pc;
     std::vector<double> h(pr * pc);
     srand(pc);
     // graded singular values like a recompression core: random orthogonal-ish mix
-    for (int i = 0; i < pr * pc; ++i) h[i] = ((rand() / (double)RAND_MAX) - 0.5) * pow(10.0, -(double)((i % pc) % 12));
+    { std::vector<double> ru(pc * pc, 0.0), rv(pc * pc, 0.0);
+      for (int c = 0; c < pc; ++c) for (int r = 0; r <= c; ++r) { ru[c * pc + r] = ((rand() / (double)RAND_MAX) - 0.5) * pow(10.0, -2.0 * r); rv[c * pc + r] = ((rand() / (double)RAND_MAX) - 0.5) * pow(10.0, -2.0 * r); }
+      for (int i = 0; i < pc; ++i) for (int j = 0; j < pc; ++j) { double a = 0; for (int l = 0; l < pc; ++l) a += ru[l * pc + i] * rv[l * pc + j]; h[j * pr + i] = a; } }
     double *din, *dout; long long* dc; int* ds;
-    cudaMalloc(&din, 8 * pr * pc); cudaMalloc(&dout, 8 * pr * pc); cudaMalloc(&dc, 8); cudaMalloc(&ds, 4);
+    cudaMalloc(&din, 8 * pr * pc); cudaMalloc(&dout, 8 * (pr | 1) * pc); cudaMalloc(&dc, 8); cudaMalloc(&ds, 4);
     cudaMemcpy(din, h.data(), 8 * pr * pc, cudaMemcpyHostToDevice);
-    for (int var = 0; var < 3; ++var) {
+    for (int var = 0; var < 4; ++var) {
     long long c = 0; int s = 0;
     for (int rep = 0; rep < 3; ++rep) {
       k_jac<<<1, 32>>>(din, pr, pc, dc, ds, dout, var);
@@ -223,8 +225,10 @@ int main() {
     }
     cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&s, ds, 4, cudaMemcpyDeviceToHost);
     const int np = pc + (pc & 1);
-    const char* nm[] = {"blk", "blkfast", "blkconst"};
-    printf("pc=%2d %-8s sweeps=%2d cycles=%8lld  per step=%.0f  (%s)\n", pc, nm[var], s, c, c / (double)(s * (np - 1)), cudaGetErrorString(cudaGetLastError()));
+    const char* nm[] = {"blk", "blkfast", "blkconst", "precond"};
+    std::vector<double> o(pr * pc); cudaMemcpy(o.data(), dout, 8 * pr * pc, cudaMemcpyDeviceToHost);
+    double smax = 0, smin = 1e300; for (int j = 0; j < pc; ++j) { double q = 0; for (int i = 0; i < pr; ++i) { double x = o[j * (pr | 1) + i]; q += x * x; } q = sqrt(q); if (q > smax) smax = q; if (q < smin) smin = q; }
+    printf("pc=%2d %-8s sweeps=%2d cycles=%8lld  per step=%.0f  smax %.15e smin %.15e (%s)\n", pc, nm[var], s, c, c / (double)((s ? s : 1) * (np - 1)), smax, smin, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
