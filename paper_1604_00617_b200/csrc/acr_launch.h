@@ -41,6 +41,10 @@ cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
 cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
                             int nleaf, Src U, Src V, RankRef rr, int node,
                             int fside, cudaStream_t st);
+// fused Schur step at a branch node with two leaf children (k_leaf.cu)
+size_t schur_leaf_smem(int bw, int R);
+cudaError_t launch_schur_leaf(const TreeDev& T, const HB* H, int nelem, int nu, int half,
+                              Src P1, Src P2, int R, cudaStream_t st);
 cudaError_t launch_leafadd(const TreeDev& T, const HB* A, const HB* B,
                            const HB* C, double sb, int nelem, cudaStream_t st);
 // int copy (e.g. device -> mapped pinned host memory, bypassing the copy

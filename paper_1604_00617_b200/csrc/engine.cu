@@ -566,6 +566,7 @@ struct Plan {
   };
   QStreams qstr[2];
   bool no_qstreams = getenv("ACR_NO_QSTREAMS") != nullptr;   // development aid
+  bool no_fuse_leaf = getenv("ACR_NO_FUSE_LEAF") != nullptr; // development aid
 
   // second stream for independent launches at latency-bound levels (disabled
   // while instrumenting so per-class event timings stay on one stream)
@@ -1281,6 +1282,23 @@ struct Plan {
     const Src P1 = s_pan(c.P1, c.ps * c.R, c.R);
     const Src P2 = s_pan(c.P2, c.ps * c.R, c.R);
     const Src P3 = s_pan(c.P3, c.ps * c.R, c.R);
+    if (ht.isleaf[a0] && ht.isleaf[a1] && !prof_on && !no_fuse_leaf &&
+        schur_leaf_smem(ht.bw, c.R) <= 200 * 1024) {
+      // both children are leaves: each half's HODLR x panel products, panel
+      // product and leaf update in one launch (k_schur_leaf)
+      inv_node(c, a0);                                 // x11
+      settle(c);
+      CK(launch_schur_leaf(dt.T, c.H, c.G, nu, 0, P1, P2, c.R, st));   // T, Hh; S = H22 + W V12^T
+      inv_node(c, a1);                                 // sinv
+      CK(launch_schur_leaf(dt.T, c.H, c.G, nu, 1, P1, P2, c.R, st));   // Z, S2; b11 = x11 + G Hh^T
+      launches += 2;
+      TruncArgs a;                                     // b12, b21
+      memset(&a, 0, sizeof(a));
+      a.mode = TM_TRUNCATE;
+      a.a = op_own(P1, P2, r_hb(c.H), -1.0);
+      run_trunc(a, ht.startA[nu], ht.startA[nu] + 2, c.H, c.G, c.R, 0);
+      return;
+    }
     inv_node(c, a0);                                   // x11
     settle(c);
     inv_hmat(c, a0, false);                            // T, Hh

@@ -950,6 +950,170 @@ cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
 }
 
 // ---------------------------------------------------------------------------
+// Fused Schur step at a branch node nu whose children are both leaves -- the
+// bottom of invert's recursion (algebra.py:214-238).  With the inverse X of
+// leaf rho just computed (in place in H), one CTA per block does what the
+// general path does in three launches (HODLR x panel, panel product, leaf
+// update):
+//   P1[rho] = X A,  P2[rho] = X^T B           A = U_nu[rho], B = V_nu[rho]
+//   K = B^T (X A);  W = alpha Lp K;  leaf(rho') += W Rp^T
+// half 0: rho = left leaf, Lp = U_nu[rho'], Rp = V_nu[rho'], alpha = -1
+//         (the Schur complement S = H22 - H21 x11 H12)
+// half 1: rho = right leaf, Lp = P1[rho'] (T), Rp = P2[rho'] (Hh), alpha = +1
+//         (b11 = x11 + x11 H12 sinv H21 x11)
+// A has rank(nu, half) columns, B rank(nu, 1 - half); a zero rank skips what
+// the general path skips.  Fixed summation order: reproducible.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(LT) k_schur_leaf(TreeDev T, const HB* H, int nu, int half,
+                                                   Src P1, Src P2) {
+  ACR_PDL_ENTRY();
+  extern __shared__ double sm[];
+  const int g = blockIdx.x, tid = threadIdx.x, n = T.n, bw = T.bw;
+  const HB hb = H[g];
+  const int r12 = hb.rk[nu * 2], r21 = hb.rk[nu * 2 + 1];
+  const int ca = half ? r21 : r12, cb = half ? r12 : r21;
+  if (!ca && !cb) return;
+  const int lo = T.lo[nu], mid = T.mid[nu], hi = T.hi[nu];
+  const int r0 = half ? mid : lo, sr = half ? hi - mid : mid - lo;    // rho
+  const int q0 = half ? lo : mid, sp = half ? mid - lo : hi - mid;    // rho'
+  const int slot = T.depth[nu];
+  const int ldx = sr + 1, lr = sr | 1, lp = sp | 1;
+  const double* Ug = hb.U + (long long)slot * hb.R * n;
+  const double* Vg = hb.V + (long long)slot * hb.R * n;
+  double* X = sm;                                   // [sr][ldx]
+  double* A = X + (long long)sr * ldx;              // [ca][lr]
+  double* B = A + (long long)ca * lr;               // [cb][lr]
+  double* TA = B + (long long)cb * lr;              // [ca][lr]
+  double* K = TA + (long long)ca * lr;              // [cb][ca]
+  double* Lp = K + (long long)cb * ca;              // [cb][lp]
+  double* Rp = Lp + (long long)cb * lp;             // [ca][lp]
+  double* Wp = Rp + (long long)ca * lp;             // [ca][lp]
+  const bool upd = ca > 0 && cb > 0;
+  {
+    const double* Lg = hb.leaf + (long long)r0 * bw;
+    for (int idx = tid; idx < sr * sr; idx += LT) {
+      const int i = idx / sr, j = idx - i * sr;
+      X[i * ldx + j] = Lg[(long long)i * bw + j];
+    }
+    for (int idx = tid; idx < ca * sr; idx += LT) {
+      const int c = idx / sr, j = idx - c * sr;
+      A[c * lr + j] = Ug[(long long)c * n + r0 + j];
+    }
+    for (int idx = tid; idx < cb * sr; idx += LT) {
+      const int c = idx / sr, j = idx - c * sr;
+      B[c * lr + j] = Vg[(long long)c * n + r0 + j];
+    }
+    if (upd) {
+      for (int idx = tid; idx < cb * sp; idx += LT) {
+        const int c = idx / sp, j = idx - c * sp;
+        Lp[c * lp + j] = half ? src_col(P1, n, g, slot, c)[q0 + j] : Ug[(long long)c * n + q0 + j];
+      }
+      for (int idx = tid; idx < ca * sp; idx += LT) {
+        const int c = idx / sp, j = idx - c * sp;
+        Rp[c * lp + j] = half ? src_col(P2, n, g, slot, c)[q0 + j] : Vg[(long long)c * n + q0 + j];
+      }
+    }
+  }
+  __syncthreads();
+  // TA = X A (kept for K, and to P1[rho]); X^T B to P2[rho]
+  for (int idx = tid; idx < (ca + cb) * sr; idx += LT) {
+    const int c = idx / sr, i = idx - c * sr;
+    double a0 = 0.0, a1 = 0.0;
+    if (c < ca) {
+      const double* xi = X + i * ldx;
+      const double* ac = A + c * lr;
+      int j = 0;
+      for (; j + 1 < sr; j += 2) {
+        a0 = fma(xi[j], ac[j], a0);
+        a1 = fma(xi[j + 1], ac[j + 1], a1);
+      }
+      if (j < sr) a0 = fma(xi[j], ac[j], a0);
+      const double v = a0 + a1;
+      TA[c * lr + i] = v;
+      src_col(P1, n, g, slot, c)[r0 + i] = v;
+    } else {
+      const double* bc = B + (c - ca) * lr;
+      int j = 0;
+      for (; j + 1 < sr; j += 2) {
+        a0 = fma(X[j * ldx + i], bc[j], a0);
+        a1 = fma(X[(j + 1) * ldx + i], bc[j + 1], a1);
+      }
+      if (j < sr) a0 = fma(X[j * ldx + i], bc[j], a0);
+      src_col(P2, n, g, slot, c - ca)[r0 + i] = a0 + a1;
+    }
+  }
+  if (!upd) return;
+  __syncthreads();
+  // K = B^T TA (cb x ca)
+  for (int idx = tid; idx < cb * ca; idx += LT) {
+    const int b = idx / ca, a = idx - b * ca;
+    const double* bb = B + b * lr;
+    const double* ta = TA + a * lr;
+    double a0 = 0.0, a1 = 0.0;
+    int i = 0;
+    for (; i + 1 < sr; i += 2) {
+      a0 = fma(bb[i], ta[i], a0);
+      a1 = fma(bb[i + 1], ta[i + 1], a1);
+    }
+    if (i < sr) a0 = fma(bb[i], ta[i], a0);
+    K[idx] = a0 + a1;
+  }
+  __syncthreads();
+  // W = alpha Lp K (sp x ca)
+  const double alpha = half ? 1.0 : -1.0;
+  for (int idx = tid; idx < ca * sp; idx += LT) {
+    const int a = idx / sp, i = idx - a * sp;
+    double z = 0.0;
+    for (int b = 0; b < cb; ++b) z = fma(Lp[b * lp + i], K[b * ca + a], z);
+    Wp[a * lp + i] = alpha * z;
+  }
+  __syncthreads();
+  // leaf(rho') += W Rp^T
+  double* Lq = hb.leaf + (long long)q0 * bw;
+  for (int base = tid; base < sp * sp; base += 4 * LT) {
+    double lv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = base + q * LT;
+      const int i = idx / sp, j = idx - i * sp;
+      lv[q] = idx < sp * sp ? Lq[(long long)i * bw + j] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = base + q * LT;
+      if (idx < sp * sp) {
+        const int i = idx / sp, j = idx - i * sp;
+        double z = 0.0;
+        for (int a = 0; a < ca; ++a) z = fma(Wp[a * lp + i], Rp[a * lp + j], z);
+        Lq[(long long)i * bw + j] = lv[q] + z;
+      }
+    }
+  }
+}
+
+// shared memory (bytes) of k_schur_leaf for leaves of at most bw rows and
+// ranks of at most R
+size_t schur_leaf_smem(int bw, int R) {
+  const size_t l = (size_t)bw | 1;
+  return 8 * ((size_t)bw * (bw + 1) + 6 * (size_t)R * l + (size_t)R * R);
+}
+
+cudaError_t launch_schur_leaf(const TreeDev& T, const HB* H, int nelem, int nu, int half,
+                              Src P1, Src P2, int R, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  const size_t smem = schur_leaf_smem(T.bw, R);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_schur_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  CK_PDL(launch_pdl(k_schur_leaf, dim3(nelem), dim3(LT), smem, st, T, H, nu, half, P1, P2));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // elementwise leaf ops
 // ---------------------------------------------------------------------------
 __global__ void k_leafadd(int len, const HB* A, const HB* B, const HB* C,
