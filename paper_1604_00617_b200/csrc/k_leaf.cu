@@ -964,7 +964,9 @@ cudaError_t launch_leaflr_n(const TreeDev& T, const HB* H, int nelem, int mu,
 // A has rank(nu, half) columns, B rank(nu, 1 - half); a zero rank skips what
 // the general path skips.  Fixed summation order: reproducible.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(LT) k_schur_leaf(TreeDev T, const HB* H, int nu, int half,
+static constexpr int ST = 512;   // threads of k_schur_leaf
+
+__global__ void __launch_bounds__(ST) k_schur_leaf(TreeDev T, const HB* H, int nu, int half,
                                                    Src P1, Src P2) {
   ACR_PDL_ENTRY();
   extern __shared__ double sm[];
@@ -991,24 +993,24 @@ __global__ void __launch_bounds__(LT) k_schur_leaf(TreeDev T, const HB* H, int n
   const bool upd = ca > 0 && cb > 0;
   {
     const double* Lg = hb.leaf + (long long)r0 * bw;
-    for (int idx = tid; idx < sr * sr; idx += LT) {
+    for (int idx = tid; idx < sr * sr; idx += ST) {
       const int i = idx / sr, j = idx - i * sr;
       X[i * ldx + j] = Lg[(long long)i * bw + j];
     }
-    for (int idx = tid; idx < ca * sr; idx += LT) {
+    for (int idx = tid; idx < ca * sr; idx += ST) {
       const int c = idx / sr, j = idx - c * sr;
       A[c * lr + j] = Ug[(long long)c * n + r0 + j];
     }
-    for (int idx = tid; idx < cb * sr; idx += LT) {
+    for (int idx = tid; idx < cb * sr; idx += ST) {
       const int c = idx / sr, j = idx - c * sr;
       B[c * lr + j] = Vg[(long long)c * n + r0 + j];
     }
     if (upd) {
-      for (int idx = tid; idx < cb * sp; idx += LT) {
+      for (int idx = tid; idx < cb * sp; idx += ST) {
         const int c = idx / sp, j = idx - c * sp;
         Lp[c * lp + j] = half ? src_col(P1, n, g, slot, c)[q0 + j] : Ug[(long long)c * n + q0 + j];
       }
-      for (int idx = tid; idx < ca * sp; idx += LT) {
+      for (int idx = tid; idx < ca * sp; idx += ST) {
         const int c = idx / sp, j = idx - c * sp;
         Rp[c * lp + j] = half ? src_col(P2, n, g, slot, c)[q0 + j] : Vg[(long long)c * n + q0 + j];
       }
@@ -1016,52 +1018,61 @@ __global__ void __launch_bounds__(LT) k_schur_leaf(TreeDev T, const HB* H, int n
   }
   __syncthreads();
   // TA = X A (kept for K, and to P1[rho]); X^T B to P2[rho]
-  for (int idx = tid; idx < (ca + cb) * sr; idx += LT) {
+  for (int idx = tid; idx < (ca + cb) * sr; idx += ST) {
     const int c = idx / sr, i = idx - c * sr;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (c < ca) {
       const double* xi = X + i * ldx;
       const double* ac = A + c * lr;
       int j = 0;
-      for (; j + 1 < sr; j += 2) {
+#pragma unroll 2
+      for (; j + 3 < sr; j += 4) {
         a0 = fma(xi[j], ac[j], a0);
         a1 = fma(xi[j + 1], ac[j + 1], a1);
+        a2 = fma(xi[j + 2], ac[j + 2], a2);
+        a3 = fma(xi[j + 3], ac[j + 3], a3);
       }
-      if (j < sr) a0 = fma(xi[j], ac[j], a0);
-      const double v = a0 + a1;
+      for (; j < sr; ++j) a0 = fma(xi[j], ac[j], a0);
+      const double v = (a0 + a1) + (a2 + a3);
       TA[c * lr + i] = v;
       src_col(P1, n, g, slot, c)[r0 + i] = v;
     } else {
       const double* bc = B + (c - ca) * lr;
       int j = 0;
-      for (; j + 1 < sr; j += 2) {
+#pragma unroll 2
+      for (; j + 3 < sr; j += 4) {
         a0 = fma(X[j * ldx + i], bc[j], a0);
         a1 = fma(X[(j + 1) * ldx + i], bc[j + 1], a1);
+        a2 = fma(X[(j + 2) * ldx + i], bc[j + 2], a2);
+        a3 = fma(X[(j + 3) * ldx + i], bc[j + 3], a3);
       }
-      if (j < sr) a0 = fma(X[j * ldx + i], bc[j], a0);
-      src_col(P2, n, g, slot, c - ca)[r0 + i] = a0 + a1;
+      for (; j < sr; ++j) a0 = fma(X[j * ldx + i], bc[j], a0);
+      src_col(P2, n, g, slot, c - ca)[r0 + i] = (a0 + a1) + (a2 + a3);
     }
   }
   if (!upd) return;
   __syncthreads();
   // K = B^T TA (cb x ca)
-  for (int idx = tid; idx < cb * ca; idx += LT) {
+  for (int idx = tid; idx < cb * ca; idx += ST) {
     const int b = idx / ca, a = idx - b * ca;
     const double* bb = B + b * lr;
     const double* ta = TA + a * lr;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int i = 0;
-    for (; i + 1 < sr; i += 2) {
+#pragma unroll 2
+    for (; i + 3 < sr; i += 4) {
       a0 = fma(bb[i], ta[i], a0);
       a1 = fma(bb[i + 1], ta[i + 1], a1);
+      a2 = fma(bb[i + 2], ta[i + 2], a2);
+      a3 = fma(bb[i + 3], ta[i + 3], a3);
     }
-    if (i < sr) a0 = fma(bb[i], ta[i], a0);
-    K[idx] = a0 + a1;
+    for (; i < sr; ++i) a0 = fma(bb[i], ta[i], a0);
+    K[idx] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
   // W = alpha Lp K (sp x ca)
   const double alpha = half ? 1.0 : -1.0;
-  for (int idx = tid; idx < ca * sp; idx += LT) {
+  for (int idx = tid; idx < ca * sp; idx += ST) {
     const int a = idx / sp, i = idx - a * sp;
     double z = 0.0;
     for (int b = 0; b < cb; ++b) z = fma(Lp[b * lp + i], K[b * ca + a], z);
@@ -1070,17 +1081,17 @@ __global__ void __launch_bounds__(LT) k_schur_leaf(TreeDev T, const HB* H, int n
   __syncthreads();
   // leaf(rho') += W Rp^T
   double* Lq = hb.leaf + (long long)q0 * bw;
-  for (int base = tid; base < sp * sp; base += 4 * LT) {
+  for (int base = tid; base < sp * sp; base += 4 * ST) {
     double lv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int idx = base + q * LT;
+      const int idx = base + q * ST;
       const int i = idx / sp, j = idx - i * sp;
       lv[q] = idx < sp * sp ? Lq[(long long)i * bw + j] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int idx = base + q * LT;
+      const int idx = base + q * ST;
       if (idx < sp * sp) {
         const int i = idx / sp, j = idx - i * sp;
         double z = 0.0;
@@ -1109,7 +1120,7 @@ cudaError_t launch_schur_leaf(const TreeDev& T, const HB* H, int nelem, int nu, 
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  CK_PDL(launch_pdl(k_schur_leaf, dim3(nelem), dim3(LT), smem, st, T, H, nu, half, P1, P2));
+  CK_PDL(launch_pdl(k_schur_leaf, dim3(nelem), dim3(ST), smem, st, T, H, nu, half, P1, P2));
   return cudaGetLastError();
 }
 
