@@ -505,6 +505,170 @@ __global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
   }
 }
 
+// Register-resident variant of the cluster panel (jb <= 32): every thread
+// keeps its row of the panel in registers, so the rank-1 update of a column
+// step is 31 FMAs on registers (the shared-memory panel paid a load and a
+// store per element), and a step costs one DSMEM round trip instead of two:
+// every CTA first reduces its warps' candidates to one and stages that row,
+// and after the cluster barrier warp 0 reads the four CTA candidates and the
+// four staged rows together.  Same pivot rule, implicit interchanges and
+// write-back order as k_lu_panel_cl.
+__global__ void __cluster_dims__(LUC, 1, 1) __launch_bounds__(LUCT, 1)
+    k_lu_panel_reg(double* A, int N, int j0, int jb, int* piv, int* info) {
+  ACR_PDL_ENTRY();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  constexpr int NW = LUCT / 32;
+  constexpr int NB = LU_NB;
+  const int crank = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Ms = N - j0;
+  const int RB = (Ms + LUC - 1) / LUC;
+  const int r0 = crank * RB;
+  const int nr = Ms - r0 < RB ? (Ms - r0 > 0 ? Ms - r0 : 0) : RB;
+  double* tile = sm + (size_t)warp * 32 * 33;              // per-warp 32 x 33 transpose tile
+  int* p2r = reinterpret_cast<int*>(sm + (size_t)NW * 32 * 33);   // position -> physical row
+  __shared__ double wv[NW], wrowbuf[NW][NB];
+  __shared__ int wpos[NW], wrow[NW];
+  __shared__ double cta_v[2], cta_row[2][NB];     // double-buffered by column parity
+  __shared__ int cta_pos[2], cta_rw[2];
+  __shared__ double prow[NB];
+  __shared__ int s_pos, s_row, s_a;
+  // rows of this warp, coalesced through the tile
+  double row[NB];
+  {
+    const int wr0 = r0 + warp * 32;                        // first row of this warp
+    for (int r = 0; r < 32; ++r) {
+      const int rr = warp * 32 + r;
+      tile[r * 33 + lane] = (rr < nr && lane < jb) ? A[(long long)(j0 + wr0 + r) * N + j0 + lane] : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NB; ++c) row[c] = tile[lane * 33 + c];
+    __syncwarp();
+  }
+  for (int q = tid; q < Ms; q += LUCT) p2r[q] = q;
+  int my_pos = tid < nr ? r0 + tid : 0x7fffffff;
+  __syncthreads();
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) {
+    if (jj >= jb) break;
+    const int par = jj & 1;
+    // warp candidate: rows not yet pivoted (position >= jj)
+    double best = -1.0;
+    int bpos = 0x7fffffff, brow = -1;
+    if (tid < nr && my_pos >= jj) {
+      best = fabs(row[jj]);
+      bpos = my_pos;
+      brow = r0 + tid;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; }
+    }
+    if (lane == 0) { wv[warp] = best; wpos[warp] = bpos; wrow[warp] = brow; }
+    if (brow >= 0 && r0 + tid == brow) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c >= jj) wrowbuf[warp][c] = row[c];
+    }
+    __syncthreads();
+    if (warp == 0) {                            // this CTA's candidate and its row
+      best = lane < NW ? wv[lane] : -1.0;
+      bpos = lane < NW ? wpos[lane] : 0x7fffffff;
+      int bw = lane;
+#pragma unroll
+      for (int o = NW / 2; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; bw = ow; }
+      }
+      bw = __shfl_sync(0xffffffffu, bw, 0);
+      best = __shfl_sync(0xffffffffu, best, 0);
+      bpos = __shfl_sync(0xffffffffu, bpos, 0);
+      cta_row[par][lane] = (best >= 0.0 && lane >= jj) ? wrowbuf[bw][lane] : 0.0;
+      if (lane == 0) { cta_v[par] = best; cta_pos[par] = bpos; cta_rw[par] = best >= 0.0 ? wrow[bw] : -1; }
+    }
+    cl.sync();                                  // every CTA's candidate and row staged
+    if (warp == 0) {
+      double rv[LUC];
+#pragma unroll
+      for (int k = 0; k < LUC; ++k) rv[k] = cl.map_shared_rank(&cta_row[par][0], k)[lane];
+      best = -1.0;
+      bpos = 0x7fffffff;
+      brow = -1;
+      int bk = lane;
+      if (lane < LUC) {
+        best = *cl.map_shared_rank(&cta_v[par], lane);
+        bpos = *cl.map_shared_rank(&cta_pos[par], lane);
+        brow = *cl.map_shared_rank(&cta_rw[par], lane);
+      }
+#pragma unroll
+      for (int o = LUC / 2; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, brow, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        if (ov > best || (ov == best && op < bpos)) { best = ov; bpos = op; brow = orr; bk = ok; }
+      }
+      bk = __shfl_sync(0xffffffffu, bk, 0);
+      bpos = __shfl_sync(0xffffffffu, bpos, 0);
+      brow = __shfl_sync(0xffffffffu, brow, 0);
+      double pr = rv[0];
+#pragma unroll
+      for (int k = 1; k < LUC; ++k)
+        if (bk == k) pr = rv[k];
+      prow[lane] = pr;
+      if (lane == 0) {
+        const int a = p2r[jj];                  // physical row now at position jj
+        s_pos = bpos;
+        s_row = brow;
+        s_a = a;
+        p2r[jj] = brow;
+        p2r[bpos] = a;
+      }
+    }
+    __syncthreads();
+    const int ppos = s_pos, prw = s_row, a = s_a;
+    if (tid < nr) {
+      if (r0 + tid == a) my_pos = ppos;
+      if (r0 + tid == prw) my_pos = jj;
+    }
+    const double pv = prow[jj];
+    if (crank == 0 && tid == 0) {
+      piv[j0 + jj] = j0 + ppos;
+      if (pv == 0.0 && *info == 0) *info = j0 + jj + 1;
+    }
+    if (tid < nr && my_pos > jj) {
+      const double rinv = pv != 0.0 ? 1.0 / pv : 0.0;
+      const double l = pv != 0.0 ? row[jj] * rinv : row[jj];
+      row[jj] = l;
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c > jj) row[c] = row[c] - l * prow[c];
+    }
+    // prow, the warp slots and the staged rows of this parity are rewritten
+    // only after barriers every reader reaches after its reads
+  }
+  cl.sync();                                    // remote reads of this CTA's staged rows done
+  // write back in final (swapped) order, coalesced through the tile
+  {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) tile[lane * 33 + c] = row[c];
+    __syncwarp();
+    for (int r = 0; r < 32; ++r) {
+      const int pos = __shfl_sync(0xffffffffu, my_pos, r);
+      if (warp * 32 + r < nr && lane < jb)
+        A[(long long)(j0 + pos) * N + j0 + lane] = tile[r * 33 + lane];
+    }
+  }
+}
+
 // Row interchanges of panel j0 applied to every column outside it (laswp):
 // a CTA stages the <= 2 jb touched rows of its 32 columns in shared memory,
 // replays the swaps there (thread per column) and writes the rows back.
@@ -582,7 +746,19 @@ cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work,
                              200 * 1024);
         attr_c = true;
       }
-      CK_PDL(launch_pdl(k_lu_panel_cl, dim3(LUC), dim3(LUCT), cbytes, st, A, N, j0, jb, piv, info));
+      static const bool noreg = getenv("ACR_LU_NOREG") != nullptr;   // A/B aid
+      const size_t rbytes = (size_t)(LUCT / 32) * 32 * 33 * sizeof(double) + (size_t)Ms * sizeof(int);
+      if (!noreg && rbytes <= 200 * 1024) {
+        static bool attr_r = false;
+        if (!attr_r) {
+          cudaFuncSetAttribute(k_lu_panel_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024);
+          attr_r = true;
+        }
+        CK_PDL(launch_pdl(k_lu_panel_reg, dim3(LUC), dim3(LUCT), rbytes, st, A, N, j0, jb, piv, info));
+      } else {
+        CK_PDL(launch_pdl(k_lu_panel_cl, dim3(LUC), dim3(LUCT), cbytes, st, A, N, j0, jb, piv, info));
+      }
       if (N - jb > 0) CK_PDL(launch_pdl(k_lu_laswp, dim3((N - jb + 31) / 32), dim3(dim3(32, 8)), 0, st, A, N, j0, jb, piv));
     } else if (sbytes <= 200 * 1024) {   // sub-panels in shared memory
       static bool attr = false;
