@@ -527,6 +527,11 @@ struct Plan {
     if (sev0) cudaEventDestroy(sev0);
     if (sev1) cudaEventDestroy(sev1);
     for (auto e : evpool) cudaEventDestroy(e);
+    if (st3) {
+      cudaStreamSynchronize(st3);
+      cudaStreamDestroy(st3);
+      for (auto e : evdef) cudaEventDestroy(e);
+    }
     if (st2) {
       cudaStreamSynchronize(st2);
       cudaStreamDestroy(st2);
@@ -564,7 +569,7 @@ struct Plan {
     cudaStream_t q0 = nullptr, q1 = nullptr;
     cudaEvent_t ef = nullptr, ej0 = nullptr, ej1 = nullptr;
   };
-  QStreams qstr[2];
+  QStreams qstr[3];
   bool no_qstreams = getenv("ACR_NO_QSTREAMS") != nullptr;   // development aid
   bool no_fuse_leaf = getenv("ACR_NO_FUSE_LEAF") != nullptr; // development aid
 
@@ -580,6 +585,19 @@ struct Plan {
       CK(cudaEventCreateWithFlags(&evj, cudaEventDisableTiming));
     }
     return st2;
+  }
+  // third stream: recompressions of a Schur complement's upper tree levels,
+  // deferred until the inversion reaches the nodes they update
+  cudaStream_t st3 = nullptr;
+  cudaEvent_t evdef[32] = {};
+  bool no_defer = getenv("ACR_NO_DEFER") != nullptr;   // development aid
+  cudaStream_t deferred() {
+    if (prof_on || no_side || no_defer) return st;
+    if (!st3) {
+      CK(cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking));
+      for (auto& e : evdef) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return st3;
   }
   void fork(cudaStream_t s) {
     if (s == st) return;
@@ -843,7 +861,11 @@ struct Plan {
                  int Rb, cudaStream_t s = nullptr) {
     if (t1 <= t0 || nelem <= 0) return;
     if (!s) s = st;
-    const bool alt = s != st;                    // own scratch slots per stream
+    // own scratch slots (and queue streams) per launching stream: main,
+    // side, deferred
+    const int bank = s == st ? 0 : (st3 != nullptr && s == st3 ? 2 : 1);
+    static const int SL_G[3] = {10, 15, 21}, SL_Q[3] = {13, 16, 22}, SL_C[3] = {14, 17, 23},
+                     SL_F[3] = {19, 20, 24};
     a.T = dt.T;
     a.out = out;
     a.eps = eps;
@@ -886,7 +908,7 @@ struct Plan {
       a.gscr = nullptr;
       a.gscr_stride = 0;
       if (pworst > SMD) {
-        a.gscr = scratch<double>(alt ? 15 : 10, (size_t)2 * nitems * pworst);
+        a.gscr = scratch<double>(SL_G[bank], (size_t)2 * nitems * pworst);
         a.gscr_stride = pworst;
       }
       fork(s);
@@ -906,7 +928,7 @@ struct Plan {
     a.warp_rmax = warp_rmax;
     a.warp_maxneed = wmax;
     if (!direct && warp_sched > 0) {
-      qc = scratch<int>(alt ? 17 : 14, 8);
+      qc = scratch<int>(SL_C[bank], 8);
       a.wq = qc + 2;
     }
     a.smem_doubles = (int)std::min(bworst, SMD);
@@ -914,13 +936,13 @@ struct Plan {
     a.gscr_stride = 0;
     a.gscr_ntasks = 0;
     if (may_big) {
-      q = scratch<int>(alt ? 16 : 13, 2 * (size_t)nitems + 2);
-      qc = scratch<int>(alt ? 17 : 14, 8);
+      q = scratch<int>(SL_Q[bank], 2 * (size_t)nitems + 2);
+      qc = scratch<int>(SL_C[bank], 8);
     }
     if (!direct && warp_sched > 0) a.wq = qc + 2;
     if ((direct || may_big) && bworst > SMD) {
       const int nblk = direct ? nitems : std::min(nitems, 148);
-      a.gscr = scratch<double>(alt ? 15 : 10, (size_t)nblk * bworst);
+      a.gscr = scratch<double>(SL_G[bank], (size_t)nblk * bworst);
       a.gscr_stride = bworst;
     }
     fork(s);
@@ -928,9 +950,9 @@ struct Plan {
     TruncAux aux;
     memset(&aux, 0, sizeof(aux));
     if (may_big) {
-      aux.cls = scratch<unsigned char>(alt ? 20 : 19, (size_t)nitems);
+      aux.cls = scratch<unsigned char>(SL_F[bank], (size_t)nitems);
       if (!prof_on && !no_qstreams) {          // instrumented runs keep one stream
-        QStreams& qs = qstr[alt ? 1 : 0];
+        QStreams& qs = qstr[bank];
         if (!qs.q0) {
           CK(cudaStreamCreateWithFlags(&qs.q0, cudaStreamNonBlocking));
           CK(cudaStreamCreateWithFlags(&qs.q1, cudaStreamNonBlocking));
@@ -1183,7 +1205,17 @@ struct Plan {
     long long ps;
     int* sing;
     bool pend = false;   // S's off-diagonal recompressions still running on the side stream
+    bool defer[32] = {}; // tree depths whose recompressions run on the deferred stream
   };
+
+  // the deferred recompressions of tree depth d must finish before anything
+  // reads or writes the factors of a node at that depth
+  void use_depth(InvCtx& c, int d) {
+    if (c.defer[d]) {
+      CK(cudaStreamWaitEvent(st, evdef[d], 0));
+      c.defer[d] = false;
+    }
+  }
 
   void invert(const HB* H, int G, int R, int* sing) {
     if (G <= 0) return;
@@ -1201,6 +1233,7 @@ struct Plan {
     c.sing = sing;
     inv_node(c, 0);
     settle(c);
+    for (int d = 0; d < 32; ++d) use_depth(c, d);
   }
 
   // the side-stream recompressions of a Schur complement must finish before
@@ -1288,6 +1321,7 @@ struct Plan {
       // product and leaf update in one launch (k_schur_leaf)
       inv_node(c, a0);                                 // x11
       settle(c);
+      use_depth(c, ht.depth[nu]);
       CK(launch_schur_leaf(dt.T, c.H, c.G, nu, 0, P1, P2, c.R, st));   // T, Hh; S = H22 + W V12^T
       inv_node(c, a1);                                 // sinv
       CK(launch_schur_leaf(dt.T, c.H, c.G, nu, 1, P1, P2, c.R, st));   // Z, S2; b11 = x11 + G Hh^T
@@ -1301,6 +1335,7 @@ struct Plan {
     }
     inv_node(c, a0);                                   // x11
     settle(c);
+    use_depth(c, ht.depth[nu]);
     inv_hmat(c, a0, false);                            // T, Hh
     {
       GPJob j;                                          // W = -U21 (V21^T T)
@@ -1319,7 +1354,6 @@ struct Plan {
       leaflr(c.H, c.G, a1, P3, s_hbV(c.H), r_hb(c.H), nu, 0, st);
       const int t0 = ht.startA[a1], t1 = ht.startA[a1 + 1];
       if (t1 > t0) {
-        fork(s2);
         TruncArgs a;
         memset(&a, 0, sizeof(a));
         a.mode = TM_COMBINE;
@@ -1328,8 +1362,34 @@ struct Plan {
         a.b.sel = SEL_FIXED;
         a.b.node = nu;
         a.b.fside = 0;
-        run_trunc(a, t0, t1, c.H, c.G, c.R, c.R, s2);
+        const cudaStream_t s3 = deferred();
+        // the subtree's tasks are listed by depth; the deepest level is needed
+        // first (right after the first leaf inverse) and goes to the side
+        // stream; a node of depth d above it is first touched once its left
+        // child has been inverted, so those levels -- the largest tasks -- run
+        // on the deferred stream meanwhile (a depth always maps to the same
+        // stream, which orders nested updates of the same nodes)
+        int td = t1;
+        if (s3 != st && s2 != st) {
+          const int dmax = ht.depth[ht.listA[(t1 - 1) * 3 + 1]];
+          while (td > t0 && ht.depth[ht.listA[(td - 1) * 3 + 1]] == dmax) --td;
+        } else {
+          td = t0;
+        }
+        fork(s2);
+        run_trunc(a, td, t1, c.H, c.G, c.R, c.R, s2);
         c.pend = s2 != st;
+        for (int e1 = td; e1 > t0;) {              // remaining depths, deepest first
+          const int d = ht.depth[ht.listA[(e1 - 1) * 3 + 1]];
+          int e0 = e1;
+          while (e0 > t0 && ht.depth[ht.listA[(e0 - 1) * 3 + 1]] == d) --e0;
+          use_depth(c, d);                         // an earlier update of this depth still pending
+          fork(s3);
+          run_trunc(a, e0, e1, c.H, c.G, c.R, c.R, s3);
+          CK(cudaEventRecord(evdef[d], s3));
+          c.defer[d] = true;
+          e1 = e0;
+        }
       }
     }
     inv_node(c, a1);                                   // sinv
