@@ -517,7 +517,7 @@ struct Plan {
   Plan(int m_, int n_, int leaf_, double eps_, int cap_, int cutoff_)
       : m(m_), n(n_), leaf(leaf_), cutoff(cutoff_), cap(cap_), eps(eps_) {
     ht.build(n, leaf);
-    scr.resize(32);
+    scr.resize(72);
   }
   ~Plan() {
     if (hmap) cudaFreeHost(hmap);
@@ -527,6 +527,12 @@ struct Plan {
     if (sev0) cudaEventDestroy(sev0);
     if (sev1) cudaEventDestroy(sev1);
     for (auto e : evpool) cudaEventDestroy(e);
+    for (int i = 0; i < NDS; ++i)
+      if (dstr[i]) {
+        cudaStreamSynchronize(dstr[i]);
+        cudaStreamDestroy(dstr[i]);
+        cudaEventDestroy(evds[i]);
+      }
     if (st3) {
       cudaStreamSynchronize(st3);
       cudaStreamDestroy(st3);
@@ -569,7 +575,7 @@ struct Plan {
     cudaStream_t q0 = nullptr, q1 = nullptr;
     cudaEvent_t ef = nullptr, ej0 = nullptr, ej1 = nullptr;
   };
-  QStreams qstr[3];
+  QStreams qstr[3 + 8];
   bool no_qstreams = getenv("ACR_NO_QSTREAMS") != nullptr;   // development aid
   bool no_fuse_leaf = getenv("ACR_NO_FUSE_LEAF") != nullptr; // development aid
 
@@ -586,6 +592,19 @@ struct Plan {
     }
     return st2;
   }
+  // streams of multiply's per-depth recompression chains
+  static constexpr int NDS = 8;
+  cudaStream_t dstr[NDS] = {};
+  cudaEvent_t evds[NDS] = {};
+  bool no_dsplit = getenv("ACR_NO_DSPLIT") != nullptr;   // development aid
+  cudaStream_t depth_stream(int i) {
+    if (!dstr[i]) {
+      CK(cudaStreamCreateWithFlags(&dstr[i], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&evds[i], cudaEventDisableTiming));
+    }
+    return dstr[i];
+  }
+
   // third stream: recompressions of a Schur complement's upper tree levels,
   // deferred until the inversion reaches the nodes they update
   cudaStream_t st3 = nullptr;
@@ -863,9 +882,12 @@ struct Plan {
     if (!s) s = st;
     // own scratch slots (and queue streams) per launching stream: main,
     // side, deferred
-    const int bank = s == st ? 0 : (st3 != nullptr && s == st3 ? 2 : 1);
-    static const int SL_G[3] = {10, 15, 21}, SL_Q[3] = {13, 16, 22}, SL_C[3] = {14, 17, 23},
-                     SL_F[3] = {19, 20, 24};
+    int bank = s == st ? 0 : (st3 != nullptr && s == st3 ? 2 : 1);
+    for (int i = 0; i < NDS; ++i)
+      if (dstr[i] != nullptr && s == dstr[i]) bank = 3 + i;
+    const int SL_G[3] = {10, 15, 21}, SL_Q[3] = {13, 16, 22}, SL_C[3] = {14, 17, 23},
+              SL_F[3] = {19, 20, 24};
+    auto slot_of = [&](const int* base3, int k) { return bank < 3 ? base3[bank] : 32 + 4 * (bank - 3) + k; };
     a.T = dt.T;
     a.out = out;
     a.eps = eps;
@@ -908,7 +930,7 @@ struct Plan {
       a.gscr = nullptr;
       a.gscr_stride = 0;
       if (pworst > SMD) {
-        a.gscr = scratch<double>(SL_G[bank], (size_t)2 * nitems * pworst);
+        a.gscr = scratch<double>(slot_of(SL_G, 0), (size_t)2 * nitems * pworst);
         a.gscr_stride = pworst;
       }
       fork(s);
@@ -928,7 +950,7 @@ struct Plan {
     a.warp_rmax = warp_rmax;
     a.warp_maxneed = wmax;
     if (!direct && warp_sched > 0) {
-      qc = scratch<int>(SL_C[bank], 8);
+      qc = scratch<int>(slot_of(SL_C, 2), 8);
       a.wq = qc + 2;
     }
     a.smem_doubles = (int)std::min(bworst, SMD);
@@ -936,13 +958,13 @@ struct Plan {
     a.gscr_stride = 0;
     a.gscr_ntasks = 0;
     if (may_big) {
-      q = scratch<int>(SL_Q[bank], 2 * (size_t)nitems + 2);
-      qc = scratch<int>(SL_C[bank], 8);
+      q = scratch<int>(slot_of(SL_Q, 1), 2 * (size_t)nitems + 2);
+      qc = scratch<int>(slot_of(SL_C, 2), 8);
     }
     if (!direct && warp_sched > 0) a.wq = qc + 2;
     if ((direct || may_big) && bworst > SMD) {
       const int nblk = direct ? nitems : std::min(nitems, 148);
-      a.gscr = scratch<double>(SL_G[bank], (size_t)nblk * bworst);
+      a.gscr = scratch<double>(slot_of(SL_G, 0), (size_t)nblk * bworst);
       a.gscr_stride = bworst;
     }
     fork(s);
@@ -950,7 +972,7 @@ struct Plan {
     TruncAux aux;
     memset(&aux, 0, sizeof(aux));
     if (may_big) {
-      aux.cls = scratch<unsigned char>(SL_F[bank], (size_t)nitems);
+      aux.cls = scratch<unsigned char>(slot_of(SL_F, 3), (size_t)nitems);
       if (!prof_on && !no_qstreams) {          // instrumented runs keep one stream
         QStreams& qs = qstr[bank];
         if (!qs.q0) {
@@ -1157,13 +1179,9 @@ struct Plan {
     a.mode = TM_COMBINE_SWAP1;
     a.a = op_own(s_pan(Yp, ps * RB, RB), s_hbV(B), r_hb(B));
     a.b = op_own(s_hbU(A), s_pan(Zp, ps * RA, RA), r_hb(A));
-    run_trunc(a, ht.startA[0], ht.startA[1], C, G, RB, RA);
     // M3: ancestors' cross terms, parent first, root last (all rank 0 with a
     // diagonal operand: every combine would pass C through unchanged)
-    for (int t = 1; t < ht.nd && !diag; ++t) {
-      int s0 = ht.startA[0];
-      while (s0 < ht.startA[1] && ht.depth[ht.listA[s0 * 3 + 1]] < t) ++s0;
-      if (s0 >= ht.startA[1]) break;
+    auto m3 = [&](int t) {
       TruncArgs b;
       memset(&b, 0, sizeof(b));
       b.mode = TM_COMBINE;
@@ -1171,7 +1189,43 @@ struct Plan {
       b.b = op_own(s_pan(PX, ps * RB, RB), s_hbV(B), r_arr(cr, nn * 2));
       b.b.sel = SEL_ANC;
       b.b.t = t;
-      run_trunc(b, s0, ht.startA[1], C, G, RC, RB);
+      return b;
+    };
+    const int t0 = ht.startA[0], t1 = ht.startA[1];
+    static const long long dsplit_max = getenv("ACR_DSPLIT_MAX") ? atoll(getenv("ACR_DSPLIT_MAX")) : 1200;
+    if (!prof_on && !no_side && !no_dsplit && !diag && ht.nd > 1 && ht.nd <= NDS + 1 &&
+        (long long)(t1 - t0) * G <= dsplit_max) {
+      // A node of depth d takes M2 and then the d rounds of M3 (one per
+      // ancestor), independently of every other node.  Launched per round over
+      // all nodes, each round lasts as long as its largest task (the root's in
+      // M2, the depth-t nodes' in round t) and the rounds add up; launched per
+      // depth, each depth's chain runs on its own stream and the step lasts as
+      // long as the longest chain.  The tasks are listed by depth.
+      std::vector<std::pair<int, int>> rng;   // [first, last) of every depth
+      for (int e0 = t0; e0 < t1;) {
+        const int d = ht.depth[ht.listA[e0 * 3 + 1]];
+        int e1 = e0;
+        while (e1 < t1 && ht.depth[ht.listA[e1 * 3 + 1]] == d) ++e1;
+        if ((int)rng.size() != d) throw InternalError("task list not ordered by depth");
+        rng.push_back({e0, e1});
+        e0 = e1;
+      }
+      const int nd = (int)rng.size();
+      for (int d = 0; d < nd; ++d) {          // the deepest level (most rounds) on the main stream, last
+        const cudaStream_t sd = d == nd - 1 ? st : depth_stream(d);
+        run_trunc(a, rng[d].first, rng[d].second, C, G, RB, RA, sd);
+        for (int t = 1; t <= d; ++t) run_trunc(m3(t), rng[d].first, rng[d].second, C, G, RC, RB, sd);
+        if (sd != st) CK(cudaEventRecord(evds[d], sd));
+      }
+      for (int d = 0; d + 1 < nd; ++d) CK(cudaStreamWaitEvent(st, evds[d], 0));
+      return;
+    }
+    run_trunc(a, t0, t1, C, G, RB, RA);
+    for (int t = 1; t < ht.nd && !diag; ++t) {
+      int s0 = t0;
+      while (s0 < t1 && ht.depth[ht.listA[s0 * 3 + 1]] < t) ++s0;
+      if (s0 >= t1) break;
+      run_trunc(m3(t), s0, t1, C, G, RC, RB);
     }
   }
 
