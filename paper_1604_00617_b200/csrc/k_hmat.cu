@@ -192,6 +192,87 @@ __global__ void __launch_bounds__(NT) k_hmatA_tc(TreeDev T, MMJobs2 JJ) {
   }
 }
 
+// Phase A for throughput-bound launches (hundreds of thousands of (entry,
+// element) pairs, each a few dozen rows by a handful of columns): one WARP per
+// pair, eight pairs per CTA.  k_hmatA_tc spends one 128-thread CTA per pair --
+// at 800 k CTAs per launch the CTA dispatch rate, not the arithmetic, set its
+// duration (1.8 ms for the level-1 products).  A warp walks all the rows of
+// its pair, 4 per mma.sync m8n8k4, so there is no cross-warp reduction either.
+template <int TMAX>
+__global__ void __launch_bounds__(256) k_hmatA_tcw(TreeDev T, MMJobs2 JJ) {
+  ACR_PDL_ENTRY();
+  const MMJob& J = JJ.j[blockIdx.z];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ei = blockIdx.x * 8 + warp;
+  if (ei >= J.nA) return;
+  const int g = blockIdx.y, n = T.n;
+  const int e0 = T.startA[J.mu0];
+  const int* ent = T.listA + (e0 + ei) * 3;
+  const int mu = ent[0], beta = ent[1], side = ent[2];
+  const int c = mm_cols(J, T, g, mu);
+  if (!c) return;
+  const HB h = J.H[g];
+  const int r = h.rk[beta * 2 + side];
+  if (!r) return;
+  const int lo = T.lo[beta], hi = T.hi[beta], mid = T.mid[beta];
+  int row, len;
+  const double* F;
+  const long long fs = (long long)T.depth[beta] * h.R * n;
+  if (!J.trans) {
+    row = side ? lo : mid;
+    len = side ? mid - lo : hi - mid;
+    F = h.V + fs + row;
+  } else {
+    row = side ? mid : lo;
+    len = side ? hi - mid : mid - lo;
+    F = h.U + fs + row;
+  }
+  const double* X = src_col(J.X, n, g, mm_slot(T, mu), 0) + row;
+  double* t = J.tbuf + ((long long)g * J.nA + ei) * J.RT * J.CT;
+  const int gi = lane >> 2, ti = lane & 3;
+  const int ta = (r + 7) >> 3, tb = (c + 7) >> 3;
+  double acc[TMAX][TMAX][2];
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+    for (int b = 0; b < TMAX; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const double* fc[TMAX];
+  const double* xc[TMAX];
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a) {
+    const int ca = a * 8 + gi;
+    fc[a] = (a < ta && ca < r) ? F + (long long)ca * n : nullptr;
+    xc[a] = (a < tb && ca < c) ? X + (long long)ca * n : nullptr;
+  }
+  for (int k0 = 0; k0 < len; k0 += 4) {
+    const int k = k0 + ti;
+    double av[TMAX], bv[TMAX];
+#pragma unroll
+    for (int a = 0; a < TMAX; ++a) {
+      av[a] = (fc[a] && k < len) ? fc[a][k] : 0.0;
+      bv[a] = (xc[a] && k < len) ? xc[a][k] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+      for (int b = 0; b < TMAX; ++b)
+        if (a < ta && b < tb)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+                       "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1]) : "d"(av[a]), "d"(bv[b]));
+  }
+  // accumulator fragment: row gi, columns 2 ti, 2 ti + 1 of every 8 x 8 tile
+#pragma unroll
+  for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+    for (int b = 0; b < TMAX; ++b)
+      if (a < ta && b < tb) {
+        const int x = a * 8 + gi, y = b * 8 + 2 * ti;
+        if (x < r && y < c) t[x * J.CT + y] = acc[a][b][0];
+        if (x < r && y + 1 < c) t[x * J.CT + y + 1] = acc[a][b][1];
+      }
+}
+
 // Fallback phase B (trees deeper than 16; k_hmatB_sm below is the main path).
 // Register tile of phase B: one thread = one leaf row i x HB_CB columns of
 // one subtree root.  The leaf row and every ancestor U (V) row element are
@@ -593,7 +674,13 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     dim3 g(nA, nelem, njobs);
     static const bool tc_off = getenv("ACR_HMATA_SCALAR") != nullptr;   // A/B aid
     const int tmax = ((rtmax > cmax ? rtmax : cmax) + 7) / 8;
-    if (!tc_off && tmax <= 4) {
+    static const long long wmin = getenv("ACR_HMATA_WMIN") ? atoll(getenv("ACR_HMATA_WMIN")) : 10000;
+    if (!tc_off && tmax <= 2 && (long long)nA * nelem * njobs >= wmin) {
+      // throughput-bound launch: a warp per (entry, element), 8 per CTA
+      dim3 gw((nA + 7) / 8, nelem, njobs);
+      if (tmax <= 1) CK_PDL(launch_pdl(k_hmatA_tcw<1>, gw, dim3(256), 0, st, T, JJ));
+      else CK_PDL(launch_pdl(k_hmatA_tcw<2>, gw, dim3(256), 0, st, T, JJ));
+    } else if (!tc_off && tmax <= 4) {
       if (tmax <= 1) CK_PDL(launch_pdl(k_hmatA_tc<128, 1>, g, dim3(128), 0, st, T, JJ));
       else if (tmax <= 2) CK_PDL(launch_pdl(k_hmatA_tc<128, 2>, g, dim3(128), 0, st, T, JJ));
       else CK_PDL(launch_pdl(k_hmatA_tc<128, 4>, g, dim3(128), 0, st, T, JJ));
