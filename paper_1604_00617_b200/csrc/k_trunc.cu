@@ -1024,10 +1024,14 @@ __device__ __forceinline__ int acquire_slots(unsigned long long* mask, int ns, i
     int s = -1;
     if (lane == 0) {
       const unsigned long long m = atomicAdd(mask, 0ull);
-      // bit k of run: slots k .. k+ns-1 all free (shifts bring in used bits)
+      // bit k of run: slots k .. k+ns-1 all free (the shifts bring in zeros =
+      // used), by doubling: O(log ns) steps for the warps that spin here
       unsigned long long run = ~m;
-      for (int i = 1; i < ns; ++i) run &= ~m >> i;
-      if (ns > 1) run &= ~0ull >> (ns - 1);
+      for (int have = 1; have < ns;) {
+        const int step = have < ns - have ? have : ns - have;
+        run &= run >> step;
+        have += step;
+      }
       if (run) {
         s = __ffsll((long long)run) - 1;
         if (atomicCAS(mask, m, m | (want << s)) != m) s = -2;
