@@ -29,6 +29,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Two warp sums for the price of one and a half: after the first exchange the
+// lower half-warp carries a, the upper half b; four single-value rounds; one
+// broadcast each.  Every value is summed over the same tree as warp_sum
+// (lane l + lane l ^ 16 first, then 8, 4, 2, 1): bitwise the same results.
+__device__ __forceinline__ void warp_sum2(double& a, double& b, int lane) {
+  const bool hi = lane & 16;
+  const double send = hi ? a : b;                 // what the other half needs
+  const double got = __shfl_xor_sync(0xffffffffu, send, 16);
+  double v = (hi ? b : a) + got;                  // lower: a_l + a_{l+16}; upper: b_l + b_{l-16}
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  a = __shfl_sync(0xffffffffu, v, 0);
+  b = __shfl_sync(0xffffffffu, v, 16);
+}
+
 // Householder reflector of a column with head alpha and tail norm^2 ss > 0
 // (LAPACK dlarfg convention): beta = -sign(alpha) r, r = |(alpha, tail)|,
 // tau = (beta - alpha) / beta = 1 + |alpha| / r, tail scale 1 / (alpha - beta)
@@ -1105,11 +1122,7 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
       if (du) for (int i = j + 1 + lane; i < mu; i += 32) su += cu[i] * cu[i];
       if (dv) for (int i = j + 1 + lane; i < mv; i += 32) sv += cv[i] * cv[i];
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      su += __shfl_xor_sync(FULL, su, o);
-      sv += __shfl_xor_sync(FULL, sv, o);
-    }
+    warp_sum2(su, sv, lane);
     double tju = 0.0, tjv = 0.0;
     if (du) warp_reflector<MR>(cu, j, mu, su, tju, lane);
     if (dv) warp_reflector<MR>(cv, j, mv, sv, tjv, lane);
@@ -1137,11 +1150,7 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
         if (au) for (int i = j + 1 + lane; i < mu; i += 32) wu += cu[i] * ccu[i];
         if (av) for (int i = j + 1 + lane; i < mv; i += 32) wv += cv[i] * ccv[i];
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        wu += __shfl_xor_sync(FULL, wu, o);
-        wv += __shfl_xor_sync(FULL, wv, o);
-      }
+      warp_sum2(wu, wv, lane);
       if (au) {
         wu = (wu + ccu[j]) * tju;
         if constexpr (MR > 0) {
@@ -1195,11 +1204,7 @@ __device__ void warp_apply_q2(const double* Wu, int mu, int pu, const double* tu
       if (tju != 0.0) for (int i = j + 1 + lane; i < mu; i += 32) wu += vu[i] * xu[i];
       if (tjv != 0.0) for (int i = j + 1 + lane; i < mv; i += 32) wv += vv[i] * xv[i];
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      wu += __shfl_xor_sync(FULL, wu, o);
-      wv += __shfl_xor_sync(FULL, wv, o);
-    }
+    warp_sum2(wu, wv, lane);
     if (tju != 0.0) {
       wu = (wu + xu[j]) * tju;
       if constexpr (MR > 0) {
