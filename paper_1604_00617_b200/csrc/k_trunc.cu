@@ -46,6 +46,37 @@ __device__ __forceinline__ void warp_sum2(double& a, double& b, int lane) {
   b = __shfl_sync(0xffffffffu, v, 16);
 }
 
+// N (2, 4 or 8) warp sums at once by halving: at every exchange half the
+// lanes keep one half of the values, so N sums cost N - 1 exchanges, the
+// remaining single-value rounds and N broadcasts instead of 5 N exchanges.
+// Every value is summed over the same tree as warp_sum: bitwise the same.
+template <int N>
+__device__ __forceinline__ void warp_sum_multi(double (&v)[N], int lane) {
+  static_assert(N == 2 || N == 4 || N == 8, "N");
+  int o = 16;
+#pragma unroll
+  for (int n = N; n > 1; n >>= 1, o >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int k = 0; k < n / 2; ++k) {
+      const double send = hi ? v[k] : v[k + n / 2];
+      const double got = __shfl_xor_sync(0xffffffffu, send, o);
+      v[k] = (hi ? v[k + n / 2] : v[k]) + got;
+    }
+  }
+  for (; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  // lane bits 4, 3, 2 (for N = 8) name the value a lane ended up with
+  const double mine = v[0];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    int src = 0;
+    if (N >= 2 && (i & (N / 2))) src |= 16;
+    if (N >= 4 && (i & (N / 4))) src |= 8;
+    if (N >= 8 && (i & (N / 8))) src |= 4;
+    v[i] = __shfl_sync(0xffffffffu, mine, src);
+  }
+}
+
 // Householder reflector of a column with head alpha and tail norm^2 ss > 0
 // (LAPACK dlarfg convention): beta = -sign(alpha) r, r = |(alpha, tail)|,
 // tau = (beta - alpha) / beta = 1 + |alpha| / r, tail scale 1 / (alpha - beta)
@@ -1280,27 +1311,21 @@ __device__ __forceinline__ void warp_out_reg(const double* Wu, const double* Wv,
       au[h] = i > j ? vu[i] : (i == j ? 1.0 : 0.0);
       av[h] = i > j ? vv[i] : (i == j ? 1.0 : 0.0);
     }
-    double wu[KC], wv[KC];
+    double w[2 * KC];                             // [c]: U side, [KC + c]: V side
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
-      wu[c] = 0.0;
-      wv[c] = 0.0;
+      w[c] = 0.0;
+      w[KC + c] = 0.0;
 #pragma unroll
       for (int h = 0; h < MR; ++h) {
-        wu[c] = fma(au[h], xu[c][h], wu[c]);
-        wv[c] = fma(av[h], xv[c][h], wv[c]);
+        w[c] = fma(au[h], xu[c][h], w[c]);
+        w[KC + c] = fma(av[h], xv[c][h], w[KC + c]);
       }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1)
-#pragma unroll
-      for (int c = 0; c < KC; ++c) {
-        wu[c] += __shfl_xor_sync(FULL, wu[c], o);
-        wv[c] += __shfl_xor_sync(FULL, wv[c], o);
-      }
+    warp_sum_multi<2 * KC>(w, lane);
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
-      const double gu = wu[c] * tju, gv = wv[c] * tjv;
+      const double gu = w[c] * tju, gv = w[KC + c] * tjv;
 #pragma unroll
       for (int h = 0; h < MR; ++h) {
         xu[c][h] = fma(-gu, au[h], xu[c][h]);
