@@ -1164,7 +1164,58 @@ __device__ void warp_qr2(double* Wu, int mu, double* tu, double* Wv, int mv, dou
     __syncwarp();
     const bool au = du && tju != 0.0, av = dv && tjv != 0.0;
     if (!au && !av) continue;
-    for (int c = j + 1; c < R; ++c) {
+    int cfirst = j + 1;
+    if constexpr (MR > 0) {
+      // four trailing columns per pass: the reflector is read once for the
+      // four, their eight sums are reduced together (warp_sum_multi), the
+      // updates follow; per column the same operations in the same order
+      for (; cfirst + 3 < R; cfirst += 4) {
+        double w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = 0.0;
+        double ru[MR], rv[MR];
+#pragma unroll
+        for (int h = 0; h < MR; ++h) {
+          const int i = lane + 32 * h;
+          ru[h] = (au && i > j) ? cu[i] : 0.0;
+          rv[h] = (av && i > j) ? cv[i] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double* ccu = Wu + (long long)(cfirst + q) * mu;
+          const double* ccv = Wv + (long long)(cfirst + q) * mv;
+#pragma unroll
+          for (int h = 0; h < MR; ++h) {
+            const int i = lane + 32 * h;
+            if (i > j) {
+              if (au) w[q] += ru[h] * ccu[i];
+              if (av) w[4 + q] += rv[h] * ccv[i];
+            }
+          }
+        }
+        warp_sum_multi<8>(w, lane);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double* ccu = Wu + (long long)(cfirst + q) * mu;
+          double* ccv = Wv + (long long)(cfirst + q) * mv;
+          if (au) {
+            const double wu = (w[q] + ccu[j]) * tju;
+#pragma unroll
+            for (int h = 0; h < MR; ++h)
+              if (lane + 32 * h > j) ccu[lane + 32 * h] -= wu * ru[h];
+            if (lane == 0) ccu[j] -= wu;
+          }
+          if (av) {
+            const double wv = (w[4 + q] + ccv[j]) * tjv;
+#pragma unroll
+            for (int h = 0; h < MR; ++h)
+              if (lane + 32 * h > j) ccv[lane + 32 * h] -= wv * rv[h];
+            if (lane == 0) ccv[j] -= wv;
+          }
+        }
+      }
+    }
+    for (int c = cfirst; c < R; ++c) {
       double* ccu = Wu + (long long)c * mu;
       double* ccv = Wv + (long long)c * mv;
       double wu = 0.0, wv = 0.0;
