@@ -502,3 +502,75 @@ def test_fused_forward_sweep_bitwise(solver_mod):
         sol.solve()                  # consumed
     sol.factor(bands, rhs=f[:, 1].contiguous())
     np.testing.assert_array_equal(sol.solve().cpu().numpy(), sol.solve(f[:, 1].contiguous()).cpu().numpy())
+
+
+def _solve_with_env(solver_mod, env, s, eps, leaf):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:                                   # the switches are read at plan creation
+        return solver_mod.acr_solve(s, Tolerance(eps), leaf_size=leaf)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_side_stream_schedules(solver_mod):
+    """The side-stream schedules only reorder independent launches.  Running
+    the queue kernels beside the warp kernel changes no launch, so the result,
+    the ranks and the report are bitwise those of the serial order.  The
+    deferred recompressions and multiply's per-depth chains split a launch by
+    tree depth, and a smaller launch may take another recompression kernel
+    (one CTA per task instead of a warp per task: same algorithm, another
+    summation order), as may the fused leaf-pair Schur step: equal to
+    roundoff, same rank decisions.  Every schedule is reproducible run to
+    run."""
+    c = P.CONFIGS["cfg3"]
+    s = P.make_config("cfg3")
+    a, ra = solver_mod.acr_solve(s, Tolerance(c["eps"]), leaf_size=c["leaf"])
+    a2, _ = solver_mod.acr_solve(s, Tolerance(c["eps"]), leaf_size=c["leaf"])
+    np.testing.assert_array_equal(a, a2)
+    b, rb = _solve_with_env(solver_mod, {"ACR_NO_QSTREAMS": "1"}, s, c["eps"], c["leaf"])
+    np.testing.assert_array_equal(a, b)
+    assert [p.to_dict() for p in ra.per_level_ranks] == [p.to_dict() for p in rb.per_level_ranks]
+    assert (ra.max_rank, ra.storage_bytes) == (rb.max_rank, rb.storage_bytes)
+    for one in ("ACR_NO_DEFER", "ACR_NO_DSPLIT", "ACR_NO_FUSE_LEAF"):
+        u, ru = _solve_with_env(solver_mod, {one: "1"}, s, c["eps"], c["leaf"])
+        u2, _ = _solve_with_env(solver_mod, {one: "1"}, s, c["eps"], c["leaf"])
+        np.testing.assert_array_equal(u, u2)
+        assert _rel(u, a) <= 1e-8, one
+        assert [p.max_by_depth for p in ru.per_level_ranks] == \
+            [p.max_by_depth for p in ra.per_level_ranks], one
+
+
+def test_deferred_and_per_depth_launches_bitwise(solver_mod):
+    """With the launch-size dependent kernel choice switched off (plan option
+    5 = 0: no one-CTA-per-task launches, every task is routed by its own
+    size), splitting a recompression launch by tree depth changes no task's
+    arithmetic: the deferred Schur-complement recompressions and multiply's
+    per-depth chains must then reproduce the serial schedule bit for bit --
+    any ordering bug between the streams would show here."""
+    c = P.CONFIGS["cfg3"]
+    s = P.make_config("cfg3")
+
+    def run(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            sol = solver_mod.AcrSolver(s.n_blocks, s.block_dim, Tolerance(c["eps"]), 1, c["leaf"])
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        sol.lib.acr_plan_set_option(sol.plan, 5, 0)
+        sol.factor(sol.device_bands(s))
+        return sol.solve(torch.as_tensor(s.rhs, device="cuda")).cpu().numpy()
+
+    ref = run({"ACR_NO_DEFER": "1", "ACR_NO_DSPLIT": "1", "ACR_NO_QSTREAMS": "1"})
+    for env in ({}, {"ACR_NO_DEFER": "1"}, {"ACR_NO_DSPLIT": "1"}):
+        for _ in range(2):
+            np.testing.assert_array_equal(run(env), ref)
