@@ -378,6 +378,7 @@ struct Level {
 struct Record {
   int m = 0, first = 0, mg = 0;
   bool right = false;               // a right neighbour (other rank) exists
+  bool diagEF = false;              // E, F are the lifted level's diagonals (rank 0, diagonal leaves)
   Batch Dinv, E, F;
   std::vector<int> hDinv, hE, hF;   // host ranks (storage accounting)
 };
@@ -1654,6 +1655,7 @@ struct Plan {
     rec.m = mm;
     rec.first = first;
     rec.mg = mg;
+    rec.diagEF = lvl == 0;
     rec.right = right;
     rec.Dinv.alloc(ht, ne, Rout, st);
     {
@@ -2050,6 +2052,29 @@ struct Plan {
     hmat(&J, 1, G, s ? s : st);
   }
 
+  // E / F of the lifted level are diagonal (from_diagonal, hodlr.py:294-314):
+  // their products with a right-hand-side panel are row scalings (bitwise the
+  // dense leaf products), reading n values per block instead of n x bw
+  void hmat_full_d(bool diag, const HB* H, int G, int R, Src X, Src Y, int k,
+                   double* tbuf = nullptr, cudaStream_t s = nullptr) {
+    static const bool off = getenv("ACR_NO_SOLVE_DIAG") != nullptr;   // A/B aid
+    if (!diag || off) return hmat_full(H, G, R, X, Y, k, tbuf, s);
+    if (G <= 0) return;
+    MMJob J;
+    memset(&J, 0, sizeof(J));
+    J.H = H;
+    J.X = X;
+    J.Y = Y;
+    J.cols_fixed = k;
+    J.alpha = 1.0;
+    J.mu0 = 0;
+    J.mu1 = 1;
+    kbegin(3);
+    CK(launch_hmat_diag(dt.T, J, G, s ? s : st));
+    kend();
+    ++launches;
+  }
+
   // ---- forward sweep fused into factor() (single GPU): right after level
   //      l's record is complete, its RHS update (reduction.py:204-216) runs
   //      on a side stream, overlapping the factorisation of the next levels
@@ -2115,9 +2140,9 @@ struct Plan {
     double* fl = ffs[l].as<double>();
     hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl, 2 * kn, k), s_pan(z.as<double>(), kn, k), k,
               t1.as<double>(), stf);
-    hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k),
+    hmat_full_d(r.diagEF, tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k),
               k, t2.as<double>(), stf);
-    hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k),
+    hmat_full_d(r.diagEF, tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k),
               s_pan(bb.as<double>(), kn, k), k, t3.as<double>(), stf);
     double* fn = ffs[l + 1].as<double>();
     CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, bb.as<double>(), kn, fn, kn, nq,
@@ -2219,10 +2244,10 @@ struct Plan {
         tp->exchange(msgs, st);
       }
       Dev tE = make_tab({{&r.E, 1, 2, no}});
-      hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
+      hmat_full_d(r.diagEF, tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
       // F_j z_{j+1}: z index i+1 (the halo slot ne for the right neighbour's block)
       Dev tF = make_tab({{&r.F, 1, 2, nq}});
-      hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k), s_pan(bb.as<double>(), kn, k), k);
+      hmat_full_d(r.diagEF, tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k), s_pan(bb.as<double>(), kn, k), k);
       f[l + 1].alloc(sizeof(double) * kn * std::max(no, 1), st);
       double* fn = f[l + 1].as<double>();
       CK(launch_rhs_combine(fl + kn, 2 * kn, a.as<double>(), kn, bb.as<double>(), kn, fn, kn, nq, (int)kn, st));
@@ -2311,14 +2336,14 @@ struct Plan {
       CK(cudaMemsetAsync(a.p, 0, sizeof(double) * kn * ne, st));
       CK(cudaMemsetAsync(b.p, 0, sizeof(double) * kn * ne, st));
       Dev tE = make_tab({{&r.E, 2, 2, ne - 1}});
-      hmat_full(tE.as<HB>(), ne - 1, r.E.R, s_pan(ul + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
+      hmat_full_d(r.diagEF, tE.as<HB>(), ne - 1, r.E.R, s_pan(ul + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
       if (r.first > 0) {
         Dev tE0 = make_tab({{&r.E, 0, 1, 1}});
-        hmat_full(tE0.as<HB>(), 1, r.E.R, s_pan(uleft.as<double>(), kn, k),
+        hmat_full_d(r.diagEF, tE0.as<HB>(), 1, r.E.R, s_pan(uleft.as<double>(), kn, k),
                   s_pan(a.as<double>(), kn, k), k);
       }
       Dev tF = make_tab({{&r.F, 0, 2, nb}});
-      hmat_full(tF.as<HB>(), nb, r.F.R, s_pan(ul + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
+      hmat_full_d(r.diagEF, tF.as<HB>(), nb, r.F.R, s_pan(ul + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
       Dev rr(sizeof(double) * kn * ne, st);
       CK(launch_rhs_combine(f[lv].as<double>(), 2 * kn, a.as<double>(), kn, b.as<double>(), kn,
                             rr.as<double>(), kn, ne, (int)kn, st));
@@ -2446,9 +2471,9 @@ struct Plan {
     hmat_full(tDi.as<HB>(), ne, r.Dinv.R, s_pan(fl.as<double>(), 2 * kn, k),
               s_pan(z.as<double>(), kn, k), k);
     Dev tE = make_tab({{&r.E, 1, 2, no}});
-    hmat_full(tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
+    hmat_full_d(r.diagEF, tE.as<HB>(), no, r.E.R, s_pan(z.as<double>(), kn, k), s_pan(a.as<double>(), kn, k), k);
     Dev tF = make_tab({{&r.F, 1, 2, nq}});
-    hmat_full(tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k),
+    hmat_full_d(r.diagEF, tF.as<HB>(), nq, r.F.R, s_pan(z.as<double>() + kn, kn, k),
               s_pan(bb.as<double>(), kn, k), k);
     Dev fn(sizeof(double) * kn * std::max(no, 1), st);
     const double* f1 = fl.as<double>() + kn;
@@ -2483,9 +2508,9 @@ struct Plan {
     CK(cudaMemsetAsync(b.p, 0, sizeof(double) * kn * ne, st));
     double* up = ul.as<double>();
     Dev tE = make_tab({{&r.E, 2, 2, ne - 1}});
-    hmat_full(tE.as<HB>(), ne - 1, r.E.R, s_pan(up + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
+    hmat_full_d(r.diagEF, tE.as<HB>(), ne - 1, r.E.R, s_pan(up + kn, 2 * kn, k), s_pan(a.as<double>() + kn, kn, k), k);
     Dev tF = make_tab({{&r.F, 0, 2, nb}});
-    hmat_full(tF.as<HB>(), nb, r.F.R, s_pan(up + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
+    hmat_full_d(r.diagEF, tF.as<HB>(), nb, r.F.R, s_pan(up + kn, 2 * kn, k), s_pan(b.as<double>(), kn, k), k);
     CK(launch_rhs_combine(fl.as<double>(), 2 * kn, a.as<double>(), kn, b.as<double>(), kn,
                           rr.as<double>(), kn, ne, (int)kn, st));
     Dev tDi = make_tab({{&r.Dinv, 0, 1, ne}});

@@ -620,6 +620,211 @@ __global__ void __launch_bounds__(NTB) k_hmatB_sm(TreeDev T, MMJobs2 JJ, int pat
   }
 }
 
+__device__ __forceinline__ void hb_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+               "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// Phase B on the FP64 tensor pipe (leaves of at most 64 rows).  The leaf is
+// staged in shared memory once (16-byte cp.async, one warp request per row;
+// row pitch = 4 mod 16 doubles so the mma.sync m8n8k4 fragment reads -- 8 rows
+// x 4 columns, or 4 x 8 transposed -- touch 16 distinct bank pairs per half
+// warp).  Warp w owns rows 8w .. 8w+7.  The columns of ALL roots are packed
+// into one list cut into 8-column tiles (a root of three columns does not pay
+// for eight: the FP64 tensor pipe is only as fast as the FMA pipe, padding is
+// not free); X is staged per window of W tiles, column-major with the leaf's
+// pitch, and every warp takes the window's tiles two at a time (independent
+// DMMA chains).  The ancestors' terms sum_k U_k t_k are one product over the
+// concatenated inner index (k, a) -- a flat table, so the loads of a tile are
+// independent of one another; a column stops contributing at its own root
+// (zero B fragments above it) -- chained onto the same accumulators, deepest
+// ancestor first.
+static constexpr int HB_FLAT = 512;
+static constexpr int HB_COLS = 256;
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, int path, int W,
+                                                        int ldl) {
+  ACR_PDL_ENTRY();
+  constexpr bool AREG = MINB < 5;       // leaf fragments kept in registers
+  extern __shared__ double sm[];
+  const MMJob& J = JJ.j[blockIdx.z];
+  const int g = blockIdx.y, bw = T.bw, n = T.n;
+  __shared__ HBRoots R;
+  __shared__ HBAnc A;
+  __shared__ int fl_n[17];              // flat inner length of the ancestors 1 .. k
+  __shared__ int fl_ka[HB_FLAT];        // (k << 16) | a
+  __shared__ int col_qb[HB_COLS];       // packed column -> (root q << 16) | column of the root
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = lane >> 2, ti = lane & 3;
+  if (threadIdx.x < 32) hb_roots_shared(T, J, g, path, R);
+  __syncthreads();
+  if (!R.cnt) return;
+  double* L = sm;                 // bw x ldl
+  double* X = L + bw * ldl;       // 8 W x ldl, column-major
+  const HB h = J.H[g];
+  const int lam = R.lam, lo = T.lo[lam], s = T.hi[lam] - lo;
+  {
+    const double* Lg = h.leaf + (long long)lo * bw;
+    if (!(s & 1)) {
+      const int ch = s >> 1;      // 16-byte chunks per row
+      for (int idx = threadIdx.x; idx < s * ch; idx += 256) {
+        const int ii = idx / ch, c = idx - ii * ch;
+        cp_async16(L + ii * ldl + 2 * c, Lg + (long long)ii * bw + 2 * c);
+      }
+    } else {
+      for (int ii = warp; ii < s; ii += 8)
+        for (int j = lane; j < s; j += 32)
+          cp_async8(L + ii * ldl + j, Lg + (long long)ii * bw + j, true);
+    }
+  }
+  hb_anc_tables(T, J, h, g, R, lo, A);
+  int ntot = 0;
+  for (int q = 0; q < R.cnt; ++q) {
+    const int nc = R.cols[q];
+    for (int b = threadIdx.x; b < nc; b += 256)
+      if (ntot + b < HB_COLS) col_qb[ntot + b] = (q << 16) | b;
+    ntot += nc;
+  }
+  if (ntot > HB_COLS) ntot = HB_COLS;   // (the launcher keeps maxdepth * cmax <= HB_COLS)
+  __syncthreads();
+  {
+    // flat (k, a) table of the ancestors' inner index, k ascending
+    const int dl = T.depth[lam];
+    int pre = 0;
+    for (int k = 1; k <= dl && k < 17; ++k) {
+      const int r = A.r[k];
+      for (int a2 = threadIdx.x; a2 < r; a2 += 256)
+        if (pre + a2 < HB_FLAT) fl_ka[pre + a2] = (k << 16) | a2;
+      pre += r;
+      if (threadIdx.x == 0) fl_n[k] = pre < HB_FLAT ? pre : HB_FLAT;
+    }
+    if (threadIdx.x == 0) fl_n[0] = 0;
+  }
+  const int i = warp * 8 + gi;
+  const bool rowok = i < s;
+  const double* Fb = (J.trans ? h.V : h.U) + i;
+  const double* La = J.trans ? L + i : L + i * ldl;
+  const int lj = J.trans ? ldl : 1;
+  double a[AREG ? 16 : 1];
+  for (int w0 = 0; w0 < ntot; w0 += 8 * W) {
+    const int wn = ntot - w0 < 8 * W ? ntot - w0 : 8 * W;
+    for (int j = warp; j < wn; j += 8) {
+      const int qb = col_qb[w0 + j];
+      const double* src = src_col(J.X, n, g, R.slot[qb >> 16], qb & 0xffff) + lo;
+      for (int ii = lane; ii < s; ii += 32) cp_async8(X + j * ldl + ii, src + ii, true);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (AREG && w0 == 0) {
+#pragma unroll
+      for (int kk = 0; kk < (AREG ? 16 : 1); ++kk) {
+        const int j = kk * 4 + ti;
+        a[kk] = (rowok && j < s) ? La[j * lj] : 0.0;
+      }
+    }
+    if (warp * 8 < s && wn <= 2) {
+      // one or two columns in all (rank-1 levels): an 8-column tile would be
+      // mostly padding, so the same lane layout runs on the FMA pipe -- lane
+      // (gi, ti) sums the inner indices = ti mod 4, two shuffles finish a row
+      const int qb0 = col_qb[w0], qb1 = col_qb[w0 + wn - 1];
+      const double* x1 = X + (wn - 1) * ldl;
+      double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int j = kk * 4 + ti;
+        if (j < s) {
+          double av;
+          if constexpr (AREG) av = a[kk];
+          else av = rowok ? La[j * lj] : 0.0;
+          p0 = fma(av, X[j], p0);
+          p1 = fma(av, x1[j], p1);
+        }
+      }
+      const int f0 = fl_n[R.steps[qb0 >> 16]], f1 = fl_n[R.steps[qb1 >> 16]];
+      const int fm = f0 > f1 ? f0 : f1;
+      const double* const* tp0 = A.t[qb0 >> 16];
+      const double* const* tp1 = A.t[qb1 >> 16];
+      const int c0 = qb0 & 0xffff, c1 = qb1 & 0xffff;
+#pragma unroll 2
+      for (int idx = ti; idx < fm; idx += 4) {
+        const int ka = fl_ka[idx];
+        const int k = ka >> 16, aa = ka & 0xffff;
+        const double f = rowok ? Fb[A.F[k] + (long long)aa * n] : 0.0;
+        if (idx < f0) p0 = fma(f, __ldg(tp0[k] + aa * J.CT + c0), p0);
+        if (idx < f1) p1 = fma(f, __ldg(tp1[k] + aa * J.CT + c1), p1);
+      }
+      p0 += __shfl_xor_sync(0xffffffffu, p0, 1);
+      p1 += __shfl_xor_sync(0xffffffffu, p1, 1);
+      p0 += __shfl_xor_sync(0xffffffffu, p0, 2);
+      p1 += __shfl_xor_sync(0xffffffffu, p1, 2);
+      if (rowok && ti == 0)
+        src_col(J.Y, n, g, R.slot[qb0 >> 16], c0)[lo + i] = J.alpha * p0;
+      if (rowok && ti == 1 && wn > 1)
+        src_col(J.Y, n, g, R.slot[qb1 >> 16], c1)[lo + i] = J.alpha * p1;
+    } else if (warp * 8 < s) {
+      for (int t0 = 0; t0 < wn; t0 += 16) {
+        const bool two = t0 + 8 < wn;
+        const int jA = t0 + gi, jB = t0 + 8 + gi;
+        const bool okA = jA < wn, okB = jB < wn;
+        const int qbA = col_qb[w0 + (okA ? jA : t0)], qbB = col_qb[w0 + (okB ? jB : t0)];
+        const double* xA = X + (okA ? jA : t0) * ldl;
+        const double* xB = X + (okB ? jB : t0) * ldl;
+        double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const int j = kk * 4 + ti;
+          if (kk * 4 < s) {
+            double av;
+            if constexpr (AREG) av = a[kk];
+            else av = (rowok && j < s) ? La[j * lj] : 0.0;
+            const double b0 = (okA && j < s) ? xA[j] : 0.0;
+            hb_dmma(y00, y01, av, b0);
+            if (two) {
+              const double b1 = (okB && j < s) ? xB[j] : 0.0;
+              hb_dmma(y10, y11, av, b1);
+            }
+          }
+        }
+        // per-lane column: its root's flat length and t panels
+        const int fA = okA ? fl_n[R.steps[qbA >> 16]] : 0;
+        const int fB = okB ? fl_n[R.steps[qbB >> 16]] : 0;
+        const int fm = __reduce_max_sync(0xffffffffu, fA > fB ? fA : fB);
+        const double* const* tA = A.t[qbA >> 16];
+        const double* const* tB = A.t[qbB >> 16];
+        const int cA = qbA & 0xffff, cB = qbB & 0xffff;
+#pragma unroll 2
+        for (int a0 = 0; a0 < fm; a0 += 4) {
+          const int idx = a0 + ti;
+          const int ka = idx < fm ? fl_ka[idx] : (1 << 16);
+          const int k = ka >> 16, aa = ka & 0xffff;
+          const double f = (idx < fm && rowok) ? Fb[A.F[k] + (long long)aa * n] : 0.0;
+          const double t0v = idx < fA ? __ldg(tA[k] + aa * J.CT + cA) : 0.0;
+          hb_dmma(y00, y01, f, t0v);
+          if (two) {
+            const double t1v = idx < fB ? __ldg(tB[k] + aa * J.CT + cB) : 0.0;
+            hb_dmma(y10, y11, f, t1v);
+          }
+        }
+        if (rowok) {
+          const int c = t0 + 2 * ti;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = c + (e & 1) + (e >> 1) * 8;
+            if (j < wn) {
+              const int qb = col_qb[w0 + j];
+              const double y = e == 0 ? y00 : e == 1 ? y01 : e == 2 ? y10 : y11;
+              src_col(J.Y, n, g, R.slot[qb >> 16], qb & 0xffff)[lo + i] = J.alpha * y;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // HODLR x panel with a DIAGONAL HODLR operand (level 0: E, F lifted from the
 // bands, diagonal leaves, rank-0 factors): every subtree product reduces to a
 // row scaling, Y[slot(mu)][:, rows(mu)] = alpha diag(H) X[slot(mu)][:, rows(mu)],
@@ -640,7 +845,7 @@ __global__ void k_hmat_diag(TreeDev T, MMJob J) {
   }
   path[np] = node;
   const double d = h.leaf[(long long)i * bw + (i - T.lo[node])];
-  for (int q = 1; q <= np; ++q) {               // mu = path[q], slot = depth(parent)
+  for (int q = 0; q <= np; ++q) {               // mu = path[q], slot = depth(parent) (root: 0)
     const int mu = path[q];
     if (mu < J.mu0 || mu >= J.mu1) continue;
     const int c = mm_cols(J, T, g, mu);
@@ -696,6 +901,9 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
   if (!attr) {
     cudaFuncSetAttribute(k_hmatB<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hmatB_sm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hmatB_tc<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hmatB<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hmatB_path<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
@@ -712,6 +920,24 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
     if (cp > (size_t)xcap) cp = xcap;
     const size_t smem = ((size_t)T.bw * cp + (size_t)T.bw * (T.bw + 1) + 1) * 8;
     dim3 g(path ? T.nleaves : nB, nelem, njobs);
+    static const bool sm_path = getenv("ACR_HMATB_SM") != nullptr;   // A/B aid
+    if (T.bw <= 64 && !sm_path && (long long)T.maxdepth * rtmax <= HB_FLAT &&
+        (long long)(path ? T.maxdepth : 1) * cmax <= HB_COLS) {
+      const int ldl = (T.bw + 11) / 16 * 16 + 4;
+      static const int xtc = getenv("ACR_HMAT_XTC") ? atoi(getenv("ACR_HMAT_XTC")) : 2;
+      // tiles (8 columns) per X window
+      int W = (int)(((size_t)cmax + 7) / 8) * (path ? T.maxdepth : 1);
+      if (W > xtc) W = xtc;
+      const size_t smtc = ((size_t)T.bw + 8 * (size_t)W) * ldl * 8;
+      static const int minb = getenv("ACR_HMAT_MINB") ? atoi(getenv("ACR_HMAT_MINB")) : 5;
+      if (minb == 5)
+        CK_PDL(launch_pdl(k_hmatB_tc<5>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl));
+      else if (minb == 4)
+        CK_PDL(launch_pdl(k_hmatB_tc<4>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl));
+      else
+        CK_PDL(launch_pdl(k_hmatB_tc<3>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl));
+      return cudaGetLastError();
+    }
     // 256 threads per leaf CTA (measured: 128 and 512 are slower)
     CK_PDL(launch_pdl(k_hmatB_sm<256>, dim3(g), dim3(256), smem, st, T, JJ, path, (int)cp));
     return cudaGetLastError();

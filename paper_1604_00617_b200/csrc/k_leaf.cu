@@ -488,7 +488,13 @@ cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
     if (bgj && s > 32) {
       // 256 threads, three CTAs per SM (measured: 128-thread CTAs at five per
       // SM are slower for batched launches too, 126 vs 85 us per 1024 leaves)
-      CK_PDL(launch_pdl(k_leafinv_bgj<256, 3>, dim3(nelem), dim3(256), 0, st, T, H, leaf, sing));
+      // ... except when the batch would take a third wave at three per SM
+      // (444 CTAs) and not at four: 64 registers, a few spills, one wave less
+      static const int four = getenv("ACR_LEAFINV_4") ? atoi(getenv("ACR_LEAFINV_4")) : 445;
+      if (four > 0 && nelem >= four)
+        CK_PDL(launch_pdl(k_leafinv_bgj<256, 4>, dim3(nelem), dim3(256), 0, st, T, H, leaf, sing));
+      else
+        CK_PDL(launch_pdl(k_leafinv_bgj<256, 3>, dim3(nelem), dim3(256), 0, st, T, H, leaf, sing));
       return cudaGetLastError();
     }
     return leafinv_reg<64>(T, H, nelem, leaf, sing, st);
