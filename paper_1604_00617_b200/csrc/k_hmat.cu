@@ -668,11 +668,10 @@ __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, i
   {
     const double* Lg = h.leaf + (long long)lo * bw;
     if (!(s & 1)) {
-      const int ch = s >> 1;      // 16-byte chunks per row
-      for (int idx = threadIdx.x; idx < s * ch; idx += 256) {
-        const int ii = idx / ch, c = idx - ii * ch;
-        cp_async16(L + ii * ldl + 2 * c, Lg + (long long)ii * bw + 2 * c);
-      }
+      // warp per row, a 16-byte chunk per lane
+      for (int ii = warp; ii < s; ii += 8)
+        for (int c = 2 * lane; c < s; c += 64)
+          cp_async16(L + ii * ldl + c, Lg + (long long)ii * bw + c);
     } else {
       for (int ii = warp; ii < s; ii += 8)
         for (int j = lane; j < s; j += 32)
@@ -772,18 +771,37 @@ __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, i
         const double* xA = X + (okA ? jA : t0) * ldl;
         const double* xB = X + (okB ? jB : t0) * ldl;
         double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;
+        if (s == 64 && !J.trans && !AREG) {
+          // full 64-row leaf, plain product: no predicates, immediate offsets
+          // (unstaged X columns of a ragged last tile are never stored)
+          const double* la = La + ti;
+          const double* xa = xA + ti;
+          const double* xb = xB + ti;
+          if (two) {
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const int j = kk * 4 + ti;
-          if (kk * 4 < s) {
-            double av;
-            if constexpr (AREG) av = a[kk];
-            else av = (rowok && j < s) ? La[j * lj] : 0.0;
-            const double b0 = (okA && j < s) ? xA[j] : 0.0;
-            hb_dmma(y00, y01, av, b0);
-            if (two) {
-              const double b1 = (okB && j < s) ? xB[j] : 0.0;
-              hb_dmma(y10, y11, av, b1);
+            for (int kk = 0; kk < 16; ++kk) {
+              const double av = la[kk * 4];
+              hb_dmma(y00, y01, av, okA ? xa[kk * 4] : 0.0);
+              hb_dmma(y10, y11, av, okB ? xb[kk * 4] : 0.0);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) hb_dmma(y00, y01, la[kk * 4], okA ? xa[kk * 4] : 0.0);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) {
+            const int j = kk * 4 + ti;
+            if (kk * 4 < s) {
+              double av;
+              if constexpr (AREG) av = a[kk];
+              else av = (rowok && j < s) ? La[j * lj] : 0.0;
+              const double b0 = (okA && j < s) ? xA[j] : 0.0;
+              hb_dmma(y00, y01, av, b0);
+              if (two) {
+                const double b1 = (okB && j < s) ? xB[j] : 0.0;
+                hb_dmma(y10, y11, av, b1);
+              }
             }
           }
         }
