@@ -81,7 +81,7 @@ __device__ __forceinline__ const int* rank_base(const RankRef& r, int g) {
 }
 
 // Slot / rank selection rules for truncation operands.
-enum { SEL_OWN = 0, SEL_ANC = 1, SEL_FIXED = 2 };
+enum { SEL_OWN = 0, SEL_ANC = 1, SEL_FIXED = 2, SEL_NODE = 3 };
 
 struct TOp {
   Src U, V;
@@ -89,6 +89,8 @@ struct TOp {
   int sel;        // SEL_OWN: slot depth(beta), rank (beta, side)
                   // SEL_ANC: alpha = anc(beta, t): slot depth(alpha), rank [alpha][child of alpha holding beta]
                   // SEL_FIXED: slot depth(node), rank (node, fside) if (node, 1-fside) != 0 else 0
+                  // SEL_NODE: slot depth(node), rank (node, fside) as stored (a snapshot that
+                  //           already carries the SEL_FIXED rule)
   int t;
   int node;
   int fside;

@@ -1259,6 +1259,7 @@ struct Plan {
     double *P1, *P2, *P3, *tb;
     long long ps;
     int* sing;
+    int* rs = nullptr;   // rank snapshot [g][nnodes][2] (see inv_node: b11 beside b12 / b21)
     bool pend = false;   // S's off-diagonal recompressions still running on the side stream
     bool defer[32] = {}; // tree depths whose recompressions run on the deferred stream
   };
@@ -1285,6 +1286,7 @@ struct Plan {
     int maxA = 1;
     for (int v = 0; v < ht.nnodes; ++v) maxA = std::max(maxA, ht.nA(v, v + 1));
     c.tb = scratch<double>(9, (size_t)G * maxA * R * R);
+    c.rs = scratch<int>(25, (size_t)G * ht.nnodes * 2);
     c.sing = sing;
     inv_node(c, 0);
     settle(c);
@@ -1336,7 +1338,8 @@ struct Plan {
   // add_lowrank(H_mu, (U, V)) with rank (nu, fside) if (nu, 1-fside) != 0:
   // factor recompressions on st, the leaves' dense update on s2 (disjoint
   // data); the caller joins s2
-  void inv_lowrank(InvCtx& c, int nu, int mu, Src U, Src V, int fside, cudaStream_t s2) {
+  void inv_lowrank(InvCtx& c, int nu, int mu, Src U, Src V, int fside, cudaStream_t s2,
+                   const int* snap = nullptr) {
     fork(s2);
     leaflr(c.H, c.G, mu, U, V, r_hb(c.H), nu, fside, s2);
     int t0 = ht.startA[mu], t1 = ht.startA[mu + 1];
@@ -1349,6 +1352,11 @@ struct Plan {
       a.b.sel = SEL_FIXED;
       a.b.node = nu;
       a.b.fside = fside;
+      if (snap) {
+        // ranks of nu from the snapshot (the caller overwrites them concurrently)
+        a.b.rank = r_arr(snap, (long long)ht.nnodes * 2);
+        a.b.sel = SEL_NODE;
+      }
       run_trunc(a, t0, t1, c.H, c.G, c.R, c.R);
     }
   }
@@ -1458,9 +1466,15 @@ struct Plan {
       j.W = P1; j.hw = 0;
       j.Z = P3;
       j.alpha = 1.0;
+      // the column count of G / Hh -- rank(nu, 1), or 0 when rank(nu, 0) is --
+      // is written to the snapshot: b11's recompressions below run beside the
+      // b12 / b21 truncation, which overwrites the ranks of nu
+      j.orank = c.rs;
+      j.ors = (long long)ht.nnodes * 2;
+      j.oside = 1;
       gp(&j, 1, dt.d_iota + nu, 1, c.G, c.R, c.R, st);
     }
-    inv_lowrank(c, nu, a0, P3, P2, 1, s2);             // b11 = x11 + G Hh^T
+    inv_lowrank(c, nu, a0, P3, P2, 1, s2, c.rs);       // b11 = x11 + G Hh^T
     TruncArgs a;                                       // b12, b21 (independent of b11)
     memset(&a, 0, sizeof(a));
     a.mode = TM_TRUNCATE;

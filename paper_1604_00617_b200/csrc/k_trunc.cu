@@ -142,7 +142,7 @@ __device__ __forceinline__ OpRes resolve_op(const TOp& op, const TreeDev& T,
   } else {
     slot = T.depth[op.node];
     r = rb[op.node * 2 + op.fside];
-    if (rb[op.node * 2 + 1 - op.fside] == 0) r = 0;
+    if (op.sel == SEL_FIXED && rb[op.node * 2 + 1 - op.fside] == 0) r = 0;
   }
   OpRes o;
   o.r = r;
