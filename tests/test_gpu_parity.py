@@ -388,6 +388,27 @@ def test_multi_rhs_columns_match_single_solves(solver_mod):
         assert _rel(u3[:, j], uj) <= 1e-13
 
 
+@pytest.mark.parametrize("n,leaf", [(50, 7), (64, 16), (128, 64)])
+def test_solve_column_counts_cover_every_panel_path(solver_mod, n, leaf):
+    """HODLR x panel phase B (k_hmatB_tc) picks its path by column count: one
+    or two columns on the FMA pipe, 8-column DMMA tiles one or two at a time,
+    several X windows beyond 16 columns; ragged trees (odd leaf sizes) take
+    the predicated fragment loads and the 8-byte staging.  Every count must
+    reproduce the single-column solves and the oracle."""
+    s = P.random_system(8, n, seed=11, k=40)
+    tol = Tolerance(1e-10)
+    sol = solver_mod.AcrSolver(s.n_blocks, s.block_dim, tol, 1, leaf)
+    sol.factor(sol.device_bands(s))
+    f = torch.as_tensor(s.rhs, device="cuda")
+    single = np.stack([sol.solve(f[:, j].contiguous()).cpu().numpy() for j in range(40)], 1)
+    uo, _ = O.acr_solve(s, tol, leaf_size=leaf)
+    assert _rel(single, uo) <= 1e-9
+    for k in (2, 3, 8, 9, 16, 17, 33, 40):
+        uk = sol.solve(f[:, :k].contiguous()).cpu().numpy()
+        assert uk.shape == (8 * n, k)
+        assert _rel(uk, single[:, :k]) <= 1e-12, k
+
+
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg5"])
 def test_config_16_rhs_against_reference(solver_mod, cfg):
     """BASELINE config 5 as benchmarked: 16 right-hand-side columns against
