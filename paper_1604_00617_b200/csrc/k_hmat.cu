@@ -113,7 +113,7 @@ template <int NT, int TMAX>
 __global__ void __launch_bounds__(NT) k_hmatA_tc(TreeDev T, MMJobs2 JJ) {
   ACR_PDL_ENTRY();
   constexpr int NW = NT / 32;
-  __shared__ double part[NW * TMAX * TMAX * 64];
+  extern __shared__ double part[];   // NW * TMAX * TMAX * 64
   const MMJob& J = JJ.j[blockIdx.z];
   if ((int)blockIdx.x >= J.nA) return;
   const int g = blockIdx.y, n = T.n;
@@ -156,22 +156,32 @@ __global__ void __launch_bounds__(NT) k_hmatA_tc(TreeDev T, MMJobs2 JJ) {
     fc[a] = (a < ta && ca < r) ? F + (long long)ca * n : nullptr;
     xc[a] = (a < tb && ca < c) ? X + (long long)ca * n : nullptr;
   }
-  for (int k0 = warp * 4; k0 < len; k0 += NW * 4) {
-    const int k = k0 + ti;
-    double av[TMAX], bv[TMAX];
+  // UL row chunks of a warp in flight: their loads are issued together (one
+  // trip to L2 per UL chunks instead of one per chunk); chunks past the end
+  // contribute exact zeros, the order of the sums is unchanged
+  constexpr int UL = TMAX >= 4 ? 2 : 4;
+  for (int k0 = warp * 4; k0 < len; k0 += NW * 4 * UL) {
+    double av[UL][TMAX], bv[UL][TMAX];
 #pragma unroll
-    for (int a = 0; a < TMAX; ++a) {
-      av[a] = (fc[a] && k < len) ? fc[a][k] : 0.0;
-      bv[a] = (xc[a] && k < len) ? xc[a][k] : 0.0;
+    for (int u = 0; u < UL; ++u) {
+      const int k = k0 + u * NW * 4 + ti;
+#pragma unroll
+      for (int a = 0; a < TMAX; ++a) {
+        av[u][a] = (fc[a] && k < len) ? fc[a][k] : 0.0;
+        bv[u][a] = (xc[a] && k < len) ? xc[a][k] : 0.0;
+      }
     }
 #pragma unroll
-    for (int a = 0; a < TMAX; ++a)
+    for (int u = 0; u < UL; ++u)
 #pragma unroll
-      for (int b = 0; b < TMAX; ++b)
-        if (a < ta && b < tb)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
-                       "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
-                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1]) : "d"(av[a]), "d"(bv[b]));
+      for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+        for (int b = 0; b < TMAX; ++b)
+          if (a < ta && b < tb)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+                         "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                         : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                         : "d"(av[u][a]), "d"(bv[u][b]));
   }
 #pragma unroll
   for (int a = 0; a < TMAX; ++a)
@@ -904,9 +914,26 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
       if (tmax <= 1) CK_PDL(launch_pdl(k_hmatA_tcw<1>, gw, dim3(256), 0, st, T, JJ));
       else CK_PDL(launch_pdl(k_hmatA_tcw<2>, gw, dim3(256), 0, st, T, JJ));
     } else if (!tc_off && tmax <= 4) {
-      if (tmax <= 1) CK_PDL(launch_pdl(k_hmatA_tc<128, 1>, g, dim3(128), 0, st, T, JJ));
-      else if (tmax <= 2) CK_PDL(launch_pdl(k_hmatA_tc<128, 2>, g, dim3(128), 0, st, T, JJ));
-      else CK_PDL(launch_pdl(k_hmatA_tc<128, 4>, g, dim3(128), 0, st, T, JJ));
+      static bool attr_a = false;
+      if (!attr_a) {
+        cudaFuncSetAttribute(k_hmatA_tc<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_hmatA_tc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_a = true;
+      }
+      // 16 warps per pair for launches of a handful of CTAs: measured no gain
+      // (most pairs of such a launch are deep nodes of 64 .. 128 rows, where
+      // the wider cross-warp sum costs what the shorter row loop saves), off
+      // unless ACR_HMATA_TINY sets a CTA-count limit
+      static const long long tiny_max = getenv("ACR_HMATA_TINY") ? atoll(getenv("ACR_HMATA_TINY")) : 0;
+      const bool tiny = (long long)nA * nelem * njobs <= tiny_max;
+      const int tm = tmax <= 1 ? 1 : tmax <= 2 ? 2 : 4;
+      const size_t sma = (size_t)(tiny ? 16 : 4) * tm * tm * 64 * 8;
+      if (tiny && tm == 4) CK_PDL(launch_pdl(k_hmatA_tc<512, 4>, g, dim3(512), sma, st, T, JJ));
+      else if (tiny && tm == 2) CK_PDL(launch_pdl(k_hmatA_tc<512, 2>, g, dim3(512), sma, st, T, JJ));
+      else if (tiny) CK_PDL(launch_pdl(k_hmatA_tc<512, 1>, g, dim3(512), sma, st, T, JJ));
+      else if (tmax <= 1) CK_PDL(launch_pdl(k_hmatA_tc<128, 1>, g, dim3(128), sma, st, T, JJ));
+      else if (tmax <= 2) CK_PDL(launch_pdl(k_hmatA_tc<128, 2>, g, dim3(128), sma, st, T, JJ));
+      else CK_PDL(launch_pdl(k_hmatA_tc<128, 4>, g, dim3(128), sma, st, T, JJ));
     } else if (nelem <= 32) CK_PDL(launch_pdl(k_hmatA<true>, dim3(g), dim3(HT), 0, st, T, JJ));
     else CK_PDL(launch_pdl(k_hmatA<false>, dim3(g), dim3(HT), 0, st, T, JJ));
     cudaError_t e = cudaGetLastError();
@@ -1075,22 +1102,31 @@ __global__ void __launch_bounds__(NT) k_gp_tc(TreeDev T, GPJobs2 JJ, const int* 
     xc[a] = (a < ta && ca < rx) ? src_col(J.X, n, g, slot, ca) + r1 : nullptr;
     yc[a] = (a < tb && ca < ry) ? src_col(J.Y, n, g, slot, ca) + r1 : nullptr;
   }
-  for (int k0 = warp * 4; k0 < l1; k0 += NW * 4) {
-    const int k = k0 + ti;
-    double av[TMAX], bv[TMAX];
+  // UL row chunks of a warp in flight (loads issued together; chunks past the
+  // end contribute exact zeros, the order of the sums is unchanged)
+  constexpr int UL = TMAX >= 4 ? 2 : 4;
+  for (int k0 = warp * 4; k0 < l1; k0 += NW * 4 * UL) {
+    double av[UL][TMAX], bv[UL][TMAX];
 #pragma unroll
-    for (int a = 0; a < TMAX; ++a) {
-      av[a] = (xc[a] && k < l1) ? xc[a][k] : 0.0;
-      bv[a] = (yc[a] && k < l1) ? yc[a][k] : 0.0;
+    for (int u = 0; u < UL; ++u) {
+      const int k = k0 + u * NW * 4 + ti;
+#pragma unroll
+      for (int a = 0; a < TMAX; ++a) {
+        av[u][a] = (xc[a] && k < l1) ? xc[a][k] : 0.0;
+        bv[u][a] = (yc[a] && k < l1) ? yc[a][k] : 0.0;
+      }
     }
 #pragma unroll
-    for (int a = 0; a < TMAX; ++a)
+    for (int u = 0; u < UL; ++u)
 #pragma unroll
-      for (int b = 0; b < TMAX; ++b)
-        if (a < ta && b < tb)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
-                       "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
-                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1]) : "d"(av[a]), "d"(bv[b]));
+      for (int a = 0; a < TMAX; ++a)
+#pragma unroll
+        for (int b = 0; b < TMAX; ++b)
+          if (a < ta && b < tb)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+                         "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                         : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                         : "d"(av[u][a]), "d"(bv[u][b]));
   }
   // partial tiles -> smem [warp][a][b][64], then K[a][b] summed over warps in order
   double* part = smp;
@@ -1120,11 +1156,18 @@ __global__ void __launch_bounds__(NT) k_gp_tc(TreeDev T, GPJobs2 JJ, const int* 
       double z[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) z[q] = 0.0;
-      for (int a = 0; a < rx; ++a) {
-        const double w = src_col(J.W, n, g, slot, a)[r2 + i];
+      for (int a0 = 0; a0 < rx; a0 += 8) {   // eight W loads in flight, same sum order
+        double w[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < nb) z[q] += w * K[a * ry + b0 + q];
+        for (int qa = 0; qa < 8; ++qa)
+          w[qa] = a0 + qa < rx ? src_col(J.W, n, g, slot, a0 + qa)[r2 + i] : 0.0;
+#pragma unroll
+        for (int qa = 0; qa < 8; ++qa)
+          if (a0 + qa < rx) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < nb) z[q] += w[qa] * K[(a0 + qa) * ry + b0 + q];
+          }
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q)
@@ -1145,7 +1188,10 @@ cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
   const int tmax = ((rxcap > rycap ? rxcap : rycap) + 7) / 8;
   if (!tc_off && rxcap > 0 && tmax <= 4) {
     const bool small = (long long)nnodes * nelem * njobs < 148LL * 4;
-    const int nw = small ? 8 : 4;
+    // a handful of CTAs in all: 16 warps per product
+    static const long long tiny_max = getenv("ACR_GP_TINY") ? atoll(getenv("ACR_GP_TINY")) : 74;
+    const bool tiny = (long long)nnodes * nelem * njobs <= tiny_max;
+    const int nw = tiny ? 16 : small ? 8 : 4;
     const int tm = tmax <= 1 ? 1 : tmax <= 2 ? 2 : 4;
     const size_t smem = ((size_t)nw * tm * tm * 64 + (size_t)rxcap * rycap) * 8;
     static bool attr_tc = false;
@@ -1156,10 +1202,17 @@ cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,
       cudaFuncSetAttribute(k_gp_tc<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_gp_tc<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_gp_tc<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_gp_tc<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr_tc = true;
     }
     dim3 g(nnodes, nelem, njobs);
-    if (small) {
+    if (tiny) {
+      if (tm == 1) CK_PDL(launch_pdl(k_gp_tc<512, 1>, g, dim3(512), smem, st, T, JJ, nodes));
+      else if (tm == 2) CK_PDL(launch_pdl(k_gp_tc<512, 2>, g, dim3(512), smem, st, T, JJ, nodes));
+      else CK_PDL(launch_pdl(k_gp_tc<512, 4>, g, dim3(512), smem, st, T, JJ, nodes));
+    } else if (small) {
       if (tm == 1) CK_PDL(launch_pdl(k_gp_tc<256, 1>, g, dim3(256), smem, st, T, JJ, nodes));
       else if (tm == 2) CK_PDL(launch_pdl(k_gp_tc<256, 2>, g, dim3(256), smem, st, T, JJ, nodes));
       else CK_PDL(launch_pdl(k_gp_tc<256, 4>, g, dim3(256), smem, st, T, JJ, nodes));
