@@ -313,6 +313,7 @@ __device__ void group_form_q(double* W, int mr, int p, const double* tau, const 
 }
 
 __constant__ bool jacobi_skip_confirm = true;
+__constant__ bool trunc_qsplit = true;    // ACR_NO_QSPLIT=1: large cores on the whole CTA
 __constant__ bool qr_lookahead = true;
 __constant__ int qr_la_max = 512;   // look-ahead QR for panels of at most this many rows (taller: every warp on the norm and the scaling)
 
@@ -407,6 +408,103 @@ __device__ int block_jacobi(double* B, int pr, int pc, double* J, int* flag) {
       }
     }
     if (!__syncthreads_or(rot)) return sweep + 1;
+  }
+  return 40;
+}
+
+// block_jacobi on a subset of the CTA: threads t = 0 .. JT-1 (whole warps),
+// named barrier `bar`, so the other warps can form the explicit Q meanwhile
+// (direct launches: a large core's Jacobi is the longest phase of the task).
+// Same pairing, lane groups and arithmetic as block_jacobi for JT threads,
+// plus warp_jacobi's rule that a sweep of sub-1e-9 rotations ends the
+// iteration (the confirmation sweep would rotate nothing).
+__device__ int group_jacobi(double* B, int pr, int pc, double* J, int t, int JT, int bar) {
+  __shared__ double gj_nb[16];
+  __shared__ int gj_flag[3][2];
+  auto sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(JT) : "memory"); };
+  const int lb = pr | 1, lj = pc | 1;
+  for (int i = t; i < pc * pc; i += JT) {
+    const int c = i / pc, r = i - c * pc;
+    J[c * lj + r] = (r == c) ? 1.0 : 0.0;
+  }
+  if (t < 6) gj_flag[t >> 1][t & 1] = 0;
+  sync();
+  if (pc < 2) return 0;
+  const int np = pc + (pc & 1), npairs = np / 2;
+  int gs = 32;
+  while (gs > 1 && gs * npairs > JT) gs >>= 1;
+  const int per = JT / gs;
+  const int sub = t & (gs - 1), grp = t / gs;
+  const double tol = sqrt((double)pr) * 2.220446049250313e-16;
+  double nb = 0.0;
+  for (int i = t; i < pr * pc; i += JT) {
+    const double x = B[(i / pr) * lb + i % pr];
+    nb += x * x;
+  }
+  nb = warp_sum(nb);
+  if ((t & 31) == 0) gj_nb[t >> 5] = nb;
+  sync();
+  nb = 0.0;
+  for (int w = 0; w < JT / 32; ++w) nb += gj_nb[w];
+  const double tiny = nb * 4.930380657631324e-32;   // (eps64 |B|_F)^2
+  const bool skipc = jacobi_skip_confirm;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rot = false, big = false;
+    const int fp = sweep % 3;
+    if (t < 2) gj_flag[(sweep + 1) % 3][t] = 0;   // last read two sweeps ago
+    for (int step = 0; step < np - 1; ++step) {
+      for (int base = 0; base < npairs; base += per) {
+        const int k = base + grp;
+        int i = 0, j = 0;
+        bool valid = k < npairs;
+        if (valid) {
+          i = rr_player(step, k, np);
+          j = rr_player(step, np - 1 - k, np);
+          valid = i < pc && j < pc;
+        }
+        double a = 0.0, b = 0.0, c = 0.0;
+        double* bi = B + (long long)i * lb;
+        double* bj = B + (long long)j * lb;
+        if (valid)
+          for (int r = sub; r < pr; r += gs) {
+            double x = bi[r], y = bj[r];
+            a += x * x;
+            b += y * y;
+            c += x * y;
+          }
+        for (int o = gs >> 1; o; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (valid && a > tiny && b > tiny && c != 0.0 &&
+            c * c > tol * tol * a * b) {
+          const double d = b - a, e = 2.0 * c;
+          double cs, sn;
+          jacobi_rot(d, e, cs, sn);
+          for (int r = sub; r < pr; r += gs) {
+            double x = bi[r], y = bj[r];
+            bi[r] = cs * x - sn * y;
+            bj[r] = sn * x + cs * y;
+          }
+          double* ji = J + (long long)i * lj;
+          double* jj = J + (long long)j * lj;
+          for (int r = sub; r < pc; r += gs) {
+            double x = ji[r], y = jj[r];
+            ji[r] = cs * x - sn * y;
+            jj[r] = sn * x + cs * y;
+          }
+          rot = true;
+          big |= c * c > 1e-18 * a * b;
+        }
+        sync();
+      }
+    }
+    if (rot) gj_flag[fp][0] = 1;
+    if (big) gj_flag[fp][1] = 1;
+    sync();
+    if (!gj_flag[fp][0]) return sweep + 1;
+    if (skipc && !gj_flag[fp][1]) return sweep + 1;
   }
   return 40;
 }
@@ -595,6 +693,7 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
   // per step costs more than the step); large cores: the whole CTA
   int sweeps;
   const bool wj = pc <= 16 && pr <= 128;      // larger cores: every warp of the CTA
+  const bool qsplit = !wj && NT >= 512 && trunc_qsplit;
   if (wj) {
     __shared__ int s_sw;
     if (tid < 32) {
@@ -613,6 +712,24 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
     }
     __syncthreads();
     sweeps = s_sw;
+  } else if (qsplit) {
+    // large core, 512-thread CTA: the Jacobi on the first eight warps, the
+    // explicit Q of both sides on the other eight (four per side) meanwhile
+    __shared__ int s_sw2;
+    if (tid < NT / 2) {
+      const int sw = group_jacobi(Bm, pr, pc, Jm, tid, NT / 2, 3);
+      if (tid == 0) s_sw2 = sw;
+    } else {
+      const int t2 = tid - NT / 2, nw2 = NT / 64, wu = nw2 / 2;
+      const int half = (t2 >> 5) >= wu ? 1 : 0;
+      const int nthr = (half ? nw2 - wu : wu) * 32;
+      const int t = half ? t2 - wu * 32 : t2;
+      Grp g{1 + half, nthr, t, nthr / 32, t >> 5, tid & 31, red + (half ? wu : 0), nullptr};
+      if (!half) group_form_q(Uw, um, pu, tauU, g);
+      else group_form_q(Vw, vm, pv, tauV, g);
+    }
+    __syncthreads();
+    sweeps = s_sw2;
   } else {
     sweeps = block_jacobi<NT>(Bm, pr, pc, Jm, iflag);
   }
@@ -674,7 +791,7 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
     const int j = ord[c];
     Cv[idx] = tr ? Bm[(long long)j * (pr | 1) + i] / sig[j] : Jm[(long long)j * (pc | 1) + i];
   }
-  if (!wj) {
+  if (!wj && !qsplit) {
     const int half = tid >= NT / 2 ? 1 : 0;
     const int t = tid - half * (NT / 2);
     Grp g{1 + half, NT / 2, t, (NT / 32) / 2, t >> 5, tid & 31, red + half * ((NT / 32) / 2),
@@ -1931,6 +2048,10 @@ void trunc_init_flags() {
   if (getenv("ACR_JACOBI_CONFIRM")) {
     const bool v = false;
     cudaMemcpyToSymbol(jacobi_skip_confirm, &v, sizeof(v));
+  }
+  if (getenv("ACR_NO_QSPLIT")) {
+    const bool v = false;
+    cudaMemcpyToSymbol(trunc_qsplit, &v, sizeof(v));
   }
   if (getenv("ACR_QR_LAMAX")) {               // development aid
     const int v = atoi(getenv("ACR_QR_LAMAX"));
