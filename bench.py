@@ -302,7 +302,15 @@ def run_ours(args):
         u_h.copy_(uu, non_blocking=True)
         return uu
 
-    e2e_step()                                      # untimed: first-use buffers
+    # the e2e steps run on a high-priority stream: the plan's fused forward
+    # sweep (its own lowest-priority stream) then only fills the SMs the
+    # factorisation's dependent chain leaves idle (ACR_BENCH_PRIO=0: default)
+    main_stream = stream
+    if os.environ.get("ACR_BENCH_PRIO", "1") != "0":
+        stream = torch.cuda.Stream(priority=-1)
+        stream.wait_stream(main_stream)
+    with torch.cuda.stream(stream):
+        e2e_step()                                  # untimed: first-use buffers
     torch.cuda.synchronize()
     barrier()
     # timed: the same per-step work through the public API, double-buffered
@@ -364,8 +372,10 @@ def run_ours(args):
     u = None
     for _ in range(2):
         ev_used = [None, None]
-        ms_p, u = e2e_pass()
+        with torch.cuda.stream(stream):
+            ms_p, u = e2e_pass()
         e2e_passes.append(ms_p)
+    stream = main_stream
     e2e_ms = min(e2e_passes)
     if dist is not None:
         t = torch.tensor([e2e_ms], device="cuda")

@@ -528,39 +528,13 @@ struct Plan {
     if (sev0) cudaEventDestroy(sev0);
     if (sev1) cudaEventDestroy(sev1);
     for (auto e : evpool) cudaEventDestroy(e);
-    for (int i = 0; i < NDS; ++i)
-      if (dstr[i]) {
-        cudaStreamSynchronize(dstr[i]);
-        cudaStreamDestroy(dstr[i]);
-        cudaEventDestroy(evds[i]);
-      }
-    if (st3) {
-      cudaStreamSynchronize(st3);
-      cudaStreamDestroy(st3);
-      for (auto e : evdef) cudaEventDestroy(e);
-    }
-    if (st2) {
-      cudaStreamSynchronize(st2);
-      cudaStreamDestroy(st2);
-      cudaEventDestroy(evf);
-      cudaEventDestroy(evj);
-    }
+    drop_chain_streams();
     if (stf) {
       cudaStreamSynchronize(stf);
       cudaStreamDestroy(stf);
       cudaEventDestroy(evfl);
       cudaEventDestroy(evfj);
     }
-    for (auto& qs : qstr)
-      if (qs.q0) {
-        cudaStreamSynchronize(qs.q0);
-        cudaStreamSynchronize(qs.q1);
-        cudaStreamDestroy(qs.q0);
-        cudaStreamDestroy(qs.q1);
-        cudaEventDestroy(qs.ef);
-        cudaEventDestroy(qs.ej0);
-        cudaEventDestroy(qs.ej1);
-      }
     if (stc) {
       cudaStreamSynchronize(stc);
       cudaStreamDestroy(stc);
@@ -580,6 +554,55 @@ struct Plan {
   bool no_qstreams = getenv("ACR_NO_QSTREAMS") != nullptr;   // development aid
   bool no_fuse_leaf = getenv("ACR_NO_FUSE_LEAF") != nullptr; // development aid
 
+  // The factor's helper streams carry parts of its dependent chain: they take
+  // the priority of the caller's stream, the fused forward right-hand-side
+  // sweep runs on a stream of the lowest priority.  A caller that passes a
+  // high-priority stream thus gets a sweep that only fills the SMs the chain
+  // leaves idle; with a default stream everything is at one priority, as
+  // before.  (ACR_NO_PRIO=1 creates every stream at the default.)
+  int chain_prio = 0;   // priority of the caller's stream when the helper streams were made
+  void make_stream(cudaStream_t* s, bool chain) {
+    static const bool off = getenv("ACR_NO_PRIO") != nullptr;
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, (off || !chain) ? lo : chain_prio));
+  }
+  // the helper streams that carry parts of the chain (side, deferred, per-depth
+  // and queue streams) are dropped when the caller's stream changes priority;
+  // they are made again, at the new priority, on first use
+  void drop_chain_streams() {
+    for (int i = 0; i < NDS; ++i)
+      if (dstr[i]) {
+        cudaStreamSynchronize(dstr[i]);
+        cudaStreamDestroy(dstr[i]);
+        cudaEventDestroy(evds[i]);
+        dstr[i] = nullptr;
+      }
+    if (st3) {
+      cudaStreamSynchronize(st3);
+      cudaStreamDestroy(st3);
+      for (auto& e : evdef) cudaEventDestroy(e);
+      st3 = nullptr;
+    }
+    if (st2) {
+      cudaStreamSynchronize(st2);
+      cudaStreamDestroy(st2);
+      cudaEventDestroy(evf);
+      cudaEventDestroy(evj);
+      st2 = nullptr;
+    }
+    for (auto& qs : qstr)
+      if (qs.q0) {
+        cudaStreamSynchronize(qs.q0);
+        cudaStreamSynchronize(qs.q1);
+        cudaStreamDestroy(qs.q0);
+        cudaStreamDestroy(qs.q1);
+        cudaEventDestroy(qs.ef);
+        cudaEventDestroy(qs.ej0);
+        cudaEventDestroy(qs.ej1);
+        qs.q0 = qs.q1 = nullptr;
+      }
+  }
   // second stream for independent launches at latency-bound levels (disabled
   // while instrumenting so per-class event timings stay on one stream)
   cudaStream_t st2 = nullptr;
@@ -587,7 +610,7 @@ struct Plan {
   cudaStream_t side() {
     if (prof_on || no_side) return st;
     if (!st2) {
-      CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+      make_stream(&st2, true);
       CK(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&evj, cudaEventDisableTiming));
     }
@@ -600,7 +623,7 @@ struct Plan {
   bool no_dsplit = getenv("ACR_NO_DSPLIT") != nullptr;   // development aid
   cudaStream_t depth_stream(int i) {
     if (!dstr[i]) {
-      CK(cudaStreamCreateWithFlags(&dstr[i], cudaStreamNonBlocking));
+      make_stream(&dstr[i], true);
       CK(cudaEventCreateWithFlags(&evds[i], cudaEventDisableTiming));
     }
     return dstr[i];
@@ -614,7 +637,7 @@ struct Plan {
   cudaStream_t deferred() {
     if (prof_on || no_side || no_defer) return st;
     if (!st3) {
-      CK(cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking));
+      make_stream(&st3, true);
       for (auto& e : evdef) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return st3;
@@ -643,6 +666,14 @@ struct Plan {
   }
   void use_stream(cudaStream_t s) {
     if (st_set && s == st) return;
+    {
+      int pr = 0;
+      CK(cudaStreamGetPriority(s, &pr));
+      if (pr != chain_prio) {
+        drop_chain_streams();
+        chain_prio = pr;
+      }
+    }
     if (st_set) {
       if (!evsw) CK(cudaEventCreateWithFlags(&evsw, cudaEventDisableTiming));
       CK(cudaEventRecord(evsw, st));
@@ -977,8 +1008,8 @@ struct Plan {
       if (!prof_on && !no_qstreams) {          // instrumented runs keep one stream
         QStreams& qs = qstr[bank];
         if (!qs.q0) {
-          CK(cudaStreamCreateWithFlags(&qs.q0, cudaStreamNonBlocking));
-          CK(cudaStreamCreateWithFlags(&qs.q1, cudaStreamNonBlocking));
+          make_stream(&qs.q0, true);
+          make_stream(&qs.q1, true);
           CK(cudaEventCreateWithFlags(&qs.ef, cudaEventDisableTiming));
           CK(cudaEventCreateWithFlags(&qs.ej0, cudaEventDisableTiming));
           CK(cudaEventCreateWithFlags(&qs.ej1, cudaEventDisableTiming));
@@ -2108,7 +2139,7 @@ struct Plan {
 
   void fwd_begin() {
     if (!stf) {
-      CK(cudaStreamCreateWithFlags(&stf, cudaStreamNonBlocking));
+      make_stream(&stf, false);
       CK(cudaEventCreateWithFlags(&evfl, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&evfj, cudaEventDisableTiming));
     }
