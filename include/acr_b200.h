@@ -95,7 +95,10 @@ int acr_solve(acr_plan_t* p, const double* rhs, int nrhs, double* u,
  * record is complete, overlapping the next levels' factorisation.  rhs
  * (m*n, nrhs) row-major, read during the call's stream work; single-GPU
  * plans.  acr_solve_back then runs the cutoff solve and back-substitution
- * into u (m*n, nrhs), once per fused factorisation. */
+ * into u (m*n, nrhs), once per fused factorisation.  The side stream has the
+ * device's lowest priority; the plan's other helper streams take the priority
+ * of `stream`, so a caller that passes a high-priority stream keeps the sweep
+ * out of the way of the factorisation's dependent chain. */
 int acr_factor_rhs(acr_plan_t* p, const double* D_sub, const double* D_diag,
                    const double* D_sup, const double* E, const double* F,
                    int inversion_order, const double* rhs, int nrhs, void* stream);

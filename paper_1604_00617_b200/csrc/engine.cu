@@ -664,16 +664,18 @@ struct Plan {
   void retag(Batch& b, cudaStream_t s) {
     retag(b.leaf, s); retag(b.U, s); retag(b.V, s); retag(b.rk, s);
   }
+  // (factor only: a solve on a stream of another priority -- say a
+  // back-substitution pushed behind the next factorisation -- keeps them)
+  void match_priority(cudaStream_t s) {
+    int pr = 0;
+    CK(cudaStreamGetPriority(s, &pr));
+    if (pr != chain_prio) {
+      drop_chain_streams();
+      chain_prio = pr;
+    }
+  }
   void use_stream(cudaStream_t s) {
     if (st_set && s == st) return;
-    {
-      int pr = 0;
-      CK(cudaStreamGetPriority(s, &pr));
-      if (pr != chain_prio) {
-        drop_chain_streams();
-        chain_prio = pr;
-      }
-    }
     if (st_set) {
       if (!evsw) CK(cudaEventCreateWithFlags(&evsw, cudaEventDisableTiming));
       CK(cudaEventRecord(evsw, st));
@@ -2878,6 +2880,7 @@ int acr_factor(acr_plan_t* h, const double* D_sub, const double* D_diag,
     return set_err(h, ACR_EARG, "unknown inversion_order");
   ACR_GUARD(h, {
     Plan& P = *h->p;
+    P.match_priority((cudaStream_t)stream);
     P.use_stream((cudaStream_t)stream);
     P.factor(D_sub, D_diag, D_sup, E, F, inversion_order);
   });
@@ -2906,6 +2909,7 @@ int acr_factor_rhs(acr_plan_t* h, const double* D_sub, const double* D_diag,
   ACR_GUARD(h, {
     Plan& P = *h->p;
     if (P.nranks() > 1) throw acr::ArgError("acr_factor_rhs: single-GPU plans only");
+    P.match_priority((cudaStream_t)stream);
     P.use_stream((cudaStream_t)stream);
     P.frhs = rhs;
     P.fk = nrhs;
