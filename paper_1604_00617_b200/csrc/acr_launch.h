@@ -98,8 +98,10 @@ cudaError_t launch_todense(const TreeDev& T, const HB* blk, int nblk,
 // work: unused (reserved), pass null
 cudaError_t lu_factor(double* A, int N, int* piv, int* info, double* work, cudaStream_t st);
 cudaError_t lu_transpose(const double* A, int N, double* At, cudaStream_t st);
+// perm (optional): row order after the interchanges, from lu_perm
 cudaError_t lu_solve(const double* A, const double* At, int N, const int* piv, double* B,
-                     int nrhs, cudaStream_t st);
+                     int nrhs, cudaStream_t st, const int* perm = nullptr);
+cudaError_t lu_perm(const int* piv, int N, int* perm, cudaStream_t st);
 cudaError_t launch_rhs_in(const double* rhs, int N, int k, int n, double* P,
                           cudaStream_t st);
 cudaError_t launch_u_out(const double* P, int N, int k, int n, double* u,

@@ -2312,13 +2312,21 @@ struct Plan {
         CK(cudaMemcpy2DAsync(B.as<double>() + (size_t)i * n, sizeof(double) * Nc,
                              f[Lt].as<double>() + i * kn, sizeof(double) * n,
                              sizeof(double) * n, k, cudaMemcpyDeviceToDevice, st));
+      // transposed LU and the row order after the interchanges: once per factor
+      const size_t lut_bytes = sizeof(double) * (size_t)Nc * Nc + sizeof(int) * (size_t)Nc;
+      const bool use_perm = (size_t)Nc * sizeof(int) <= 160 * 1024;
       if (!lut_ok) {
-        if (lut.n < sizeof(double) * (size_t)Nc * Nc) lut.alloc(sizeof(double) * (size_t)Nc * Nc, st);
+        if (lut.n < lut_bytes) lut.alloc(lut_bytes, st);
         CK(lu_transpose(lu.as<double>(), Nc, lut.as<double>(), st));
         ++launches;
+        if (use_perm) {
+          CK(lu_perm(piv.as<int>(), Nc, reinterpret_cast<int*>(lut.as<double>() + (size_t)Nc * Nc), st));
+          ++launches;
+        }
         lut_ok = true;
       }
-      CK(lu_solve(lu.as<double>(), lut.as<double>(), Nc, piv.as<int>(), B.as<double>(), k, st));
+      CK(lu_solve(lu.as<double>(), lut.as<double>(), Nc, piv.as<int>(), B.as<double>(), k, st,
+                  use_perm ? reinterpret_cast<const int*>(lut.as<double>() + (size_t)Nc * Nc) : nullptr));
       ++launches;
       for (int i = 0; i < mc; ++i)
         CK(cudaMemcpy2DAsync(uu[Lt].as<double>() + i * kn, sizeof(double) * n,

@@ -831,34 +831,62 @@ __global__ void k_transpose(const double* A, int N, double* At) {
   }
 }
 
+// row order after the factorisation's interchanges (perm[i] = original row
+// that ends up in position i): computed once per factorisation, so a solve
+// gathers its right-hand side instead of replaying N dependent swaps
+__global__ void k_lu_perm(const int* piv, int N, int* perm) {
+  extern __shared__ int pm[];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) pm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int j = 0; j < N; ++j) {
+      const int p = piv[j];
+      if (p != j) { const int t = pm[j]; pm[j] = pm[p]; pm[p] = t; }
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) perm[i] = pm[i];
+}
+
+// One CTA per right-hand-side column, y in shared memory.  Per 32-row block:
+// the diagonal block (prefetched into the other buffer during the previous
+// step) is solved by one warp, then every remaining row takes its update with
+// 16 loads in flight (At = A^T: coalesced across the rows).
 __global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, const double* At,
-                                                      int N, const int* piv, double* B) {
+                                                      int N, const int* piv, const int* perm,
+                                                      double* B) {
   extern __shared__ double y[];                 // N doubles, then N ints
   int* pv = reinterpret_cast<int*>(y + N);
-  __shared__ double T[32][33];
+  __shared__ double Tb[2][32][33];
   double* b = B + (long long)blockIdx.x * N;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < N; i += LS_T) { y[i] = b[i]; pv[i] = piv[i]; }
-  __syncthreads();
-  if (tid == 0)
-    for (int j = 0; j < N; ++j) {
-      const int p = pv[j];
-      if (p != j) { const double t = y[j]; y[j] = y[p]; y[p] = t; }
-    }
+  if (perm) {
+    for (int i = tid; i < N; i += LS_T) y[i] = b[perm[i]];
+  } else {
+    for (int i = tid; i < N; i += LS_T) { y[i] = b[i]; pv[i] = piv[i]; }
+    __syncthreads();
+    if (tid == 0)
+      for (int j = 0; j < N; ++j) {
+        const int p = pv[j];
+        if (p != j) { const double t = y[j]; y[j] = y[p]; y[p] = t; }
+      }
+  }
+  const int tr = tid >> 5, tc = tid & 31;       // this thread's element of a diagonal block
+  auto diag_elem = [&](int b0) {
+    const int r = b0 + tr, c = b0 + tc;
+    return (b0 >= 0 && b0 < N && r < N && c < N) ? A[(long long)r * N + c] : 0.0;
+  };
+  int cur = 0;
+  Tb[0][tr][tc] = diag_elem(0);
   __syncthreads();
   // forward: unit lower L
   for (int b0 = 0; b0 < N; b0 += 32) {
     const int bs = N - b0 < 32 ? N - b0 : 32;
-    for (int idx = tid; idx < bs * bs; idx += LS_T) {
-      const int r = idx / bs, c = idx - r * bs;
-      T[r][c] = A[(long long)(b0 + r) * N + b0 + c];
-    }
-    __syncthreads();
+    const double tn = diag_elem(b0 + 32);        // next block, in flight during this step
     if (tid < 32) {
       double v = lane < bs ? y[b0 + lane] : 0.0;
       for (int k = 0; k < bs; ++k) {
         const double yk = __shfl_sync(0xffffffffu, v, k);
-        if (lane > k && lane < bs) v -= T[lane][k] * yk;
+        if (lane > k && lane < bs) v -= Tb[cur][lane][k] * yk;
       }
       if (lane < bs) y[b0 + lane] = v;
     }
@@ -866,32 +894,33 @@ __global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, const
     for (int i = b0 + bs + tid; i < N; i += LS_T) {
       const double* ar = At + (long long)b0 * N + i;   // A[i][b0 + k] = ar[k N]
       double v = y[i];
-      for (int kb = 0; kb < bs; kb += 8) {       // 8 loads in flight, order kept
-        double a[8];
+      for (int kb = 0; kb < bs; kb += 16) {      // 16 loads in flight, order kept
+        double a[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = kb + u < bs ? ar[(long long)(kb + u) * N] : 0.0;
+        for (int u = 0; u < 16; ++u) a[u] = kb + u < bs ? ar[(long long)(kb + u) * N] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 16; ++u)
           if (kb + u < bs) v -= a[u] * y[b0 + kb + u];
       }
       y[i] = v;
     }
+    Tb[cur ^ 1][tr][tc] = tn;
+    cur ^= 1;
     __syncthreads();
   }
   // backward: upper U (non-unit diagonal), blocks from the bottom
-  for (int b0 = ((N - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
+  const int blast = ((N - 1) / 32) * 32;
+  Tb[cur][tr][tc] = diag_elem(blast);
+  __syncthreads();
+  for (int b0 = blast; b0 >= 0; b0 -= 32) {
     const int bs = N - b0 < 32 ? N - b0 : 32;
-    for (int idx = tid; idx < bs * bs; idx += LS_T) {
-      const int r = idx / bs, c = idx - r * bs;
-      T[r][c] = A[(long long)(b0 + r) * N + b0 + c];
-    }
-    __syncthreads();
+    const double tn = diag_elem(b0 - 32);
     if (tid < 32) {
       double v = lane < bs ? y[b0 + lane] : 0.0;
       for (int k = bs - 1; k >= 0; --k) {
-        if (lane == k) v = v / T[k][k];
+        if (lane == k) v = v / Tb[cur][k][k];
         const double yk = __shfl_sync(0xffffffffu, v, k);
-        if (lane < k) v -= T[lane][k] * yk;
+        if (lane < k) v -= Tb[cur][lane][k] * yk;
       }
       if (lane < bs) y[b0 + lane] = v;
     }
@@ -899,19 +928,33 @@ __global__ void __launch_bounds__(LS_T, 1) k_lu_solve_blk(const double* A, const
     for (int i = tid; i < b0; i += LS_T) {
       const double* ar = At + (long long)b0 * N + i;   // A[i][b0 + k] = ar[k N]
       double v = y[i];
-      for (int kb = bs - 1; kb >= 0; kb -= 8) {  // descending, 8 loads in flight
-        double a[8];
+      for (int kb = bs - 1; kb >= 0; kb -= 16) {  // descending, 16 loads in flight
+        double a[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = kb - u >= 0 ? ar[(long long)(kb - u) * N] : 0.0;
+        for (int u = 0; u < 16; ++u) a[u] = kb - u >= 0 ? ar[(long long)(kb - u) * N] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 16; ++u)
           if (kb - u >= 0) v -= a[u] * y[b0 + kb - u];
       }
       y[i] = v;
     }
+    Tb[cur ^ 1][tr][tc] = tn;
+    cur ^= 1;
     __syncthreads();
   }
   for (int i = tid; i < N; i += LS_T) b[i] = y[i];
+}
+
+cudaError_t lu_perm(const int* piv, int N, int* perm, cudaStream_t st) {
+  const size_t smem = (size_t)N * sizeof(int);
+  if (smem > 160 * 1024) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lu_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  k_lu_perm<<<1, 1024, smem, st>>>(piv, N, perm);
+  return cudaGetLastError();
 }
 
 cudaError_t lu_transpose(const double* A, int N, double* At, cudaStream_t st) {
@@ -921,7 +964,7 @@ cudaError_t lu_transpose(const double* A, int N, double* At, cudaStream_t st) {
 }
 
 cudaError_t lu_solve(const double* A, const double* At, int N, const int* piv, double* B,
-                     int nrhs, cudaStream_t st) {
+                     int nrhs, cudaStream_t st, const int* perm) {
   if (!nrhs) return cudaSuccess;
   const size_t smem = (size_t)N * (sizeof(double) + sizeof(int));
   if (smem <= 160 * 1024 && At) {
@@ -931,7 +974,7 @@ cudaError_t lu_solve(const double* A, const double* At, int N, const int* piv, d
                            160 * 1024);
       attr = true;
     }
-    k_lu_solve_blk<<<nrhs, LS_T, smem, st>>>(A, At, N, piv, B);
+    k_lu_solve_blk<<<nrhs, LS_T, smem, st>>>(A, At, N, piv, perm, B);
   } else {
     k_lu_solve<<<nrhs, 1024, 0, st>>>(A, N, piv, B);
   }
