@@ -17,6 +17,26 @@ for k, v in seen.items():
     print(k)
     for m in want:
         if m in v: print(f"   {m}: {v[m]}")
+# pipe utilisation and DRAM bytes from the raw page (FP64 / tensor-pipe counters)
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rr = list(csv.reader(io.StringIO(raw)))
+if len(rr) >= 3:
+    pipes = ["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+             "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+             "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+             "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+             "smsp__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+    h, u, v = rr[0], rr[1], rr[-1]
+    print("pipes / traffic (raw page):")
+    for m in pipes:
+        if m in h:
+            i = h.index(m)
+            print(f"   {m}: {v[i]} {u[i]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hi = [i for i, r in enumerate(rows[:50]) if "Warp Stall Sampling (All Samples)" in r]
