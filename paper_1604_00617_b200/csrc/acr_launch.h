@@ -34,6 +34,9 @@ long long pair_need_doubles(int m, int R);
 // leaf kernels (k_leaf.cu)
 cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
                            int* sing, cudaStream_t st);
+// tridiagonal leaves (lifted level); a nonzero off the band raises *fail |= 1 << 28
+cudaError_t launch_leafinv_tri(const TreeDev& T, const HB* H, int nelem, int leaf, int* sing,
+                               int* fail, cudaStream_t st);
 // diag: 0 general (DMMA), 1 A diagonal, 2 B diagonal (exact fast path)
 cudaError_t launch_leafgemm(const TreeDev& T, const HB* A, const HB* B,
                             const HB* C, int nelem, Src PX, RankRef xr, int diag,

@@ -1293,6 +1293,7 @@ struct Plan {
     long long ps;
     int* sing;
     int* rs = nullptr;   // rank snapshot [g][nnodes][2] (see inv_node: b11 beside b12 / b21)
+    bool tri = false;    // leaves are tridiagonal (lifted level): banded leaf inverse
     bool pend = false;   // S's off-diagonal recompressions still running on the side stream
     bool defer[32] = {}; // tree depths whose recompressions run on the deferred stream
   };
@@ -1306,9 +1307,13 @@ struct Plan {
     }
   }
 
-  void invert(const HB* H, int G, int R, int* sing) {
+  // tri: every leaf the inversion meets is tridiagonal (the lifted level);
+  // the banded leaf kernel checks it and raises TRI_FAIL in the overflow flag
+  bool tri_ok = getenv("ACR_NO_TRI") == nullptr;
+  void invert(const HB* H, int G, int R, int* sing, bool tri = false) {
     if (G <= 0) return;
     InvCtx c;
+    c.tri = tri && tri_ok && ht.bw <= 64;
     c.H = H;
     c.G = G;
     c.R = R;
@@ -1402,7 +1407,8 @@ struct Plan {
         hflops[1] += (double)c.G * 2.0 * sz * sz * sz;
         hbytes[1] += (double)c.G * 16.0 * sz * sz;        // leaf_inv: read + write
       }
-      CK(launch_leafinv(dt.T, c.H, c.G, nu, c.sing, st));
+      if (c.tri) CK(launch_leafinv_tri(dt.T, c.H, c.G, nu, c.sing, ovf.as<int>(), st));
+      else CK(launch_leafinv(dt.T, c.H, c.G, nu, c.sing, st));
       kend();
       ++launches;
       return;
@@ -1713,7 +1719,7 @@ struct Plan {
       kend();
       elem_bytes(ne, 2.0 * n * ht.bw);       // leaves copied (+ factors below the rank)
       ++launches;
-      invert(tDi.as<HB>(), ne, rec.Dinv.R, sg);
+      invert(tDi.as<HB>(), ne, rec.Dinv.R, sg, lvl == 0);
     }
     // 1b. halo: our first even block to the left, the right neighbour's to us
     Batch hDi;
@@ -1833,6 +1839,13 @@ struct Plan {
               mm, mg, Rout, h_ovf,
               std::chrono::duration<double, std::milli>(now - t_prev).count());
       t_prev = now;
+    }
+    if (h_ovf >= (1 << 28) && h_ovf < (1 << 29)) {
+      // a leaf of the lifted level was not tridiagonal after all: redo the
+      // level with the dense leaf inverse (never seen; the check is the guard)
+      tri_ok = false;
+      need = -1;
+      return false;
     }
     if (h_ovf) {
       if (h_ovf >= (1 << 29)) throw InternalError("truncation work area too small");
@@ -1987,7 +2000,7 @@ struct Plan {
       int tries = 0;
       size_t soff = 0;
       while (!reduce(L, Rout, lvl, order, nx, rec, need, dlev, nullptr, false, &soff)) {
-        Rout = std::max(need, 2 * Rout);
+        if (need >= 0) Rout = std::max(need, 2 * Rout);
         rec = Record();
         nx = Level();
         if (++tries > 8) throw InternalError("rank capacity retries exhausted");
@@ -2493,7 +2506,7 @@ struct Plan {
     Level nx;
     int need = 0, tries = 0;
     while (!reduce(L, Rout, L.lvl, 0, nx, rec, need, false, perm, true)) {
-      Rout = std::max(need, 2 * Rout);
+      if (need >= 0) Rout = std::max(need, 2 * Rout);
       rec = Record();
       nx = Level();
       if (++tries > 8) throw InternalError("rank capacity retries exhausted");

@@ -477,6 +477,169 @@ static cudaError_t leafinv_reg(const TreeDev& T, const HB* H, int nelem, int lea
   return cudaGetLastError();
 }
 
+// Inverse of a TRIDIAGONAL leaf (the lifted level: D is given by its three
+// bands and the Schur complements of its inversion only change a corner
+// entry, so every leaf a level-0 inversion meets is exactly tridiagonal).
+// Elimination with partial pivoting restricted to the band -- the pivot choice
+// of getrf on such a matrix (rows k and k+1 are the only candidates, the
+// first maximum wins), LAPACK dgttrf's recurrences -- by one thread, then
+// thread j solves for column j of the inverse (dgtts2).  O(s^2) per leaf
+// instead of 2 s^3.  The structure is checked while the leaf is read: any
+// nonzero off the band raises `fail` (the level is then redone with the
+// dense kernel), so a wrong assumption cannot produce a wrong inverse.
+static constexpr int TRI_FAIL = 1 << 28;
+
+__global__ void __launch_bounds__(64) k_leafinv_tri(TreeDev T, const HB* H, int leaf, int* sing,
+                                                    int* fail) {
+  ACR_PDL_ENTRY();
+  const int g = blockIdx.x, tid = threadIdx.x, bw = T.bw;
+  const int lo = T.lo[leaf], s = T.hi[leaf] - lo;
+  double* L = H[g].leaf + (long long)lo * bw;
+  __shared__ double dl[64], dd[64], du[64], du2[64], rd[64];
+  __shared__ int ip[64];
+  __shared__ int s_bad;
+  // read the leaf by rows (coalesced), keep the band, check the rest
+  bool nz = false;
+  if (tid == 0) s_bad = 0;
+  if (tid < s) { dl[tid] = 0.0; du[tid] = 0.0; du2[tid] = 0.0; }
+  __syncthreads();
+  // (all the loads of a 32-row half issued before any of them is used: one
+  // trip to memory per half instead of one per row)
+#pragma unroll
+  for (int h0 = 0; h0 < 64; h0 += 32) {
+    double v[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      v[q] = (tid < s && h0 + q < s) ? L[(long long)(h0 + q) * bw + tid] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int r = h0 + q;
+      if (r < s) {
+        if (tid == r) dd[r] = v[q];
+        else if (tid == r - 1) dl[tid] = v[q];   // sub-diagonal entry (r, r-1) -> dl[r-1]
+        else if (tid == r + 1) du[r] = v[q];     // super-diagonal entry (r, r+1) -> du[r]
+        else if (v[q] != 0.0) nz = true;
+      }
+    }
+  }
+  if (__syncthreads_or(nz)) {
+    if (tid == 0) atomicMax(fail, TRI_FAIL);
+    return;
+  }
+  if (tid == 0) {
+    // the running diagonal and super-diagonal entries stay in registers (the
+    // chain of a step is one division and one FMA; the band loads of the next
+    // step do not depend on it)
+    int bad = 0;
+    double dk = dd[0], uk = s > 1 ? du[0] : 0.0;        // d(k), du(k) as updated so far
+    for (int k = 0; k + 1 < s; ++k) {
+      const double lk = dl[k], dn = dd[k + 1];
+      const double un = k + 2 < s ? du[k + 1] : 0.0;
+      if (fabs(dk) >= fabs(lk)) {                // no interchange
+        ip[k] = 0;
+        double dn2 = dn;
+        if (dk != 0.0) {
+          const double f = lk / dk;
+          dl[k] = f;
+          dn2 = dn - f * uk;
+        } else {
+          bad = 1;
+        }
+        dd[k] = dk;
+        du[k] = uk;
+        du2[k] = 0.0;
+        dk = dn2;
+        uk = un;
+      } else {                                   // rows k, k+1 interchanged
+        const double f = dk / lk;
+        dd[k] = lk;
+        dl[k] = f;
+        du[k] = dn;
+        du2[k] = un;                             // (zero beyond the band's end)
+        ip[k] = 1;
+        dk = uk - f * dn;
+        uk = -f * un;
+      }
+    }
+    if (s > 0) dd[s - 1] = dk;
+    for (int k = 0; k < s; ++k)
+      if (dd[k] == 0.0) bad = 1;
+    s_bad = bad;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) {
+      int ps = 0;
+      for (int v = 0; v < T.nnodes; ++v)
+        if (T.isleaf[v] && T.lo[v] < lo) ++ps;
+      atomicMin(sing + g, ps);
+    }
+    return;
+  }
+  if (tid < s) rd[tid] = 1.0 / dd[tid];
+  __syncthreads();
+  int nf = 0;
+  if (tid < s) {
+    // The right-hand side e_tid lives in column tid of the leaf itself (every
+    // thread has read what it needs of the input; a store by this thread is
+    // only ever read back by this thread): no shared-memory copy, so a dozen
+    // CTAs fit an SM.
+    double* b = L + tid;                         // b(i) = L[i * bw + tid]
+    // forward: L and the interchanges; entries above tid - 1 are zero (not
+    // stored), the running entry b(k) is carried in a register
+    const int k0 = tid > 0 ? tid - 1 : 0;
+    double bk = k0 == tid ? 1.0 : 0.0;           // b(k0)
+    for (int k = k0; k + 1 < s; ++k) {
+      const double bn = k + 1 == tid ? 1.0 : 0.0;   // b(k+1) before the step (untouched so far)
+      if (!ip[k]) {
+        b[(long long)k * bw] = bk;
+        bk = bn - dl[k] * bk;
+      } else {
+        b[(long long)k * bw] = bn;
+        bk = bk - dl[k] * bn;
+      }
+    }
+    // back: U with two super-diagonals, x(i+1) and x(i+2) carried in
+    // registers; the forward results come back 16 rows at a time
+    double x1 = bk * rd[s - 1], x2 = 0.0;
+    if (!isfinite(x1)) nf = 1;
+    b[(long long)(s - 1) * bw] = x1;
+    for (int i0 = s - 2; i0 >= 0; i0 -= 16) {
+      double y[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int i = i0 - q;
+        y[q] = (i >= k0) ? b[(long long)i * bw] : 0.0;   // i >= k0 >= 0
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int i = i0 - q;
+        if (i >= 0) {
+          const double x = (y[q] - du[i] * x1 - du2[i] * x2) * rd[i];
+          if (!isfinite(x)) nf = 1;
+          b[(long long)i * bw] = x;
+          x2 = x1;
+          x1 = x;
+        }
+      }
+    }
+  }
+  if (__syncthreads_or(nf) && tid == 0) {
+    int ps = 0;
+    for (int v = 0; v < T.nnodes; ++v)
+      if (T.isleaf[v] && T.lo[v] < lo) ++ps;
+    atomicMin(sing + g, ps);
+  }
+}
+
+cudaError_t launch_leafinv_tri(const TreeDev& T, const HB* H, int nelem, int leaf, int* sing,
+                               int* fail, cudaStream_t st) {
+  if (!nelem) return cudaSuccess;
+  if (T.bw > 64) return cudaErrorInvalidValue;
+  CK_PDL(launch_pdl(k_leafinv_tri, dim3(nelem), dim3(64), 0, st, T, H, leaf, sing, fail));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_leafinv(const TreeDev& T, const HB* H, int nelem, int leaf,
                            int* sing, cudaStream_t st) {
   if (!nelem) return cudaSuccess;
