@@ -1310,10 +1310,11 @@ struct Plan {
   // tri: every leaf the inversion meets is tridiagonal (the lifted level);
   // the banded leaf kernel checks it and raises TRI_FAIL in the overflow flag
   bool tri_ok = getenv("ACR_NO_TRI") == nullptr;
+  bool tri_all = getenv("ACR_TRI_ALL") != nullptr;   // test aid: ask for it at every level (exercises the fallback)
   void invert(const HB* H, int G, int R, int* sing, bool tri = false) {
     if (G <= 0) return;
     InvCtx c;
-    c.tri = tri && tri_ok && ht.bw <= 64;
+    c.tri = (tri || tri_all) && tri_ok && ht.bw <= 64;
     c.H = H;
     c.G = G;
     c.R = R;

@@ -388,6 +388,45 @@ def test_multi_rhs_columns_match_single_solves(solver_mod):
         assert _rel(u3[:, j], uj) <= 1e-13
 
 
+@pytest.mark.parametrize("shift", [6.0, 1.0, 0.25])
+def test_lifted_level_banded_leaf_inverse(solver_mod, shift, monkeypatch):
+    """The lifted level inverts its (exactly tridiagonal) leaves with the banded
+    kernel k_leafinv_tri -- getrf's pivot rule restricted to the band.  With a
+    small diagonal shift the leaves are indefinite and rows are interchanged;
+    the result must agree with the dense leaf inverse (ACR_NO_TRI=1) and the
+    oracle, ranks included."""
+    s = P.random_system(8, 32, seed=17, shift=shift)
+    tol = Tolerance(1e-12)
+    u1, r1 = solver_mod.acr_solve(s, tol, leaf_size=8)
+    monkeypatch.setenv("ACR_NO_TRI", "1")
+    u2, r2 = solver_mod.acr_solve(s, tol, leaf_size=8)
+    monkeypatch.delenv("ACR_NO_TRI")
+    uo, ro = O.acr_solve(s, tol, leaf_size=8)
+    scale = max(1.0, ro.residual / 1e-13)          # ill-conditioned draws move all three alike
+    assert _rel(u1, u2) <= 1e-11 * scale
+    assert _rel(u1, uo) <= 1e-9 * scale
+    # rank decisions: identical, except that the ill-conditioned draw (1e-12
+    # threshold against roundoff amplified by the conditioning) may flip one
+    slack = 0 if shift >= 1.0 else 1
+    for p, q in zip(r1.per_level_ranks, r2.per_level_ranks):
+        assert all(abs(a - b) <= slack for a, b in zip(p.max_by_depth, q.max_by_depth))
+
+
+def test_banded_leaf_inverse_falls_back_on_dense_leaves(solver_mod, monkeypatch):
+    """k_leafinv_tri checks the band structure while it reads a leaf.  Asked to
+    run on a reduced level (ACR_TRI_ALL=1), it meets dense leaves, raises its
+    flag, and the level is redone with the dense inverse: the result is the
+    default run's, bit for bit."""
+    s = P.random_system(8, 32, seed=19)
+    tol = Tolerance(1e-10)
+    u1, r1 = solver_mod.acr_solve(s, tol, leaf_size=8)
+    monkeypatch.setenv("ACR_TRI_ALL", "1")
+    u2, r2 = solver_mod.acr_solve(s, tol, leaf_size=8)
+    monkeypatch.delenv("ACR_TRI_ALL")
+    assert np.array_equal(u1, u2)
+    assert r1.levels == r2.levels >= 2
+
+
 @pytest.mark.parametrize("n,leaf", [(50, 7), (64, 16), (128, 64)])
 def test_solve_column_counts_cover_every_panel_path(solver_mod, n, leaf):
     """HODLR x panel phase B (k_hmatB_tc) picks its path by column count: one
