@@ -1062,6 +1062,7 @@ __global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
   // loads issued in batches of 4 before their shared-memory stores
   double* u = sm;
   double* v = u + r * s;
+  int nzu = 0, nzv = 0;
   for (int base = tid; base < r * s; base += 4 * LT) {
     double a[4], b[4];
 #pragma unroll
@@ -1075,9 +1076,15 @@ __global__ void __launch_bounds__(LT) k_leaflr(TreeDev T, const HB* H, int mu,
     for (int q = 0; q < 4; ++q) {
       const int idx = base + q * LT;
       if (idx < r * s) { u[idx] = a[q]; v[idx] = b[q]; }
+      nzu |= a[q] != 0.0;
+      nzv |= b[q] != 0.0;
     }
   }
-  __syncthreads();
+  // the leaf's rows of U, or of V, are exact zeros (the lifted level: a Schur
+  // update W V12^T touches one corner entry of one leaf): the update adds
+  // exact zeros, the leaf is neither read nor written
+  if (!__syncthreads_or(nzu)) return;
+  if (!__syncthreads_or(nzv)) return;
   // leaf += u v^T: 8 leaf entries per thread in flight (same sum order)
   double* L = H[g].leaf + (long long)lo * bw;
   for (int base = tid; base < s * s; base += 8 * LT) {
