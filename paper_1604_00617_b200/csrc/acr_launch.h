@@ -71,7 +71,7 @@ cudaError_t launch_build_tab(HB* tab, HB base, long long sl, long long sf,
 
 // HODLR x panel (k_hmat.cu)
 cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
-                        int nelem, cudaStream_t st);
+                        int nelem, cudaStream_t st, int zskip = 0);
 // HODLR x panel for a diagonal HODLR operand (row scaling; level 0)
 cudaError_t launch_hmat_diag(const TreeDev& T, const MMJob& job, int nelem, cudaStream_t st);
 cudaError_t launch_gp(const TreeDev& T, const GPJob* jobs, int njobs,

@@ -837,9 +837,9 @@ struct Plan {
   unsigned long long* ctrp() { return prof_on ? dctr.as<unsigned long long>() : nullptr; }
   // instrumented launch wrappers: class events around the kernel, census
   // kernel (algorithmic FLOP / bytes from the device ranks) after it
-  void hmat(const MMJob* J, int nj, int G, cudaStream_t s) {
+  void hmat(const MMJob* J, int nj, int G, cudaStream_t s, bool zskip = false) {
     kbegin(3);
-    CK(launch_hmat(dt.T, J, nj, G, s));
+    CK(launch_hmat(dt.T, J, nj, G, s, zskip ? 1 : 0));
     kend();
     launches += 2;
     if (prof_on) CK(launch_census_hmat(dt.T, J, nj, G, ctrp(), s));
@@ -1371,7 +1371,7 @@ struct Plan {
     // the two jobs need distinct t-buffers
     double* tb2 = scratch<double>(11, (size_t)c.G * std::max(J[0].nA, 1) * c.R * c.R);
     J[1].tbuf = tb2;
-    hmat(J, 2, c.G, st);
+    hmat(J, 2, c.G, st, c.tri);   // lifted level: panels with one nonzero row
   }
 
   // add_lowrank(H_mu, (U, V)) with rank (nu, fside) if (nu, 1-fside) != 0:

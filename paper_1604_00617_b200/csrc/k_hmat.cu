@@ -655,7 +655,7 @@ static constexpr int HB_COLS = 256;
 
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, int path, int W,
-                                                        int ldl) {
+                                                        int ldl, int zskip) {
   ACR_PDL_ENTRY();
   constexpr bool AREG = MINB < 5;       // leaf fragments kept in registers
   extern __shared__ double sm[];
@@ -675,7 +675,22 @@ __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, i
   double* X = L + bw * ldl;       // 8 W x ldl, column-major
   const HB h = J.H[g];
   const int lam = R.lam, lo = T.lo[lam], s = T.hi[lam] - lo;
-  {
+  // zskip (the lifted level's inversion: panels with a single nonzero row):
+  // when every X row of this leaf is an exact zero the leaf product is zero,
+  // and neither the leaf nor X is fetched -- only the ancestors' terms remain
+  bool have_leaf = true;
+  if (zskip) {
+    int nzx = 0;
+    for (int q = 0; q < R.cnt; ++q) {
+      const int slot = R.slot[q], nc = R.cols[q];
+      for (int idx = threadIdx.x; idx < nc * s; idx += 256) {
+        const int b = idx / s, ii = idx - b * s;
+        nzx |= src_col(J.X, n, g, slot, b)[lo + ii] != 0.0;
+      }
+    }
+    have_leaf = __syncthreads_or(nzx) != 0;
+  }
+  if (have_leaf) {
     const double* Lg = h.leaf + (long long)lo * bw;
     if (!(s & 1)) {
       // warp per row, a 16-byte chunk per lane
@@ -719,14 +734,14 @@ __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, i
   double a[AREG ? 16 : 1];
   for (int w0 = 0; w0 < ntot; w0 += 8 * W) {
     const int wn = ntot - w0 < 8 * W ? ntot - w0 : 8 * W;
-    for (int j = warp; j < wn; j += 8) {
+    for (int j = warp; j < wn && have_leaf; j += 8) {
       const int qb = col_qb[w0 + j];
       const double* src = src_col(J.X, n, g, R.slot[qb >> 16], qb & 0xffff) + lo;
       for (int ii = lane; ii < s; ii += 32) cp_async8(X + j * ldl + ii, src + ii, true);
     }
     cp_async_wait_all();
     __syncthreads();
-    if (AREG && w0 == 0) {
+    if (AREG && w0 == 0 && have_leaf) {
 #pragma unroll
       for (int kk = 0; kk < (AREG ? 16 : 1); ++kk) {
         const int j = kk * 4 + ti;
@@ -743,7 +758,7 @@ __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, i
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         const int j = kk * 4 + ti;
-        if (j < s) {
+        if (j < s && have_leaf) {
           double av;
           if constexpr (AREG) av = a[kk];
           else av = rowok ? La[j * lj] : 0.0;
@@ -781,7 +796,9 @@ __global__ void __launch_bounds__(256, MINB) k_hmatB_tc(TreeDev T, MMJobs2 JJ, i
         const double* xA = X + (okA ? jA : t0) * ldl;
         const double* xB = X + (okB ? jB : t0) * ldl;
         double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;
-        if (s == 64 && !J.trans && !AREG) {
+        if (!have_leaf) {
+          // zero leaf product: the accumulators start from the ancestors' terms
+        } else if (s == 64 && !J.trans && !AREG) {
           // full 64-row leaf, plain product: no predicates, immediate offsets
           // (unstaged X columns of a ragged last tile are never stored)
           const double* la = La + ti;
@@ -890,7 +907,7 @@ cudaError_t launch_hmat_diag(const TreeDev& T, const MMJob& job, int nelem, cuda
 }
 
 cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
-                        int nelem, cudaStream_t st) {
+                        int nelem, cudaStream_t st, int zskip) {
   if (!nelem || !njobs) return cudaSuccess;
   MMJobs2 JJ;
   JJ.j[0] = jobs[0];
@@ -976,11 +993,11 @@ cudaError_t launch_hmat(const TreeDev& T, const MMJob* jobs, int njobs,
       const size_t smtc = ((size_t)T.bw + 8 * (size_t)W) * ldl * 8;
       static const int minb = getenv("ACR_HMAT_MINB") ? atoi(getenv("ACR_HMAT_MINB")) : 5;
       if (minb == 5)
-        CK_PDL(launch_pdl(k_hmatB_tc<5>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl));
+        CK_PDL(launch_pdl(k_hmatB_tc<5>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl, zskip));
       else if (minb == 4)
-        CK_PDL(launch_pdl(k_hmatB_tc<4>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl));
+        CK_PDL(launch_pdl(k_hmatB_tc<4>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl, zskip));
       else
-        CK_PDL(launch_pdl(k_hmatB_tc<3>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl));
+        CK_PDL(launch_pdl(k_hmatB_tc<3>, dim3(g), dim3(256), smtc, st, T, JJ, (int)path, W, ldl, zskip));
       return cudaGetLastError();
     }
     // 256 threads per leaf CTA (measured: 128 and 512 are slower)
