@@ -7,6 +7,7 @@
 // hmat, phase B: per leaf lambda below mu,
 //   Y[rows lambda] = L X[rows lambda]  (+ U t of each ancestor inside the
 //   subtree, deepest first -- the reference's recursion order)
+//   k_hmatB_tc (FP64 tensor pipe, leaves of at most 64 rows) / k_hmatB_sm
 #include "acr_types.cuh"
 #include "acr_launch.h"
 #include "acr_pdl.cuh"

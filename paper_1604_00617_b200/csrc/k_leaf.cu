@@ -1,6 +1,8 @@
 // Dense-leaf kernels of the batched HODLR arithmetic.
 //   k_leafinv   leaf inverse, reference algebra.py:199-207 (np.linalg.solve(L, I)
-//               with partial pivoting; singular / non-finite flagged per block)
+//               with partial pivoting; singular / non-finite flagged per block);
+//               k_leafinv_tri: the same for the exactly tridiagonal leaves of
+//               the lifted level (banded elimination, getrf's pivot rule)
 //   k_leafgemm  leaf products of multiply (algebra.py:162-163) followed by the
 //               ancestors' cross terms, deepest first (algebra.py:165-168 via
 //               add_lowrank's exact dense update, algebra.py:134-135)
