@@ -693,7 +693,10 @@ __device__ __forceinline__ void trunc_block_full(const TruncArgs& A, const TaskC
   // per step costs more than the step); large cores: the whole CTA
   int sweeps;
   const bool wj = pc <= 16 && pr <= 128;      // larger cores: every warp of the CTA
-  const bool qsplit = !wj && NT >= 512 && trunc_qsplit;
+  // (cores of up to 40 columns: a larger core's Jacobi is bound by its work,
+  // not by the chain of its steps, and wants all sixteen warps -- config 4,
+  // ranks up to 101: 1.27 s with this limit, 1.90 s without)
+  const bool qsplit = !wj && NT >= 512 && trunc_qsplit && pc <= 40;
   if (wj) {
     __shared__ int s_sw;
     if (tid < 32) {
